@@ -1,0 +1,558 @@
+// The extern "C" boundary (include/pq_b200.h): argument checks with the reference's messages,
+// host<->device staging for PQ_HOST calls, and exception -> return-code mapping.  No entry point
+// has a CPU fallback; without an sm_100 device, context creation fails.
+#include "pq_b200.h"
+
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+
+using namespace pqb;
+
+namespace pqb {
+std::string& last_error_slot() {
+    thread_local std::string msg;
+    return msg;
+}
+}  // namespace pqb
+
+namespace {
+
+void need(bool ok, const char* what) {
+    if (!ok) throw std::invalid_argument(what);
+}
+
+void need_ctx(pq_ctx* c) {
+    if (!c) throw std::invalid_argument("pq: null context");
+    cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+}
+
+long long dim_of(int d, const int* shape) {
+    need(d >= 1 && d <= 3 && shape, "KroneckerSum: need one to three factors");
+    long long n = 1;
+    for (int k = 0; k < d; ++k) {
+        need(shape[k] > 0, "KroneckerSum: factors must be square and nonempty");
+        n *= shape[k];
+    }
+    return n;
+}
+
+// Device view of a caller vector: device pointers pass through; host data is staged.
+const double* stage_in(pq_ctx& c, const double* p, size_t count, int space, const char* slot) {
+    if (space == PQ_DEVICE || count == 0) return p;
+    double* d = ws(c, slot, count);
+    cuda_check(cudaMemcpyAsync(d, p, count * sizeof(double), cudaMemcpyHostToDevice, c.stream), "H2D");
+    return d;
+}
+double* stage_out(pq_ctx& c, double* p, size_t count, int space, const char* slot) {
+    if (space == PQ_DEVICE) return p;
+    return ws(c, slot, count);
+}
+void finish_out(pq_ctx& c, double* host, const double* dev, size_t count, int space) {
+    if (space == PQ_DEVICE) return;
+    cuda_check(cudaMemcpyAsync(host, dev, count * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "D2H");
+}
+void finish(pq_ctx& c, int space) {
+    if (space == PQ_HOST) cuda_check(cudaStreamSynchronize(c.stream), "stream sync");
+    int err = 0;
+    // singular LU flag (dense.hpp:167) -- checked whenever the host already waits
+    if (space == PQ_HOST) {
+        cuda_check(cudaMemcpy(&err, c.d_err, sizeof(int), cudaMemcpyDeviceToHost), "err readback");
+        if (err) {
+            cudaMemset(c.d_err, 0, sizeof(int));
+            throw std::runtime_error("lu_solve: singular matrix");
+        }
+    }
+}
+
+NodesWeights rule_from(int m, const double* nodes, const double* weights) {
+    need(m >= 1 && nodes && weights, "phi_fixed: rule needs at least one point");
+    NodesWeights r;
+    r.x.assign(nodes, nodes + m);
+    r.w.assign(weights, weights + m);
+    return r;
+}
+
+int check_kind(int kind) {
+    need(kind == PQ_GAUSS_LEGENDRE || kind == PQ_CLENSHAW_CURTIS, "pq: unknown quadrature kind");
+    return kind;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* pq_version(void) { return "phiquad-b200 0.1 (sm_100a, FP64 DMMA)"; }
+const char* pq_last_error(void) { return last_error_slot().c_str(); }
+
+int pq_ctx_create(int device, pq_ctx** out) {
+    return guarded([&] {
+        need(out != nullptr, "pq_ctx_create: null out");
+        int count = 0;
+        if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+            cudaGetLastError();
+            throw CudaError("pq_ctx_create: no CUDA device (the engine has no CPU fallback)");
+        }
+        need(device >= 0 && device < count, "pq_ctx_create: device index out of range");
+        cudaDeviceProp prop{};
+        cuda_check(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+        if (prop.major != 10)
+            throw CudaError("pq_ctx_create: kernels are built for sm_100a; device is sm_" + std::to_string(prop.major) +
+                            std::to_string(prop.minor));
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        auto* c = new pq_ctx();
+        c->device = device;
+        cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+        c->own_stream = true;
+        cuda_check(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc(err)");
+        cuda_check(cudaMemset(c->d_err, 0, sizeof(int)), "memset(err)");
+        cuda_check(cudaMalloc(&c->d_int, 64 * sizeof(int)), "cudaMalloc(int)");
+        cuda_check(cudaMalloc(&c->d_small, 1024 * sizeof(double)), "cudaMalloc(small)");
+        cuda_check(cudaMallocHost(&c->h_small, 1024 * sizeof(double)), "cudaMallocHost(small)");
+        *out = c;
+    });
+}
+
+int pq_ctx_destroy(pq_ctx* c) {
+    return guarded([&] {
+        if (!c) return;
+        cudaSetDevice(c->device);
+        cudaStreamSynchronize(c->stream);
+        for (auto& kv : c->bufs)
+            if (kv.second.p) cudaFree(kv.second.p);
+        if (c->arena.host) cudaFreeHost(c->arena.host);
+        if (c->arena.dev) cudaFree(c->arena.dev);
+        if (c->arena.done) cudaEventDestroy(c->arena.done);
+        cudaFree(c->d_err);
+        cudaFree(c->d_int);
+        cudaFree(c->d_small);
+        cudaFreeHost(c->h_small);
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        delete c;
+    });
+}
+
+int pq_ctx_set_stream(pq_ctx* c, void* stream) {
+    return guarded([&] {
+        need_ctx(c);
+        cuda_check(cudaStreamSynchronize(c->stream), "sync old stream");
+        if (c->own_stream) cudaStreamDestroy(c->stream);
+        if (stream) {
+            c->stream = static_cast<cudaStream_t>(stream);
+            c->own_stream = false;
+        } else {
+            cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+            c->own_stream = true;
+        }
+        if (c->arena.done) {
+            cudaEventDestroy(c->arena.done);
+            cuda_check(cudaEventCreateWithFlags(&c->arena.done, cudaEventDisableTiming), "event");
+            cuda_check(cudaEventRecord(c->arena.done, c->stream), "record");
+        }
+    });
+}
+
+void* pq_ctx_stream(const pq_ctx* c) { return c ? static_cast<void*>(c->stream) : nullptr; }
+
+int pq_ctx_synchronize(pq_ctx* c) {
+    return guarded([&] {
+        need_ctx(c);
+        finish(*c, PQ_HOST);
+    });
+}
+
+uint64_t pq_ctx_launches(const pq_ctx* c) { return c ? c->launches : 0; }
+
+int pq_ctx_set_workspace_limit(pq_ctx* c, uint64_t bytes) {
+    return guarded([&] {
+        need_ctx(c);
+        c->ws_limit = bytes;
+    });
+}
+
+int pq_ctx_release_workspace(pq_ctx* c) {
+    return guarded([&] {
+        need_ctx(c);
+        cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        for (auto& kv : c->bufs)
+            if (kv.second.p) cudaFree(kv.second.p);
+        c->bufs.clear();
+    });
+}
+
+int pq_ctx_set_profiling(pq_ctx* c, int on) {
+    return guarded([&] {
+        need_ctx(c);
+        c->profiling = on != 0;
+    });
+}
+
+int pq_ctx_phase_times(pq_ctx* c, double* ms6) {
+    return guarded([&] {
+        need_ctx(c);
+        need(ms6 != nullptr, "pq_ctx_phase_times: null out");
+        for (int i = 0; i < 6; ++i) ms6[i] = c->phase_ms[i];
+    });
+}
+
+// ---------------------------------------------------------------- host estimator -----------
+
+int pq_gauss_legendre(int m, double* nodes, double* weights) {
+    return guarded([&] {
+        const NodesWeights r = gauss_legendre01(m);
+        std::memcpy(nodes, r.x.data(), sizeof(double) * m);
+        std::memcpy(weights, r.w.data(), sizeof(double) * m);
+    });
+}
+
+int pq_clenshaw_curtis(int m, double* nodes, double* weights) {
+    return guarded([&] {
+        const NodesWeights r = clenshaw_curtis01(m);
+        std::memcpy(nodes, r.x.data(), sizeof(double) * m);
+        std::memcpy(weights, r.w.data(), sizeof(double) * m);
+    });
+}
+
+int pq_cached_rule(int kind, int m, const double** nodes, const double** weights) {
+    return guarded([&] {
+        const NodesWeights& r = memo_rule(check_kind(kind), m);
+        *nodes = r.x.data();
+        *weights = r.w.data();
+    });
+}
+
+int pq_quartic_roots(const double* c4, double* roots8) {
+    return guarded([&] {
+        auto z = quartic_zeros(Quartic{c4[0], c4[1], c4[2], c4[3]});
+        for (int k = 0; k < 4; ++k) {
+            roots8[2 * k] = z[static_cast<size_t>(k)].real();
+            roots8[2 * k + 1] = z[static_cast<size_t>(k)].imag();
+        }
+    });
+}
+
+int pq_real_roots_greater_one(const double* c4, double* roots4, int* count) {
+    return guarded([&] {
+        auto r = real_zeros_above_one(Quartic{c4[0], c4[1], c4[2], c4[3]});
+        *count = static_cast<int>(r.size());
+        for (size_t i = 0; i < r.size(); ++i) roots4[i] = r[i];
+    });
+}
+
+int pq_log_bound_at_rho(double n, int p, double alpha, double beta, int kind, double rho, double* out) {
+    return guarded([&] { *out = log_bound_rho(BoundArgs{n, p, alpha, beta, check_kind(kind)}, rho); });
+}
+
+int pq_bound_quartic(double n, int p, double alpha, double beta, int kind, double* c4) {
+    return guarded([&] {
+        const Quartic q = stationary_quartic(BoundArgs{n, p, alpha, beta, check_kind(kind)});
+        for (int k = 0; k < 4; ++k) c4[k] = q[static_cast<size_t>(k)];
+    });
+}
+
+int pq_theorem_bound(double n, int p, double alpha, double beta, int kind, double* out) {
+    return guarded([&] { *out = log_theorem_bound(BoundArgs{n, p, alpha, beta, check_kind(kind)}); });
+}
+
+int pq_corollary_bound(double n, int p, double alpha, double beta, int kind, double* out) {
+    return guarded([&] { *out = log_corollary_bound(BoundArgs{n, p, alpha, beta, check_kind(kind)}); });
+}
+
+int pq_quaderr(double n, int p, double alpha, double beta, int kind, double* out) {
+    return guarded([&] { *out = log_quaderr(n, p, alpha, beta, check_kind(kind)); });
+}
+
+int pq_quadnodes(double eps, int p, double alpha, double beta, int kind, int* n) {
+    return guarded([&] { *n = node_count(eps, p, alpha, beta, check_kind(kind)); });
+}
+
+int pq_setup_quadrature(double eps, int p, double alpha, double beta, int kind, double c1, double c2, int d, int* l,
+                        int* n, double* cost) {
+    return guarded([&] {
+        const Plan pl = plan_quadrature(eps, p, alpha, beta, check_kind(kind), Cost{c1, c2, d});
+        *l = pl.l;
+        *n = pl.n;
+        *cost = pl.cost;
+    });
+}
+
+int pq_infnorm_bound(int d, const int* shape, const double* factors, double* out) {
+    return guarded([&] {
+        dim_of(d, shape);
+        double s = 0.0;
+        size_t off = 0;
+        for (int k = 0; k < d; ++k) {
+            const int n = shape[k];
+            double best = 0.0;
+            for (int i = 0; i < n; ++i) {
+                double rs = 0.0;
+                for (int j = 0; j < n; ++j) rs += std::abs(factors[off + static_cast<size_t>(i) * n + j]);
+                if (rs > best) best = rs;
+            }
+            s += best;
+            off += static_cast<size_t>(n) * n;
+        }
+        *out = s;
+    });
+}
+
+// ---------------------------------------------------------------- device primitives --------
+
+int pq_expm(pq_ctx* c, int n, int batch, const double* a, const double* scale, double* out, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        need(n >= 0 && batch >= 0, "expm: bad extent");
+        if (n == 0 || batch == 0) return;
+        const size_t nn = static_cast<size_t>(n) * n;
+        if (space == PQ_HOST)
+            for (size_t e = 0; e < nn; ++e)
+                if (!std::isfinite(a[e])) throw std::invalid_argument("DenseMatrix: non-finite entry");
+        const double* da = stage_in(*c, a, nn, space, "hin_a");
+        double* dout = stage_out(*c, out, nn * batch, space, "hout");
+        std::vector<double> sc(static_cast<size_t>(batch), 1.0);
+        if (scale) {
+            if (space == PQ_HOST) {
+                std::memcpy(sc.data(), scale, sizeof(double) * batch);
+            } else {
+                cuda_check(cudaMemcpy(sc.data(), scale, sizeof(double) * batch, cudaMemcpyDeviceToHost), "scale");
+            }
+        }
+        arena_begin(*c);
+        double one_norm = -1.0;  // unknown for device input: counts are read back
+        if (space == PQ_HOST) {
+            std::vector<double> col(static_cast<size_t>(n), 0.0);
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j) col[static_cast<size_t>(j)] += std::abs(a[static_cast<size_t>(i) * n + j]);
+            one_norm = 0.0;
+            for (double v : col) one_norm = std::max(one_norm, v);
+        }
+        expm_batch(*c, n, batch, da, 0, sc, one_norm, dout);
+        finish_out(*c, out, dout, nn * batch, space);
+        finish(*c, space);
+    });
+}
+
+int pq_mode_apply(pq_ctx* c, int d, const int* shape, const double* mats, const double* x, double* y, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        const long long N = dim_of(d, shape);
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, mats, "mats");
+        const double* dx = stage_in(*c, x, N, space, "hin_x");
+        double* dy = stage_out(*c, y, N, space, "hout");
+        const double* E[3] = {op.F[0], op.F[1], op.F[2]};
+        long long Es[3] = {0, 0, 0};
+        mode_chain(*c, d, op.n, E, Es, dx, N, dy, N, 1, Epilogue{});
+        finish_out(*c, y, dy, N, space);
+        finish(*c, space);
+    });
+}
+
+int pq_kron_matvec(pq_ctx* c, int d, const int* shape, const double* factors, const double* x, double* y, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        const long long N = dim_of(d, shape);
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        const double* dx = stage_in(*c, x, N, space, "hin_x");
+        double* dy = stage_out(*c, y, N, space, "hout");
+        kron_matvec_dev(*c, op, 1.0, dx, dy);
+        finish_out(*c, y, dy, N, space);
+        finish(*c, space);
+    });
+}
+
+int pq_exp_action(pq_ctx* c, int d, const int* shape, const double* factors, const double* b, double* y, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        const long long N = dim_of(d, shape);
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        const double* db = stage_in(*c, b, N, space, "hin_b");
+        double* dy = stage_out(*c, y, N, space, "hout0");
+        exp_action_dev(*c, op, 1.0, 1, db, dy);
+        finish_out(*c, y, dy, N, space);
+        finish(*c, space);
+    });
+}
+
+// ---------------------------------------------------------------- phi engine ---------------
+
+int pq_phi_fixed(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs, int p, int m,
+                 const double* nodes, const double* weights, double* out, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        need(p >= 1, "phi_fixed: need p >= 1");
+        need(nb >= 0, "phi_fixed: need nb >= 0");
+        const long long N = dim_of(d, shape);
+        const NodesWeights rule = rule_from(m, nodes, weights);
+        if (nb == 0) return;
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        const double* db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
+        double* dout = stage_out(*c, out, static_cast<size_t>(nb) * p * N, space, "hout");
+        phi_fixed_dev(*c, op, 1.0, nb, db, p, rule, dout);
+        finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
+        finish(*c, space);
+    });
+}
+
+int pq_phi_adaptive(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs, int p,
+                    double eps, double* out, int* points_used, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        need(p >= 1, "phi_adaptive: need p >= 1");
+        need(eps > 0.0, "phi_adaptive: need eps > 0");
+        need(nb >= 1, "phi_adaptive: need at least one right-hand side");
+        const long long N = dim_of(d, shape);
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        const double* db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
+        double* dout = stage_out(*c, out, static_cast<size_t>(nb) * p * N, space, "hout");
+        phi_adaptive_dev(*c, op, 1.0, nb, db, p, eps, dout, points_used);
+        finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
+        finish(*c, space);
+    });
+}
+
+int pq_squaring_step(pq_ctx* c, int d, const int* shape, const double* exps, int p, double* y, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        need(p >= 1, "squaring_step: need p >= 1");
+        const long long N = dim_of(d, shape);
+        arena_begin(*c);
+        DevOp ex = upload_op(*c, d, shape, exps, "exps");
+        // exps are already exponentials: pass them as the override of the step's E
+        double* dy = space == PQ_DEVICE ? y : ws(*c, "hio_y", static_cast<size_t>(p) * N);
+        if (space == PQ_HOST)
+            cuda_check(cudaMemcpyAsync(dy, y, sizeof(double) * p * N, cudaMemcpyHostToDevice, c->stream), "H2D");
+        size_t total = 0;
+        for (int k = 0; k < d; ++k) total += static_cast<size_t>(shape[k]) * shape[k];
+        squaring_steps_dev(*c, ex, 1.0, 1, p, 1, dy, ex.F[0]);
+        (void)total;
+        finish_out(*c, y, dy, static_cast<size_t>(p) * N, space);
+        finish(*c, space);
+    });
+}
+
+int pq_phi_with_plan(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs, int p, int l,
+                     int n, int kind, double eps, double* out, int* points_used, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        need(l >= 0, "phi_with_plan: need l >= 0");
+        check_kind(kind);
+        need(p >= 1, kind == PQ_GAUSS_LEGENDRE ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
+        if (kind == PQ_GAUSS_LEGENDRE) need(n + 1 >= 1, "gauss_legendre: need at least one point");
+        const long long N = dim_of(d, shape);
+        if (nb == 0) return;
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        const double* db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
+        double* dout = stage_out(*c, out, static_cast<size_t>(nb) * p * N, space, "hout");
+        phi_with_plan_dev(*c, op, 1.0, nb, db, p, l, n, kind, eps, dout, points_used);
+        finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
+        finish(*c, space);
+    });
+}
+
+static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
+                          const pq_phi_request* req, double* out0, double* out, pq_phi_info* info, int space) {
+    need_ctx(c);
+    need(req != nullptr, "phiquadmv: null request");
+    need(req->p >= 1, "phiquadmv: need p >= 1");
+    check_kind(req->mode);
+    const long long N = dim_of(d, shape);
+    need(nb >= 1, "phiquadmv: need at least one right-hand side");
+    const int p = req->p;
+    arena_begin(*c);
+    DevOp op = upload_op(*c, d, shape, factors, "factors");
+    const double* db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
+    double* dout = stage_out(*c, out, static_cast<size_t>(nb) * p * N, space, "hout");
+    PlanInfo pi;
+    phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi);
+    if (out0) {
+        double* d0 = stage_out(*c, out0, static_cast<size_t>(nb) * N, space, "hout0");
+        exp_action_dev(*c, op, 1.0, nb, db, d0);
+        finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
+    }
+    finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
+    finish(*c, space);
+    if (info) {
+        info->l = pi.l;
+        info->n = pi.n;
+        info->points = pi.points;
+        info->mode = pi.mode;
+        info->planned = pi.planned;
+        info->alpha = pi.alpha;
+        info->beta = pi.beta;
+        info->plan_cost = pi.cost;
+    }
+}
+
+int pq_phiquadmv(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
+                 const pq_phi_request* req, double* out, pq_phi_info* info, int space) {
+    return guarded([&] { run_phiquadmv(c, d, shape, factors, nb, bs, req, nullptr, out, info, space); });
+}
+
+int pq_phi_0p(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
+              const pq_phi_request* req, double* out0, double* out, pq_phi_info* info, int space) {
+    return guarded([&] {
+        need(out0 != nullptr, "phi_0p: null phi_0 output");
+        run_phiquadmv(c, d, shape, factors, nb, bs, req, out0, out, info, space);
+    });
+}
+
+int pq_phi_lincomb(pq_ctx* c, int d, const int* shape, const double* factors, int p, const double* bs, int m,
+                   const double* nodes, const double* weights, double* out, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        need(p >= 1, "phi_lincomb: need at least one vector");
+        const long long N = dim_of(d, shape);
+        const NodesWeights rule = rule_from(m, nodes, weights);
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        const double* db = stage_in(*c, bs, static_cast<size_t>(p) * N, space, "hin_b");
+        double* dout = stage_out(*c, out, N, space, "hout");
+        phi_lincomb_dev(*c, op, 1.0, p, db, rule, dout);
+        finish_out(*c, out, dout, N, space);
+        finish(*c, space);
+    });
+}
+
+int pq_phi_nodes_partial(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs, int p,
+                         int l, int m, const double* nodes, const double* weights, int rank, int world, int zero,
+                         double* acc) {
+    return guarded([&] {
+        need_ctx(c);
+        need(p >= 1, "phi_fixed: need p >= 1");
+        need(l >= 0, "phi_with_plan: need l >= 0");
+        need(world >= 1 && rank >= 0 && rank < world, "phi_nodes_partial: bad rank/world");
+        dim_of(d, shape);
+        const NodesWeights rule = rule_from(m, nodes, weights);
+        std::vector<int> mine;
+        for (int i = rank; i < m; i += world) mine.push_back(i);
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        // nodes on 2^-l A: fold the exact power of two into the operator scale
+        phi_nodes_partial_dev(*c, op, std::ldexp(1.0, -l), nb, bs, p, rule, mine, zero, acc);
+    });
+}
+
+int pq_squaring_chain(pq_ctx* c, int d, const int* shape, const double* factors, int nb, int p, int l, double* y) {
+    return guarded([&] {
+        need_ctx(c);
+        need(l >= 0, "phi_with_plan: need l >= 0");
+        need(p >= 1, "squaring_step: need p >= 1");
+        dim_of(d, shape);
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        squaring_steps_dev(*c, op, 1.0, nb, p, l, y, nullptr);
+    });
+}
+
+}  // extern "C"

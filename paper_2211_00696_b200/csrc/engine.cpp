@@ -1,0 +1,779 @@
+// The phi pipeline on the device (reference: phiaction.hpp, kron.hpp, integrators.hpp).
+//
+// Data layout in HBM (N = prod n_k doubles per vector, vec order):
+//   factors      d blocks n_k x n_k, uploaded once per call
+//   node E       per dim k: q blocks n_k x n_k (expm((1-theta_i) 2^-l A_k)), contiguous
+//   chainA/B     Qc*N mode-product intermediates (Qc = node chunk fitting the workspace budget)
+//   nodeV        Qc*N node vectors v_i = (E_i0 (x) E_i1 (x) E_i2) b, consumed by the combine
+//   out / sqT    nb*p*N phi columns, ping-pong through the l squaring steps
+//   ccpool       adaptive CC: every node vector of the current ladder rule (reused next level)
+#include "engine.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+namespace pqb {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw CudaError(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------------ context helpers ------
+
+static size_t budget_bytes(pq_ctx& c) {
+    if (c.ws_limit == 0) {
+        size_t fr = 0, tot = 0;
+        cuda_check(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+        size_t held = 0;
+        for (auto& kv : c.bufs) held += kv.second.bytes;
+        c.ws_limit = static_cast<uint64_t>(0.85 * static_cast<double>(fr + held));
+    }
+    return static_cast<size_t>(c.ws_limit);
+}
+
+void* ws_bytes(pq_ctx& c, const std::string& name, size_t bytes) {
+    DevBuf& b = c.bufs[name];
+    if (b.bytes >= bytes && b.p) return b.p;
+    if (b.p) {
+        cuda_check(cudaStreamSynchronize(c.stream), "sync before realloc");
+        cudaFree(b.p);
+        b.p = nullptr;
+        b.bytes = 0;
+    }
+    const size_t want = std::max<size_t>(bytes, 256);
+    cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw CudaError("device workspace '" + name + "': cannot allocate " + std::to_string(want >> 20) + " MiB");
+    }
+    b.bytes = want;
+    return b.p;
+}
+
+double* ws(pq_ctx& c, const std::string& name, size_t count) {
+    return static_cast<double*>(ws_bytes(c, name, count * sizeof(double)));
+}
+
+void arena_begin(pq_ctx& c) {
+    ParamArena& a = c.arena;
+    if (!a.host) {
+        a.cap = size_t(8) << 20;
+        cuda_check(cudaMallocHost(reinterpret_cast<void**>(&a.host), a.cap), "cudaMallocHost(arena)");
+        cuda_check(cudaMalloc(reinterpret_cast<void**>(&a.dev), a.cap), "cudaMalloc(arena)");
+        cuda_check(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming), "event(arena)");
+        cuda_check(cudaEventRecord(a.done, c.stream), "record(arena)");
+    }
+    // the previous call's uploads must have left the pinned buffer before we overwrite it
+    cuda_check(cudaEventSynchronize(a.done), "arena wait");
+    a.used = a.flushed = 0;
+}
+
+const void* arena_push(pq_ctx& c, const void* data, size_t bytes) {
+    ParamArena& a = c.arena;
+    const size_t off = (a.used + 15) & ~size_t(15);
+    if (off + bytes > a.cap) {
+        arena_flush(c);
+        arena_begin(c);
+        return arena_push(c, data, bytes);
+    }
+    std::memcpy(a.host + off, data, bytes);
+    a.used = off + bytes;
+    return a.dev + off;
+}
+
+void arena_flush(pq_ctx& c) {
+    ParamArena& a = c.arena;
+    if (a.used > a.flushed) {
+        cuda_check(cudaMemcpyAsync(a.dev + a.flushed, a.host + a.flushed, a.used - a.flushed, cudaMemcpyHostToDevice,
+                                   c.stream),
+                   "arena upload");
+        a.flushed = a.used;
+        cuda_check(cudaEventRecord(a.done, c.stream), "record(arena)");
+    }
+}
+
+void count_launch(pq_ctx& c, int n) { c.launches += static_cast<uint64_t>(n); }
+
+void check_launch(pq_ctx& c) {
+    (void)c;
+    cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+// ------------------------------------------------------------------ operator upload ------
+
+DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const std::string& slot) {
+    if (d < 1 || d > 3) throw std::invalid_argument("KroneckerSum: need one to three factors");
+    DevOp op;
+    op.d = d;
+    size_t total = 0;
+    for (int k = 0; k < d; ++k) {
+        if (shape[k] <= 0) throw std::invalid_argument("KroneckerSum: factors must be square and nonempty");
+        op.n[k] = shape[k];
+        op.N *= shape[k];
+        total += static_cast<size_t>(shape[k]) * shape[k];
+    }
+    op.host.assign(factors, factors + total);
+    for (double v : op.host)
+        if (!std::isfinite(v)) throw std::invalid_argument("DenseMatrix: non-finite entry");
+    double* dev = ws(c, slot, total);
+    cuda_check(cudaMemcpyAsync(dev, factors, total * sizeof(double), cudaMemcpyHostToDevice, c.stream), "upload factors");
+    size_t off = 0;
+    for (int k = 0; k < d; ++k) {
+        const int n = op.n[k];
+        const double* f = op.host.data() + off;
+        op.F[k] = dev + off;
+        // dense.hpp:122-141 (host copies; the planner's alpha uses the inf-norms)
+        std::vector<double> col(static_cast<size_t>(n), 0.0);
+        double best_row = 0.0;
+        for (int i = 0; i < n; ++i) {
+            double rs = 0.0;
+            for (int j = 0; j < n; ++j) {
+                const double a = std::abs(f[static_cast<size_t>(i) * n + j]);
+                rs += a;
+                col[static_cast<size_t>(j)] += a;
+            }
+            if (rs > best_row) best_row = rs;
+        }
+        op.inf_norm[k] = best_row;
+        op.one_norm[k] = *std::max_element(col.begin(), col.end());
+        off += static_cast<size_t>(n) * n;
+    }
+    return op;
+}
+
+// ------------------------------------------------------------------ batched expm ---------
+
+static constexpr double kTheta13 = 5.371920351148152;
+
+static int squaring_bound(double abs_scale, double one_norm) {
+    const double b = abs_scale * one_norm * (1.0 + 1e-10);
+    if (!(b > kTheta13)) return 0;
+    return static_cast<int>(std::ceil(std::log2(b / kTheta13))) + 0;
+}
+
+static GemmArgs square_batch(int n, int count, const double* A, const double* B, double* C) {
+    GemmArgs g;
+    g.A = A;
+    g.B = B;
+    g.C = C;
+    g.M = g.N = g.K = n;
+    g.lda = g.ldb = g.ldc = n;
+    g.Z = count;
+    g.sA1 = g.sB1 = g.sC1 = static_cast<long long>(n) * n;
+    return g;
+}
+
+// dense.hpp:194-228 for a batch: out[i] = expm(scales[i] * fl(op_scale * base)).
+static void expm_batch_scaled(pq_ctx& c, int n, int count, const double* base, long long base_stride, double op_scale,
+                              const std::vector<double>& scales, double base_one_norm, double* out) {
+    if (count <= 0) return;
+    const size_t nn = static_cast<size_t>(n) * n, blk = nn * count;
+    double* w = ws(c, "expm", 11 * blk);
+    double *X = w, *A2 = w + blk, *A4 = w + 2 * blk, *A6 = w + 3 * blk, *TZ = w + 4 * blk, *WZ = w + 6 * blk,
+           *W2 = w + 8 * blk, *V = w + 9 * blk, *U = w + 10 * blk;
+    int* s_dev = static_cast<int*>(ws_bytes(c, "expm_s", sizeof(int) * count));
+    const double* scale_dev = static_cast<const double*>(arena_push(c, scales.data(), sizeof(double) * count));
+    arena_flush(c);
+
+    int s_max = 0;
+    if (base_one_norm >= 0.0) {
+        for (double sc : scales) s_max = std::max(s_max, squaring_bound(std::abs(sc * op_scale), base_one_norm));
+    }
+    cudaStream_t st = c.stream;
+    launch_expm_prep(n, count, base, base_stride, op_scale, scale_dev, X, s_dev, st);
+    count_launch(c);
+    if (base_one_norm < 0.0) {  // unknown norm (standalone device expm): read the counts back
+        int* d_max = c.d_int;
+        launch_imax(s_dev, count, d_max, st);
+        count_launch(c);
+        int h = 0;
+        cuda_check(cudaMemcpyAsync(&h, d_max, sizeof(int), cudaMemcpyDeviceToHost, st), "expm s readback");
+        cuda_check(cudaStreamSynchronize(st), "expm s sync");
+        s_max = h;
+    }
+    count_launch(c, launch_gemm(square_batch(n, count, X, X, A2), st));
+    count_launch(c, launch_gemm(square_batch(n, count, A2, A2, A4), st));
+    count_launch(c, launch_gemm(square_batch(n, count, A2, A4, A6), st));
+    launch_pade_mid(n, count, A2, A4, A6, TZ, TZ + blk, st);
+    count_launch(c);
+    {
+        GemmArgs g = square_batch(n, 2 * count, A6, TZ, WZ);
+        g.zdiv = count;
+        g.sA1 = 0;
+        g.sA2 = static_cast<long long>(nn);
+        g.sB1 = g.sC1 = static_cast<long long>(blk);
+        g.sB2 = g.sC2 = static_cast<long long>(nn);
+        count_launch(c, launch_gemm(g, st));
+    }
+    launch_pade_fin(n, count, WZ, WZ + blk, A2, A4, A6, W2, V, st);
+    count_launch(c);
+    count_launch(c, launch_gemm(square_batch(n, count, X, W2, U), st));
+    double* P = TZ;
+    double* Q = (s_max % 2 == 0) ? out : WZ;
+    double* other = (s_max % 2 == 0) ? WZ : out;
+    launch_pade_pq(static_cast<long long>(blk), V, U, P, Q, st);
+    count_launch(c);
+    launch_lu_solve(n, count, P, Q, c.d_err, st);
+    count_launch(c);
+    double* cur = Q;
+    for (int r = 0; r < s_max; ++r) {
+        GemmArgs g = square_batch(n, count, cur, cur, other);
+        g.sq_count = s_dev;
+        g.sq_round = r;
+        count_launch(c, launch_gemm(g, st));
+        std::swap(cur, other);
+    }
+    if (cur != out) cuda_check(cudaMemcpyAsync(out, cur, blk * sizeof(double), cudaMemcpyDeviceToDevice, st), "expm copy");
+    check_launch(c);
+}
+
+void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_stride, const std::vector<double>& scales,
+                double base_one_norm, double* out) {
+    expm_batch_scaled(c, n, count, base, base_stride, 1.0, scales, base_one_norm, out);
+}
+
+// ------------------------------------------------------------------ mode products --------
+
+// One mode product of the chain (kron.hpp:65-87 accumulate_mode_apply, as a GEMM).
+static GemmArgs mode_gemm(int d, const int* n, int k, const double* E, long long E_stride, const double* x,
+                          long long x_stride, double* y, long long y_stride, int Z1, long long N) {
+    long long O = 1, I = 1;
+    for (int i = 0; i < k; ++i) O *= n[i];
+    for (int i = k + 1; i < d; ++i) I *= n[i];
+    const int nk = n[k];
+    GemmArgs g;
+    if (I > 1) {
+        // Y_o = E_k X_o, X_o an nk x I row-major slab
+        g.A = E;
+        g.lda = nk;
+        g.B = x;
+        g.ldb = I;
+        g.C = y;
+        g.ldc = I;
+        g.K = nk;
+        g.N = static_cast<int>(I);
+        if (O == 1 && x_stride == 0 && E_stride == static_cast<long long>(nk) * nk && y_stride == N && Z1 > 1) {
+            // shared input, consecutive E blocks: stack the node exponentials along M (one GEMM)
+            g.M = Z1 * nk;
+            g.Z = 1;
+        } else {
+            g.M = nk;
+            g.Z = static_cast<int>(Z1 * O);
+            g.zdiv = static_cast<int>(O);
+            g.sA1 = E_stride;
+            g.sB1 = x_stride;
+            g.sB2 = nk * I;
+            g.sC1 = y_stride;
+            g.sC2 = nk * I;
+        }
+    } else {
+        // last mode: Y (O x nk) = X (O x nk) E_k^T ; E_k row-major is E_k^T column-major
+        g.A = x;
+        g.lda = nk;
+        g.B = E;
+        g.b_kmajor = 1;
+        g.ldb = nk;
+        g.C = y;
+        g.ldc = nk;
+        g.M = static_cast<int>(O);
+        g.N = nk;
+        g.K = nk;
+        g.Z = Z1;
+        g.sA1 = x_stride;
+        g.sB1 = E_stride;
+        g.sC1 = y_stride;
+    }
+    (void)d;
+    return g;
+}
+
+void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride, const double* x,
+                long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep) {
+    long long N = 1;
+    for (int k = 0; k < d; ++k) N *= n[k];
+    double* tmp[2] = {nullptr, nullptr};
+    if (d > 1) tmp[0] = ws(c, "chainA", static_cast<size_t>(Z1) * N);
+    if (d > 2) tmp[1] = ws(c, "chainB", static_cast<size_t>(Z1) * N);
+    const double* src = x;
+    long long sstride = x_stride;
+    for (int k = 0; k < d; ++k) {
+        const bool last = k == d - 1;
+        double* dst = last ? y : tmp[k % 2];
+        const long long dstride = last ? y_stride : N;
+        GemmArgs g = mode_gemm(d, n, k, E[k], E_stride[k], src, sstride, dst, dstride, Z1, N);
+        if (last) {
+            g.alpha_z = ep.alpha_z;
+            g.ext = ep.ext;
+            g.ext_s = ep.ext_s;
+            g.coef = ep.coef;
+            g.cld = ep.cld;
+            g.nterms = ep.nterms;
+            g.accumulate = ep.accumulate;
+            if (ep.cld > 0) g.ext_group = ep.cld;
+        }
+        count_launch(c, launch_gemm(g, c.stream));
+        src = dst;
+        sstride = dstride;
+    }
+    check_launch(c);
+}
+
+// kron.hpp:111-119: y = sum_k mode_k(A_k) x (factor scaled by `scale` first when != 1).
+void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, double* y) {
+    const double* F[3] = {op.F[0], op.F[1], op.F[2]};
+    if (scale != 1.0) {
+        size_t total = 0;
+        for (int k = 0; k < op.d; ++k) total += static_cast<size_t>(op.n[k]) * op.n[k];
+        double* sf = ws(c, "kmv_scaled", total);
+        launch_scale_copy(static_cast<long long>(total), scale, op.F[0], sf, c.stream);
+        count_launch(c);
+        size_t off = 0;
+        for (int k = 0; k < op.d; ++k) {
+            F[k] = sf + off;
+            off += static_cast<size_t>(op.n[k]) * op.n[k];
+        }
+    }
+    for (int k = 0; k < op.d; ++k) {
+        GemmArgs g = mode_gemm(op.d, op.n, k, F[k], 0, x, 0, y, 0, 1, op.N);
+        g.accumulate = k > 0;
+        count_launch(c, launch_gemm(g, c.stream));
+    }
+    check_launch(c);
+}
+
+// kron.hpp:123-128 (phi_0): expm of every (scaled) factor, then one mode chain per RHS.
+void exp_action_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* b, double* y) {
+    const double* E[3];
+    long long Es[3] = {0, 0, 0};
+    for (int k = 0; k < op.d; ++k) {
+        double* e = ws(c, "phi0E" + std::to_string(k), static_cast<size_t>(op.n[k]) * op.n[k]);
+        expm_batch_scaled(c, op.n[k], 1, op.F[k], 0, scale, {1.0}, op.one_norm[k], e);
+        E[k] = e;
+    }
+    mode_chain(c, op.d, op.n, E, Es, b, op.N, y, op.N, nb, Epilogue{});
+}
+
+double max_inf_norm_dev(pq_ctx& c, const double* v, long long N, int ncols) {
+    double* out = ws(c, "colstats", 2 * static_cast<size_t>(ncols));
+    launch_colstats(N, ncols, v, nullptr, out, c.stream);
+    count_launch(c);
+    std::vector<double> h(2 * static_cast<size_t>(ncols));
+    cuda_check(cudaMemcpyAsync(h.data(), out, h.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "norm readback");
+    cuda_check(cudaStreamSynchronize(c.stream), "norm sync");
+    double best = 0.0;
+    for (int k = 0; k < ncols; ++k) best = std::max(best, h[2 * k + 1]);
+    return best;
+}
+
+// ------------------------------------------------------------------ the node sweep -------
+
+// phiaction.hpp:102-107: coefficient w_i theta_i^{j-1}/(j-1)! by the same running product.
+static void node_coefs(const NodesWeights& r, const std::vector<int>& idx, int p, std::vector<double>& out) {
+    out.assign(idx.size() * static_cast<size_t>(p), 0.0);
+    for (size_t a = 0; a < idx.size(); ++a) {
+        const double th = r.x[static_cast<size_t>(idx[a])];
+        double coeff = r.w[static_cast<size_t>(idx[a])];
+        for (int j = 1; j <= p; ++j) {
+            out[a * p + (j - 1)] = coeff;
+            coeff *= th / j;
+        }
+    }
+}
+
+static int node_chunk(pq_ctx& c, long long N, int q, int per_node_vectors) {
+    const double budget = static_cast<double>(budget_bytes(c)) * 0.9;
+    const double per = static_cast<double>(N) * sizeof(double) * per_node_vectors;
+    int qc = static_cast<int>(budget / per);
+    if (qc < 1) qc = 1;
+    return std::min(q, qc);
+}
+
+// Exponentials of the selected nodes: E_k[a] = expm((1 - theta_{idx[a]}) 2^-lshift fl(s A_k)).
+static void node_exponentials(pq_ctx& c, const DevOp& op, double s, int lshift, const NodesWeights& rule,
+                              const std::vector<int>& idx, const double* E[3], long long Es[3], const char* tag) {
+    const int q = static_cast<int>(idx.size());
+    std::vector<double> sc(static_cast<size_t>(q));
+    for (int a = 0; a < q; ++a) sc[static_cast<size_t>(a)] = std::ldexp(1.0 - rule.x[static_cast<size_t>(idx[a])], -lshift);
+    for (int k = 0; k < op.d; ++k) {
+        const size_t nn = static_cast<size_t>(op.n[k]) * op.n[k];
+        double* e = ws(c, std::string(tag) + std::to_string(k), nn * q);
+        expm_batch_scaled(c, op.n[k], q, op.F[k], 0, s, sc, op.one_norm[k], e);
+        E[k] = e;
+        Es[k] = static_cast<long long>(nn);
+    }
+}
+
+// For nodes idx (ascending), v_i = e^{(1-theta_i) A'} b_m, A' = 2^-lshift fl(s A); either
+// combined into acc [nb][p][N] (zeroing first if `zero`) or stored into pool slots
+// pool + (slot[a]*nb + m)*N (slots consecutive).
+static void node_sweep(pq_ctx& c, const DevOp& op, double s, int lshift, int nb, const double* bs, int p,
+                       const NodesWeights& rule, const std::vector<int>& idx, double* acc, int zero, double* pool,
+                       int slot0) {
+    const int q = static_cast<int>(idx.size());
+    if (q == 0) {
+        if (acc && zero) cuda_check(cudaMemsetAsync(acc, 0, sizeof(double) * nb * p * op.N, c.stream), "zero acc");
+        return;
+    }
+    const double* E[3];
+    long long Es[3];
+    node_exponentials(c, op, s, lshift, rule, idx, E, Es, "nodeE");
+    const long long N = op.N;
+    if (pool) {
+        const int qc = node_chunk(c, N, q, 2);
+        for (int m = 0; m < nb; ++m)
+            for (int a0 = 0; a0 < q; a0 += qc) {
+                const int cnt = std::min(qc, q - a0);
+                const double* Ec[3];
+                for (int k = 0; k < op.d; ++k) Ec[k] = E[k] + a0 * Es[k];
+                mode_chain(c, op.d, op.n, Ec, Es, bs + m * N, 0, pool + (static_cast<long long>(slot0 + a0) * nb + m) * N,
+                           nb * N, cnt, Epilogue{});
+            }
+        return;
+    }
+    std::vector<double> coef;
+    node_coefs(rule, idx, p, coef);
+    const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
+    std::vector<int> slots(static_cast<size_t>(q));
+    std::iota(slots.begin(), slots.end(), 0);
+    const int qc = node_chunk(c, N, q, 3);
+    // slot table: chunk-local indices 0..qc-1
+    const int* slot_dev = static_cast<const int*>(arena_push(c, slots.data(), slots.size() * sizeof(int)));
+    arena_flush(c);
+    double* V = ws(c, "nodeV", static_cast<size_t>(qc) * N);
+    for (int m = 0; m < nb; ++m)
+        for (int a0 = 0; a0 < q; a0 += qc) {
+            const int cnt = std::min(qc, q - a0);
+            const double* Ec[3];
+            for (int k = 0; k < op.d; ++k) Ec[k] = E[k] + a0 * Es[k];
+            mode_chain(c, op.d, op.n, Ec, Es, bs + m * N, 0, V, N, cnt, Epilogue{});
+            launch_combine(N, p, cnt, V, N, slot_dev, coef_dev + static_cast<size_t>(a0) * p, acc + static_cast<long long>(m) * p * N,
+                           N, (zero && a0 == 0) ? 1 : 0, c.stream);
+            count_launch(c);
+        }
+    check_launch(c);
+}
+
+// phiaction.hpp:134-145 (Alg. 1 on an explicit rule).
+void phi_fixed_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, const NodesWeights& rule,
+                   double* out) {
+    std::vector<int> idx(static_cast<size_t>(rule.size()));
+    std::iota(idx.begin(), idx.end(), 0);
+    node_sweep(c, op, scale, 0, nb, bs, p, rule, idx, out, 1, nullptr, 0);
+}
+
+static void phi_fixed_shift(pq_ctx& c, const DevOp& op, double scale, int lshift, int nb, const double* bs, int p,
+                            const NodesWeights& rule, double* out) {
+    std::vector<int> idx(static_cast<size_t>(rule.size()));
+    std::iota(idx.begin(), idx.end(), 0);
+    node_sweep(c, op, scale, lshift, nb, bs, p, rule, idx, out, 1, nullptr, 0);
+}
+
+void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p,
+                           const NodesWeights& rule, const std::vector<int>& nodes, int zero, double* acc) {
+    node_sweep(c, op, scale, 0, nb, bs, p, rule, nodes, acc, zero, nullptr, 0);
+}
+
+// phiaction.hpp:156-245 (Alg. 2): nested CC ladder, node vectors kept in a device pool,
+// all sums rebuilt in ascending node order at every level.
+static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double scale, int lshift, int nb, const double* bs, int p,
+                               double eps, double* out, int* points_used) {
+    if (p < 1) throw std::invalid_argument("phi_adaptive: need p >= 1");
+    if (!(eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
+    const long long N = op.N;
+    const size_t col = static_cast<size_t>(nb) * p * N;
+    int half = 3;
+    const NodesWeights* rule = &memo_rule(kClenshaw, 2 * half + 1);
+    // slot of rule node i in the pool
+    std::vector<int> slot_of(static_cast<size_t>(rule->size()));
+    std::iota(slot_of.begin(), slot_of.end(), 0);
+    int used = rule->size();
+    auto pool_for = [&](int slots) { return ws(c, "ccpool", static_cast<size_t>(slots) * nb * N); };
+    double* pool = pool_for(used);
+    {
+        std::vector<int> idx(slot_of);
+        node_sweep(c, op, scale, lshift, nb, bs, p, *rule, idx, nullptr, 0, pool, 0);
+    }
+    double* accs[2] = {out, ws(c, "ccacc", col)};
+    int cur = 0;
+    auto combine_all = [&](const NodesWeights& r, const std::vector<int>& slots, double* acc) {
+        std::vector<int> idx(static_cast<size_t>(r.size()));
+        std::iota(idx.begin(), idx.end(), 0);
+        std::vector<double> coef;
+        node_coefs(r, idx, p, coef);
+        const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
+        std::vector<int> sl(slots.begin(), slots.end());
+        const int* sl_dev = static_cast<const int*>(arena_push(c, sl.data(), sl.size() * sizeof(int)));
+        arena_flush(c);
+        for (int m = 0; m < nb; ++m) {
+            launch_combine(N, p, r.size(), pool + static_cast<long long>(m) * N, static_cast<long long>(nb) * N, sl_dev,
+                           coef_dev, acc + static_cast<long long>(m) * p * N, N, 1, c.stream);
+            count_launch(c);
+        }
+    };
+    combine_all(*rule, slot_of, accs[cur]);
+    double* stats = ws(c, "ccstats", 2 * static_cast<size_t>(nb) * p);
+    std::vector<double> hstats(2 * static_cast<size_t>(nb) * p);
+    while (true) {
+        const int half_next = 2 * half;
+        if (half_next > (1 << 14)) throw ConvergenceFailure("phi_adaptive: no convergence within the node budget");
+        const NodesWeights& fine = memo_rule(kClenshaw, 2 * half_next + 1);
+        const int fresh = fine.size() / 2;
+        // grow the pool (keeps contents)
+        const int need = used + fresh;
+        {
+            DevBuf& b = c.bufs["ccpool"];
+            const size_t want = static_cast<size_t>(need) * nb * N * sizeof(double);
+            if (b.bytes < want) {
+                double* np = nullptr;
+                cuda_check(cudaStreamSynchronize(c.stream), "pool grow sync");
+                if (cudaMalloc(&np, want) != cudaSuccess) {
+                    cudaGetLastError();
+                    throw CudaError("adaptive CC node pool: out of device memory");
+                }
+                cuda_check(cudaMemcpy(np, b.p, static_cast<size_t>(used) * nb * N * sizeof(double), cudaMemcpyDeviceToDevice),
+                           "pool copy");
+                cudaFree(b.p);
+                b.p = np;
+                b.bytes = want;
+            }
+            pool = static_cast<double*>(b.p);
+        }
+        std::vector<int> fine_slot(static_cast<size_t>(fine.size()));
+        for (int i = 0; i < rule->size(); ++i) fine_slot[static_cast<size_t>(2 * i)] = slot_of[static_cast<size_t>(i)];
+        std::vector<int> odd(static_cast<size_t>(fresh));
+        for (int k = 0; k < fresh; ++k) {
+            odd[static_cast<size_t>(k)] = 2 * k + 1;
+            fine_slot[static_cast<size_t>(2 * k + 1)] = used + k;
+        }
+        node_sweep(c, op, scale, lshift, nb, bs, p, fine, odd, nullptr, 0, pool, used);
+        used = need;
+        const int nxt = 1 - cur;
+        combine_all(fine, fine_slot, accs[nxt]);
+        half = half_next;
+        rule = &fine;
+        slot_of = std::move(fine_slot);
+        // phiaction.hpp:225-240: max over columns of ||y - y_prev||_inf / ||y||_inf
+        launch_colstats(N, nb * p, accs[nxt], accs[cur], stats, c.stream);
+        count_launch(c);
+        cuda_check(cudaMemcpyAsync(hstats.data(), stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+                   "cc stats readback");
+        cuda_check(cudaStreamSynchronize(c.stream), "cc stats sync");
+        cur = nxt;
+        double err = 0.0;
+        for (int k = 0; k < nb * p; ++k) {
+            const double diff = hstats[2 * k], norm = hstats[2 * k + 1];
+            if (diff == 0.0) continue;
+            err = std::max(err, norm == 0.0 ? std::numeric_limits<double>::infinity() : diff / norm);
+        }
+        if (err <= eps) break;
+    }
+    if (accs[cur] != out)
+        cuda_check(cudaMemcpyAsync(out, accs[cur], col * sizeof(double), cudaMemcpyDeviceToDevice, c.stream), "cc copy");
+    if (points_used) *points_used = rule->size();
+}
+
+void phi_adaptive_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, double eps, double* out,
+                      int* points_used) {
+    phi_adaptive_shift(c, op, scale, 0, nb, bs, p, eps, out, points_used);
+}
+
+// phiaction.hpp:255-272 + 290-301: l doubling steps, E_k = expm(2^-l A_k) squared after each
+// step but the last.  y [nb][p][N] holds phi_j(2^-l A) b on entry; the result lands in y when l
+// is even and in `partner` when l is odd (ping-pong, no copy).
+static double* squaring_pingpong(pq_ctx& c, const DevOp& op, double scale, int l, int nb, int p, double* y,
+                                 double* partner, const double* const* exps_in) {
+    if (l <= 0) return y;
+    const long long N = op.N;
+    const double* E[3];
+    double* Ew[3];
+    long long Es[3] = {0, 0, 0};
+    for (int k = 0; k < op.d; ++k) {
+        const size_t nn = static_cast<size_t>(op.n[k]) * op.n[k];
+        Ew[k] = ws(c, "sqE" + std::to_string(k), 2 * nn);
+        if (exps_in)
+            cuda_check(cudaMemcpyAsync(Ew[k], exps_in[k], nn * sizeof(double), cudaMemcpyDeviceToDevice, c.stream), "exps");
+        else
+            expm_batch_scaled(c, op.n[k], 1, op.F[k], 0, scale, {std::ldexp(1.0, -l)}, op.one_norm[k], Ew[k]);
+        E[k] = Ew[k];
+    }
+    // epilogue tables for column z1 = m*p + (i-1): alpha = 2^-i, coef_t = 2^-i/(i-1-t)!, t < i
+    std::vector<double> inv(static_cast<size_t>(p), 1.0);
+    {
+        double f = 1.0;
+        for (int k = 1; k < p; ++k) {
+            f *= k;
+            inv[static_cast<size_t>(k)] = 1.0 / f;
+        }
+    }
+    const int Z1 = nb * p;
+    std::vector<double> alpha(static_cast<size_t>(Z1)), coef(static_cast<size_t>(Z1) * p, 0.0);
+    std::vector<int> nterms(static_cast<size_t>(Z1));
+    for (int m = 0; m < nb; ++m)
+        for (int i = 1; i <= p; ++i) {
+            const int z1 = m * p + i - 1;
+            const double sc = std::ldexp(1.0, -i);
+            alpha[static_cast<size_t>(z1)] = sc;
+            nterms[static_cast<size_t>(z1)] = i;
+            for (int t = 0; t < i; ++t) coef[static_cast<size_t>(z1) * p + t] = sc * inv[static_cast<size_t>(i - 1 - t)];
+        }
+    Epilogue ep;
+    ep.alpha_z = static_cast<const double*>(arena_push(c, alpha.data(), alpha.size() * sizeof(double)));
+    ep.coef = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
+    ep.nterms = static_cast<const int*>(arena_push(c, nterms.data(), nterms.size() * sizeof(int)));
+    ep.cld = p;
+    ep.ext_s = N;
+    arena_flush(c);
+    double* cur = y;
+    double* nxt = partner;
+    for (int step = 0; step < l; ++step) {
+        ep.ext = cur;
+        mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, ep);
+        std::swap(cur, nxt);
+        if (step < l - 1) {
+            for (int k = 0; k < op.d; ++k) {
+                const size_t nn = static_cast<size_t>(op.n[k]) * op.n[k];
+                double* dst = (E[k] == Ew[k]) ? Ew[k] + nn : Ew[k];
+                count_launch(c, launch_gemm(square_batch(op.n[k], 1, E[k], E[k], dst), c.stream));
+                E[k] = dst;
+            }
+        }
+    }
+    check_launch(c);
+    return cur;
+}
+
+void squaring_steps_dev(pq_ctx& c, const DevOp& op, double scale, int nb, int p, int l, double* y,
+                        const double* exps_override) {
+    double* partner = ws(c, "sqT", static_cast<size_t>(nb) * p * op.N);
+    const double* ex[3] = {nullptr, nullptr, nullptr};
+    if (exps_override) {
+        size_t off = 0;
+        for (int k = 0; k < op.d; ++k) {
+            ex[k] = exps_override + off;
+            off += static_cast<size_t>(op.n[k]) * op.n[k];
+        }
+    }
+    double* res = squaring_pingpong(c, op, scale, l, nb, p, y, partner, exps_override ? ex : nullptr);
+    if (res != y)
+        cuda_check(cudaMemcpyAsync(y, res, sizeof(double) * nb * p * op.N, cudaMemcpyDeviceToDevice, c.stream), "sq copy");
+}
+
+// phiaction.hpp:277-303.
+void phi_with_plan_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n, int kind,
+                       double eps, double* out, int* points_used) {
+    if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
+    if (p < 1) throw std::invalid_argument(kind == kGauss ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
+    // quadrature result goes where the l-step ping-pong will end in `out`
+    double* partner = l > 0 ? ws(c, "sqT", static_cast<size_t>(nb) * p * op.N) : nullptr;
+    double* first = (l % 2 == 1) ? partner : out;
+    if (kind == kGauss) {
+        const NodesWeights& rule = memo_rule(kGauss, n + 1);
+        phi_fixed_shift(c, op, scale, l, nb, bs, p, rule, first);
+        if (points_used) *points_used = rule.size();
+    } else {
+        phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, first, points_used);
+    }
+    if (l > 0) {
+        double* res = squaring_pingpong(c, op, scale, l, nb, p, first, first == out ? partner : out, nullptr);
+        if (res != out)
+            cuda_check(cudaMemcpyAsync(out, res, sizeof(double) * nb * p * op.N, cudaMemcpyDeviceToDevice, c.stream),
+                       "plan copy");
+    }
+}
+
+// phiaction.hpp:307-346.
+void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l, int l,
+                   double c1, double c2, double* out, PlanInfo* info) {
+    if (p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
+    double alpha = 0.0;
+    for (int k = 0; k < op.d; ++k) alpha += op.inf_norm[k];
+    const double beta = nb > 0 ? max_inf_norm_dev(c, bs, op.N, nb) : 0.0;
+    Cost cost{c1, c2, op.d};
+    int n = 0;
+    bool planned = false;
+    double plan_cost = 0.0;
+    if (has_l) {
+        if (l < 0) throw std::invalid_argument("phiquadmv: need l >= 0");
+        if (alpha > 0.0 && beta > 0.0)
+            n = node_count(eps, p, std::ldexp(alpha, -l), beta, mode);
+        else
+            n = mode == kGauss ? 2 : 4;
+        plan_cost = cost(n, l, p);
+    } else if (alpha > 0.0 && beta > 0.0) {
+        const Plan pl = plan_quadrature(eps, p, alpha, beta, mode, cost);
+        l = pl.l;
+        n = pl.n;
+        plan_cost = pl.cost;
+        planned = true;
+    } else {
+        l = 0;
+        n = mode == kGauss ? 2 : 4;
+        plan_cost = cost(n, l, p);
+        planned = true;
+    }
+    int points = 0;
+    phi_with_plan_dev(c, op, 1.0, nb, bs, p, l, n, mode, eps, out, &points);
+    if (info) {
+        info->l = l;
+        info->n = n;
+        info->points = points;
+        info->mode = mode;
+        info->planned = planned ? 1 : 0;
+        info->alpha = alpha;
+        info->beta = beta;
+        info->cost = plan_cost;
+    }
+}
+
+// phiaction.hpp:355-389: one sweep of the combined integrand sum_j theta^{j-1}/(j-1)! b_j.
+void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const double* bs, const NodesWeights& rule,
+                     double* out) {
+    if (p < 1) throw std::invalid_argument("phi_lincomb: need at least one vector");
+    const int q = rule.size();
+    const long long N = op.N;
+    std::vector<int> idx(static_cast<size_t>(q));
+    std::iota(idx.begin(), idx.end(), 0);
+    const double* E[3];
+    long long Es[3];
+    node_exponentials(c, op, scale, 0, rule, idx, E, Es, "lincE");
+    // mixing coefficients per node (coeff = 1, coeff *= theta/j) and final weights
+    std::vector<double> mix(static_cast<size_t>(q) * p), wts(static_cast<size_t>(q));
+    for (int i = 0; i < q; ++i) {
+        double coeff = 1.0;
+        for (int j = 1; j <= p; ++j) {
+            mix[static_cast<size_t>(i) * p + j - 1] = coeff;
+            coeff *= rule.x[static_cast<size_t>(i)] / j;
+        }
+        wts[static_cast<size_t>(i)] = rule.w[static_cast<size_t>(i)];
+    }
+    std::vector<int> bslots(static_cast<size_t>(p)), vslots(static_cast<size_t>(q));
+    std::iota(bslots.begin(), bslots.end(), 0);
+    std::iota(vslots.begin(), vslots.end(), 0);
+    const double* mix_dev = static_cast<const double*>(arena_push(c, mix.data(), mix.size() * sizeof(double)));
+    const double* w_dev = static_cast<const double*>(arena_push(c, wts.data(), wts.size() * sizeof(double)));
+    const int* bsl = static_cast<const int*>(arena_push(c, bslots.data(), bslots.size() * sizeof(int)));
+    const int* vsl = static_cast<const int*>(arena_push(c, vslots.data(), vslots.size() * sizeof(int)));
+    arena_flush(c);
+    const int qc = node_chunk(c, N, q, 4);
+    double* M = ws(c, "lincMix", static_cast<size_t>(qc) * N);
+    double* V = ws(c, "lincV", static_cast<size_t>(qc) * N);
+    for (int a0 = 0; a0 < q; a0 += qc) {
+        const int cnt = std::min(qc, q - a0);
+        for (int a = 0; a < cnt; ++a) {
+            // mix_i = sum_j c_ij b_j, one output column (p = 1) over the p inputs as "nodes"
+            launch_combine(N, 1, p, bs, N, bsl, mix_dev + static_cast<size_t>(a0 + a) * p, M + static_cast<long long>(a) * N,
+                           N, 1, c.stream);
+            count_launch(c);
+        }
+        const double* Ec[3];
+        for (int k = 0; k < op.d; ++k) Ec[k] = E[k] + a0 * Es[k];
+        mode_chain(c, op.d, op.n, Ec, Es, M, N, V, N, cnt, Epilogue{});
+        launch_combine(N, 1, cnt, V, N, vsl, w_dev + a0, out, N, a0 == 0 ? 1 : 0, c.stream);
+        count_launch(c);
+    }
+    check_launch(c);
+}
+
+}  // namespace pqb

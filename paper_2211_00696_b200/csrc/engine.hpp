@@ -1,0 +1,151 @@
+// Internal host-side engine: context, device workspace and the phi pipeline built from the
+// kernels in kernels.cu.  Everything here is stream-ordered on ctx.stream; the only host syncs
+// are the ones a host decision needs (beta for the planner, the adaptive CC error per level,
+// expm squaring counts for standalone pq_expm) and the final copy-out of PQ_HOST calls.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "estimator.hpp"
+#include "kernels.hpp"
+
+namespace pqb {
+
+struct CudaError : std::runtime_error {
+    explicit CudaError(const std::string& w) : std::runtime_error(w) {}
+};
+void cuda_check(cudaError_t e, const char* what);
+
+// A device buffer that only grows (cudaMalloc is a device-wide sync; steady state never reallocates).
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+};
+
+// Pinned staging arena for small per-call parameter tables (rule coefficients, epilogue tables).
+struct ParamArena {
+    char* host = nullptr;
+    char* dev = nullptr;
+    size_t cap = 0, used = 0, flushed = 0;
+    cudaEvent_t done = nullptr;
+};
+
+struct Engine;
+
+}  // namespace pqb
+
+struct pq_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    uint64_t launches = 0;
+    uint64_t ws_limit = 0;
+    std::map<std::string, pqb::DevBuf> bufs;
+    pqb::ParamArena arena;
+    int* d_err = nullptr;        // device error flag (singular LU)
+    double* h_small = nullptr;   // pinned readback scratch
+    double* d_small = nullptr;   // device scratch for reductions
+    int* d_int = nullptr;        // device int scratch (expm squaring counts)
+    bool profiling = false;
+    double phase_ms[6] = {0, 0, 0, 0, 0, 0};
+};
+
+namespace pqb {
+
+// The Kronecker-sum operator resident on the device.  `scale` multiplies every factor lazily
+// (the reference's KroneckerSum::scaled, kron.hpp:44-49, one rounding per entry) -- expm and
+// kron_matvec apply it on the fly, so ETD stages never re-upload factors.
+struct DevOp {
+    int d = 0;
+    int n[3] = {1, 1, 1};
+    long long N = 1;
+    const double* F[3] = {nullptr, nullptr, nullptr};  // device, row-major n_k x n_k (unscaled)
+    double one_norm[3] = {0, 0, 0};                    // host: 1-norms of the unscaled factors
+    double inf_norm[3] = {0, 0, 0};                    // host: inf-norms of the unscaled factors
+    std::vector<double> host;                          // host copy (concatenated), for host math
+};
+
+// Epilogue applied at the last mode of a mode chain (see GemmArgs).
+struct Epilogue {
+    const double* alpha_z = nullptr;
+    const double* ext = nullptr;
+    long long ext_s = 0;
+    const double* coef = nullptr;
+    int cld = 0;
+    const int* nterms = nullptr;
+    int accumulate = 0;
+};
+
+// ---- C-ABI error plumbing (capi.cpp owns the thread-local message) ----
+std::string& last_error_slot();
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return 0;
+    } catch (const ConvergenceFailure& e) {
+        last_error_slot() = e.what();
+        return 2;
+    } catch (const std::invalid_argument& e) {
+        last_error_slot() = e.what();
+        return 1;
+    } catch (const std::out_of_range& e) {
+        last_error_slot() = e.what();
+        return 4;
+    } catch (const std::runtime_error& e) {
+        last_error_slot() = e.what();
+        return 3;
+    } catch (const std::exception& e) {
+        last_error_slot() = e.what();
+        return 5;
+    }
+}
+
+// ---- context helpers (engine.cpp) ----
+double* ws(pq_ctx& c, const std::string& name, size_t count);          // device doubles
+void* ws_bytes(pq_ctx& c, const std::string& name, size_t bytes);
+void arena_begin(pq_ctx& c);
+const void* arena_push(pq_ctx& c, const void* data, size_t bytes);     // returns device address
+void arena_flush(pq_ctx& c);
+void count_launch(pq_ctx& c, int n = 1);
+void check_launch(pq_ctx& c);
+
+// ---- device building blocks ----
+DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const std::string& slot);
+// E[i] = expm(scale[i] * base) for i < count; base is one device n x n matrix (or a strided batch).
+void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_stride,
+                const std::vector<double>& scales, double base_one_norm, double* out);
+// y[z1] = (E_0[z1] (x) ... (x) E_{d-1}[z1]) x[z1] for z1 < Z1, epilogue fused into the last mode.
+void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride,
+                const double* x, long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep);
+void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, double* y);
+void exp_action_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* b, double* y);
+double max_inf_norm_dev(pq_ctx& c, const double* v, long long N, int ncols);  // syncs
+
+// phi pipeline on device pointers.  `scale` multiplies the operator (e.g. -sigma*tau).
+void phi_fixed_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p,
+                   const NodesWeights& rule, double* out);
+void phi_adaptive_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, double eps,
+                      double* out, int* points_used);
+void squaring_steps_dev(pq_ctx& c, const DevOp& op, double scale, int nb, int p, int l, double* y,
+                        const double* exps_override = nullptr);
+void phi_with_plan_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n,
+                       int kind, double eps, double* out, int* points_used);
+struct PlanInfo {
+    int l = 0, n = 0, points = 0, mode = 0, planned = 0;
+    double alpha = 0, beta = 0, cost = 0;
+};
+void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l,
+                   int l, double c1, double c2, double* out, PlanInfo* info);
+void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p,
+                           const NodesWeights& rule, const std::vector<int>& nodes, int zero, double* acc);
+void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const double* bs, const NodesWeights& rule,
+                     double* out);
+
+}  // namespace pqb

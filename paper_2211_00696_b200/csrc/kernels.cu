@@ -1,0 +1,397 @@
+// sm_100a kernels of the phi engine.
+//
+//  * k_gemm: FP64 mode products on the DMMA tensor pipe (mma.sync m8n8k4 f64 -> SASS DMMA.8x8x4;
+//    tcgen05 has no f64 kind).  cp.async multi-stage shared-memory pipeline with padded,
+//    bank-conflict-free tiles, register-blocked warp tiles, fused epilogue (per-batch scale,
+//    accumulate, and up to `cld` weighted extra addends -- the modified-squaring combination of
+//    phiaction.hpp:260-268 is applied while the tile is still in registers).
+//  * batched Pade-13 expm pieces (dense.hpp:194-228) and a one-CTA-per-matrix LU solve with
+//    partial pivoting (dense.hpp:153-190).
+//  * HBM-bound helpers: the ascending-node phi combine (phiaction.hpp:96-111), column max-norms
+//    for the adaptive CC error (phiaction.hpp:225-239), ETD elementwise terms.
+#include "kernels.hpp"
+
+#include <cstdio>
+#include <stdexcept>
+
+namespace pqb {
+
+// ================================================================ DMMA GEMM =================
+// (kernel template in gemm.cuh, instantiated in gemm_nk.cu / gemm_kk.cu)
+
+int launch_gemm_nk(const GemmArgs& g, bool vec2, int shape, cudaStream_t s);
+int launch_gemm_kk(const GemmArgs& g, bool vec2, int shape, cudaStream_t s);
+
+static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+int launch_gemm(const GemmArgs& g, cudaStream_t s) {
+    if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.Z <= 0) return 0;
+    // 16-byte cp.async needs every row start and batch offset 16-byte aligned.
+    const bool vec2 = (g.K % 2 == 0) && (g.b_kmajor || g.N % 2 == 0) && g.lda % 2 == 0 && g.ldb % 2 == 0 &&
+                      g.sA1 % 2 == 0 && g.sA2 % 2 == 0 && g.sB1 % 2 == 0 && g.sB2 % 2 == 0 && al16(g.A) &&
+                      al16(g.B);
+    const int shape = (g.M >= 96 && g.N >= 96) ? 0 : (g.M >= 96 ? 1 : (g.N >= 96 ? 2 : 3));
+    return g.b_kmajor ? launch_gemm_kk(g, vec2, shape, s) : launch_gemm_nk(g, vec2, shape, s);
+}
+
+// ======================================================= batched Pade-13 expm ==============
+
+namespace {
+__constant__ double kPade[14] = {64764752532480000.0, 32382376266240000.0, 7771770303897600.0,
+                                 1187353796428800.0,  129060195264000.0,   10559470521600.0,
+                                 670442572800.0,      33522128640.0,       1323241920.0,
+                                 40840800.0,          960960.0,            16380.0,
+                                 182.0,               1.0};
+constexpr double kTheta13 = 5.371920351148152;
+}  // namespace
+
+// One CTA per matrix.  1-norm exactly as dense.hpp:133-141 (column sums accumulated in row order
+// over the entries of scale*base as dense.hpp:77-82 rounds them).
+__global__ void k_expm_prep(int n, const double* __restrict__ base, long long base_stride, double op_scale,
+                            const double* __restrict__ scale, double* __restrict__ X, int* __restrict__ s_out) {
+    const int z = blockIdx.x;
+    const double c = scale ? scale[z] : 1.0;
+    const double* a = base + z * base_stride;
+    double* x = X + (long long)z * n * n;
+    __shared__ double red[32];
+    __shared__ int s_sh;
+    double best = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+        double colsum = 0.0;
+        for (int i = 0; i < n; ++i)
+            colsum = __dadd_rn(colsum, fabs(__dmul_rn(c, __dmul_rn(op_scale, a[(long long)i * n + j]))));
+        best = colsum > best ? colsum : best;
+    }
+    for (int o = 16; o > 0; o >>= 1) best = fmax(best, __shfl_xor_sync(0xffffffffu, best, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double nrm = 0.0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) nrm = fmax(nrm, red[w]);
+        int s = 0;
+        if (nrm > kTheta13) s = (int)ceil(log2(nrm / kTheta13));
+        s_sh = s;
+        if (s_out) s_out[z] = s;
+    }
+    __syncthreads();
+    const double f = ldexp(1.0, -s_sh);
+    for (long long e = threadIdx.x; e < (long long)n * n; e += blockDim.x)
+        x[e] = __dmul_rn(f, __dmul_rn(c, __dmul_rn(op_scale, a[e])));
+}
+
+void launch_expm_prep(int n, int count, const double* base, long long base_stride, double op_scale,
+                      const double* scale, double* X, int* s_out, cudaStream_t s) {
+    const int thr = n >= 256 ? 256 : (n >= 64 ? 128 : 32);
+    k_expm_prep<<<count, thr, 0, s>>>(n, base, base_stride, op_scale, scale, X, s_out);
+}
+
+__global__ void k_scale_copy(long long total, double op_scale, const double* __restrict__ a, double* __restrict__ out) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
+        out[e] = __dmul_rn(op_scale, a[e]);
+}
+
+// T1 = (b13 A6 + b11 A4) + b9 A2 ; Zc = (b12 A6 + b10 A4) + b8 A2
+__global__ void k_pade_mid(long long total, const double* __restrict__ A2, const double* __restrict__ A4,
+                           const double* __restrict__ A6, double* __restrict__ T1, double* __restrict__ Zc) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const double a2 = A2[e], a4 = A4[e], a6 = A6[e];
+        T1[e] = __dadd_rn(__dadd_rn(__dmul_rn(a6, kPade[13]), __dmul_rn(a4, kPade[11])), __dmul_rn(a2, kPade[9]));
+        Zc[e] = __dadd_rn(__dadd_rn(__dmul_rn(a6, kPade[12]), __dmul_rn(a4, kPade[10])), __dmul_rn(a2, kPade[8]));
+    }
+}
+
+// W2 = (((W + b7 A6) + b5 A4) + b3 A2) + b1 I ;  V = (((Z + b6 A6) + b4 A4) + b2 A2) + b0 I
+__global__ void k_pade_fin(int n, long long total, const double* __restrict__ W, const double* __restrict__ Z,
+                           const double* __restrict__ A2, const double* __restrict__ A4,
+                           const double* __restrict__ A6, double* __restrict__ W2, double* __restrict__ V) {
+    const long long nn = (long long)n * n;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const long long r = e % nn;
+        const bool diag = (r / n) == (r % n);
+        const double a2 = A2[e], a4 = A4[e], a6 = A6[e];
+        double w = __dadd_rn(__dadd_rn(__dadd_rn(W[e], __dmul_rn(a6, kPade[7])), __dmul_rn(a4, kPade[5])),
+                             __dmul_rn(a2, kPade[3]));
+        double v = __dadd_rn(__dadd_rn(__dadd_rn(Z[e], __dmul_rn(a6, kPade[6])), __dmul_rn(a4, kPade[4])),
+                             __dmul_rn(a2, kPade[2]));
+        W2[e] = __dadd_rn(w, diag ? kPade[1] : 0.0);
+        V[e] = __dadd_rn(v, diag ? kPade[0] : 0.0);
+    }
+}
+
+__global__ void k_pade_pq(long long total, const double* __restrict__ V, const double* __restrict__ U,
+                          double* __restrict__ P, double* __restrict__ Q) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const double v = V[e], u = U[e];
+        P[e] = __dsub_rn(v, u);
+        Q[e] = __dadd_rn(v, u);
+    }
+}
+
+static unsigned grid_for(long long total, int thr) {
+    long long b = (total + thr - 1) / thr;
+    if (b > 148LL * 32) b = 148LL * 32;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+void launch_scale_copy(long long total, double op_scale, const double* a, double* out, cudaStream_t s) {
+    k_scale_copy<<<grid_for(total, 256), 256, 0, s>>>(total, op_scale, a, out);
+}
+
+void launch_pade_mid(int n, int count, const double* A2, const double* A4, const double* A6, double* T1, double* Zc,
+                     cudaStream_t s) {
+    const long long total = (long long)count * n * n;
+    k_pade_mid<<<grid_for(total, 256), 256, 0, s>>>(total, A2, A4, A6, T1, Zc);
+}
+void launch_pade_fin(int n, int count, const double* W, const double* Z, const double* A2, const double* A4,
+                     const double* A6, double* W2, double* V, cudaStream_t s) {
+    const long long total = (long long)count * n * n;
+    k_pade_fin<<<grid_for(total, 256), 256, 0, s>>>(n, total, W, Z, A2, A4, A6, W2, V);
+}
+void launch_pade_pq(long long total, const double* V, const double* U, double* P, double* Q, cudaStream_t s) {
+    k_pade_pq<<<grid_for(total, 256), 256, 0, s>>>(total, V, U, P, Q);
+}
+
+// LU with partial pivoting (first maximal |a_ik|, dense.hpp:156-164), forward elimination of
+// the n right-hand sides, then column-oriented back substitution.  In place: Q <- P^{-1} Q.
+__global__ void __launch_bounds__(1024) k_lu_solve(int n, double* __restrict__ P, double* __restrict__ Q,
+                                                   int* __restrict__ err) {
+    double* a = P + (long long)blockIdx.x * n * n;
+    double* b = Q + (long long)blockIdx.x * n * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    __shared__ double rv[32];
+    __shared__ int ri[32];
+    __shared__ int piv_sh;
+    for (int k = 0; k < n; ++k) {
+        double best = -1.0;
+        int bi = n;
+        for (int i = k + tid; i < n; i += nt) {
+            const double v = fabs(a[(long long)i * n + k]);
+            if (v > best) {
+                best = v;
+                bi = i;
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > best || (ov == best && oi < bi)) {
+                best = ov;
+                bi = oi;
+            }
+        }
+        if ((tid & 31) == 0) {
+            rv[tid >> 5] = best;
+            ri[tid >> 5] = bi;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            double bv = rv[0];
+            int bidx = ri[0];
+            for (int w = 1; w < (nt + 31) / 32; ++w)
+                if (rv[w] > bv || (rv[w] == bv && ri[w] < bidx)) {
+                    bv = rv[w];
+                    bidx = ri[w];
+                }
+            if (bv == 0.0) {
+                atomicExch(err, 1);
+                bidx = -1;
+            }
+            piv_sh = bidx;
+        }
+        __syncthreads();
+        const int piv = piv_sh;
+        if (piv < 0) return;
+        if (piv != k) {
+            for (int j = tid; j < n; j += nt) {
+                double t = a[(long long)k * n + j];
+                a[(long long)k * n + j] = a[(long long)piv * n + j];
+                a[(long long)piv * n + j] = t;
+                t = b[(long long)k * n + j];
+                b[(long long)k * n + j] = b[(long long)piv * n + j];
+                b[(long long)piv * n + j] = t;
+            }
+            __syncthreads();
+        }
+        const double akk = a[(long long)k * n + k];
+        const int rows = n - k - 1;
+        for (int i = k + 1 + tid; i < n; i += nt) {
+            const double f = a[(long long)i * n + k] / akk;
+            if (f != 0.0) a[(long long)i * n + k] = f;
+            else a[(long long)i * n + k] = 0.0;
+        }
+        __syncthreads();
+        const int wa = n - k - 1, w = wa + n;
+        const long long work = (long long)rows * w;
+        for (long long e = tid; e < work; e += nt) {
+            const int r = (int)(e / w), c = (int)(e - (long long)r * w);
+            const int i = k + 1 + r;
+            const double f = a[(long long)i * n + k];
+            if (f == 0.0) continue;
+            if (c < wa) {
+                const int j = k + 1 + c;
+                a[(long long)i * n + j] = __dsub_rn(a[(long long)i * n + j], __dmul_rn(f, a[(long long)k * n + j]));
+            } else {
+                const int j = c - wa;
+                b[(long long)i * n + j] = __dsub_rn(b[(long long)i * n + j], __dmul_rn(f, b[(long long)k * n + j]));
+            }
+        }
+        __syncthreads();
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        const double akk = a[(long long)k * n + k];
+        for (int j = tid; j < n; j += nt) b[(long long)k * n + j] = b[(long long)k * n + j] / akk;
+        __syncthreads();
+        const long long work = (long long)k * n;
+        for (long long e = tid; e < work; e += nt) {
+            const int i = (int)(e / n), j = (int)(e - (long long)i * n);
+            b[e] = __dsub_rn(b[e], __dmul_rn(a[(long long)i * n + k], b[(long long)k * n + j]));
+        }
+        __syncthreads();
+    }
+}
+
+void launch_lu_solve(int n, int count, double* P, double* Q, int* err, cudaStream_t s) {
+    const int thr = n >= 128 ? 1024 : (n >= 32 ? 256 : 64);
+    k_lu_solve<<<count, thr, 0, s>>>(n, P, Q, err);
+}
+
+__global__ void k_imax(const int* v, int count, int* out) {
+    int m = 0;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) m = max(m, v[i]);
+    for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (threadIdx.x == 0) *out = m;
+}
+void launch_imax(const int* v, int count, int* out, cudaStream_t s) { k_imax<<<1, 32, 0, s>>>(v, count, out); }
+
+__global__ void k_identity(int n, long long total, double* out) {
+    const long long nn = (long long)n * n;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const long long r = e % nn;
+        out[e] = (r / n) == (r % n) ? 1.0 : 0.0;
+    }
+}
+void launch_fill_identity(int n, int count, double* out, cudaStream_t s) {
+    const long long total = (long long)count * n * n;
+    k_identity<<<grid_for(total, 256), 256, 0, s>>>(n, total, out);
+}
+
+// ==================================================================== HBM-bound ============
+
+// acc_j += c_ij v_i over nodes i in ascending order; P register accumulators.
+template <int P>
+__global__ void k_combine(long long N, int q, const double* __restrict__ V, long long vstride,
+                          const int* __restrict__ slots, const double* __restrict__ coef, double* acc,
+                          long long acc_stride, int zero) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
+        double y[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) y[j] = zero ? 0.0 : acc[j * acc_stride + t];
+        for (int i = 0; i < q; ++i) {
+            const double v = __ldg(V + slots[i] * vstride + t);
+#pragma unroll
+            for (int j = 0; j < P; ++j) y[j] = __dadd_rn(y[j], __dmul_rn(coef[i * P + j], v));
+        }
+#pragma unroll
+        for (int j = 0; j < P; ++j) acc[j * acc_stride + t] = y[j];
+    }
+}
+
+__global__ void k_combine_any(long long N, int p, int q, const double* __restrict__ V, long long vstride,
+                              const int* __restrict__ slots, const double* __restrict__ coef, double* acc,
+                              long long acc_stride, int zero) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
+        for (int j = 0; j < p; ++j) {
+            double y = zero ? 0.0 : acc[j * acc_stride + t];
+            for (int i = 0; i < q; ++i) y = __dadd_rn(y, __dmul_rn(coef[i * p + j], V[slots[i] * vstride + t]));
+            acc[j * acc_stride + t] = y;
+        }
+    }
+}
+
+void launch_combine(long long N, int p, int q, const double* V, long long vstride, const int* slots, const double* coef,
+                    double* acc, long long acc_stride, int zero, cudaStream_t s) {
+    const unsigned grid = grid_for(N, 256);
+    switch (p) {
+#define PQ_COMB(PP) \
+    case PP: k_combine<PP><<<grid, 256, 0, s>>>(N, q, V, vstride, slots, coef, acc, acc_stride, zero); break;
+        PQ_COMB(1) PQ_COMB(2) PQ_COMB(3) PQ_COMB(4) PQ_COMB(5) PQ_COMB(6) PQ_COMB(7) PQ_COMB(8)
+#undef PQ_COMB
+        default: k_combine_any<<<grid, 256, 0, s>>>(N, p, q, V, vstride, slots, coef, acc, acc_stride, zero);
+    }
+}
+
+// nonnegative doubles order like their bit patterns
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+    atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+__global__ void k_colstats(long long N, const double* __restrict__ y, const double* __restrict__ yp, double* out) {
+    const int c = blockIdx.y;
+    const double* yc = y + c * N;
+    const double* pc = yp ? yp + c * N : nullptr;
+    double dmax = 0.0, nmax = 0.0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
+        const double v = yc[t];
+        nmax = fmax(nmax, fabs(v));
+        if (pc) dmax = fmax(dmax, fabs(v - pc[t]));
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        nmax = fmax(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+    }
+    __shared__ double sd[32], sn[32];
+    if ((threadIdx.x & 31) == 0) {
+        sd[threadIdx.x >> 5] = dmax;
+        sn[threadIdx.x >> 5] = nmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)blockDim.x / 32; ++w) {
+            dmax = fmax(dmax, sd[w]);
+            nmax = fmax(nmax, sn[w]);
+        }
+        if (!yp) dmax = nmax;
+        atomic_max_nonneg(out + 2 * c, dmax);
+        atomic_max_nonneg(out + 2 * c + 1, nmax);
+    }
+}
+
+void launch_colstats(long long N, int ncols, const double* y, const double* yp, double* out, cudaStream_t s) {
+    cudaMemsetAsync(out, 0, sizeof(double) * 2 * ncols, s);
+    long long bx = (N + 255) / 256;
+    const long long cap = (148LL * 8 + ncols - 1) / ncols;
+    if (bx > cap) bx = cap;
+    if (bx < 1) bx = 1;
+    k_colstats<<<dim3((unsigned)bx, (unsigned)ncols), 256, 0, s>>>(N, y, yp, out);
+}
+
+__global__ void k_cubic_minus(long long N, double s1, double s3, const double* __restrict__ u,
+                              const double* __restrict__ au, double* __restrict__ out) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
+        const double x = u[t];
+        const double f = __dadd_rn(__dmul_rn(s1, x), __dmul_rn(s3, __dmul_rn(__dmul_rn(x, x), x)));
+        out[t] = __dsub_rn(f, au[t]);
+    }
+}
+void launch_cubic_minus(long long N, double s1, double s3, const double* u, const double* au, double* out,
+                        cudaStream_t s) {
+    k_cubic_minus<<<grid_for(N, 256), 256, 0, s>>>(N, s1, s3, u, au, out);
+}
+
+__global__ void k_axpy(long long N, double c, const double* __restrict__ x, double* __restrict__ y) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x)
+        y[t] = __dadd_rn(y[t], __dmul_rn(c, x[t]));
+}
+void launch_axpy(long long N, double c, const double* x, double* y, cudaStream_t s) {
+    k_axpy<<<grid_for(N, 256), 256, 0, s>>>(N, c, x, y);
+}
+
+__global__ void k_sub(long long N, const double* __restrict__ x, const double* __restrict__ au, double* __restrict__ y) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x)
+        y[t] = __dsub_rn(x[t], au[t]);
+}
+void launch_sub(long long N, const double* x, const double* au, double* y, cudaStream_t s) {
+    k_sub<<<grid_for(N, 256), 256, 0, s>>>(N, x, au, y);
+}
+
+}  // namespace pqb

@@ -1,0 +1,73 @@
+// Device kernels of the phi engine and their host-side launchers (all stream-ordered, no syncs).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace pqb {
+
+// Batched FP64 GEMM on the DMMA tensor pipe, the engine's only FLOP sink:
+//   C[z][m][n] = alpha(z1) * sum_k A[z][m][k] B[z][k][n]  (+ C_old if accumulate)
+//                + sum_{t < nterms(z1)} coef[z1*cld + t] * ext[t*ext_s + z2*sC2 + m*ldc + n]
+// A is row-major (k contiguous).  B is row-major K x N ("n contiguous") or, when b_kmajor, stored
+// as N x K rows ("k contiguous").  z = z1*zdiv + z2 indexes a two-level batch with independent
+// strides, which maps every mode product of the engine (node-batched, column-batched, shared
+// inputs with stride 0) onto one launch.
+struct GemmArgs {
+    const double* A = nullptr;
+    const double* B = nullptr;
+    double* C = nullptr;
+    int M = 0, N = 0, K = 0;
+    long long lda = 0, ldb = 0, ldc = 0;
+    int b_kmajor = 0;
+    int Z = 1, zdiv = 1, z_off = 0;
+    long long sA1 = 0, sA2 = 0, sB1 = 0, sB2 = 0, sC1 = 0, sC2 = 0;
+    double alpha = 1.0;
+    const double* alpha_z = nullptr;  // per z1 (device)
+    const double* ext = nullptr;      // extra addends (device)
+    long long ext_s = 0;              // stride between addend vectors
+    int ext_group = 1;                // batch z1 reads addends (z1/ext_group)*ext_group + t
+    const double* coef = nullptr;     // per z1 rows of cld coefficients (device)
+    int cld = 0;
+    const int* nterms = nullptr;      // per z1 (device)
+    int accumulate = 0;
+    const int* sq_count = nullptr;    // expm squaring: z with sq_round >= sq_count[z] copies A
+    int sq_round = 0;
+};
+int launch_gemm(const GemmArgs& g, cudaStream_t s);  // returns number of kernel launches
+
+// ---- batched Pade-13 expm building blocks (dense.hpp:194-228) ----
+// X[z] = (scale[z] * (op_scale * base)) * 2^-s_z  (each product rounded, as the reference's
+// KroneckerSum::scaled then DenseMatrix scaled), s_z from the 1-norm of the rounded argument.
+void launch_expm_prep(int n, int count, const double* base, long long base_stride, double op_scale,
+                      const double* scale, double* X, int* s_out, cudaStream_t s);
+// out = op_scale * a (elementwise, rounded once)
+void launch_scale_copy(long long total, double op_scale, const double* a, double* out, cudaStream_t s);
+void launch_pade_mid(int n, int count, const double* A2, const double* A4, const double* A6, double* T1,
+                     double* Zc, cudaStream_t s);
+void launch_pade_fin(int n, int count, const double* W, const double* Z, const double* A2, const double* A4,
+                     const double* A6, double* W2, double* V, cudaStream_t s);
+void launch_pade_pq(long long total, const double* V, const double* U, double* P, double* Q, cudaStream_t s);
+// Solves P X = Q in place (X -> Q) with partial pivoting, one CTA per matrix; err[0] = 1 on a zero pivot.
+void launch_lu_solve(int n, int count, double* P, double* Q, int* err, cudaStream_t s);
+// max over z of s_z -> *out (device int)
+void launch_imax(const int* v, int count, int* out, cudaStream_t s);
+
+// ---- HBM-bound helpers ----
+// acc[j][t] = (zero ? 0 : acc[j][t]) + sum_{i ascending} coef[i*p + j] * V[slot[i]][t]
+// (exact reference order: separate multiply and add per node, phiaction.hpp:96-111).
+void launch_combine(long long N, int p, int q, const double* V, long long vstride, const int* slots,
+                    const double* coef, double* acc, long long acc_stride, int zero, cudaStream_t s);
+// per column c < ncols: out[2c] = max|y_c - yp_c| (yp may be null -> max|y_c|), out[2c+1] = max|y_c|.
+void launch_colstats(long long N, int ncols, const double* y, const double* yp, double* out, cudaStream_t s);
+// out = s1*u + s3*u^3 - au   (Allen-Cahn source minus A u)
+void launch_cubic_minus(long long N, double s1, double s3, const double* u, const double* au, double* out,
+                        cudaStream_t s);
+// y = y + c * x
+void launch_axpy(long long N, double c, const double* x, double* y, cudaStream_t s);
+// y = x - au  (generic source already evaluated)
+void launch_sub(long long N, const double* x, const double* au, double* y, cudaStream_t s);
+// y = y + c * x  for a strided batch of cnt columns sharing c (used for U += tau phi_k)
+void launch_fill_identity(int n, int count, double* out, cudaStream_t s);
+
+}  // namespace pqb

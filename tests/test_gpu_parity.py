@@ -1,0 +1,202 @@
+"""GPU parity: the sm_100a engine (through the C ABI) against the compiled reference
+(oracle/_ref, the unmodified reference headers) on identical seeded inputs.
+Tolerances: 1e-13 relative for single mode products / matvecs, 1e-12 for expm, 1e-11
+relative 2-norm for the phi pipeline at identical (l, n) (BASELINE.json north_star)."""
+import numpy as np
+import pytest
+
+from conftest import lap1d, rel2, relinf
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = [(5,), (7, 9), (2, 3, 4), (3, 4, 5), (17, 33, 65), (64, 64, 64), (128, 16, 8)]
+
+
+def rand_mats(rng, shape, scale=1.0):
+    return [rng.uniform(-scale, scale, (n, n)) for n in shape]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_mode_apply(pq, ref, shape):
+    rng = np.random.default_rng(sum(shape))
+    ms = rand_mats(rng, shape)
+    x = rng.standard_normal(int(np.prod(shape)))
+    got = pq.mode_apply(ms, list(shape), x)
+    want = ref.mode_apply(ms, x)
+    assert relinf(got, want) < 1e-13
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+def test_kron_matvec(pq, ref, shape):
+    rng = np.random.default_rng(7 + sum(shape))
+    fs = rand_mats(rng, shape)
+    x = rng.standard_normal(int(np.prod(shape)))
+    got = pq.kron_matvec(pq.KroneckerSum(fs), x)
+    assert relinf(got, ref.kron_matvec(fs, x)) < 1e-13
+
+
+@pytest.mark.parametrize("n,scale", [(1, 3.0), (2, 0.5), (5, 2.0), (17, 10.0), (64, 0.05), (128, 1.0), (129, 4.0)])
+def test_expm(pq, ref, n, scale):
+    rng = np.random.default_rng(n)
+    a = rng.uniform(-scale, scale, (n, n))
+    got = pq.expm(a)
+    want = ref.expm(a)
+    assert relinf(got, want) < 1e-12
+
+
+def test_expm_batch_scales(pq, ref):
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1, 1, (33, 33))
+    sc = [0.0, 0.1, 1.0, 7.5, -3.0]
+    got = pq.expm(a, sc)
+    for i, s in enumerate(sc):
+        assert relinf(got[i], ref.expm(s * a)) < 1e-12
+
+
+def test_expm_laplacian_large_norm(pq, ref):
+    a = -1e-3 * lap1d(128)
+    assert relinf(pq.expm(a), ref.expm(a)) < 1e-11
+
+
+@pytest.mark.parametrize("shape", [(2, 3), (2, 3, 4), (16, 16), (9, 10, 11)])
+def test_exp_action(pq, ref, shape):
+    rng = np.random.default_rng(11 + sum(shape))
+    fs = rand_mats(rng, shape, 0.7)
+    b = rng.standard_normal(int(np.prod(shape)))
+    got = pq.exp_action(pq.KroneckerSum(fs), b)
+    assert rel2(got, ref.exp_action(fs, b)) < 1e-12
+
+
+@pytest.mark.parametrize("p", [1, 2, 3, 4, 5, 6])
+def test_phi_fixed_small(pq, ref, p):
+    rng = np.random.default_rng(303 + p)
+    fs = [rng.uniform(-0.7, 0.7, (3, 3)), rng.uniform(-0.7, 0.7, (4, 4))]
+    b = rng.uniform(-1, 1, 12)
+    rule = pq.cached_rule(pq.QuadKind.gauss_legendre, 40)
+    got = pq.phi_fixed(pq.KroneckerSum(fs), b, p, rule)
+    want = ref.phi_fixed(fs, b, p, 0, 40)[0]
+    for j in range(p):
+        assert rel2(got.col(j + 1), want[j]) < 1e-12
+    dense = ref.phi_dense_oracle(fs, b, p)
+    for j in range(p):
+        assert relinf(got.col(j + 1), dense[j]) < 1e-12
+
+
+def test_phi_zero_matrix_factorials(pq, ref):
+    # A = 0: every node exponential is exactly I, so the columns are sum_i w_i theta_i^{j-1}/(j-1)! b
+    # accumulated in ascending node order -- bit-identical to the reference, and b/j! to rounding
+    # (test_phiaction.cpp:58-69).
+    rng = np.random.default_rng(11)
+    zs = [np.zeros((3, 3)), np.zeros((2, 2))]
+    b = rng.uniform(-1, 1, 6)
+    cols = pq.phi_fixed(pq.KroneckerSum(zs), b, 5, pq.cached_rule(pq.QuadKind.gauss_legendre, 8))
+    want = ref.phi_fixed(zs, b, 5, 0, 8)[0]
+    assert np.array_equal(np.asarray(cols.cols), want)
+    f = 1.0
+    for j in range(1, 6):
+        f *= j
+        assert np.max(np.abs(cols.col(j) - b / f)) <= 1e-14
+
+
+def test_phi_scalar_closed_forms(pq):
+    rule = pq.cached_rule(pq.QuadKind.gauss_legendre, 40)
+    one = pq.KroneckerSum([np.array([[1.0]])])
+    two = pq.KroneckerSum([np.array([[2.0]])])
+    assert abs(pq.phi_fixed(one, [1.0], 1, rule).col(1)[0] - (np.e - 1)) <= 1e-13 * (np.e - 1)
+    c2 = pq.phi_fixed(two, [1.0], 2, rule)
+    assert abs(c2.col(1)[0] - (np.e ** 2 - 1) / 2) <= 1e-13 * (np.e ** 2 - 1) / 2
+    assert abs(c2.col(2)[0] - (np.e ** 2 - 3) / 4) <= 1e-13 * (np.e ** 2 - 3) / 4
+
+
+def test_adaptive_bitwise_equals_final_fixed_rule(pq):
+    rng = np.random.default_rng(404)
+    a = pq.KroneckerSum([rng.uniform(-0.5, 0.5, (4, 4)), rng.uniform(-0.5, 0.5, (3, 3))])
+    b = rng.uniform(-1, 1, 12)
+    info = {}
+    ad = pq.phi_adaptive(a, b, 4, 1e-13, info=info)
+    pts = info["points_used"]
+    assert pts >= 13
+    fx = pq.phi_fixed(a, b, 4, pq.cached_rule(pq.QuadKind.clenshaw_curtis, pts))
+    assert np.array_equal(np.asarray(ad.cols), np.asarray(fx.cols))
+
+
+def test_adaptive_vs_reference(pq, ref):
+    rng = np.random.default_rng(505)
+    for _ in range(3):
+        fs = [rng.uniform(-1, 1, (3, 3)), rng.uniform(-1, 1, (3, 3))]
+        b = rng.uniform(-1, 1, 9)
+        info = {}
+        got = pq.phi_adaptive(pq.KroneckerSum(fs), b, 5, 1e-13, info=info)
+        want, pts = ref.phi_adaptive(fs, b, 5, 1e-13)
+        assert info["points_used"] == pts
+        for j in range(5):
+            assert rel2(got.col(j + 1), want[0][j]) < 1e-11
+
+
+def test_adaptive_refuses_unreachable_tolerance(pq):
+    a = pq.KroneckerSum([np.array([[-1.0, 0.2], [0.1, -2.0]])])
+    with pytest.raises(pq.ConvergenceError):
+        pq.phi_adaptive(a, [1.0, 1.0], 2, 1e-30)
+
+
+def test_squaring_step(pq, ref):
+    rng = np.random.default_rng(9)
+    shape = (5, 6, 7)
+    fs = rand_mats(rng, shape, 0.3)
+    exps = [ref.expm(f) for f in fs]
+    y = rng.standard_normal((4, int(np.prod(shape))))
+    cols = pq.PhiColumns(int(np.prod(shape)), y.copy())
+    pq.squaring_step(cols, exps, list(shape))
+    want = ref.squaring_step(exps, y)
+    assert rel2(cols.cols, want) < 1e-12
+
+
+@pytest.mark.parametrize("kind,l,n", [(0, 0, 12), (0, 3, 9), (1, 0, 0), (1, 2, 0), (0, 5, 14)])
+def test_phi_with_plan_laplacian(pq, ref, kind, l, n):
+    rng = np.random.default_rng(100 + l)
+    fs = [-2e-3 * lap1d(12), -2e-3 * lap1d(10), -2e-3 * lap1d(9)]
+    b = rng.standard_normal(12 * 10 * 9)
+    got = pq.phi_with_plan(pq.KroneckerSum(fs), [b], 4, l, n, pq.QuadKind(kind), 1e-12)[0]
+    want, pts = ref.phi_with_plan(fs, b, 4, l, n, kind, 1e-12)
+    for j in range(4):
+        assert rel2(got.col(j + 1), want[0][j]) < 1e-11
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_phiquadmv_planned_multi_rhs(pq, ref, kind):
+    rng = np.random.default_rng(77 + kind)
+    fs = [-5e-3 * lap1d(16), -5e-3 * lap1d(16)]
+    bs = rng.standard_normal((3, 256))
+    info = pq.PhiInfo()
+    req = pq.PhiRequest(p=3, eps=1e-10, mode=pq.QuadKind(kind))
+    got = pq.phiquadmv_multi(pq.KroneckerSum(fs), list(bs), req, info)
+    want, rinfo = ref.phiquadmv(fs, bs, 3, 1e-10, kind)
+    assert (info.l, info.n, info.points) == (rinfo["l"], rinfo["n"], rinfo["points"])
+    assert info.alpha == rinfo["alpha"] and info.beta == rinfo["beta"]
+    for m in range(3):
+        for j in range(3):
+            assert rel2(got[m].col(j + 1), want[m][j]) < 1e-11
+
+
+def test_phi_lincomb(pq, ref):
+    rng = np.random.default_rng(21)
+    fs = [rng.uniform(-0.5, 0.5, (4, 4)), rng.uniform(-0.5, 0.5, (5, 5))]
+    bs = rng.standard_normal((3, 20))
+    got = pq.phi_lincomb(pq.KroneckerSum(fs), list(bs), pq.cached_rule(pq.QuadKind.gauss_legendre, 20))
+    want = ref.phi_lincomb(fs, bs, 0, 20)
+    assert rel2(got, want) < 1e-12
+
+
+@pytest.mark.parametrize("tab", [0, 1, 2, 3])
+def test_integrate_allen_cahn_small(pq, ref, tab):
+    n = 8
+    eps_d = 0.01
+    fs = [eps_d * lap1d(n)] * 3
+    rng = np.random.default_rng(5)
+    u0 = rng.uniform(-0.9, 0.9, n ** 3)
+    tabs = [pq.exp_euler_tableau(), pq.exp_rk2_tableau(), pq.exp_rk3_tableau(), pq.etdrk4_tableau()]
+    res = pq.integrate(pq.KroneckerSum(fs), ("cubic", 1.0, -1.0), u0, 0.0, 0.01, 5, tabs[tab],
+                       pq.PhiRequest(eps=1e-14))
+    want, calls = ref.integrate(fs, 1, u0, 0.0, 0.01, 5, tab, eps=1e-14)
+    assert res.phi_calls == calls
+    assert rel2(res.u, want) < 1e-11
