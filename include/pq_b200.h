@@ -74,6 +74,10 @@ PQ_API int pq_ctx_release_workspace(pq_ctx* ctx);
  * [5] phi_0 exp-action.  Only filled when profiling is on (adds events, no syncs). */
 PQ_API int pq_ctx_set_profiling(pq_ctx* ctx, int on);
 PQ_API int pq_ctx_phase_times(pq_ctx* ctx, double* ms6);
+/* With profiling on, every DMMA GEMM launch (mode products and expm products) is bracketed by
+ * CUDA events on the context stream.  Returns (synchronising) the number of such launches, their
+ * summed device time in ms and their summed algorithmic FLOPs (2*M*N*K per batch entry, dense). */
+PQ_API int pq_ctx_gemm_stats(pq_ctx* ctx, int reset, uint64_t* launches, double* ms, double* flops);
 
 /* host estimator: rules, roots, bounds, planner (no GPU) --------------------------------- */
 /* quadrature.hpp:31 gauss_legendre, :67 clenshaw_curtis — ascending nodes on [0,1]. */

@@ -132,6 +132,7 @@ int pq_ctx_destroy(pq_ctx* c) {
         cudaFree(c->d_int);
         cudaFree(c->d_small);
         cudaFreeHost(c->h_small);
+        for (auto e : c->ev_pool) cudaEventDestroy(e);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -189,6 +190,20 @@ int pq_ctx_set_profiling(pq_ctx* c, int on) {
     return guarded([&] {
         need_ctx(c);
         c->profiling = on != 0;
+    });
+}
+
+int pq_ctx_gemm_stats(pq_ctx* c, int reset, uint64_t* launches, double* ms, double* flops) {
+    return guarded([&] {
+        need_ctx(c);
+        prof_collect(*c);
+        if (launches) *launches = c->prof_launches;
+        if (ms) *ms = c->prof_ms;
+        if (flops) *flops = c->prof_flops;
+        if (reset) {
+            c->prof_launches = 0;
+            c->prof_ms = c->prof_flops = 0.0;
+        }
     });
 }
 
@@ -474,12 +489,9 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
     const double* db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
     double* dout = stage_out(*c, out, static_cast<size_t>(nb) * p * N, space, "hout");
     PlanInfo pi;
-    phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi);
-    if (out0) {
-        double* d0 = stage_out(*c, out0, static_cast<size_t>(nb) * N, space, "hout0");
-        exp_action_dev(*c, op, 1.0, nb, db, d0);
-        finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
-    }
+    double* d0 = out0 ? stage_out(*c, out0, static_cast<size_t>(nb) * N, space, "hout0") : nullptr;
+    phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi, d0);
+    if (out0) finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
     finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
     finish(*c, space);
     if (info) {

@@ -96,6 +96,45 @@ void arena_flush(pq_ctx& c) {
 
 void count_launch(pq_ctx& c, int n) { c.launches += static_cast<uint64_t>(n); }
 
+static cudaEvent_t prof_event(pq_ctx& c) {
+    if (c.ev_used == c.ev_pool.size()) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreate(&e), "event create");
+        c.ev_pool.push_back(e);
+    }
+    return c.ev_pool[c.ev_used++];
+}
+
+int gemm(pq_ctx& c, const GemmArgs& g) {
+    if (!c.profiling) {
+        const int k = launch_gemm(g, c.stream);
+        count_launch(c, k);
+        return k;
+    }
+    if (c.ev_used + 2 > 4096) prof_collect(c);
+    cudaEvent_t a = prof_event(c), b = prof_event(c);
+    cuda_check(cudaEventRecord(a, c.stream), "event record");
+    const int k = launch_gemm(g, c.stream);
+    cuda_check(cudaEventRecord(b, c.stream), "event record");
+    count_launch(c, k);
+    c.ev_flops.push_back(2.0 * g.M * static_cast<double>(g.N) * g.K * g.Z);
+    c.prof_launches += static_cast<uint64_t>(k);
+    return k;
+}
+
+void prof_collect(pq_ctx& c) {
+    if (c.ev_used == 0) return;
+    cuda_check(cudaStreamSynchronize(c.stream), "prof sync");
+    for (size_t i = 0; i + 1 < c.ev_used; i += 2) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, c.ev_pool[i], c.ev_pool[i + 1]), "event elapsed");
+        c.prof_ms += ms;
+        c.prof_flops += c.ev_flops[i / 2];
+    }
+    c.ev_used = 0;
+    c.ev_flops.clear();
+}
+
 void check_launch(pq_ctx& c) {
     (void)c;
     cuda_check(cudaGetLastError(), "kernel launch");
@@ -143,14 +182,16 @@ DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const
     return op;
 }
 
+
 // ------------------------------------------------------------------ batched expm ---------
 
 static constexpr double kTheta13 = 5.371920351148152;
 
+// Upper bound of the expm squaring count for ||scale * A||_1 (device norms round differently).
 static int squaring_bound(double abs_scale, double one_norm) {
     const double b = abs_scale * one_norm * (1.0 + 1e-10);
     if (!(b > kTheta13)) return 0;
-    return static_cast<int>(std::ceil(std::log2(b / kTheta13))) + 0;
+    return static_cast<int>(std::ceil(std::log2(b / kTheta13)));
 }
 
 static GemmArgs square_batch(int n, int count, const double* A, const double* B, double* C) {
@@ -165,37 +206,54 @@ static GemmArgs square_batch(int n, int count, const double* A, const double* B,
     return g;
 }
 
-// dense.hpp:194-228 for a batch: out[i] = expm(scales[i] * fl(op_scale * base)).
-static void expm_batch_scaled(pq_ctx& c, int n, int count, const double* base, long long base_stride, double op_scale,
-                              const std::vector<double>& scales, double base_one_norm, double* out) {
+struct ExpmEntry {
+    long long base_off;  // doubles from `base`
+    double scale;        // exact multiplier applied after fl(op_scale * a)
+    double one_norm;     // host 1-norm of the base matrix (< 0: unknown -> read counts back)
+};
+
+// dense.hpp:194-228 for a batch of n x n matrices: out[z] = expm(scale_z * fl(op_scale * base_z)).
+// Six batched DMMA products, two elementwise Pade combinations, one LU solve for all z, then
+// max_z s_z squaring rounds in which a finished matrix is carried through unchanged.
+static void expm_core(pq_ctx& c, int n, const double* base, double op_scale, const std::vector<ExpmEntry>& es,
+                      double* out) {
+    const int count = static_cast<int>(es.size());
     if (count <= 0) return;
     const size_t nn = static_cast<size_t>(n) * n, blk = nn * count;
     double* w = ws(c, "expm", 11 * blk);
     double *X = w, *A2 = w + blk, *A4 = w + 2 * blk, *A6 = w + 3 * blk, *TZ = w + 4 * blk, *WZ = w + 6 * blk,
            *W2 = w + 8 * blk, *V = w + 9 * blk, *U = w + 10 * blk;
     int* s_dev = static_cast<int*>(ws_bytes(c, "expm_s", sizeof(int) * count));
-    const double* scale_dev = static_cast<const double*>(arena_push(c, scales.data(), sizeof(double) * count));
-    arena_flush(c);
-
+    std::vector<double> scales(static_cast<size_t>(count));
+    std::vector<long long> offs(static_cast<size_t>(count));
     int s_max = 0;
-    if (base_one_norm >= 0.0) {
-        for (double sc : scales) s_max = std::max(s_max, squaring_bound(std::abs(sc * op_scale), base_one_norm));
+    bool known = true;
+    for (int z = 0; z < count; ++z) {
+        scales[static_cast<size_t>(z)] = es[static_cast<size_t>(z)].scale;
+        offs[static_cast<size_t>(z)] = es[static_cast<size_t>(z)].base_off;
+        if (es[static_cast<size_t>(z)].one_norm < 0.0)
+            known = false;
+        else
+            s_max = std::max(s_max, squaring_bound(std::abs(es[static_cast<size_t>(z)].scale * op_scale),
+                                                   es[static_cast<size_t>(z)].one_norm));
     }
+    const double* scale_dev = static_cast<const double*>(arena_push(c, scales.data(), sizeof(double) * count));
+    const long long* off_dev = static_cast<const long long*>(arena_push(c, offs.data(), sizeof(long long) * count));
+    arena_flush(c);
     cudaStream_t st = c.stream;
-    launch_expm_prep(n, count, base, base_stride, op_scale, scale_dev, X, s_dev, st);
+    launch_expm_prep(n, count, base, 0, off_dev, op_scale, scale_dev, X, s_dev, st);
     count_launch(c);
-    if (base_one_norm < 0.0) {  // unknown norm (standalone device expm): read the counts back
-        int* d_max = c.d_int;
-        launch_imax(s_dev, count, d_max, st);
+    if (!known) {  // standalone device expm: read the squaring counts back
+        launch_imax(s_dev, count, c.d_int, st);
         count_launch(c);
         int h = 0;
-        cuda_check(cudaMemcpyAsync(&h, d_max, sizeof(int), cudaMemcpyDeviceToHost, st), "expm s readback");
+        cuda_check(cudaMemcpyAsync(&h, c.d_int, sizeof(int), cudaMemcpyDeviceToHost, st), "expm s readback");
         cuda_check(cudaStreamSynchronize(st), "expm s sync");
         s_max = h;
     }
-    count_launch(c, launch_gemm(square_batch(n, count, X, X, A2), st));
-    count_launch(c, launch_gemm(square_batch(n, count, A2, A2, A4), st));
-    count_launch(c, launch_gemm(square_batch(n, count, A2, A4, A6), st));
+    gemm(c, square_batch(n, count, X, X, A2));
+    gemm(c, square_batch(n, count, A2, A2, A4));
+    gemm(c, square_batch(n, count, A2, A4, A6));
     launch_pade_mid(n, count, A2, A4, A6, TZ, TZ + blk, st);
     count_launch(c);
     {
@@ -205,24 +263,30 @@ static void expm_batch_scaled(pq_ctx& c, int n, int count, const double* base, l
         g.sA2 = static_cast<long long>(nn);
         g.sB1 = g.sC1 = static_cast<long long>(blk);
         g.sB2 = g.sC2 = static_cast<long long>(nn);
-        count_launch(c, launch_gemm(g, st));
+        gemm(c, g);
     }
     launch_pade_fin(n, count, WZ, WZ + blk, A2, A4, A6, W2, V, st);
     count_launch(c);
-    count_launch(c, launch_gemm(square_batch(n, count, X, W2, U), st));
+    gemm(c, square_batch(n, count, X, W2, U));
     double* P = TZ;
     double* Q = (s_max % 2 == 0) ? out : WZ;
     double* other = (s_max % 2 == 0) ? WZ : out;
     launch_pade_pq(static_cast<long long>(blk), V, U, P, Q, st);
     count_launch(c);
-    launch_lu_solve(n, count, P, Q, c.d_err, st);
-    count_launch(c);
+    if (n <= 128) {
+        int* piv = static_cast<int*>(ws_bytes(c, "expm_piv", sizeof(int) * count * n));
+        launch_lu_factor_solve(n, count, P, Q, piv, c.d_err, st);
+        count_launch(c, 2);
+    } else {
+        launch_lu_solve(n, count, P, Q, c.d_err, st);
+        count_launch(c);
+    }
     double* cur = Q;
     for (int r = 0; r < s_max; ++r) {
         GemmArgs g = square_batch(n, count, cur, cur, other);
         g.sq_count = s_dev;
         g.sq_round = r;
-        count_launch(c, launch_gemm(g, st));
+        gemm(c, g);
         std::swap(cur, other);
     }
     if (cur != out) cuda_check(cudaMemcpyAsync(out, cur, blk * sizeof(double), cudaMemcpyDeviceToDevice, st), "expm copy");
@@ -231,7 +295,78 @@ static void expm_batch_scaled(pq_ctx& c, int n, int count, const double* base, l
 
 void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_stride, const std::vector<double>& scales,
                 double base_one_norm, double* out) {
-    expm_batch_scaled(c, n, count, base, base_stride, 1.0, scales, base_one_norm, out);
+    std::vector<ExpmEntry> es;
+    for (int z = 0; z < count; ++z) es.push_back({z * base_stride, scales[static_cast<size_t>(z)], base_one_norm});
+    expm_core(c, n, base, 1.0, es, out);
+}
+
+// All 1-D exponentials one phi call needs, computed in ONE batch per distinct factor size:
+//   node[k] + a*n_k^2 = expm((1 - theta_a) 2^-l fl(s A_k))   (phiaction.hpp:90, :197)
+//   sq[k]             = expm(2^-l fl(s A_k))                  (phiaction.hpp:294-296)
+//   phi0[k]           = expm(fl(s A_k))                       (kron.hpp:125)
+// Bitwise-identical factors are exponentiated once (e.g. the isotropic Laplacians of configs
+// 1, 3, 4, 5): dims sharing a factor share the pointers.
+struct PhiExps {
+    const double* node[3] = {nullptr, nullptr, nullptr};
+    const double* sq[3] = {nullptr, nullptr, nullptr};
+    const double* phi0[3] = {nullptr, nullptr, nullptr};
+};
+
+static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, const std::vector<double>& thetas,
+                                bool want_sq, bool want_phi0, const std::string& tag) {
+    PhiExps px;
+    const int q = static_cast<int>(thetas.size());
+    const int per = q + (want_sq ? 1 : 0) + (want_phi0 ? 1 : 0);
+    if (per == 0) return px;
+    // canonical factors
+    int canon[3] = {0, 1, 2};
+    size_t off[3] = {0, 0, 0};
+    for (int k = 1; k < op.d; ++k) off[k] = off[k - 1] + static_cast<size_t>(op.n[k - 1]) * op.n[k - 1];
+    for (int k = 0; k < op.d; ++k) {
+        canon[k] = k;
+        for (int j = 0; j < k; ++j)
+            if (canon[j] == j && op.n[j] == op.n[k] &&
+                std::memcmp(op.host.data() + off[j], op.host.data() + off[k],
+                            sizeof(double) * op.n[k] * op.n[k]) == 0) {
+                canon[k] = j;
+                break;
+            }
+    }
+    // one batch per distinct n over the canonical factors with that n
+    std::vector<int> done(3, 0);
+    const double* base = op.F[0];  // factors are contiguous on the device
+    for (int k = 0; k < op.d; ++k) {
+        if (canon[k] != k || done[k]) continue;
+        const int n = op.n[k];
+        std::vector<int> group;
+        for (int j = k; j < op.d; ++j)
+            if (canon[j] == j && op.n[j] == n) {
+                group.push_back(j);
+                done[j] = 1;
+            }
+        std::vector<ExpmEntry> es;
+        for (int f : group) {
+            const long long bo = static_cast<long long>(off[f]);
+            for (int a = 0; a < q; ++a) es.push_back({bo, std::ldexp(1.0 - thetas[static_cast<size_t>(a)], -l), op.one_norm[f]});
+            if (want_sq) es.push_back({bo, std::ldexp(1.0, -l), op.one_norm[f]});
+            if (want_phi0) es.push_back({bo, 1.0, op.one_norm[f]});
+        }
+        const size_t nn = static_cast<size_t>(n) * n;
+        double* out = ws(c, tag + "_n" + std::to_string(n), es.size() * nn);
+        expm_core(c, n, base, s, es, out);
+        for (size_t g = 0; g < group.size(); ++g) {
+            double* e = out + g * per * nn;
+            px.node[group[g]] = e;
+            px.sq[group[g]] = want_sq ? e + q * nn : nullptr;
+            px.phi0[group[g]] = want_phi0 ? e + (q + (want_sq ? 1 : 0)) * nn : nullptr;
+        }
+    }
+    for (int k = 0; k < op.d; ++k) {
+        px.node[k] = px.node[canon[k]];
+        px.sq[k] = px.sq[canon[k]];
+        px.phi0[k] = px.phi0[canon[k]];
+    }
+    return px;
 }
 
 // ------------------------------------------------------------------ mode products --------
@@ -313,7 +448,7 @@ void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const lo
             g.accumulate = ep.accumulate;
             if (ep.cld > 0) g.ext_group = ep.cld;
         }
-        count_launch(c, launch_gemm(g, c.stream));
+        gemm(c, g);
         src = dst;
         sstride = dstride;
     }
@@ -338,21 +473,20 @@ void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, 
     for (int k = 0; k < op.d; ++k) {
         GemmArgs g = mode_gemm(op.d, op.n, k, F[k], 0, x, 0, y, 0, 1, op.N);
         g.accumulate = k > 0;
-        count_launch(c, launch_gemm(g, c.stream));
+        gemm(c, g);
     }
     check_launch(c);
 }
 
+static void apply_phi0(pq_ctx& c, const DevOp& op, const PhiExps& px, int nb, const double* b, double* y) {
+    long long Es[3] = {0, 0, 0};
+    mode_chain(c, op.d, op.n, px.phi0, Es, b, op.N, y, op.N, nb, Epilogue{});
+}
+
 // kron.hpp:123-128 (phi_0): expm of every (scaled) factor, then one mode chain per RHS.
 void exp_action_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* b, double* y) {
-    const double* E[3];
-    long long Es[3] = {0, 0, 0};
-    for (int k = 0; k < op.d; ++k) {
-        double* e = ws(c, "phi0E" + std::to_string(k), static_cast<size_t>(op.n[k]) * op.n[k]);
-        expm_batch_scaled(c, op.n[k], 1, op.F[k], 0, scale, {1.0}, op.one_norm[k], e);
-        E[k] = e;
-    }
-    mode_chain(c, op.d, op.n, E, Es, b, op.N, y, op.N, nb, Epilogue{});
+    const PhiExps px = phi_exponentials(c, op, scale, 0, {}, false, true, "phi0E");
+    apply_phi0(c, op, px, nb, b, y);
 }
 
 double max_inf_norm_dev(pq_ctx& c, const double* v, long long N, int ncols) {
@@ -390,36 +524,23 @@ static int node_chunk(pq_ctx& c, long long N, int q, int per_node_vectors) {
     return std::min(q, qc);
 }
 
-// Exponentials of the selected nodes: E_k[a] = expm((1 - theta_{idx[a]}) 2^-lshift fl(s A_k)).
-static void node_exponentials(pq_ctx& c, const DevOp& op, double s, int lshift, const NodesWeights& rule,
-                              const std::vector<int>& idx, const double* E[3], long long Es[3], const char* tag) {
-    const int q = static_cast<int>(idx.size());
-    std::vector<double> sc(static_cast<size_t>(q));
-    for (int a = 0; a < q; ++a) sc[static_cast<size_t>(a)] = std::ldexp(1.0 - rule.x[static_cast<size_t>(idx[a])], -lshift);
-    for (int k = 0; k < op.d; ++k) {
-        const size_t nn = static_cast<size_t>(op.n[k]) * op.n[k];
-        double* e = ws(c, std::string(tag) + std::to_string(k), nn * q);
-        expm_batch_scaled(c, op.n[k], q, op.F[k], 0, s, sc, op.one_norm[k], e);
-        E[k] = e;
-        Es[k] = static_cast<long long>(nn);
-    }
+static std::vector<double> thetas_of(const NodesWeights& r, const std::vector<int>& idx) {
+    std::vector<double> t;
+    for (int i : idx) t.push_back(r.x[static_cast<size_t>(i)]);
+    return t;
 }
 
-// For nodes idx (ascending), v_i = e^{(1-theta_i) A'} b_m, A' = 2^-lshift fl(s A); either
-// combined into acc [nb][p][N] (zeroing first if `zero`) or stored into pool slots
-// pool + (slot[a]*nb + m)*N (slots consecutive).
-static void node_sweep(pq_ctx& c, const DevOp& op, double s, int lshift, int nb, const double* bs, int p,
-                       const NodesWeights& rule, const std::vector<int>& idx, double* acc, int zero, double* pool,
+// For the selected nodes (exponentials E[k] + a*Es[k], a < q), v_a = (E_a0 (x) E_a1 (x) E_a2) b_m;
+// either combined into acc [nb][p][N] with coefficients coef [q][p] (zeroing first if `zero`),
+// or stored into pool + (slot0 + a)*nb*N + m*N.
+static void node_sweep(pq_ctx& c, const DevOp& op, const double* const* E, const long long* Es, int q, int nb,
+                       const double* bs, int p, const std::vector<double>* coef, double* acc, int zero, double* pool,
                        int slot0) {
-    const int q = static_cast<int>(idx.size());
+    const long long N = op.N;
     if (q == 0) {
-        if (acc && zero) cuda_check(cudaMemsetAsync(acc, 0, sizeof(double) * nb * p * op.N, c.stream), "zero acc");
+        if (acc && zero) cuda_check(cudaMemsetAsync(acc, 0, sizeof(double) * nb * p * N, c.stream), "zero acc");
         return;
     }
-    const double* E[3];
-    long long Es[3];
-    node_exponentials(c, op, s, lshift, rule, idx, E, Es, "nodeE");
-    const long long N = op.N;
     if (pool) {
         const int qc = node_chunk(c, N, q, 2);
         for (int m = 0; m < nb; ++m)
@@ -432,15 +553,12 @@ static void node_sweep(pq_ctx& c, const DevOp& op, double s, int lshift, int nb,
             }
         return;
     }
-    std::vector<double> coef;
-    node_coefs(rule, idx, p, coef);
-    const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
+    const double* coef_dev = static_cast<const double*>(arena_push(c, coef->data(), coef->size() * sizeof(double)));
     std::vector<int> slots(static_cast<size_t>(q));
     std::iota(slots.begin(), slots.end(), 0);
-    const int qc = node_chunk(c, N, q, 3);
-    // slot table: chunk-local indices 0..qc-1
     const int* slot_dev = static_cast<const int*>(arena_push(c, slots.data(), slots.size() * sizeof(int)));
     arena_flush(c);
+    const int qc = node_chunk(c, N, q, 3);
     double* V = ws(c, "nodeV", static_cast<size_t>(qc) * N);
     for (int m = 0; m < nb; ++m)
         for (int a0 = 0; a0 < q; a0 += qc) {
@@ -448,52 +566,72 @@ static void node_sweep(pq_ctx& c, const DevOp& op, double s, int lshift, int nb,
             const double* Ec[3];
             for (int k = 0; k < op.d; ++k) Ec[k] = E[k] + a0 * Es[k];
             mode_chain(c, op.d, op.n, Ec, Es, bs + m * N, 0, V, N, cnt, Epilogue{});
-            launch_combine(N, p, cnt, V, N, slot_dev, coef_dev + static_cast<size_t>(a0) * p, acc + static_cast<long long>(m) * p * N,
-                           N, (zero && a0 == 0) ? 1 : 0, c.stream);
+            launch_combine(N, p, cnt, V, N, slot_dev, coef_dev + static_cast<size_t>(a0) * p,
+                           acc + static_cast<long long>(m) * p * N, N, (zero && a0 == 0) ? 1 : 0, c.stream);
             count_launch(c);
         }
     check_launch(c);
 }
 
-// phiaction.hpp:134-145 (Alg. 1 on an explicit rule).
+// phiaction.hpp:134-145 (Alg. 1 on an explicit rule) on 2^-l fl(s A).
+static void phi_fixed_shift(pq_ctx& c, const DevOp& op, double s, int l, int nb, const double* bs, int p,
+                            const NodesWeights& rule, const PhiExps& px, double* out) {
+    std::vector<int> idx(static_cast<size_t>(rule.size()));
+    std::iota(idx.begin(), idx.end(), 0);
+    std::vector<double> coef;
+    node_coefs(rule, idx, p, coef);
+    long long Es[3];
+    for (int k = 0; k < op.d; ++k) Es[k] = static_cast<long long>(op.n[k]) * op.n[k];
+    (void)s;
+    (void)l;
+    node_sweep(c, op, px.node, Es, rule.size(), nb, bs, p, &coef, out, 1, nullptr, 0);
+}
+
 void phi_fixed_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, const NodesWeights& rule,
                    double* out) {
     std::vector<int> idx(static_cast<size_t>(rule.size()));
     std::iota(idx.begin(), idx.end(), 0);
-    node_sweep(c, op, scale, 0, nb, bs, p, rule, idx, out, 1, nullptr, 0);
-}
-
-static void phi_fixed_shift(pq_ctx& c, const DevOp& op, double scale, int lshift, int nb, const double* bs, int p,
-                            const NodesWeights& rule, double* out) {
-    std::vector<int> idx(static_cast<size_t>(rule.size()));
-    std::iota(idx.begin(), idx.end(), 0);
-    node_sweep(c, op, scale, lshift, nb, bs, p, rule, idx, out, 1, nullptr, 0);
+    const PhiExps px = phi_exponentials(c, op, scale, 0, thetas_of(rule, idx), false, false, "nodeE");
+    phi_fixed_shift(c, op, scale, 0, nb, bs, p, rule, px, out);
 }
 
 void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p,
                            const NodesWeights& rule, const std::vector<int>& nodes, int zero, double* acc) {
-    node_sweep(c, op, scale, 0, nb, bs, p, rule, nodes, acc, zero, nullptr, 0);
+    const PhiExps px = phi_exponentials(c, op, scale, 0, thetas_of(rule, nodes), false, false, "nodeE");
+    std::vector<double> coef;
+    node_coefs(rule, nodes, p, coef);
+    long long Es[3];
+    for (int k = 0; k < op.d; ++k) Es[k] = static_cast<long long>(op.n[k]) * op.n[k];
+    node_sweep(c, op, px.node, Es, static_cast<int>(nodes.size()), nb, bs, p, &coef, acc, zero, nullptr, 0);
 }
 
-// phiaction.hpp:156-245 (Alg. 2): nested CC ladder, node vectors kept in a device pool,
-// all sums rebuilt in ascending node order at every level.
-static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double scale, int lshift, int nb, const double* bs, int p,
-                               double eps, double* out, int* points_used) {
+// phiaction.hpp:156-245 (Alg. 2): nested CC ladder, node vectors kept in a device pool, all sums
+// rebuilt in ascending node order at every level.  The first three levels (7 -> 13 -> 25 points)
+// take their exponentials from `px25` (the 25-point rule's nodes, exponentiated in the call's
+// single expm batch: CC nodes nest bitwise, so 7-rule node i is 25-rule node 4i); deeper levels
+// exponentiate their fresh nodes on demand.
+static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int nb, const double* bs, int p,
+                               double eps, const PhiExps& px25, double* out, int* points_used) {
     if (p < 1) throw std::invalid_argument("phi_adaptive: need p >= 1");
     if (!(eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
     const long long N = op.N;
     const size_t col = static_cast<size_t>(nb) * p * N;
+    long long nn[3];
+    for (int k = 0; k < op.d; ++k) nn[k] = static_cast<long long>(op.n[k]) * op.n[k];
     int half = 3;
     const NodesWeights* rule = &memo_rule(kClenshaw, 2 * half + 1);
-    // slot of rule node i in the pool
     std::vector<int> slot_of(static_cast<size_t>(rule->size()));
     std::iota(slot_of.begin(), slot_of.end(), 0);
     int used = rule->size();
-    auto pool_for = [&](int slots) { return ws(c, "ccpool", static_cast<size_t>(slots) * nb * N); };
-    double* pool = pool_for(used);
+    double* pool = ws(c, "ccpool", static_cast<size_t>(used) * nb * N);
     {
-        std::vector<int> idx(slot_of);
-        node_sweep(c, op, scale, lshift, nb, bs, p, *rule, idx, nullptr, 0, pool, 0);
+        const double* E[3];
+        long long Es[3];
+        for (int k = 0; k < op.d; ++k) {
+            E[k] = px25.node[k];
+            Es[k] = 4 * nn[k];
+        }
+        node_sweep(c, op, E, Es, rule->size(), nb, bs, p, nullptr, nullptr, 0, pool, 0);
     }
     double* accs[2] = {out, ws(c, "ccacc", col)};
     int cur = 0;
@@ -503,8 +641,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double scale, int lsh
         std::vector<double> coef;
         node_coefs(r, idx, p, coef);
         const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
-        std::vector<int> sl(slots.begin(), slots.end());
-        const int* sl_dev = static_cast<const int*>(arena_push(c, sl.data(), sl.size() * sizeof(int)));
+        const int* sl_dev = static_cast<const int*>(arena_push(c, slots.data(), slots.size() * sizeof(int)));
         arena_flush(c);
         for (int m = 0; m < nb; ++m) {
             launch_combine(N, p, r.size(), pool + static_cast<long long>(m) * N, static_cast<long long>(nb) * N, sl_dev,
@@ -515,12 +652,12 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double scale, int lsh
     combine_all(*rule, slot_of, accs[cur]);
     double* stats = ws(c, "ccstats", 2 * static_cast<size_t>(nb) * p);
     std::vector<double> hstats(2 * static_cast<size_t>(nb) * p);
+    int level = 0;
     while (true) {
         const int half_next = 2 * half;
         if (half_next > (1 << 14)) throw ConvergenceFailure("phi_adaptive: no convergence within the node budget");
         const NodesWeights& fine = memo_rule(kClenshaw, 2 * half_next + 1);
         const int fresh = fine.size() / 2;
-        // grow the pool (keeps contents)
         const int need = used + fresh;
         {
             DevBuf& b = c.bufs["ccpool"];
@@ -547,7 +684,24 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double scale, int lsh
             odd[static_cast<size_t>(k)] = 2 * k + 1;
             fine_slot[static_cast<size_t>(2 * k + 1)] = used + k;
         }
-        node_sweep(c, op, scale, lshift, nb, bs, p, fine, odd, nullptr, 0, pool, used);
+        ++level;
+        const double* E[3];
+        long long Es[3];
+        PhiExps pxl;
+        if (level <= 2) {
+            // 13-rule odd node 2k+1 = 25-rule node 4k+2 ; 25-rule odd node 2k+1 itself
+            for (int k = 0; k < op.d; ++k) {
+                E[k] = px25.node[k] + (level == 1 ? 2 : 1) * nn[k];
+                Es[k] = (level == 1 ? 4 : 2) * nn[k];
+            }
+        } else {
+            pxl = phi_exponentials(c, op, s, l, thetas_of(fine, odd), false, false, "ccE");
+            for (int k = 0; k < op.d; ++k) {
+                E[k] = pxl.node[k];
+                Es[k] = nn[k];
+            }
+        }
+        node_sweep(c, op, E, Es, fresh, nb, bs, p, nullptr, nullptr, 0, pool, used);
         used = need;
         const int nxt = 1 - cur;
         combine_all(fine, fine_slot, accs[nxt]);
@@ -576,29 +730,64 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double scale, int lsh
 
 void phi_adaptive_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, double eps, double* out,
                       int* points_used) {
-    phi_adaptive_shift(c, op, scale, 0, nb, bs, p, eps, out, points_used);
+    const NodesWeights& r25 = memo_rule(kClenshaw, 25);
+    const PhiExps px = phi_exponentials(c, op, scale, 0, r25.x, false, false, "nodeE");
+    phi_adaptive_shift(c, op, scale, 0, nb, bs, p, eps, px, out, points_used);
 }
 
-// phiaction.hpp:255-272 + 290-301: l doubling steps, E_k = expm(2^-l A_k) squared after each
-// step but the last.  y [nb][p][N] holds phi_j(2^-l A) b on entry; the result lands in y when l
-// is even and in `partner` when l is odd (ping-pong, no copy).
-static double* squaring_pingpong(pq_ctx& c, const DevOp& op, double scale, int l, int nb, int p, double* y,
-                                 double* partner, const double* const* exps_in) {
+// phiaction.hpp:255-272 + 290-301: l doubling steps with E_k (= expm(2^-l A_k) on entry),
+// squared after each step but the last.  y [nb][p][N] holds phi_j(2^-l A) b on entry; the
+// result lands in y when l is even and in `partner` when l is odd (ping-pong, no copy).
+static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int p, double* y, double* partner,
+                                 const double* const* E_in) {
     if (l <= 0) return y;
     const long long N = op.N;
-    const double* E[3];
-    double* Ew[3];
-    long long Es[3] = {0, 0, 0};
+    // Distinct exponentials grouped by size, copied into contiguous ping-pong slots so each
+    // step's E <- E E is one batched DMMA launch per size (dims sharing an exponential share it).
+    struct Group {
+        int n = 0;
+        std::vector<int> dims;  // first dim of each distinct exponential
+        double* buf = nullptr;  // [2][count][n*n]
+    };
+    std::vector<Group> groups;
+    int slot_dim[3] = {-1, -1, -1};  // k -> (group, index)
+    int slot_idx[3] = {0, 0, 0};
     for (int k = 0; k < op.d; ++k) {
-        const size_t nn = static_cast<size_t>(op.n[k]) * op.n[k];
-        Ew[k] = ws(c, "sqE" + std::to_string(k), 2 * nn);
-        if (exps_in)
-            cuda_check(cudaMemcpyAsync(Ew[k], exps_in[k], nn * sizeof(double), cudaMemcpyDeviceToDevice, c.stream), "exps");
-        else
-            expm_batch_scaled(c, op.n[k], 1, op.F[k], 0, scale, {std::ldexp(1.0, -l)}, op.one_norm[k], Ew[k]);
-        E[k] = Ew[k];
+        int same = -1;
+        for (int j = 0; j < k; ++j)
+            if (E_in[j] == E_in[k]) same = j;
+        if (same >= 0) {
+            slot_dim[k] = slot_dim[same];
+            slot_idx[k] = slot_idx[same];
+            continue;
+        }
+        int gi = -1;
+        for (size_t g = 0; g < groups.size(); ++g)
+            if (groups[g].n == op.n[k]) gi = static_cast<int>(g);
+        if (gi < 0) {
+            groups.push_back(Group{op.n[k], {}, nullptr});
+            gi = static_cast<int>(groups.size()) - 1;
+        }
+        slot_dim[k] = gi;
+        slot_idx[k] = static_cast<int>(groups[static_cast<size_t>(gi)].dims.size());
+        groups[static_cast<size_t>(gi)].dims.push_back(k);
     }
-    // epilogue tables for column z1 = m*p + (i-1): alpha = 2^-i, coef_t = 2^-i/(i-1-t)!, t < i
+    for (size_t g = 0; g < groups.size(); ++g) {
+        Group& G = groups[g];
+        const size_t nn = static_cast<size_t>(G.n) * G.n;
+        G.buf = ws(c, "sqE" + std::to_string(g), 2 * G.dims.size() * nn);
+        for (size_t i = 0; i < G.dims.size(); ++i)
+            cuda_check(cudaMemcpyAsync(G.buf + i * nn, E_in[G.dims[i]], nn * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       c.stream),
+                       "sq exps");
+    }
+    int parity = 0;
+    auto cur_E = [&](int k) {
+        const Group& G = groups[static_cast<size_t>(slot_dim[k])];
+        const size_t nn = static_cast<size_t>(G.n) * G.n;
+        return G.buf + (static_cast<size_t>(parity) * G.dims.size() + slot_idx[k]) * nn;
+    };
+    // combination table: coef[i][j] = 2^-(i+1) / (i-j)!  (inverse_factorials, phiaction.hpp:58-66)
     std::vector<double> inv(static_cast<size_t>(p), 1.0);
     {
         double f = 1.0;
@@ -607,37 +796,32 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, double scale, int l
             inv[static_cast<size_t>(k)] = 1.0 / f;
         }
     }
-    const int Z1 = nb * p;
-    std::vector<double> alpha(static_cast<size_t>(Z1)), coef(static_cast<size_t>(Z1) * p, 0.0);
-    std::vector<int> nterms(static_cast<size_t>(Z1));
-    for (int m = 0; m < nb; ++m)
-        for (int i = 1; i <= p; ++i) {
-            const int z1 = m * p + i - 1;
-            const double sc = std::ldexp(1.0, -i);
-            alpha[static_cast<size_t>(z1)] = sc;
-            nterms[static_cast<size_t>(z1)] = i;
-            for (int t = 0; t < i; ++t) coef[static_cast<size_t>(z1) * p + t] = sc * inv[static_cast<size_t>(i - 1 - t)];
-        }
-    Epilogue ep;
-    ep.alpha_z = static_cast<const double*>(arena_push(c, alpha.data(), alpha.size() * sizeof(double)));
-    ep.coef = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
-    ep.nterms = static_cast<const int*>(arena_push(c, nterms.data(), nterms.size() * sizeof(int)));
-    ep.cld = p;
-    ep.ext_s = N;
+    std::vector<double> coef(static_cast<size_t>(p) * p, 0.0);
+    for (int i = 0; i < p; ++i)
+        for (int j = 0; j <= i; ++j)
+            coef[static_cast<size_t>(i) * p + j] = std::ldexp(1.0, -(i + 1)) * inv[static_cast<size_t>(i - j)];
+    const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
     arena_flush(c);
+    const int Z1 = nb * p;
+    long long Es[3] = {0, 0, 0};
     double* cur = y;
     double* nxt = partner;
     for (int step = 0; step < l; ++step) {
-        ep.ext = cur;
-        mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, ep);
+        const double* E[3];
+        for (int k = 0; k < op.d; ++k) E[k] = cur_E(k);
+        mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, Epilogue{});
+        launch_sq_combine(N, p, nb, nxt, cur, coef_dev, c.stream);
+        count_launch(c);
         std::swap(cur, nxt);
         if (step < l - 1) {
-            for (int k = 0; k < op.d; ++k) {
-                const size_t nn = static_cast<size_t>(op.n[k]) * op.n[k];
-                double* dst = (E[k] == Ew[k]) ? Ew[k] + nn : Ew[k];
-                count_launch(c, launch_gemm(square_batch(op.n[k], 1, E[k], E[k], dst), c.stream));
-                E[k] = dst;
+            for (const Group& G : groups) {
+                const size_t nn = static_cast<size_t>(G.n) * G.n;
+                const int cnt = static_cast<int>(G.dims.size());
+                double* src = G.buf + static_cast<size_t>(parity) * cnt * nn;
+                double* dst = G.buf + static_cast<size_t>(1 - parity) * cnt * nn;
+                gemm(c, square_batch(G.n, cnt, src, src, dst));
             }
+            parity = 1 - parity;
         }
     }
     check_launch(c);
@@ -647,45 +831,54 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, double scale, int l
 void squaring_steps_dev(pq_ctx& c, const DevOp& op, double scale, int nb, int p, int l, double* y,
                         const double* exps_override) {
     double* partner = ws(c, "sqT", static_cast<size_t>(nb) * p * op.N);
-    const double* ex[3] = {nullptr, nullptr, nullptr};
+    const double* E[3] = {nullptr, nullptr, nullptr};
     if (exps_override) {
         size_t off = 0;
         for (int k = 0; k < op.d; ++k) {
-            ex[k] = exps_override + off;
+            E[k] = exps_override + off;
             off += static_cast<size_t>(op.n[k]) * op.n[k];
         }
+    } else {
+        const PhiExps px = phi_exponentials(c, op, scale, l, {}, true, false, "sqE0");
+        for (int k = 0; k < op.d; ++k) E[k] = px.sq[k];
     }
-    double* res = squaring_pingpong(c, op, scale, l, nb, p, y, partner, exps_override ? ex : nullptr);
+    double* res = squaring_pingpong(c, op, l, nb, p, y, partner, E);
     if (res != y)
         cuda_check(cudaMemcpyAsync(y, res, sizeof(double) * nb * p * op.N, cudaMemcpyDeviceToDevice, c.stream), "sq copy");
 }
 
-// phiaction.hpp:277-303.
-void phi_with_plan_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n, int kind,
-                       double eps, double* out, int* points_used) {
+// phiaction.hpp:277-303, plus (when phi0_out) kron.hpp:123-128 phi_0 from the same expm batch.
+static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n,
+                         int kind, double eps, double* out, int* points_used, double* phi0_out) {
     if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
     if (p < 1) throw std::invalid_argument(kind == kGauss ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
-    // quadrature result goes where the l-step ping-pong will end in `out`
+    const NodesWeights& rule = kind == kGauss ? memo_rule(kGauss, n + 1) : memo_rule(kClenshaw, 25);
+    const PhiExps px = phi_exponentials(c, op, scale, l, rule.x, l > 0, phi0_out != nullptr, "nodeE");
     double* partner = l > 0 ? ws(c, "sqT", static_cast<size_t>(nb) * p * op.N) : nullptr;
-    double* first = (l % 2 == 1) ? partner : out;
+    double* first = (l % 2 == 1) ? partner : out;  // the l-step ping-pong then ends in `out`
     if (kind == kGauss) {
-        const NodesWeights& rule = memo_rule(kGauss, n + 1);
-        phi_fixed_shift(c, op, scale, l, nb, bs, p, rule, first);
+        phi_fixed_shift(c, op, scale, l, nb, bs, p, rule, px, first);
         if (points_used) *points_used = rule.size();
     } else {
-        phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, first, points_used);
+        phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, px, first, points_used);
     }
     if (l > 0) {
-        double* res = squaring_pingpong(c, op, scale, l, nb, p, first, first == out ? partner : out, nullptr);
+        double* res = squaring_pingpong(c, op, l, nb, p, first, first == out ? partner : out, px.sq);
         if (res != out)
             cuda_check(cudaMemcpyAsync(out, res, sizeof(double) * nb * p * op.N, cudaMemcpyDeviceToDevice, c.stream),
                        "plan copy");
     }
+    if (phi0_out) apply_phi0(c, op, px, nb, bs, phi0_out);
 }
 
-// phiaction.hpp:307-346.
+void phi_with_plan_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n, int kind,
+                       double eps, double* out, int* points_used) {
+    phi_call_dev(c, op, scale, nb, bs, p, l, n, kind, eps, out, points_used, nullptr);
+}
+
+// phiaction.hpp:307-346 (+ phi_0 when phi0_out).
 void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l, int l,
-                   double c1, double c2, double* out, PlanInfo* info) {
+                   double c1, double c2, double* out, PlanInfo* info, double* phi0_out) {
     if (p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
     double alpha = 0.0;
     for (int k = 0; k < op.d; ++k) alpha += op.inf_norm[k];
@@ -714,7 +907,7 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
         planned = true;
     }
     int points = 0;
-    phi_with_plan_dev(c, op, 1.0, nb, bs, p, l, n, mode, eps, out, &points);
+    phi_call_dev(c, op, 1.0, nb, bs, p, l, n, mode, eps, out, &points, phi0_out);
     if (info) {
         info->l = l;
         info->n = n;
@@ -733,11 +926,9 @@ void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const doub
     if (p < 1) throw std::invalid_argument("phi_lincomb: need at least one vector");
     const int q = rule.size();
     const long long N = op.N;
-    std::vector<int> idx(static_cast<size_t>(q));
-    std::iota(idx.begin(), idx.end(), 0);
-    const double* E[3];
+    const PhiExps px = phi_exponentials(c, op, scale, 0, rule.x, false, false, "lincE");
     long long Es[3];
-    node_exponentials(c, op, scale, 0, rule, idx, E, Es, "lincE");
+    for (int k = 0; k < op.d; ++k) Es[k] = static_cast<long long>(op.n[k]) * op.n[k];
     // mixing coefficients per node (coeff = 1, coeff *= theta/j) and final weights
     std::vector<double> mix(static_cast<size_t>(q) * p), wts(static_cast<size_t>(q));
     for (int i = 0; i < q; ++i) {
@@ -768,7 +959,7 @@ void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const doub
             count_launch(c);
         }
         const double* Ec[3];
-        for (int k = 0; k < op.d; ++k) Ec[k] = E[k] + a0 * Es[k];
+        for (int k = 0; k < op.d; ++k) Ec[k] = px.node[k] + a0 * Es[k];
         mode_chain(c, op.d, op.n, Ec, Es, M, N, V, N, cnt, Epilogue{});
         launch_combine(N, 1, cnt, V, N, vsl, w_dev + a0, out, N, a0 == 0 ? 1 : 0, c.stream);
         count_launch(c);

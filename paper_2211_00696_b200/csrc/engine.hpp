@@ -54,6 +54,12 @@ struct pq_ctx {
     int* d_int = nullptr;        // device int scratch (expm squaring counts)
     bool profiling = false;
     double phase_ms[6] = {0, 0, 0, 0, 0, 0};
+    // GEMM (DMMA) launch records while profiling: (start, stop) events + algorithmic flops
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<double> ev_flops;
+    double prof_ms = 0.0, prof_flops = 0.0;
+    uint64_t prof_launches = 0;
 };
 
 namespace pqb {
@@ -114,6 +120,9 @@ void arena_begin(pq_ctx& c);
 const void* arena_push(pq_ctx& c, const void* data, size_t bytes);     // returns device address
 void arena_flush(pq_ctx& c);
 void count_launch(pq_ctx& c, int n = 1);
+// launch_gemm + launch counting + (when profiling) per-launch events and algorithmic flops
+int gemm(pq_ctx& c, const GemmArgs& g);
+void prof_collect(pq_ctx& c);  // syncs, folds recorded events into prof_ms/prof_flops
 void check_launch(pq_ctx& c);
 
 // ---- device building blocks ----
@@ -142,7 +151,7 @@ struct PlanInfo {
     double alpha = 0, beta = 0, cost = 0;
 };
 void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l,
-                   int l, double c1, double c2, double* out, PlanInfo* info);
+                   int l, double c1, double c2, double* out, PlanInfo* info, double* phi0_out = nullptr);
 void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p,
                            const NodesWeights& rule, const std::vector<int>& nodes, int zero, double* acc);
 void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const double* bs, const NodesWeights& rule,

@@ -1,13 +1,17 @@
 // FP64 DMMA mode-product GEMM template (see kernels.cu header comment); instantiated in
 // gemm_nk.cu (B row-major, "n contiguous") and gemm_kk.cu (B stored k-contiguous).
+//
+// Structure: ST-stage cp.async pipeline (16-byte LDGSTS, zero-fill predicates) into padded
+// shared-memory tiles; each warp owns a WM x WN register tile of m8n8k4 accumulators; one
+// barrier per BK slice.  Per-thread global source pointers are computed once (no per-stage
+// 64-bit address arithmetic) and the epilogue is compact (the extra-addend loop is not
+// unrolled) so the whole kernel stays inside the instruction cache.
 #pragma once
 #include <stdexcept>
 
 #include "kernels.hpp"
 
 namespace pqb {
-
-// ================================================================ DMMA GEMM =================
 
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
@@ -16,13 +20,12 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
 }
 
 template <int VEC>
-__device__ __forceinline__ void cp_async(double* dst, const double* src, bool ok) {
-    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+__device__ __forceinline__ void cp_async(unsigned dst, const double* src, bool ok) {
     const int bytes = ok ? 8 * VEC : 0;  // 0 -> zero-fill, nothing read
     if constexpr (VEC == 2)
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
     else
-        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src), "r"(bytes));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(bytes));
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 template <int N>
@@ -46,6 +49,7 @@ struct TileCfg {
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC>
 __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, 1) k_gemm(const GemmArgs g) {
     using T = TileCfg<BM, BN, BK, WM, WN, ST, BKM>;
+    constexpr int NT = T::NT;
     extern __shared__ __align__(16) double smem[];
     double* sA = smem;
     double* sB = smem + ST * T::ASZ;
@@ -62,42 +66,70 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, 1) k
 
     if (g.sq_count && g.sq_round >= g.sq_count[z]) {
         // expm squaring already finished for this matrix: carry it through unchanged.
-        for (int e = tid; e < BM * BN; e += T::NT) {
+        for (int e = tid; e < BM * BN; e += NT) {
             const int m = m0 + e / BN, n = n0 + e % BN;
             if (m < g.M && n < g.N) C[(long long)m * g.ldc + n] = A[(long long)m * g.lda + n];
         }
         return;
     }
 
-    auto load_stage = [&](int stage, int kt) {
-        const int k0 = kt * BK;
-        double* dA = sA + stage * T::ASZ;
-        double* dB = sB + stage * T::BSZ;
-        constexpr int KV = BK / VEC;
+    // ---- per-thread load descriptors (fixed across k slices) ----
+    constexpr int KV = BK / VEC;
+    constexpr int A_CH = BM * KV, A_IT = (A_CH + NT - 1) / NT;
+    constexpr int B_CH = BKM ? BN * KV : BK * (BN / VEC), B_IT = (B_CH + NT - 1) / NT;
+    const double* a_src[A_IT];
+    unsigned a_dst[A_IT];
+    int a_k[A_IT];
+    bool a_ok[A_IT];
+    const unsigned sA_base = static_cast<unsigned>(__cvta_generic_to_shared(sA));
+    const unsigned sB_base = static_cast<unsigned>(__cvta_generic_to_shared(sB));
 #pragma unroll
-        for (int c = tid; c < BM * KV; c += T::NT) {
-            const int r = c / KV, kc = (c % KV) * VEC;
-            const int gm = m0 + r, gk = k0 + kc;
-            const bool ok = gm < g.M && gk < g.K;
-            cp_async<VEC>(dA + r * T::SA + kc, ok ? A + (long long)gm * g.lda + gk : A, ok);
-        }
+    for (int it = 0; it < A_IT; ++it) {
+        const int c = tid + it * NT;
+        const int r = c / KV, kc = (c % KV) * VEC;
+        a_ok[it] = c < A_CH && m0 + r < g.M;
+        a_src[it] = A + (long long)(a_ok[it] ? m0 + r : 0) * g.lda + kc;
+        a_dst[it] = sA_base + 8u * (r * T::SA + kc);
+        a_k[it] = kc;
+    }
+    const double* b_src[B_IT];
+    unsigned b_dst[B_IT];
+    int b_k[B_IT];
+    bool b_ok[B_IT];
+    long long b_kstep;  // global stride of one k row of B
+#pragma unroll
+    for (int it = 0; it < B_IT; ++it) {
+        const int c = tid + it * NT;
         if constexpr (BKM) {
-#pragma unroll
-            for (int c = tid; c < BN * KV; c += T::NT) {
-                const int r = c / KV, kc = (c % KV) * VEC;
-                const int gn = n0 + r, gk = k0 + kc;
-                const bool ok = gn < g.N && gk < g.K;
-                cp_async<VEC>(dB + r * T::SB + kc, ok ? B + (long long)gn * g.ldb + gk : B, ok);
-            }
+            const int r = c / KV, kc = (c % KV) * VEC;  // r = n, kc = k
+            b_ok[it] = c < B_CH && n0 + r < g.N;
+            b_src[it] = B + (long long)(b_ok[it] ? n0 + r : 0) * g.ldb + kc;
+            b_dst[it] = sB_base + 8u * (r * T::SB + kc);
+            b_k[it] = kc;
         } else {
             constexpr int NV = BN / VEC;
+            const int r = c / NV, nc = (c % NV) * VEC;  // r = k, nc = n
+            b_ok[it] = c < B_CH && n0 + nc < g.N;
+            b_src[it] = B + (long long)r * g.ldb + (b_ok[it] ? n0 + nc : 0);
+            b_dst[it] = sB_base + 8u * (r * T::SB + nc);
+            b_k[it] = r;
+        }
+    }
+    b_kstep = BKM ? 1 : g.ldb;
+
+    auto load_stage = [&](int stage, int kt) {
+        const int k0 = kt * BK;
 #pragma unroll
-            for (int c = tid; c < BK * NV; c += T::NT) {
-                const int r = c / NV, nc = (c % NV) * VEC;
-                const int gk = k0 + r, gn = n0 + nc;
-                const bool ok = gk < g.K && gn < g.N;
-                cp_async<VEC>(dB + r * T::SB + nc, ok ? B + (long long)gk * g.ldb + gn : B, ok);
-            }
+        for (int it = 0; it < A_IT; ++it) {
+            if (A_CH % NT != 0 && tid + it * NT >= A_CH) continue;
+            const bool ok = a_ok[it] && k0 + a_k[it] < g.K;
+            cp_async<VEC>(a_dst[it] + 8u * stage * T::ASZ, ok ? a_src[it] + k0 : A, ok);
+        }
+#pragma unroll
+        for (int it = 0; it < B_IT; ++it) {
+            if (B_CH % NT != 0 && tid + it * NT >= B_CH) continue;
+            const bool ok = b_ok[it] && k0 + b_k[it] < g.K;
+            cp_async<VEC>(b_dst[it] + 8u * stage * T::BSZ, ok ? b_src[it] + (long long)k0 * b_kstep : B, ok);
         }
     };
 
@@ -113,6 +145,9 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, 1) k
         if (s < KT) load_stage(s, s);
         cp_commit();
     }
+    const double* tA0 = sA + (wm * WM + gid) * T::SA + tig;
+    const double* tB0 = BKM ? sB + (wn * WN + gid) * T::SB + tig : sB + tig * T::SB + wn * WN + gid;
+#pragma unroll 1
     for (int kt = 0; kt < KT; ++kt) {
         cp_wait<ST - 2>();
         __syncthreads();
@@ -122,9 +157,8 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, 1) k
             cp_commit();
         }
         const int st = kt % ST;
-        const double* tA = sA + st * T::ASZ + (wm * WM + gid) * T::SA + tig;
-        const double* tB = BKM ? sB + st * T::BSZ + (wn * WN + gid) * T::SB + tig
-                               : sB + st * T::BSZ + tig * T::SB + wn * WN + gid;
+        const double* tA = tA0 + st * T::ASZ;
+        const double* tB = tB0 + st * T::BSZ;
 #pragma unroll
         for (int kk = 0; kk < BK; kk += 4) {
             double a[T::MI], b[T::NI];
@@ -140,27 +174,71 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, 1) k
     }
     cp_wait<0>();
 
-    // ---- epilogue (registers -> global), order of the reference's scalar updates ----
+    // ---- epilogue (registers -> global) ----
     const double alpha = g.alpha_z ? g.alpha_z[z1] : g.alpha;
     const int nt = g.nterms ? g.nterms[z1] : 0;
+    const int mb = m0 + wm * WM + gid, nbase = n0 + wn * WN + 2 * tig;
     const double* crow = g.coef ? g.coef + (long long)z1 * g.cld : nullptr;
     const double* ext = g.ext ? g.ext + (long long)(z1 / g.ext_group) * g.ext_group * g.ext_s + z2 * g.sC2 : nullptr;
+    // each thread owns 2 consecutive columns -> 16-byte accesses when everything is aligned
+    const bool v2 = (g.ldc % 2 == 0) && (g.sC1 % 2 == 0) && (g.sC2 % 2 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0) &&
+                    (!ext || (g.ext_s % 2 == 0 && (reinterpret_cast<uintptr_t>(ext) & 15) == 0));
+    // out = alpha*acc (+ C_old) + sum_t coef_t * ext_t  -- the reference's update order
+    // (phiaction.hpp:260-268), applied term by term so each term's loads are independent.
+    if (alpha != 1.0) {
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+            for (int j = 0; j < T::NI; ++j) {
+                acc[i][j][0] = __dmul_rn(alpha, acc[i][j][0]);
+                acc[i][j][1] = __dmul_rn(alpha, acc[i][j][1]);
+            }
+    }
+    auto add_term = [&](const double* src, double coef, bool plain) {
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i) {
+            const int m = mb + i * 8;
+            if (m >= g.M) continue;
+            const double* row = src + (long long)m * g.ldc;
+#pragma unroll
+            for (int j = 0; j < T::NI; ++j) {
+                const int n = nbase + j * 8;
+                double x0 = 0.0, x1 = 0.0;
+                if (v2 && n + 1 < g.N) {
+                    const double2 v = *reinterpret_cast<const double2*>(row + n);
+                    x0 = v.x;
+                    x1 = v.y;
+                } else {
+                    if (n < g.N) x0 = row[n];
+                    if (n + 1 < g.N) x1 = row[n + 1];
+                }
+                if (plain) {  // accumulate: C_old + v
+                    acc[i][j][0] = __dadd_rn(x0, acc[i][j][0]);
+                    acc[i][j][1] = __dadd_rn(x1, acc[i][j][1]);
+                } else {
+                    acc[i][j][0] = __dadd_rn(acc[i][j][0], __dmul_rn(coef, x0));
+                    acc[i][j][1] = __dadd_rn(acc[i][j][1], __dmul_rn(coef, x1));
+                }
+            }
+        }
+    };
+    if (g.accumulate) add_term(C, 1.0, true);
+#pragma unroll 1
+    for (int t = 0; t < nt; ++t) add_term(ext + (long long)t * g.ext_s, crow[t], false);
 #pragma unroll
     for (int i = 0; i < T::MI; ++i) {
-        const int m = m0 + wm * WM + i * 8 + gid;
+        const int m = mb + i * 8;
         if (m >= g.M) continue;
+        double* row = C + (long long)m * g.ldc;
 #pragma unroll
         for (int j = 0; j < T::NI; ++j) {
-            const int nb = n0 + wn * WN + j * 8 + 2 * tig;
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-                const int n = nb + e;
-                if (n >= g.N) continue;
-                const long long off = (long long)m * g.ldc + n;
-                double v = __dmul_rn(alpha, acc[i][j][e]);
-                if (g.accumulate) v = __dadd_rn(C[off], v);
-                for (int t = 0; t < nt; ++t) v = __dadd_rn(v, __dmul_rn(crow[t], ext[t * g.ext_s + off]));
-                C[off] = v;
+            const int n = nbase + j * 8;
+            if (v2 && n + 1 < g.N) {
+                *reinterpret_cast<double2*>(row + n) = make_double2(acc[i][j][0], acc[i][j][1]);
+            } else {
+                if (n < g.N) row[n] = acc[i][j][0];
+                if (n + 1 < g.N) row[n + 1] = acc[i][j][1];
             }
         }
     }
@@ -188,15 +266,20 @@ static int launch_cfg(const GemmArgs& g, cudaStream_t s) {
     return launches;
 }
 
-
-// Tile shapes: id 0 = 128x128 (8 warps of 64x32), 1 = 128x64, 2 = 64x128, 3 = 64x64.
+// Tile shapes: 0 = 128x128 (8 warps of 64x32), 1 = 128x64, 2 = 64x128, 3 = 64x64, 4 = 32x32.
+#ifndef PQ_BK_BIG
+#define PQ_BK_BIG 32
+#endif
 template <bool BKM>
 int launch_gemm_family(const GemmArgs& g, bool vec2, int shape, cudaStream_t s) {
+    constexpr int BKB = PQ_BK_BIG;
+    constexpr int STB = BKB == 32 ? 3 : 4;
     switch (shape) {
-        case 0: return vec2 ? launch_cfg<128, 128, 16, 64, 32, 3, BKM, 2>(g, s) : launch_cfg<128, 128, 16, 64, 32, 3, BKM, 1>(g, s);
-        case 1: return vec2 ? launch_cfg<128, 64, 16, 64, 32, 3, BKM, 2>(g, s) : launch_cfg<128, 64, 16, 64, 32, 3, BKM, 1>(g, s);
-        case 2: return vec2 ? launch_cfg<64, 128, 16, 32, 64, 3, BKM, 2>(g, s) : launch_cfg<64, 128, 16, 32, 64, 3, BKM, 1>(g, s);
-        default: return vec2 ? launch_cfg<64, 64, 16, 32, 32, 3, BKM, 2>(g, s) : launch_cfg<64, 64, 16, 32, 32, 3, BKM, 1>(g, s);
+        case 0: return vec2 ? launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 1>(g, s);
+        case 1: return vec2 ? launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 1>(g, s);
+        case 2: return vec2 ? launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 2>(g, s) : launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 1>(g, s);
+        case 3: return vec2 ? launch_cfg<64, 64, 16, 32, 32, 3, BKM, 2>(g, s) : launch_cfg<64, 64, 16, 32, 32, 3, BKM, 1>(g, s);
+        default: return vec2 ? launch_cfg<32, 32, 16, 16, 16, 3, BKM, 2>(g, s) : launch_cfg<32, 32, 16, 16, 16, 3, BKM, 1>(g, s);
     }
 }
 

@@ -30,7 +30,12 @@ int launch_gemm(const GemmArgs& g, cudaStream_t s) {
     const bool vec2 = (g.K % 2 == 0) && (g.b_kmajor || g.N % 2 == 0) && g.lda % 2 == 0 && g.ldb % 2 == 0 &&
                       g.sA1 % 2 == 0 && g.sA2 % 2 == 0 && g.sB1 % 2 == 0 && g.sB2 % 2 == 0 && al16(g.A) &&
                       al16(g.B);
-    const int shape = (g.M >= 96 && g.N >= 96) ? 0 : (g.M >= 96 ? 1 : (g.N >= 96 ? 2 : 3));
+    // 64x64x16 tiles (4 warps of 32x32, 3 CTAs/SM) measured fastest on every mode-product shape
+    // (tools/gemm_tune.cu, profiles/r01_gemm_tune.txt); small batched products (expm) drop to
+    // 32x32 tiles until the grid covers the 148 SMs twice.
+    auto ctas = [&](int bm, int bn) { return (long long)((g.M + bm - 1) / bm) * ((g.N + bn - 1) / bn) * g.Z; };
+    int shape = 3;
+    if (ctas(64, 64) < 296) shape = 4;
     return g.b_kmajor ? launch_gemm_kk(g, vec2, shape, s) : launch_gemm_nk(g, vec2, shape, s);
 }
 
@@ -47,11 +52,12 @@ constexpr double kTheta13 = 5.371920351148152;
 
 // One CTA per matrix.  1-norm exactly as dense.hpp:133-141 (column sums accumulated in row order
 // over the entries of scale*base as dense.hpp:77-82 rounds them).
-__global__ void k_expm_prep(int n, const double* __restrict__ base, long long base_stride, double op_scale,
-                            const double* __restrict__ scale, double* __restrict__ X, int* __restrict__ s_out) {
+__global__ void k_expm_prep(int n, const double* __restrict__ base, long long base_stride,
+                            const long long* __restrict__ base_off, double op_scale, const double* __restrict__ scale,
+                            double* __restrict__ X, int* __restrict__ s_out) {
     const int z = blockIdx.x;
     const double c = scale ? scale[z] : 1.0;
-    const double* a = base + z * base_stride;
+    const double* a = base + (base_off ? base_off[z] : z * base_stride);
     double* x = X + (long long)z * n * n;
     __shared__ double red[32];
     __shared__ int s_sh;
@@ -79,10 +85,10 @@ __global__ void k_expm_prep(int n, const double* __restrict__ base, long long ba
         x[e] = __dmul_rn(f, __dmul_rn(c, __dmul_rn(op_scale, a[e])));
 }
 
-void launch_expm_prep(int n, int count, const double* base, long long base_stride, double op_scale,
-                      const double* scale, double* X, int* s_out, cudaStream_t s) {
+void launch_expm_prep(int n, int count, const double* base, long long base_stride, const long long* base_off,
+                      double op_scale, const double* scale, double* X, int* s_out, cudaStream_t s) {
     const int thr = n >= 256 ? 256 : (n >= 64 ? 128 : 32);
-    k_expm_prep<<<count, thr, 0, s>>>(n, base, base_stride, op_scale, scale, X, s_out);
+    k_expm_prep<<<count, thr, 0, s>>>(n, base, base_stride, base_off, op_scale, scale, X, s_out);
 }
 
 __global__ void k_scale_copy(long long total, double op_scale, const double* __restrict__ a, double* __restrict__ out) {
@@ -250,9 +256,240 @@ __global__ void __launch_bounds__(1024) k_lu_solve(int n, double* __restrict__ P
     }
 }
 
+// Shared-memory variant for n <= 128: CTA (z, slice) holds all of P and a `w`-column slice of Q
+// in shared memory (P eliminated redundantly per slice), 8 threads per row, 3 barriers per pivot.
+// The multipliers are recomputed per row (f = a_ik / a_kk, exactly the reference's rounding) and
+// never stored, since the right-hand sides are eliminated alongside.
+constexpr int kLuTR = 8;  // threads per row
+
+__global__ void __launch_bounds__(1024) k_lu_smem(int n, int w, int slices, const double* __restrict__ Pg,
+                                                  double* __restrict__ Qg, int* __restrict__ err) {
+    extern __shared__ __align__(16) double sh[];
+    const int z = blockIdx.x / slices, sl = blockIdx.x % slices;
+    const int c0 = sl * w, wc = min(w, n - c0);  // this CTA's Q columns [c0, c0 + wc)
+    const int ld = n + w + 8;                    // padded row: P | Q slice
+    const double* P = Pg + (long long)z * n * n;
+    double* Q = Qg + (long long)z * n * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < n * n; e += nt) sh[(e / n) * ld + e % n] = P[e];
+    for (int e = tid; e < n * wc; e += nt) sh[(e / wc) * ld + n + e % wc] = Q[(long long)(e / wc) * n + c0 + e % wc];
+    __shared__ int piv_sh;
+    __syncthreads();
+    const int row = tid / kLuTR, lane8 = tid % kLuTR;
+    const int width = n + wc;
+    for (int k = 0; k < n; ++k) {
+        if (tid < 32) {  // warp 0: first maximal |a_ik|, i >= k
+            double best = -1.0;
+            int bi = n;
+            for (int i = k + tid; i < n; i += 32) {
+                const double v = fabs(sh[i * ld + k]);
+                if (v > best) {
+                    best = v;
+                    bi = i;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ov > best || (ov == best && oi < bi)) {
+                    best = ov;
+                    bi = oi;
+                }
+            }
+            if (tid == 0) {
+                if (best == 0.0) {
+                    atomicExch(err, 1);
+                    bi = -1;
+                }
+                piv_sh = bi;
+            }
+        }
+        __syncthreads();
+        const int piv = piv_sh;
+        if (piv < 0) return;
+        if (piv != k && row == k) {
+            for (int j = lane8; j < width; j += kLuTR) {
+                const double t = sh[k * ld + j];
+                sh[k * ld + j] = sh[piv * ld + j];
+                sh[piv * ld + j] = t;
+            }
+        }
+        __syncthreads();
+        if (row > k && row < n) {
+            const double f = sh[row * ld + k] / sh[k * ld + k];
+            if (f != 0.0)
+                for (int j = k + 1 + lane8; j < width; j += kLuTR)
+                    sh[row * ld + j] = __dsub_rn(sh[row * ld + j], __dmul_rn(f, sh[k * ld + j]));
+        }
+        __syncthreads();
+    }
+    for (int k = n - 1; k >= 0; --k) {
+        if (row == k) {
+            const double akk = sh[k * ld + k];
+            for (int j = n + lane8; j < width; j += kLuTR) sh[k * ld + j] = sh[k * ld + j] / akk;
+        }
+        __syncthreads();
+        if (row < k) {
+            const double aik = sh[row * ld + k];
+            if (aik != 0.0)
+                for (int j = n + lane8; j < width; j += kLuTR)
+                    sh[row * ld + j] = __dsub_rn(sh[row * ld + j], __dmul_rn(aik, sh[k * ld + j]));
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < n * wc; e += nt) Q[(long long)(e / wc) * n + c0 + e % wc] = sh[(e / wc) * ld + n + e % wc];
+}
+
+// --- factor-then-solve path for n <= 128 -------------------------------------------------
+// (1) k_lu_factor: one CTA per matrix factors P = L U with partial pivoting entirely in shared
+//     memory (the reference's elimination, dense.hpp:156-173, on P only), writes L\U back over P
+//     and the pivot rows to piv[z][k].
+// (2) k_lu_trsm: CTA (z, 32-column slice of Q) applies the row swaps and the forward elimination
+//     in the reference's per-element order (b_ij -= f_ik b_kj, k ascending), then a
+//     column-oriented back substitution, Q slice staged in shared memory.
+__global__ void __launch_bounds__(1024) k_lu_factor(int n, double* __restrict__ Pg, int* __restrict__ piv,
+                                                    int* __restrict__ err) {
+    extern __shared__ __align__(16) double sh[];
+    const int ld = n + 1;  // odd stride: column reads (pivot search) spread over the banks
+    double* P = Pg + (long long)blockIdx.x * n * n;
+    int* pv = piv + (long long)blockIdx.x * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < n * n; e += nt) sh[(e / n) * ld + e % n] = P[e];
+    __shared__ int piv_sh;
+    __syncthreads();
+    const int row = tid / kLuTR, lane8 = tid % kLuTR;
+    for (int k = 0; k < n; ++k) {
+        if (tid < 32) {
+            double best = -1.0;
+            int bi = n;
+            for (int i = k + tid; i < n; i += 32) {
+                const double v = fabs(sh[i * ld + k]);
+                if (v > best) {
+                    best = v;
+                    bi = i;
+                }
+            }
+            for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ov > best || (ov == best && oi < bi)) {
+                    best = ov;
+                    bi = oi;
+                }
+            }
+            if (tid == 0) {
+                if (best == 0.0) {
+                    atomicExch(err, 1);
+                    bi = -1;
+                }
+                piv_sh = bi;
+                pv[k] = bi;
+            }
+        }
+        __syncthreads();
+        const int p = piv_sh;
+        if (p < 0) return;
+        if (p != k)
+            for (int j = tid; j < n; j += nt) {
+                const double t = sh[k * ld + j];
+                sh[k * ld + j] = sh[p * ld + j];
+                sh[p * ld + j] = t;
+            }
+        __syncthreads();
+        if (row > k && row < n) {
+            const double aik = sh[row * ld + k];
+            const double f = aik / sh[k * ld + k];
+            __syncwarp(0xFFu << (tid & 24));  // the row's 8 lanes have read a_ik
+            if (lane8 == 0) sh[row * ld + k] = f;  // L entry (0 when the reference skips the row)
+            if (f != 0.0)
+                for (int j = k + 1 + lane8; j < n; j += kLuTR)
+                    sh[row * ld + j] = __dsub_rn(sh[row * ld + j], __dmul_rn(f, sh[k * ld + j]));
+        }
+        __syncthreads();
+    }
+    for (int e = tid; e < n * n; e += nt) P[e] = sh[(e / n) * ld + e % n];
+}
+
+constexpr int kTrsmW = 32;  // RHS columns per CTA
+
+__global__ void __launch_bounds__(256) k_lu_trsm(int n, const double* __restrict__ LUg, const int* __restrict__ piv,
+                                                 double* __restrict__ Qg, int slices) {
+    extern __shared__ __align__(16) double sb[];  // n x kTrsmW slice of Q
+    __shared__ double colk[128];
+    const int z = blockIdx.x / slices, sl = blockIdx.x % slices;
+    const int c0 = sl * kTrsmW, wc = min(kTrsmW, n - c0);
+    const double* LU = LUg + (long long)z * n * n;
+    const int* pv = piv + (long long)z * n;
+    double* Q = Qg + (long long)z * n * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < n * kTrsmW; e += nt) {
+        const int i = e / kTrsmW, j = e % kTrsmW;
+        sb[e] = j < wc ? Q[(long long)i * n + c0 + j] : 0.0;
+    }
+    __syncthreads();
+    const int j = tid % kTrsmW, rg = tid / kTrsmW, nrg = nt / kTrsmW;  // column j, row group
+    // forward: at step k swap rows k <-> piv[k], then b_ij -= l_ik b_kj for i > k
+    for (int k = 0; k < n; ++k) {
+        const int p = pv[k];
+        if (p != k && rg == 0) {
+            const double t = sb[k * kTrsmW + j];
+            sb[k * kTrsmW + j] = sb[p * kTrsmW + j];
+            sb[p * kTrsmW + j] = t;
+        }
+        for (int i = k + 1 + tid; i < n; i += nt) colk[i] = LU[(long long)i * n + k];
+        __syncthreads();
+        const double bk = sb[k * kTrsmW + j];
+        for (int i = k + 1 + rg; i < n; i += nrg) {
+            const double f = colk[i];
+            if (f != 0.0) sb[i * kTrsmW + j] = __dsub_rn(sb[i * kTrsmW + j], __dmul_rn(f, bk));
+        }
+        __syncthreads();
+    }
+    // back substitution, column oriented: x_k = b_k / u_kk ; b_i -= u_ik x_k (i < k)
+    for (int k = n - 1; k >= 0; --k) {
+        for (int i = tid; i <= k; i += nt) colk[i] = LU[(long long)i * n + k];
+        __syncthreads();
+        const double xk = sb[k * kTrsmW + j] / colk[k];
+        for (int i = rg; i < k; i += nrg) sb[i * kTrsmW + j] = __dsub_rn(sb[i * kTrsmW + j], __dmul_rn(colk[i], xk));
+        __syncthreads();
+        if (rg == 0) sb[k * kTrsmW + j] = xk;
+    }
+    __syncthreads();
+    for (int e = tid; e < n * kTrsmW; e += nt) {
+        const int i = e / kTrsmW, jj = e % kTrsmW;
+        if (jj < wc) Q[(long long)i * n + c0 + jj] = sb[e];
+    }
+}
+
+void launch_lu_factor_solve(int n, int count, double* P, double* Q, int* piv, int* err, cudaStream_t s) {
+    const int smem = n * (n + 1) * 8;
+    static int attr = 0;
+    if (smem > attr) {
+        cudaFuncSetAttribute(k_lu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = 200 * 1024;
+    }
+    const int thr = ((n * kLuTR + 31) / 32) * 32;
+    k_lu_factor<<<count, thr, smem, s>>>(n, P, piv, err);
+    const int slices = (n + kTrsmW - 1) / kTrsmW;
+    k_lu_trsm<<<count * slices, 256, n * kTrsmW * 8, s>>>(n, P, piv, Q, slices);
+}
+
 void launch_lu_solve(int n, int count, double* P, double* Q, int* err, cudaStream_t s) {
-    const int thr = n >= 128 ? 1024 : (n >= 32 ? 256 : 64);
-    k_lu_solve<<<count, thr, 0, s>>>(n, P, Q, err);
+    if (n <= 128) {
+        int slices = 1;
+        while ((long long)n * (n + (n + slices - 1) / slices + 8) * 8 > 220 * 1024) ++slices;
+        const int w = (n + slices - 1) / slices;
+        const int smem = n * (n + w + 8) * 8;
+        static int attr = 0;  // opt-in size already granted
+        if (smem > attr) {
+            cudaFuncSetAttribute(k_lu_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+            attr = 220 * 1024;
+        }
+        const int thr = ((n * kLuTR + 31) / 32) * 32;
+        k_lu_smem<<<count * slices, thr, smem, s>>>(n, w, slices, P, Q, err);
+        return;
+    }
+    k_lu_solve<<<count, 1024, 0, s>>>(n, P, Q, err);
 }
 
 __global__ void k_imax(const int* v, int count, int* out) {
@@ -293,6 +530,54 @@ __global__ void k_combine(long long N, int q, const double* __restrict__ V, long
         }
 #pragma unroll
         for (int j = 0; j < P; ++j) acc[j * acc_stride + t] = y[j];
+    }
+}
+
+// Doubling combination of one squaring step (phiaction.hpp:260-268), in place over T:
+//   T_i <- 2^-i T_i + sum_{j<=i} (2^-i / (i-j)!) Y_j     (= 2^-i (E y_i + sum_j y_j/(i-j)!))
+// for every RHS m (columns [m][i][N]); each element of Y_1..Y_p and T_1..T_p read once.
+template <int P>
+__global__ void k_sq_combine(long long N, int nb, double* __restrict__ T, const double* __restrict__ Y,
+                             const double* __restrict__ coef) {
+    const long long total = N * nb;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const long long m = e / N, t = e - m * N;
+        const long long base = m * P * N + t;
+        double y[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) y[j] = Y[base + j * N];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            double v = __dmul_rn(ldexp(1.0, -(i + 1)), T[base + i * N]);
+#pragma unroll
+            for (int j = 0; j <= i; ++j) v = __dadd_rn(v, __dmul_rn(coef[i * P + j], y[j]));
+            T[base + i * N] = v;
+        }
+    }
+}
+
+__global__ void k_sq_combine_any(long long N, int p, int nb, double* __restrict__ T, const double* __restrict__ Y,
+                                 const double* __restrict__ coef) {
+    const long long total = N * nb;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const long long m = e / N, t = e - m * N;
+        const long long base = m * p * N + t;
+        for (int i = 0; i < p; ++i) {
+            double v = __dmul_rn(ldexp(1.0, -(i + 1)), T[base + i * N]);
+            for (int j = 0; j <= i; ++j) v = __dadd_rn(v, __dmul_rn(coef[i * p + j], Y[base + j * N]));
+            T[base + i * N] = v;
+        }
+    }
+}
+
+void launch_sq_combine(long long N, int p, int nb, double* T, const double* Y, const double* coef, cudaStream_t s) {
+    const unsigned grid = grid_for(N * nb, 256);
+    switch (p) {
+#define PQ_SQC(PP) \
+    case PP: k_sq_combine<PP><<<grid, 256, 0, s>>>(N, nb, T, Y, coef); break;
+        PQ_SQC(1) PQ_SQC(2) PQ_SQC(3) PQ_SQC(4) PQ_SQC(5) PQ_SQC(6) PQ_SQC(7) PQ_SQC(8)
+#undef PQ_SQC
+        default: k_sq_combine_any<<<grid, 256, 0, s>>>(N, p, nb, T, Y, coef);
     }
 }
 

@@ -39,8 +39,9 @@ int launch_gemm(const GemmArgs& g, cudaStream_t s);  // returns number of kernel
 // ---- batched Pade-13 expm building blocks (dense.hpp:194-228) ----
 // X[z] = (scale[z] * (op_scale * base)) * 2^-s_z  (each product rounded, as the reference's
 // KroneckerSum::scaled then DenseMatrix scaled), s_z from the 1-norm of the rounded argument.
-void launch_expm_prep(int n, int count, const double* base, long long base_stride, double op_scale,
-                      const double* scale, double* X, int* s_out, cudaStream_t s);
+// base_off (device, nullable) gives each batch entry its own base matrix offset.
+void launch_expm_prep(int n, int count, const double* base, long long base_stride, const long long* base_off,
+                      double op_scale, const double* scale, double* X, int* s_out, cudaStream_t s);
 // out = op_scale * a (elementwise, rounded once)
 void launch_scale_copy(long long total, double op_scale, const double* a, double* out, cudaStream_t s);
 void launch_pade_mid(int n, int count, const double* A2, const double* A4, const double* A6, double* T1,
@@ -50,6 +51,9 @@ void launch_pade_fin(int n, int count, const double* W, const double* Z, const d
 void launch_pade_pq(long long total, const double* V, const double* U, double* P, double* Q, cudaStream_t s);
 // Solves P X = Q in place (X -> Q) with partial pivoting, one CTA per matrix; err[0] = 1 on a zero pivot.
 void launch_lu_solve(int n, int count, double* P, double* Q, int* err, cudaStream_t s);
+// n <= 128: shared-memory factorisation of P (L\U over P, pivots in piv[count*n]) + a batched
+// triangular solve of Q over 32-column slices.  Q <- P^{-1} Q.
+void launch_lu_factor_solve(int n, int count, double* P, double* Q, int* piv, int* err, cudaStream_t s);
 // max over z of s_z -> *out (device int)
 void launch_imax(const int* v, int count, int* out, cudaStream_t s);
 
@@ -58,6 +62,9 @@ void launch_imax(const int* v, int count, int* out, cudaStream_t s);
 // (exact reference order: separate multiply and add per node, phiaction.hpp:96-111).
 void launch_combine(long long N, int p, int q, const double* V, long long vstride, const int* slots,
                     const double* coef, double* acc, long long acc_stride, int zero, cudaStream_t s);
+// In-place doubling combination of a squaring step: T_i <- 2^-i T_i + sum_{j<=i} coef[i*p+j] Y_j
+// (coef[i][j] = 2^-(i+1)/(i-j)!), columns laid out [nb][p][N].
+void launch_sq_combine(long long N, int p, int nb, double* T, const double* Y, const double* coef, cudaStream_t s);
 // per column c < ncols: out[2c] = max|y_c - yp_c| (yp may be null -> max|y_c|), out[2c+1] = max|y_c|.
 void launch_colstats(long long N, int ncols, const double* y, const double* yp, double* out, cudaStream_t s);
 // out = s1*u + s3*u^3 - au   (Allen-Cahn source minus A u)

@@ -67,6 +67,15 @@ class Context:
     def synchronize(self) -> None:
         check(lib.pq_ctx_synchronize(self.handle))
 
+    def set_profiling(self, on: bool) -> None:
+        check(lib.pq_ctx_set_profiling(self.handle, 1 if on else 0))
+
+    def gemm_stats(self, reset: bool = True) -> tuple:
+        """(launches, device ms, algorithmic FLOPs) of the DMMA GEMM launches recorded while profiling."""
+        n, ms, fl = C.c_uint64(), C.c_double(), C.c_double()
+        check(lib.pq_ctx_gemm_stats(self.handle, 1 if reset else 0, C.byref(n), C.byref(ms), C.byref(fl)))
+        return int(n.value), ms.value, fl.value
+
     def set_workspace_limit(self, nbytes: int) -> None:
         check(lib.pq_ctx_set_workspace_limit(self.handle, nbytes))
 

@@ -1,0 +1,123 @@
+// Tile-configuration sweep for the FP64 DMMA mode-product GEMM (gemm.cuh) on the exact shapes of
+// the phi pipeline at n = 128 (config 2) and n = 256 / 512 (configs 3 / 5).
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2211_00696_b200/csrc \
+//          -o tools/gemm_tune tools/gemm_tune.cu
+#include <cstdio>
+#include <vector>
+
+#include "gemm.cuh"
+
+using namespace pqb;
+
+#define CK(x)                                                                      \
+    do {                                                                           \
+        cudaError_t e = (x);                                                       \
+        if (e != cudaSuccess) {                                                    \
+            printf("CUDA %s @%d\n", cudaGetErrorString(e), __LINE__);              \
+            return 1;                                                              \
+        }                                                                          \
+    } while (0)
+
+struct Case {
+    const char* name;
+    GemmArgs g;
+    double flops;
+};
+
+template <int BM, int BN, int BK, int WM, int WN, int ST>
+float run(const Case& c, int reps, cudaEvent_t e0, cudaEvent_t e1) {
+    GemmArgs g = c.g;
+    auto f = [&] {
+        if (g.b_kmajor) launch_cfg<BM, BN, BK, WM, WN, ST, true, 2>(g, 0);
+        else launch_cfg<BM, BN, BK, WM, WN, ST, false, 2>(g, 0);
+    };
+    f();
+    cudaDeviceSynchronize();
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) f();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+        printf("  launch error %s\n", cudaGetErrorString(err));
+        return -1;
+    }
+    return ms / reps;
+}
+
+int main(int argc, char** argv) {
+    const int n = argc > 1 ? atoi(argv[1]) : 128;
+    const int Z = argc > 2 ? atoi(argv[2]) : 12;  // nodes (or columns)
+    const long long N = (long long)n * n * n;
+    double *X, *Y, *E, *EXT;
+    CK(cudaMalloc(&X, sizeof(double) * N * Z));
+    CK(cudaMalloc(&Y, sizeof(double) * N * Z));
+    CK(cudaMalloc(&EXT, sizeof(double) * N * Z));
+    CK(cudaMalloc(&E, sizeof(double) * n * n * Z));
+    cudaMemset(X, 0, sizeof(double) * N * Z);
+    cudaMemset(E, 0, sizeof(double) * n * n * Z);
+    cudaMemset(EXT, 0, sizeof(double) * N * Z);
+    double *coef, *alpha;
+    int* nterms;
+    CK(cudaMalloc(&coef, 64 * 64 * 8));
+    CK(cudaMalloc(&alpha, 64 * 8));
+    CK(cudaMalloc(&nterms, 64 * 4));
+    std::vector<int> hn(64);
+    for (int i = 0; i < 64; ++i) hn[i] = 1 + i % 4;
+    cudaMemcpy(nterms, hn.data(), 64 * 4, cudaMemcpyHostToDevice);
+    cudaMemset(coef, 0, 64 * 64 * 8);
+    cudaMemset(alpha, 0, 64 * 8);
+    const double fl = 2.0 * N * n * Z;
+    std::vector<Case> cases;
+    {  // mode 0, stacked nodes: (Z n x n) . (n x n^2)
+        GemmArgs g;
+        g.A = E; g.lda = n; g.B = X; g.ldb = (long long)n * n; g.C = Y; g.ldc = (long long)n * n;
+        g.M = Z * n; g.N = n * n; g.K = n; g.Z = 1;
+        cases.push_back({"mode0", g, fl});
+    }
+    {  // mode 1: batch (Z * n) of (n x n) . (n x n)
+        GemmArgs g;
+        g.A = E; g.lda = n; g.B = X; g.ldb = n; g.C = Y; g.ldc = n;
+        g.M = n; g.N = n; g.K = n; g.Z = Z * n; g.zdiv = n;
+        g.sA1 = (long long)n * n; g.sB1 = N; g.sB2 = (long long)n * n; g.sC1 = N; g.sC2 = (long long)n * n;
+        cases.push_back({"mode1", g, fl});
+    }
+    {  // mode 2 (last): X (n^2 x n) . E^T, batch Z
+        GemmArgs g;
+        g.A = X; g.lda = n; g.B = E; g.b_kmajor = 1; g.ldb = n; g.C = Y; g.ldc = n;
+        g.M = n * n; g.N = n; g.K = n; g.Z = Z;
+        g.sA1 = N; g.sB1 = (long long)n * n; g.sC1 = N;
+        cases.push_back({"mode2", g, fl});
+    }
+    {  // mode 2 + squaring epilogue (p = 4 groups: 1..4 extra addends)
+        GemmArgs g = cases.back().g;
+        g.sB1 = 0;
+        g.alpha_z = alpha; g.ext = EXT; g.ext_s = N; g.ext_group = 4; g.coef = coef; g.cld = 4; g.nterms = nterms;
+        cases.push_back({"mode2+sq", g, fl});
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (const Case& c : cases) {
+        printf("%-9s n=%d Z=%d  GFLOP=%.2f\n", c.name, n, Z, c.flops / 1e9);
+#define T(BM, BN, BK, WM, WN, ST)                                                                      \
+    {                                                                                                  \
+        float ms = run<BM, BN, BK, WM, WN, ST>(c, 5, e0, e1);                                          \
+        if (ms > 0)                                                                                    \
+            printf("  %3dx%3dx%2d w%2dx%2d st%d : %8.1f us  %6.2f TF/s\n", BM, BN, BK, WM, WN, ST, ms * 1e3, \
+                   c.flops / (ms * 1e-3) / 1e12);                                                      \
+    }
+        T(128, 128, 32, 64, 32, 3)
+        T(128, 128, 16, 64, 32, 4)
+        T(128, 128, 16, 32, 64, 4)
+        T(128, 64, 16, 64, 32, 3)
+        T(128, 64, 32, 64, 32, 2)
+        T(128, 64, 16, 32, 32, 3)
+        T(64, 128, 16, 32, 64, 3)
+        T(64, 64, 16, 32, 32, 3)
+        T(64, 64, 32, 32, 32, 3)
+    }
+    return 0;
+}
