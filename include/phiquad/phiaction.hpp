@@ -1,0 +1,192 @@
+#pragma once
+// The phi engine (reference phiaction.hpp:20-389) on the B200.  Same types and signatures; the
+// node sweep, combine, modified squaring and phi_0 run as sm_100a kernels behind pq_*.  `threads`
+// is accepted and ignored: results are bitwise independent of it, as in the reference.
+#include <optional>
+#include <stdexcept>
+#include <vector>
+
+#include "phiquad/b200.hpp"
+#include "phiquad/bounds.hpp"
+#include "phiquad/dense.hpp"
+#include "phiquad/kron.hpp"
+#include "phiquad/quadrature.hpp"
+#include "phiquad/util.hpp"
+
+namespace phiquad {
+
+struct PhiColumns {
+    int dim = 0;
+    std::vector<std::vector<double>> cols;
+    int p() const { return static_cast<int>(cols.size()); }
+    const std::vector<double>& col(int j) const {
+        if (j < 1 || j > p()) throw std::out_of_range("PhiColumns::col: index out of range");
+        return cols[static_cast<size_t>(j - 1)];
+    }
+};
+
+struct PhiRequest {
+    int p = 1;
+    double eps = 1e-14;
+    QuadKind mode = QuadKind::gauss_legendre;
+    std::optional<int> l;
+    CostModel cost;
+    int threads = 1;
+};
+
+struct PhiInfo {
+    int l = 0;
+    int n = 0;
+    int points = 0;
+    QuadKind mode = QuadKind::gauss_legendre;
+    double alpha = 0.0;
+    double beta = 0.0;
+    bool planned = false;
+    double plan_cost = 0.0;
+};
+
+namespace detail {
+
+inline std::vector<double> gather(const std::vector<std::vector<double>>& bs, int dim, const char* who) {
+    std::vector<double> flat;
+    flat.reserve(bs.size() * static_cast<size_t>(dim));
+    for (const auto& b : bs) {
+        if (static_cast<int>(b.size()) != dim) throw std::invalid_argument(std::string(who) + ": vector length mismatch");
+        flat.insert(flat.end(), b.begin(), b.end());
+    }
+    return flat;
+}
+
+inline std::vector<PhiColumns> scatter(const std::vector<double>& flat, int nb, int p, int dim) {
+    std::vector<PhiColumns> out(static_cast<size_t>(nb));
+    for (int m = 0; m < nb; ++m) {
+        out[static_cast<size_t>(m)].dim = dim;
+        for (int j = 0; j < p; ++j) {
+            const auto* s = flat.data() + (static_cast<size_t>(m) * p + j) * dim;
+            out[static_cast<size_t>(m)].cols.emplace_back(s, s + dim);
+        }
+    }
+    return out;
+}
+
+inline pq_phi_request abi_request(const PhiRequest& r) {
+    pq_phi_request c{};
+    c.p = r.p;
+    c.eps = r.eps;
+    c.mode = abi_kind(r.mode);
+    c.has_l = r.l.has_value() ? 1 : 0;
+    c.l = r.l.value_or(0);
+    c.c1 = r.cost.c1;
+    c.c2 = r.cost.c2;
+    c.threads = r.threads;
+    return c;
+}
+
+}  // namespace detail
+
+inline std::vector<PhiColumns> phi_fixed_multi(const KroneckerSum& a, const std::vector<std::vector<double>>& bs, int p,
+                                               const QuadratureRule& rule, int threads = 1) {
+    (void)threads;
+    if (p < 1) throw std::invalid_argument("phi_fixed: need p >= 1");
+    const int dim = a.dim();
+    const auto flat = detail::gather(bs, dim, "phi_fixed");
+    const auto f = detail::flatten(a);
+    std::vector<double> out(bs.size() * static_cast<size_t>(p) * dim);
+    b200::check(pq_phi_fixed(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
+                             flat.data(), p, rule.points(), rule.nodes.data(), rule.weights.data(), out.data(), PQ_HOST));
+    return detail::scatter(out, static_cast<int>(bs.size()), p, dim);
+}
+
+inline PhiColumns phi_fixed(const KroneckerSum& a, const std::vector<double>& b, int p, const QuadratureRule& rule,
+                            int threads = 1) {
+    return std::move(phi_fixed_multi(a, {b}, p, rule, threads).front());
+}
+
+inline std::vector<PhiColumns> phi_adaptive_multi(const KroneckerSum& a, const std::vector<std::vector<double>>& bs,
+                                                  int p, double eps, int threads = 1, int* points_used = nullptr) {
+    (void)threads;
+    if (p < 1) throw std::invalid_argument("phi_adaptive: need p >= 1");
+    if (!(eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
+    const int dim = a.dim();
+    const auto flat = detail::gather(bs, dim, "phi_adaptive");
+    const auto f = detail::flatten(a);
+    std::vector<double> out(bs.size() * static_cast<size_t>(p) * dim);
+    int pts = 0;
+    b200::check(pq_phi_adaptive(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
+                                flat.data(), p, eps, out.data(), &pts, PQ_HOST));
+    if (points_used) *points_used = pts;
+    return detail::scatter(out, static_cast<int>(bs.size()), p, dim);
+}
+
+inline PhiColumns phi_adaptive(const KroneckerSum& a, const std::vector<double>& b, int p, double eps, int threads = 1,
+                               int* points_used = nullptr) {
+    return std::move(phi_adaptive_multi(a, {b}, p, eps, threads, points_used).front());
+}
+
+/// phi_i(2A) b = 2^-i (e^A phi_i(A) b + sum_{j<=i} phi_j(A) b/(i-j)!), in place.
+inline void squaring_step(PhiColumns& y, const std::vector<DenseMatrix>& exps, const std::vector<int>& shape) {
+    const int p = y.p();
+    if (p == 0) return;
+    const auto f = detail::flatten(exps);
+    if (f.shape != shape) throw std::invalid_argument("mode_apply: factor extent mismatch");
+    const int dim = static_cast<int>(detail::shape_product(shape));
+    auto flat = detail::gather(y.cols, dim, "mode_apply");
+    b200::check(pq_squaring_step(b200::context(), static_cast<int>(shape.size()), shape.data(), f.data.data(), p,
+                                 flat.data(), PQ_HOST));
+    y.cols = detail::scatter(flat, 1, p, dim).front().cols;
+}
+
+inline std::vector<PhiColumns> phi_with_plan(const KroneckerSum& a, const std::vector<std::vector<double>>& bs, int p,
+                                             int l, int n, QuadKind mode, double eps, int threads = 1,
+                                             int* points_used = nullptr) {
+    (void)threads;
+    if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
+    const int dim = a.dim();
+    const auto flat = detail::gather(bs, dim, mode == QuadKind::gauss_legendre ? "phi_fixed" : "phi_adaptive");
+    const auto f = detail::flatten(a);
+    std::vector<double> out(bs.size() * static_cast<size_t>(std::max(p, 0)) * dim);
+    int pts = 0;
+    b200::check(pq_phi_with_plan(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
+                                 flat.data(), p, l, n, abi_kind(mode), eps, out.data(), &pts, PQ_HOST));
+    if (points_used) *points_used = pts;
+    return detail::scatter(out, static_cast<int>(bs.size()), p, dim);
+}
+
+inline std::vector<PhiColumns> phiquadmv_multi(const KroneckerSum& a, const std::vector<std::vector<double>>& bs,
+                                               const PhiRequest& req, PhiInfo* info = nullptr) {
+    if (req.p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
+    const int dim = a.dim();
+    const auto flat = detail::gather(bs, dim, "phiquadmv");
+    const auto f = detail::flatten(a);
+    const pq_phi_request r = detail::abi_request(req);
+    pq_phi_info pi{};
+    std::vector<double> out(bs.size() * static_cast<size_t>(req.p) * dim);
+    b200::check(pq_phiquadmv(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
+                             flat.data(), &r, out.data(), &pi, PQ_HOST));
+    if (info)
+        *info = PhiInfo{pi.l,     pi.n,    pi.points,          pi.mode == PQ_GAUSS_LEGENDRE ? QuadKind::gauss_legendre
+                                                                                         : QuadKind::clenshaw_curtis,
+                        pi.alpha, pi.beta, pi.planned != 0, pi.plan_cost};
+    return detail::scatter(out, static_cast<int>(bs.size()), req.p, dim);
+}
+
+inline PhiColumns phiquadmv(const KroneckerSum& a, const std::vector<double>& b, const PhiRequest& req,
+                            PhiInfo* info = nullptr) {
+    return std::move(phiquadmv_multi(a, {b}, req, info).front());
+}
+
+/// sum_j phi_j(A) b_j in one quadrature sweep (no scaling/squaring).
+inline std::vector<double> phi_lincomb(const KroneckerSum& a, const std::vector<std::vector<double>>& bs,
+                                       const QuadratureRule& rule, int threads = 1) {
+    (void)threads;
+    if (bs.empty()) throw std::invalid_argument("phi_lincomb: need at least one vector");
+    const int dim = a.dim();
+    const auto flat = detail::gather(bs, dim, "phi_lincomb");
+    const auto f = detail::flatten(a);
+    std::vector<double> y(static_cast<size_t>(dim));
+    b200::check(pq_phi_lincomb(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
+                               flat.data(), rule.points(), rule.nodes.data(), rule.weights.data(), y.data(), PQ_HOST));
+    return y;
+}
+
+}  // namespace phiquad

@@ -116,8 +116,9 @@ void source_minus(pq_ctx& c, Source& src, double t, const double* u, const doubl
             src.hf.assign(static_cast<size_t>(N), 0.0);
             cuda_check(cudaMemcpyAsync(src.hu.data(), u, N * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "D2H u");
             cuda_check(cudaStreamSynchronize(c.stream), "callback sync");
-            if (src.s.cb(t, src.hu.data(), src.hf.data(), N, src.s.user) != 0)
-                throw std::runtime_error("erk_step: source callback failed");
+            const int rc = src.s.cb(t, src.hu.data(), src.hf.data(), N, src.s.user);
+            if (rc == 2) throw std::invalid_argument("erk_step: source length mismatch");
+            if (rc != 0) throw std::runtime_error("erk_step: source callback failed");
             double* fd = ws(c, "etd_f", static_cast<size_t>(N));
             cuda_check(cudaMemcpyAsync(fd, src.hf.data(), N * sizeof(double), cudaMemcpyHostToDevice, c.stream), "H2D f");
             cuda_check(cudaStreamSynchronize(c.stream), "callback sync");

@@ -1,0 +1,50 @@
+"""Drop-in check: tests/cpp/dropin_check.cpp, written against the reference's C++ API, compiled
+against this repo's include/phiquad + libpq_b200.so and run on the B200; its output must match the
+output of the same source compiled against the reference headers (tests/golden/
+dropin_ref_output.txt): integers exactly, values to 1e-11 relative 2-norm per named vector."""
+import re
+import subprocess
+from collections import defaultdict
+from pathlib import Path
+
+import numpy as np
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+
+
+def parse(text):
+    vals = defaultdict(dict)
+    for line in text.splitlines():
+        key, v = line.rsplit(" ", 1)
+        m = re.match(r"(.*)\[(\d+)\]$", key)
+        if m:
+            vals[m.group(1)][int(m.group(2))] = float(v)
+        else:
+            vals[key][0] = float(v)
+    return {k: np.array([d[i] for i in sorted(d)]) for k, d in vals.items()}
+
+
+def test_dropin_header_builds():
+    r = subprocess.run(["make", "-s", "-C", str(ROOT / "tests" / "cpp"), "_bin/dropin_b200"], capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+def test_dropin_matches_reference_build():
+    test_dropin_header_builds()
+    out = subprocess.run([str(ROOT / "tests" / "cpp" / "_bin" / "dropin_b200")], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr
+    got = parse(out.stdout)
+    want = parse((ROOT / "tests" / "golden" / "dropin_ref_output.txt").read_text())
+    assert set(got) == set(want)
+    for k, w in want.items():
+        g = got[k]
+        assert g.shape == w.shape, k
+        if w.size == 1 and float(w[0]).is_integer() and not k.startswith(("gl5", "cc9", "quaderr", "infnorm")):
+            assert g[0] == w[0], k  # plans, point counts, call counts, error codes
+        else:
+            den = max(np.linalg.norm(w), 1e-300)
+            assert np.linalg.norm(g - w) / den <= 1e-11, (k, np.linalg.norm(g - w) / den)
