@@ -1,0 +1,68 @@
+"""Multi-GPU phi actions, one process per GPU (torch.distributed for the plumbing).
+
+Two independent ways the path shards:
+
+* right-hand sides: every rank evaluates its own b's end to end -- no data-path collective
+  (bench.py's default N-GPU mode, weak scaling);
+* quadrature nodes (Gauss rule): rank r sweeps nodes i with i % world == r on its GPU
+  (pq_phi_nodes_partial: node exponentials, mode products, weighted partial sums in ascending
+  node order), the partial sums are combined with ONE all-reduce (NCCL over NVLink on B200s),
+  then every rank runs the l modified-squaring steps (pq_squaring_chain).  The squaring is
+  sequential in the step index and is replicated, not sharded.
+
+Parity: summing the partials changes only the association of the node sum, so results match
+phi_with_plan to rounding (tests/test_sharded.py pins the host logic with world size 2 on gloo).
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Callable, Optional
+
+import numpy as np
+
+from . import _lib as L
+from .phiquad import Context, KroneckerSum, QuadKind, cached_rule, default_context
+
+
+def node_partition(q: int, rank: int, world: int) -> list:
+    """Round-robin split of the q rule nodes (the C ABI's pq_phi_nodes_partial uses the same)."""
+    if not (0 <= rank < world):
+        raise ValueError("node_partition: bad rank/world")
+    return list(range(rank, q, world))
+
+
+def combine_partials(partials: list):
+    """Host-side statement of the reduction: the full accumulator is the sum of the ranks'."""
+    total = partials[0].copy()
+    for p in partials[1:]:
+        total = total + p
+    return total
+
+
+def phi_with_plan_sharded(a: KroneckerSum, bs, p: int, l: int, n: int, group=None, ctx: Optional[Context] = None,
+                          all_reduce: Optional[Callable] = None):
+    """Gauss-rule phi_1..phi_p of `a` on device-resident bs ([nb, N] float64 CUDA tensor), nodes
+    sharded over the ranks of `group`.  Returns [nb, p, N] on every rank."""
+    import torch
+    import torch.distributed as dist
+
+    ctx = ctx or default_context()
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    bs = bs.reshape(-1, a.dim()).contiguous()
+    nb, N = bs.shape
+    rule = cached_rule(QuadKind.gauss_legendre, n + 1)
+    x = np.ascontiguousarray(rule.nodes)
+    w = np.ascontiguousarray(rule.weights)
+    acc = torch.empty((nb, p, N), dtype=torch.float64, device=bs.device)
+    d, sh, fac = a._abi()
+    L.check(L.lib.pq_phi_nodes_partial(ctx.handle, d, sh, fac, nb, C.c_void_p(bs.data_ptr()), p, l, rule.points(),
+                                       x.ctypes.data_as(L.dp), w.ctypes.data_as(L.dp), rank, world, 1,
+                                       C.c_void_p(acc.data_ptr())))
+    if world > 1:
+        # engine stream -> collective -> engine stream, ordered by host syncs at the hand-offs
+        L.check(L.lib.pq_ctx_synchronize(ctx.handle))
+        (all_reduce or dist.all_reduce)(acc, group=group)
+        torch.cuda.current_stream().synchronize()
+    L.check(L.lib.pq_squaring_chain(ctx.handle, d, sh, fac, nb, p, l, C.c_void_p(acc.data_ptr())))
+    return acc
