@@ -197,7 +197,9 @@ def run_ours(args, world, rank, local) -> None:
     nb = 1 if args.config != 3 else w.nb
     a = pq.KroneckerSum(w.factors)
     ctx = pq.Context(local)
-    stream = torch.cuda.current_stream()
+    # one dedicated stream shared by torch (inputs, L2 flush, events) and the engine
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     req = pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode))
     N = w.N

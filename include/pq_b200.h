@@ -60,7 +60,8 @@ PQ_API const char* pq_last_error(void);
 /* context: one device, one stream, a growable device workspace --------------------------- */
 PQ_API int pq_ctx_create(int device, pq_ctx** out);
 PQ_API int pq_ctx_destroy(pq_ctx* ctx);
-/* Use an external stream (e.g. torch.cuda.current_stream().cuda_stream); NULL = own stream. */
+/* Use an external stream (e.g. torch.cuda.current_stream().cuda_stream); NULL = own stream;
+ * the legacy default stream is (void*)1 (cudaStreamLegacy), not NULL. */
 PQ_API int pq_ctx_set_stream(pq_ctx* ctx, void* cuda_stream);
 PQ_API void* pq_ctx_stream(const pq_ctx* ctx);
 PQ_API int pq_ctx_synchronize(pq_ctx* ctx);

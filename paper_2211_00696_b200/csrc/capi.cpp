@@ -133,6 +133,12 @@ int pq_ctx_destroy(pq_ctx* c) {
         cudaFree(c->d_small);
         cudaFreeHost(c->h_small);
         for (auto e : c->ev_pool) cudaEventDestroy(e);
+        if (c->side) {
+            cudaStreamSynchronize(c->side);
+            cudaStreamDestroy(c->side);
+            cudaEventDestroy(c->ev_fork);
+            cudaEventDestroy(c->ev_join);
+        }
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });

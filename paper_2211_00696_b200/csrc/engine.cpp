@@ -425,12 +425,12 @@ static GemmArgs mode_gemm(int d, const int* n, int k, const double* E, long long
 }
 
 void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride, const double* x,
-                long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep) {
+                long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep, const char* tmp_tag) {
     long long N = 1;
     for (int k = 0; k < d; ++k) N *= n[k];
     double* tmp[2] = {nullptr, nullptr};
-    if (d > 1) tmp[0] = ws(c, "chainA", static_cast<size_t>(Z1) * N);
-    if (d > 2) tmp[1] = ws(c, "chainB", static_cast<size_t>(Z1) * N);
+    if (d > 1) tmp[0] = ws(c, std::string(tmp_tag) + "A", static_cast<size_t>(Z1) * N);
+    if (d > 2) tmp[1] = ws(c, std::string(tmp_tag) + "B", static_cast<size_t>(Z1) * N);
     const double* src = x;
     long long sstride = x_stride;
     for (int k = 0; k < d; ++k) {
@@ -480,7 +480,7 @@ void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, 
 
 static void apply_phi0(pq_ctx& c, const DevOp& op, const PhiExps& px, int nb, const double* b, double* y) {
     long long Es[3] = {0, 0, 0};
-    mode_chain(c, op.d, op.n, px.phi0, Es, b, op.N, y, op.N, nb, Epilogue{});
+    mode_chain(c, op.d, op.n, px.phi0, Es, b, op.N, y, op.N, nb, Epilogue{}, "phi0");
 }
 
 // kron.hpp:123-128 (phi_0): expm of every (scaled) factor, then one mode chain per RHS.
@@ -618,20 +618,24 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
     const size_t col = static_cast<size_t>(nb) * p * N;
     long long nn[3];
     for (int k = 0; k < op.d; ++k) nn[k] = static_cast<long long>(op.n[k]) * op.n[k];
+    // The reference always evaluates the 13-point level before its first convergence test
+    // (phiaction.hpp:175-240), so levels 0 and 1 are swept as ONE batch: the 13 nodes of the
+    // 13-point rule (= 25-rule nodes 0, 2, ..., 24) into pool slots 0..12.  Per-node results do
+    // not depend on the batch they are computed in, so this is bit-identical to two sweeps.
     int half = 3;
     const NodesWeights* rule = &memo_rule(kClenshaw, 2 * half + 1);
     std::vector<int> slot_of(static_cast<size_t>(rule->size()));
-    std::iota(slot_of.begin(), slot_of.end(), 0);
-    int used = rule->size();
+    for (int i = 0; i < rule->size(); ++i) slot_of[static_cast<size_t>(i)] = 2 * i;  // 7-rule i = 13-rule 2i
+    int used = 13;
     double* pool = ws(c, "ccpool", static_cast<size_t>(used) * nb * N);
     {
         const double* E[3];
         long long Es[3];
         for (int k = 0; k < op.d; ++k) {
             E[k] = px25.node[k];
-            Es[k] = 4 * nn[k];
+            Es[k] = 2 * nn[k];
         }
-        node_sweep(c, op, E, Es, rule->size(), nb, bs, p, nullptr, nullptr, 0, pool, 0);
+        node_sweep(c, op, E, Es, 13, nb, bs, p, nullptr, nullptr, 0, pool, 0);
     }
     double* accs[2] = {out, ws(c, "ccacc", col)};
     int cur = 0;
@@ -658,7 +662,9 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         if (half_next > (1 << 14)) throw ConvergenceFailure("phi_adaptive: no convergence within the node budget");
         const NodesWeights& fine = memo_rule(kClenshaw, 2 * half_next + 1);
         const int fresh = fine.size() / 2;
-        const int need = used + fresh;
+        ++level;
+        const bool preswept = level == 1;  // 13-point nodes already in slots 0..12
+        const int need = preswept ? used : used + fresh;
         {
             DevBuf& b = c.bufs["ccpool"];
             const size_t want = static_cast<size_t>(need) * nb * N * sizeof(double);
@@ -682,26 +688,27 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         std::vector<int> odd(static_cast<size_t>(fresh));
         for (int k = 0; k < fresh; ++k) {
             odd[static_cast<size_t>(k)] = 2 * k + 1;
-            fine_slot[static_cast<size_t>(2 * k + 1)] = used + k;
+            fine_slot[static_cast<size_t>(2 * k + 1)] = preswept ? 2 * k + 1 : used + k;
         }
-        ++level;
-        const double* E[3];
-        long long Es[3];
-        PhiExps pxl;
-        if (level <= 2) {
-            // 13-rule odd node 2k+1 = 25-rule node 4k+2 ; 25-rule odd node 2k+1 itself
-            for (int k = 0; k < op.d; ++k) {
-                E[k] = px25.node[k] + (level == 1 ? 2 : 1) * nn[k];
-                Es[k] = (level == 1 ? 4 : 2) * nn[k];
+        if (!preswept) {
+            const double* E[3];
+            long long Es[3];
+            PhiExps pxl;
+            if (level == 2) {
+                // 25-rule odd nodes 2k+1, exponentiated in the call's expm batch
+                for (int k = 0; k < op.d; ++k) {
+                    E[k] = px25.node[k] + nn[k];
+                    Es[k] = 2 * nn[k];
+                }
+            } else {
+                pxl = phi_exponentials(c, op, s, l, thetas_of(fine, odd), false, false, "ccE");
+                for (int k = 0; k < op.d; ++k) {
+                    E[k] = pxl.node[k];
+                    Es[k] = nn[k];
+                }
             }
-        } else {
-            pxl = phi_exponentials(c, op, s, l, thetas_of(fine, odd), false, false, "ccE");
-            for (int k = 0; k < op.d; ++k) {
-                E[k] = pxl.node[k];
-                Es[k] = nn[k];
-            }
+            node_sweep(c, op, E, Es, fresh, nb, bs, p, nullptr, nullptr, 0, pool, used);
         }
-        node_sweep(c, op, E, Es, fresh, nb, bs, p, nullptr, nullptr, 0, pool, used);
         used = need;
         const int nxt = 1 - cur;
         combine_all(fine, fine_slot, accs[nxt]);

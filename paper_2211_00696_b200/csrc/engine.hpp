@@ -53,6 +53,9 @@ struct pq_ctx {
     double* d_small = nullptr;   // device scratch for reductions
     int* d_int = nullptr;        // device int scratch (expm squaring counts)
     bool profiling = false;
+    // side stream for work independent of the node sweep (phi_0), joined back before returning
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     double phase_ms[6] = {0, 0, 0, 0, 0, 0};
     // GEMM (DMMA) launch records while profiling: (start, stop) events + algorithmic flops
     std::vector<cudaEvent_t> ev_pool;
@@ -132,7 +135,8 @@ void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_
                 const std::vector<double>& scales, double base_one_norm, double* out);
 // y[z1] = (E_0[z1] (x) ... (x) E_{d-1}[z1]) x[z1] for z1 < Z1, epilogue fused into the last mode.
 void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride,
-                const double* x, long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep);
+                const double* x, long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep,
+                const char* tmp_tag = "chain");
 void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, double* y);
 void exp_action_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* b, double* y);
 double max_inf_norm_dev(pq_ctx& c, const double* v, long long N, int ncols);  // syncs

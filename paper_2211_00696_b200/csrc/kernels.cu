@@ -35,7 +35,7 @@ int launch_gemm(const GemmArgs& g, cudaStream_t s) {
     // 32x32 tiles until the grid covers the 148 SMs twice.
     auto ctas = [&](int bm, int bn) { return (long long)((g.M + bm - 1) / bm) * ((g.N + bn - 1) / bn) * g.Z; };
     int shape = 3;
-    if (ctas(64, 64) < 296) shape = 4;
+    if (ctas(64, 64) < 296 || (g.M <= 128 && g.N <= 128 && ctas(64, 64) < 888)) shape = 4;
     return g.b_kmajor ? launch_gemm_kk(g, vec2, shape, s) : launch_gemm_nk(g, vec2, shape, s);
 }
 

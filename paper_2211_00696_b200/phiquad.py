@@ -58,7 +58,12 @@ class Context:
             check(lib.pq_ctx_set_stream(h, C.c_void_p(stream)))
 
     def set_stream(self, stream: Optional[int]) -> None:
-        check(lib.pq_ctx_set_stream(self.handle, C.c_void_p(stream) if stream else None))
+        """Run on an external CUDA stream handle (e.g. torch.cuda.current_stream().cuda_stream).
+        Handle 0 is the legacy default stream (passed as cudaStreamLegacy); None = own stream."""
+        if stream is None:
+            check(lib.pq_ctx_set_stream(self.handle, None))
+        else:
+            check(lib.pq_ctx_set_stream(self.handle, C.c_void_p(stream if stream != 0 else 1)))
 
     @property
     def launches(self) -> int:
@@ -95,9 +100,20 @@ _default: Optional[Context] = None
 
 
 def default_context() -> Context:
+    """Process-wide context on device 0.  When torch has initialised CUDA, the context follows
+    torch's current stream, so device tensors produced by torch are consumed in stream order (an
+    explicitly created Context keeps its own stream; order it with synchronize() or set_stream())."""
     global _default
     if _default is None:
         _default = Context(0)
+        _default._bound = None
+    import sys
+    torch = sys.modules.get("torch")
+    if torch is not None and torch.cuda.is_initialized():
+        s = torch.cuda.current_stream().cuda_stream
+        if _default._bound != s:
+            _default.set_stream(s)
+            _default._bound = s
     return _default
 
 

@@ -60,9 +60,11 @@ def phi_with_plan_sharded(a: KroneckerSum, bs, p: int, l: int, n: int, group=Non
                                        x.ctypes.data_as(L.dp), w.ctypes.data_as(L.dp), rank, world, 1,
                                        C.c_void_p(acc.data_ptr())))
     if world > 1:
-        # engine stream -> collective -> engine stream, ordered by host syncs at the hand-offs
-        L.check(L.lib.pq_ctx_synchronize(ctx.handle))
+        # the default context runs on torch's current stream, which NCCL orders against
+        if getattr(ctx, "_bound", None) is None:
+            L.check(L.lib.pq_ctx_synchronize(ctx.handle))
         (all_reduce or dist.all_reduce)(acc, group=group)
-        torch.cuda.current_stream().synchronize()
+        if getattr(ctx, "_bound", None) is None:
+            torch.cuda.current_stream().synchronize()
     L.check(L.lib.pq_squaring_chain(ctx.handle, d, sh, fac, nb, p, l, C.c_void_p(acc.data_ptr())))
     return acc

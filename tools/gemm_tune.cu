@@ -97,6 +97,13 @@ int main(int argc, char** argv) {
         g.alpha_z = alpha; g.ext = EXT; g.ext_s = N; g.ext_group = 4; g.coef = coef; g.cld = 4; g.nterms = nterms;
         cases.push_back({"mode2+sq", g, fl});
     }
+    {  // batched square products of the expm (Z matrices of n x n), as in expm_core
+        const int cnt = argc > 3 ? atoi(argv[3]) : 81;
+        GemmArgs g;
+        g.A = E; g.B = X; g.C = Y; g.M = g.N = g.K = n; g.lda = g.ldb = g.ldc = n; g.Z = cnt;
+        g.sA1 = 0; g.sB1 = g.sC1 = (long long)n * n;
+        cases.push_back({"expm-sq", g, 2.0 * n * n * n * (double)cnt});
+    }
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
@@ -118,6 +125,9 @@ int main(int argc, char** argv) {
         T(64, 128, 16, 32, 64, 3)
         T(64, 64, 16, 32, 32, 3)
         T(64, 64, 32, 32, 32, 3)
+        T(32, 32, 16, 16, 16, 3)
+        T(32, 64, 16, 16, 32, 3)
+        T(64, 32, 16, 32, 16, 3)
     }
     return 0;
 }

@@ -28,7 +28,9 @@ def main():
     w = config(args.config, args.n)
     a = pq.KroneckerSum(w.factors)
     ctx = pq.Context(0)
-    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
     req = pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode))
     b = torch.from_numpy(w.rhs(0)).cuda()
     out0 = torch.empty(w.N, dtype=torch.float64, device="cuda")
