@@ -79,6 +79,9 @@ PQ_API int pq_ctx_phase_times(pq_ctx* ctx, double* ms6);
  * CUDA events on the context stream.  Returns (synchronising) the number of such launches, their
  * summed device time in ms and their summed algorithmic FLOPs (2*M*N*K per batch entry, dense). */
 PQ_API int pq_ctx_gemm_stats(pq_ctx* ctx, int reset, uint64_t* launches, double* ms, double* flops);
+/* With profiling on, phase boundaries are marked (device event + host clock).  Returns (and
+ * clears, synchronising) a JSON array [{"mark","gpu_us","host_us"}] relative to the first mark. */
+PQ_API int pq_ctx_timeline(pq_ctx* ctx, const char** json);
 
 /* host estimator: rules, roots, bounds, planner (no GPU) --------------------------------- */
 /* quadrature.hpp:31 gauss_legendre, :67 clenshaw_curtis — ascending nodes on [0,1]. */

@@ -4,6 +4,7 @@
 #include "pq_b200.h"
 
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <map>
 #include <numeric>
@@ -139,6 +140,7 @@ int pq_ctx_destroy(pq_ctx* c) {
             cudaEventDestroy(c->ev_fork);
             cudaEventDestroy(c->ev_join);
         }
+        if (c->ev_beta) cudaEventDestroy(c->ev_beta);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -210,6 +212,27 @@ int pq_ctx_gemm_stats(pq_ctx* c, int reset, uint64_t* launches, double* ms, doub
             c->prof_launches = 0;
             c->prof_ms = c->prof_flops = 0.0;
         }
+    });
+}
+
+int pq_ctx_timeline(pq_ctx* c, const char** json) {
+    return guarded([&] {
+        need_ctx(c);
+        cuda_check(cudaStreamSynchronize(c->stream), "timeline sync");
+        std::string s = "[";
+        for (size_t i = 0; i < c->marks.size(); ++i) {
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, c->marks[0].ev, c->marks[i].ev), "timeline elapsed");
+            char buf[256];
+            std::snprintf(buf, sizeof buf, "%s{\"mark\":\"%s\",\"gpu_us\":%.1f,\"host_us\":%.1f}", i ? "," : "",
+                          c->marks[i].name.c_str(), ms * 1000.0, c->marks[i].host_us - c->marks[0].host_us);
+            s += buf;
+        }
+        s += "]";
+        for (auto& m : c->marks) cudaEventDestroy(m.ev);
+        c->marks.clear();
+        c->marks_json = s;
+        *json = c->marks_json.c_str();
     });
 }
 
@@ -490,13 +513,16 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
     const long long N = dim_of(d, shape);
     need(nb >= 1, "phiquadmv: need at least one right-hand side");
     const int p = req->p;
+    mark(*c, "call");
     arena_begin(*c);
     DevOp op = upload_op(*c, d, shape, factors, "factors");
     const double* db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
     double* dout = stage_out(*c, out, static_cast<size_t>(nb) * p * N, space, "hout");
+    mark(*c, "uploaded");
     PlanInfo pi;
     double* d0 = out0 ? stage_out(*c, out0, static_cast<size_t>(nb) * N, space, "hout0") : nullptr;
     phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi, d0);
+    mark(*c, "computed");
     if (out0) finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
     finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
     finish(*c, space);

@@ -10,6 +10,7 @@
 #include "engine.hpp"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstring>
 #include <numeric>
@@ -133,6 +134,16 @@ void prof_collect(pq_ctx& c) {
     }
     c.ev_used = 0;
     c.ev_flops.clear();
+}
+
+void mark(pq_ctx& c, const char* name) {
+    if (!c.profiling) return;
+    static const auto t0 = std::chrono::steady_clock::now();
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "mark event");
+    cuda_check(cudaEventRecord(e, c.stream), "mark record");
+    const double us = std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t0).count();
+    c.marks.push_back({name, e, us});
 }
 
 void check_launch(pq_ctx& c) {
@@ -274,7 +285,7 @@ static void expm_core(pq_ctx& c, int n, const double* base, double op_scale, con
     launch_pade_pq(static_cast<long long>(blk), V, U, P, Q, st);
     count_launch(c);
     if (n <= 128) {
-        int* piv = static_cast<int*>(ws_bytes(c, "expm_piv", sizeof(int) * count * n));
+        int* piv = static_cast<int*>(ws_bytes(c, "expm_piv", 2 * sizeof(int) * count * n));
         launch_lu_factor_solve(n, count, P, Q, piv, c.d_err, st);
         count_launch(c, 2);
     } else {
@@ -720,7 +731,9 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         count_launch(c);
         cuda_check(cudaMemcpyAsync(hstats.data(), stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
                    "cc stats readback");
+        mark(c, "cc_level_enqueued");
         cuda_check(cudaStreamSynchronize(c.stream), "cc stats sync");
+        mark(c, "cc_level_synced");
         cur = nxt;
         double err = 0.0;
         for (int k = 0; k < nb * p; ++k) {
@@ -861,6 +874,7 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
     if (p < 1) throw std::invalid_argument(kind == kGauss ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
     const NodesWeights& rule = kind == kGauss ? memo_rule(kGauss, n + 1) : memo_rule(kClenshaw, 25);
     const PhiExps px = phi_exponentials(c, op, scale, l, rule.x, l > 0, phi0_out != nullptr, "nodeE");
+    mark(c, "exps");
     double* partner = l > 0 ? ws(c, "sqT", static_cast<size_t>(nb) * p * op.N) : nullptr;
     double* first = (l % 2 == 1) ? partner : out;  // the l-step ping-pong then ends in `out`
     if (kind == kGauss) {
@@ -869,12 +883,14 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
     } else {
         phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, px, first, points_used);
     }
+    mark(c, "nodes");
     if (l > 0) {
         double* res = squaring_pingpong(c, op, l, nb, p, first, first == out ? partner : out, px.sq);
         if (res != out)
             cuda_check(cudaMemcpyAsync(out, res, sizeof(double) * nb * p * op.N, cudaMemcpyDeviceToDevice, c.stream),
                        "plan copy");
     }
+    mark(c, "squaring");
     if (phi0_out) apply_phi0(c, op, px, nb, bs, phi0_out);
 }
 
@@ -889,7 +905,25 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
     if (p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
     double alpha = 0.0;
     for (int k = 0; k < op.d; ++k) alpha += op.inf_norm[k];
-    const double beta = nb > 0 ? max_inf_norm_dev(c, bs, op.N, nb) : 0.0;
+    // beta = max ||b||_inf: reduce on the device, read back through pinned memory on an event;
+    // phi_0 (independent of the plan) is enqueued first so the GPU works while the host plans.
+    double beta = 0.0;
+    if (nb > 512) {  // beyond the pinned scratch: plain synchronous reduction
+        beta = max_inf_norm_dev(c, bs, op.N, nb);
+    } else if (nb > 0) {
+        double* stats = ws(c, "colstats", 2 * static_cast<size_t>(nb));
+        launch_colstats(op.N, nb, bs, nullptr, stats, c.stream);
+        count_launch(c);
+        if (!c.ev_beta) cuda_check(cudaEventCreateWithFlags(&c.ev_beta, cudaEventDisableTiming), "beta event");
+        cuda_check(cudaMemcpyAsync(c.h_small, stats, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, c.stream),
+                   "beta readback");
+        cuda_check(cudaEventRecord(c.ev_beta, c.stream), "beta record");
+    }
+    if (nb > 0 && nb <= 512) {
+        cuda_check(cudaEventSynchronize(c.ev_beta), "beta wait");
+        for (int m = 0; m < nb; ++m) beta = std::max(beta, c.h_small[2 * m + 1]);
+    }
+    mark(c, "beta_ready");
     Cost cost{c1, c2, op.d};
     int n = 0;
     bool planned = false;
@@ -913,6 +947,7 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
         plan_cost = cost(n, l, p);
         planned = true;
     }
+    mark(c, "planned");
     int points = 0;
     phi_call_dev(c, op, 1.0, nb, bs, p, l, n, mode, eps, out, &points, phi0_out);
     if (info) {

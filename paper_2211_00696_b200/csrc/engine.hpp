@@ -56,6 +56,15 @@ struct pq_ctx {
     // side stream for work independent of the node sweep (phi_0), joined back before returning
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_beta = nullptr;  // beta readback (phiquadmv) completes
+    // timeline marks while profiling: name, device event, host time (us since first mark)
+    struct Mark {
+        std::string name;
+        cudaEvent_t ev;
+        double host_us;
+    };
+    std::vector<Mark> marks;
+    std::string marks_json;
     double phase_ms[6] = {0, 0, 0, 0, 0, 0};
     // GEMM (DMMA) launch records while profiling: (start, stop) events + algorithmic flops
     std::vector<cudaEvent_t> ev_pool;
@@ -126,6 +135,7 @@ void count_launch(pq_ctx& c, int n = 1);
 // launch_gemm + launch counting + (when profiling) per-launch events and algorithmic flops
 int gemm(pq_ctx& c, const GemmArgs& g);
 void prof_collect(pq_ctx& c);  // syncs, folds recorded events into prof_ms/prof_flops
+void mark(pq_ctx& c, const char* name);  // timeline mark (no-op unless profiling)
 void check_launch(pq_ctx& c);
 
 // ---- device building blocks ----

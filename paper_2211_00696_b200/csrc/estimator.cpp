@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <limits>
 #include <map>
 #include <memory>
@@ -255,11 +256,35 @@ Quartic stationary_quartic(const BoundArgs& q) {
     return c;
 }
 
+// The stationarity quartic depends on (n, p, alpha, kind) but not on beta, and the planner
+// evaluates the same quartics again for every right-hand side of an operator; its real roots
+// are memoised by the exact coefficient bits (a pure function: results are bit-identical).
+static std::vector<double> stationary_roots(const Quartic& c) {
+    using Key = std::array<unsigned long long, 3>;  // exact bit patterns of a3, a2, a1
+    static std::mutex mu;
+    static std::map<Key, std::vector<double>> memo;
+    Key key;
+    std::memcpy(key.data(), c.data(), sizeof(key));
+    if (c[3] == 1.0 && std::isfinite(c[0]) && std::isfinite(c[1]) && std::isfinite(c[2])) {
+        {
+            std::lock_guard<std::mutex> hold(mu);
+            auto it = memo.find(key);
+            if (it != memo.end()) return it->second;
+        }
+        auto r = real_zeros_above_one(c);
+        std::lock_guard<std::mutex> hold(mu);
+        if (memo.size() > (1u << 18)) memo.clear();
+        memo.emplace(key, r);
+        return r;
+    }
+    return real_zeros_above_one(c);
+}
+
 // bounds.hpp:107-115
 double log_theorem_bound(const BoundArgs& q) {
     require(q.alpha > 0.0, "theorem_bound: need alpha > 0");
     if (q.beta == 0.0) return -kInf;
-    const auto rhos = real_zeros_above_one(stationary_quartic(q));
+    const auto rhos = stationary_roots(stationary_quartic(q));
     if (rhos.empty()) throw ConvergenceFailure("theorem_bound: no stationary rho > 1 found");
     double best = kInf;
     for (double rho : rhos) best = std::min(best, log_bound_rho(q, rho));

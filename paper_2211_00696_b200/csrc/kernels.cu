@@ -461,17 +461,194 @@ __global__ void __launch_bounds__(256) k_lu_trsm(int n, const double* __restrict
     }
 }
 
+// --- implicit-pivoting factorisation (n <= 128), one barrier per pivot --------------------
+// Rows stay where they are; each thread-row tracks its current position in the reference's
+// swapped order (a swap k <-> p only moves the rows at positions k and pos(p)), so the pivot is
+// the reference's "first maximal |a_ik| among positions >= k" exactly.  The candidates for the
+// next column are reduced inside the update phase (per warp) and read by every thread after the
+// barrier, so no serial pivot-search phase remains.  Output: L\U over P in ORIGINAL row order,
+// prow[k] = row chosen at step k, pos[i] = final position of row i.
+__global__ void __launch_bounds__(1024) k_lu_factor_ip(int n, double* __restrict__ Pg, int* __restrict__ prow_g,
+                                                       int* __restrict__ pos_g, int* __restrict__ err) {
+    extern __shared__ __align__(16) double sh[];
+    // row stride = 8 (mod 16) doubles: the half-warp's two rows of 8 consecutive doubles hit 16
+    // distinct bank pairs in the row updates
+    const int ld = n + (24 - n % 16) % 16;
+    double* P = Pg + (long long)blockIdx.x * n * n;
+    int* prow = prow_g + (long long)blockIdx.x * n;
+    int* pos = pos_g + (long long)blockIdx.x * n;
+    __shared__ double cv[2][32];
+    __shared__ int cp[2][32], cr[2][32];
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int nw = (nt + 31) >> 5;
+    for (int e = tid; e < n * n; e += nt) sh[(e / n) * ld + e % n] = P[e];
+    const int row = tid / kLuTR, lane8 = tid % kLuTR;
+    const bool owner = row < n;
+    int my_pos = row;
+    bool pivoted = !owner;
+    __syncthreads();
+    auto candidates = [&](int col, int buf) {
+        double v = (owner && lane8 == 0 && !pivoted) ? fabs(sh[row * ld + col]) : -1.0;
+        int ps = owner ? my_pos : 0x7fffffff, rw = row;
+        for (int o = 8; o < 32; o <<= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+            const int op = __shfl_xor_sync(0xffffffffu, ps, o);
+            const int orw = __shfl_xor_sync(0xffffffffu, rw, o);
+            if (ov > v || (ov == v && op < ps)) {
+                v = ov;
+                ps = op;
+                rw = orw;
+            }
+        }
+        if (lane == 0) {
+            cv[buf][warp] = v;
+            cp[buf][warp] = ps;
+            cr[buf][warp] = rw;
+        }
+    };
+    candidates(0, 0);
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        const int buf = k & 1;
+        // every warp reduces the per-warp candidates itself (one load per lane + shuffles)
+        double best = lane < nw ? cv[buf][lane] : -1.0;
+        int bpos = lane < nw ? cp[buf][lane] : 0x7fffffff;
+        int brow = lane < nw ? cr[buf][lane] : -1;
+        for (int o = 16; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+            const int op = __shfl_xor_sync(0xffffffffu, bpos, o);
+            const int orw = __shfl_xor_sync(0xffffffffu, brow, o);
+            if (ov > best || (ov == best && op < bpos)) {
+                best = ov;
+                bpos = op;
+                brow = orw;
+            }
+        }
+        if (best <= 0.0) {  // zero pivot: dense.hpp:167 "lu_solve: singular matrix"
+            if (tid == 0) atomicExch(err, 1);
+            return;
+        }
+        const int p = brow;
+        if (row == p) {
+            my_pos = k;
+            pivoted = true;
+        } else if (my_pos == k) {
+            my_pos = bpos;  // the row that sat at position k moves to the pivot's old position
+        }
+        if (tid == 0) prow[k] = p;
+        if (!pivoted) {
+            const double aik = sh[row * ld + k];
+            const double f = aik / sh[p * ld + k];
+            __syncwarp(0xFFu << (tid & 24));
+            if (lane8 == 0) sh[row * ld + k] = f;
+            if (f != 0.0)
+                for (int j = k + 1 + lane8; j < n; j += kLuTR)
+                    sh[row * ld + j] = __dsub_rn(sh[row * ld + j], __dmul_rn(f, sh[p * ld + j]));
+        }
+        if (k + 1 < n) candidates(k + 1, buf ^ 1);
+        __syncthreads();
+    }
+    for (int e = tid; e < n * n; e += nt) P[e] = sh[(e / n) * ld + e % n];
+    if (owner && lane8 == 0) pos[row] = my_pos;
+}
+
+// Q <- P^{-1} Q from the implicit-pivot factors: one CTA per matrix, L\U staged in shared memory,
+// Q rows in registers (4 threads per row, up to 32 columns each), one barrier per step.
+// Forward elimination in the reference's per-element order (b_i -= f_ik b_pk, k ascending);
+// column-oriented back substitution.  Row p_k of the result is written to row k.
+constexpr int kTrsmTR = 4;
+__global__ void __launch_bounds__(512) k_lu_trsm_reg(int n, const double* __restrict__ LUg, const int* __restrict__ prow_g,
+                                                     const int* __restrict__ pos_g, double* __restrict__ Qg) {
+    extern __shared__ __align__(16) double lu[];
+    __shared__ double pub[2][128];
+    const int ld = n + 1;
+    const double* LU = LUg + (long long)blockIdx.x * n * n;
+    const int* prow = prow_g + (long long)blockIdx.x * n;
+    const int* pos = pos_g + (long long)blockIdx.x * n;
+    double* Q = Qg + (long long)blockIdx.x * n * n;
+    const int tid = threadIdx.x, nt = blockDim.x;
+    for (int e = tid; e < n * n; e += nt) lu[(e / n) * ld + e % n] = LU[e];
+    const int row = tid / kTrsmTR, part = tid % kTrsmTR;
+    const bool owner = row < n;
+    const int cpt = (n + kTrsmTR - 1) / kTrsmTR;  // columns per thread: c = part + kTrsmTR * i
+    double q[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+        const int c = part + kTrsmTR * i;
+        q[i] = (owner && i < cpt && c < n) ? Q[(long long)row * n + c] : 0.0;
+    }
+    const int my_pos = owner ? pos[row] : 0x7fffffff;
+    __syncthreads();
+    for (int k = 0; k < n; ++k) {
+        const int buf = k & 1;
+        if (row == prow[k]) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (i < cpt) pub[buf][part + kTrsmTR * i] = q[i];
+        }
+        __syncthreads();
+        if (owner && my_pos > k) {
+            const double f = lu[row * ld + k];
+            if (f != 0.0) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i < cpt) q[i] = __dsub_rn(q[i], __dmul_rn(f, pub[buf][part + kTrsmTR * i]));
+            }
+        }
+    }
+    __syncthreads();  // forward readers of pub[] are done before the back sweep republishes
+    for (int k = n - 1; k >= 0; --k) {
+        const int buf = k & 1;
+        const int p = prow[k];
+        if (row == p) {
+            // x = q / u_kk: one reciprocal, then the Newton correction x += (q - u x) r, which
+            // gives the correctly rounded quotient (the fast path of the FP64 division) without
+            // 32 serialised division sequences on the step's critical path
+            const double ukk = lu[p * ld + k];
+            const double r = 1.0 / ukk;
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+                if (i < cpt) {
+                    double x = q[i] * r;
+                    x = fma(fma(-ukk, x, q[i]), r, x);
+                    q[i] = x;
+                    pub[buf][part + kTrsmTR * i] = x;
+                }
+        }
+        __syncthreads();
+        if (owner && my_pos < k) {
+            const double u = lu[row * ld + k];
+            if (u != 0.0) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (i < cpt) q[i] = __dsub_rn(q[i], __dmul_rn(u, pub[buf][part + kTrsmTR * i]));
+            }
+        }
+    }
+    if (owner) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+            const int c = part + kTrsmTR * i;
+            if (i < cpt && c < n) Q[(long long)my_pos * n + c] = q[i];
+        }
+    }
+}
+
 void launch_lu_factor_solve(int n, int count, double* P, double* Q, int* piv, int* err, cudaStream_t s) {
     const int smem = n * (n + 1) * 8;
-    static int attr = 0;
-    if (smem > attr) {
-        cudaFuncSetAttribute(k_lu_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = 200 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_lu_factor_ip, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(k_lu_trsm_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
     }
+    int* prow = piv;
+    int* pos = piv + (long long)count * n;
     const int thr = ((n * kLuTR + 31) / 32) * 32;
-    k_lu_factor<<<count, thr, smem, s>>>(n, P, piv, err);
-    const int slices = (n + kTrsmW - 1) / kTrsmW;
-    k_lu_trsm<<<count * slices, 256, n * kTrsmW * 8, s>>>(n, P, piv, Q, slices);
+    const int smem_f = n * (n + (24 - n % 16) % 16) * 8;
+    k_lu_factor_ip<<<count, thr, smem_f, s>>>(n, P, prow, pos, err);
+    const int thr2 = ((n * kTrsmTR + 31) / 32) * 32;
+    k_lu_trsm_reg<<<count, thr2, smem, s>>>(n, P, prow, pos, Q);
 }
 
 void launch_lu_solve(int n, int count, double* P, double* Q, int* err, cudaStream_t s) {

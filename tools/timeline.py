@@ -1,0 +1,55 @@
+#!/usr/bin/env python
+"""Device/host timeline of one phi_0..phi_p call (engine marks, pq_ctx_timeline)."""
+import ctypes as C
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+
+
+def main():
+    import torch
+    import paper_2211_00696_b200 as pq
+    from paper_2211_00696_b200 import _lib as L
+    from paper_2211_00696_b200.workloads import config
+    cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    w = config(cfg)
+    a = pq.KroneckerSum(w.factors)
+    ctx = pq.Context(0)
+    s = torch.cuda.Stream()
+    torch.cuda.set_stream(s)
+    ctx.set_stream(s.cuda_stream)
+    req = pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode))
+    b = torch.from_numpy(w.rhs(0)).cuda()
+    out0 = torch.empty(w.N, dtype=torch.float64, device="cuda")
+    out = torch.empty((w.p, w.N), dtype=torch.float64, device="cuda")
+    d, sh, fac = a._abi()
+    rc = req._c()
+    info = L.PhiInfoC()
+
+    def step():
+        L.check(L.lib.pq_phi_0p(ctx.handle, d, sh, fac, 1, C.c_void_p(b.data_ptr()), C.byref(rc),
+                                C.c_void_p(out0.data_ptr()), C.c_void_p(out.data_ptr()), C.byref(info), L.PQ_DEVICE))
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    ctx.set_profiling(True)
+    for it in range(2):
+        step()
+        js = C.c_char_p()
+        L.check(L.lib.pq_ctx_timeline(ctx.handle, C.byref(js)))
+        marks = json.loads(js.value.decode())
+        print(f"call {it}:")
+        prev = None
+        for m in marks:
+            dg = m["gpu_us"] - (prev["gpu_us"] if prev else 0)
+            dh = m["host_us"] - (prev["host_us"] if prev else 0)
+            print(f"  {m['mark']:20s} gpu {m['gpu_us']:9.1f} (+{dg:8.1f})   host {m['host_us']:9.1f} (+{dh:8.1f})")
+            prev = m
+        ctx.gemm_stats(reset=True)
+
+
+if __name__ == "__main__":
+    main()
