@@ -239,14 +239,17 @@ static void expm_core(pq_ctx& c, int n, const double* base, double op_scale, con
     std::vector<long long> offs(static_cast<size_t>(count));
     int s_max = 0;
     bool known = true;
+    std::vector<int> hint(static_cast<size_t>(count), 0);  // host upper bound of each s_z
     for (int z = 0; z < count; ++z) {
         scales[static_cast<size_t>(z)] = es[static_cast<size_t>(z)].scale;
         offs[static_cast<size_t>(z)] = es[static_cast<size_t>(z)].base_off;
-        if (es[static_cast<size_t>(z)].one_norm < 0.0)
+        if (es[static_cast<size_t>(z)].one_norm < 0.0) {
             known = false;
-        else
-            s_max = std::max(s_max, squaring_bound(std::abs(es[static_cast<size_t>(z)].scale * op_scale),
-                                                   es[static_cast<size_t>(z)].one_norm));
+        } else {
+            hint[static_cast<size_t>(z)] = squaring_bound(std::abs(es[static_cast<size_t>(z)].scale * op_scale),
+                                                          es[static_cast<size_t>(z)].one_norm);
+            s_max = std::max(s_max, hint[static_cast<size_t>(z)]);
+        }
     }
     const double* scale_dev = static_cast<const double*>(arena_push(c, scales.data(), sizeof(double) * count));
     const long long* off_dev = static_cast<const long long*>(arena_push(c, offs.data(), sizeof(long long) * count));
@@ -292,15 +295,32 @@ static void expm_core(pq_ctx& c, int n, const double* base, double op_scale, con
         launch_lu_solve(n, count, P, Q, c.d_err, st);
         count_launch(c);
     }
+    if (!known) std::fill(hint.begin(), hint.end(), s_max);
+    // Squaring rounds cover only the suffix that may still need them: matrices before the first
+    // z with hint_z > r are finished and are flushed to `out` from wherever the ping-pong left them.
     double* cur = Q;
+    int z_done = 0;
+    auto flush = [&](int z_from, int z_to) {
+        if (z_to > z_from && cur != out)
+            cuda_check(cudaMemcpyAsync(out + static_cast<size_t>(z_from) * nn, cur + static_cast<size_t>(z_from) * nn,
+                                       static_cast<size_t>(z_to - z_from) * nn * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       st),
+                       "expm copy");
+    };
     for (int r = 0; r < s_max; ++r) {
-        GemmArgs g = square_batch(n, count, cur, cur, other);
-        g.sq_count = s_dev;
+        int z0 = z_done;
+        while (z0 < count && hint[static_cast<size_t>(z0)] <= r) ++z0;
+        flush(z_done, z0);
+        z_done = z0;
+        if (z0 >= count) break;
+        GemmArgs g = square_batch(n, count - z0, cur + static_cast<size_t>(z0) * nn, cur + static_cast<size_t>(z0) * nn,
+                                  other + static_cast<size_t>(z0) * nn);
+        g.sq_count = s_dev + z0;
         g.sq_round = r;
         gemm(c, g);
         std::swap(cur, other);
     }
-    if (cur != out) cuda_check(cudaMemcpyAsync(out, cur, blk * sizeof(double), cudaMemcpyDeviceToDevice, st), "expm copy");
+    flush(z_done, count);
     check_launch(c);
 }
 
@@ -355,21 +375,24 @@ static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, con
                 group.push_back(j);
                 done[j] = 1;
             }
+        // batch layout [nodes of every factor][squaring matrices][phi_0 matrices]: the large-norm
+        // phi_0 arguments form the suffix, so only they take expm squaring rounds
         std::vector<ExpmEntry> es;
         for (int f : group) {
             const long long bo = static_cast<long long>(off[f]);
             for (int a = 0; a < q; ++a) es.push_back({bo, std::ldexp(1.0 - thetas[static_cast<size_t>(a)], -l), op.one_norm[f]});
-            if (want_sq) es.push_back({bo, std::ldexp(1.0, -l), op.one_norm[f]});
-            if (want_phi0) es.push_back({bo, 1.0, op.one_norm[f]});
         }
-        const size_t nn = static_cast<size_t>(n) * n;
+        if (want_sq)
+            for (int f : group) es.push_back({static_cast<long long>(off[f]), std::ldexp(1.0, -l), op.one_norm[f]});
+        if (want_phi0)
+            for (int f : group) es.push_back({static_cast<long long>(off[f]), 1.0, op.one_norm[f]});
+        const size_t nn = static_cast<size_t>(n) * n, ng = group.size();
         double* out = ws(c, tag + "_n" + std::to_string(n), es.size() * nn);
         expm_core(c, n, base, s, es, out);
-        for (size_t g = 0; g < group.size(); ++g) {
-            double* e = out + g * per * nn;
-            px.node[group[g]] = e;
-            px.sq[group[g]] = want_sq ? e + q * nn : nullptr;
-            px.phi0[group[g]] = want_phi0 ? e + (q + (want_sq ? 1 : 0)) * nn : nullptr;
+        for (size_t g = 0; g < ng; ++g) {
+            px.node[group[g]] = out + g * q * nn;
+            px.sq[group[g]] = want_sq ? out + (ng * q + g) * nn : nullptr;
+            px.phi0[group[g]] = want_phi0 ? out + (ng * q + (want_sq ? ng : 0) + g) * nn : nullptr;
         }
     }
     for (int k = 0; k < op.d; ++k) {

@@ -244,6 +244,161 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, 1) k
     }
 }
 
+// Persistent variant for large launches: CTA c processes tiles c, c + grid, c + 2 grid, ...
+// (tile = (z, n-tile, m-tile), m fastest) as ONE flattened (tile, k-slice) loop, so the cp.async
+// pipeline runs across tile boundaries: the next tile's first slices are in flight while the
+// current tile's epilogue stores.  Plain stores only (no fused epilogue terms, no squaring skip).
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC>
+__global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, 1)
+    k_gemm_persist(const GemmArgs g, int tiles_m, int tiles_n, int total_tiles) {
+    using T = TileCfg<BM, BN, BK, WM, WN, ST, BKM>;
+    constexpr int NT = T::NT;
+    extern __shared__ __align__(16) double smem[];
+    double* sA = smem;
+    double* sB = smem + ST * T::ASZ;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / T::NWN, wn = warp % T::NWN;
+    const int gid = lane >> 2, tig = lane & 3;
+    const int KT = (g.K + BK - 1) / BK;
+    const int my_tiles = (total_tiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;
+    const int total_iters = my_tiles * KT;
+    const int per_z = tiles_m * tiles_n;
+
+    struct TileBase {
+        const double* A;
+        const double* B;
+        double* C;
+        int m0, n0;
+    };
+    auto tile_base = [&](int local) {
+        const int t = (int)blockIdx.x + local * (int)gridDim.x;
+        const int z = t / per_z, r = t - z * per_z;
+        const int nt = r / tiles_m, mt = r - nt * tiles_m;
+        const int z1 = z / g.zdiv, z2 = z - z1 * g.zdiv;
+        return TileBase{g.A + z1 * g.sA1 + z2 * g.sA2, g.B + z1 * g.sB1 + z2 * g.sB2, g.C + z1 * g.sC1 + z2 * g.sC2,
+                        mt * BM, nt * BN};
+    };
+
+    constexpr int KV = BK / VEC;
+    constexpr int A_CH = BM * KV, A_IT = (A_CH + NT - 1) / NT;
+    constexpr int NV = BN / VEC;
+    constexpr int B_CH = BKM ? BN * KV : BK * NV, B_IT = (B_CH + NT - 1) / NT;
+    const unsigned sA_base = static_cast<unsigned>(__cvta_generic_to_shared(sA));
+    const unsigned sB_base = static_cast<unsigned>(__cvta_generic_to_shared(sB));
+
+    auto load_iter = [&](int it) {
+        const int local = it / KT, kt = it - local * KT, stage = it % ST;
+        const TileBase tb = tile_base(local);
+        const int k0 = kt * BK;
+#pragma unroll
+        for (int i = 0; i < A_IT; ++i) {
+            const int c = tid + i * NT;
+            if (A_CH % NT != 0 && c >= A_CH) continue;
+            const int r = c / KV, kc = (c % KV) * VEC;
+            const bool ok = tb.m0 + r < g.M && k0 + kc < g.K;
+            cp_async<VEC>(sA_base + 8u * (stage * T::ASZ + r * T::SA + kc),
+                          ok ? tb.A + (long long)(tb.m0 + r) * g.lda + k0 + kc : g.A, ok);
+        }
+#pragma unroll
+        for (int i = 0; i < B_IT; ++i) {
+            const int c = tid + i * NT;
+            if (B_CH % NT != 0 && c >= B_CH) continue;
+            if constexpr (BKM) {
+                const int r = c / KV, kc = (c % KV) * VEC;
+                const bool ok = tb.n0 + r < g.N && k0 + kc < g.K;
+                cp_async<VEC>(sB_base + 8u * (stage * T::BSZ + r * T::SB + kc),
+                              ok ? tb.B + (long long)(tb.n0 + r) * g.ldb + k0 + kc : g.B, ok);
+            } else {
+                const int r = c / NV, nc = (c % NV) * VEC;
+                const bool ok = k0 + r < g.K && tb.n0 + nc < g.N;
+                cp_async<VEC>(sB_base + 8u * (stage * T::BSZ + r * T::SB + nc),
+                              ok ? tb.B + (long long)(k0 + r) * g.ldb + tb.n0 + nc : g.B, ok);
+            }
+        }
+    };
+
+    double acc[T::MI][T::NI][2];
+#pragma unroll
+    for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+        for (int j = 0; j < T::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+    for (int s = 0; s < ST - 1; ++s) {
+        if (s < total_iters) load_iter(s);
+        cp_commit();
+    }
+    const double* tA0 = sA + (wm * WM + gid) * T::SA + tig;
+    const double* tB0 = BKM ? sB + (wn * WN + gid) * T::SB + tig : sB + tig * T::SB + wn * WN + gid;
+    const bool v2 = (g.ldc % 2 == 0) && (g.sC1 % 2 == 0) && (g.sC2 % 2 == 0) &&
+                    ((reinterpret_cast<uintptr_t>(g.C) & 15) == 0);
+#pragma unroll 1
+    for (int it = 0; it < total_iters; ++it) {
+        cp_wait<ST - 2>();
+        __syncthreads();
+        if (it + ST - 1 < total_iters) load_iter(it + ST - 1);
+        cp_commit();
+        const int st = it % ST;
+        const double* tA = tA0 + st * T::ASZ;
+        const double* tB = tB0 + st * T::BSZ;
+#pragma unroll
+        for (int kk = 0; kk < BK; kk += 4) {
+            double a[T::MI], b[T::NI];
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i) a[i] = tA[i * 8 * T::SA + kk];
+#pragma unroll
+            for (int j = 0; j < T::NI; ++j) b[j] = BKM ? tB[j * 8 * T::SB + kk] : tB[kk * T::SB + j * 8];
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+        }
+        const int local = it / KT;
+        if (it - local * KT == KT - 1) {  // tile done: store while the next tile's slices load
+            const TileBase tb = tile_base(local);
+            const int mb = tb.m0 + wm * WM + gid, nbase = tb.n0 + wn * WN + 2 * tig;
+#pragma unroll
+            for (int i = 0; i < T::MI; ++i) {
+                const int m = mb + i * 8;
+                double* row = tb.C + (long long)m * g.ldc;
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j) {
+                    const int n = nbase + j * 8;
+                    const double v0 = g.alpha == 1.0 ? acc[i][j][0] : __dmul_rn(g.alpha, acc[i][j][0]);
+                    const double v1 = g.alpha == 1.0 ? acc[i][j][1] : __dmul_rn(g.alpha, acc[i][j][1]);
+                    if (m < g.M) {
+                        if (v2 && n + 1 < g.N) {
+                            *reinterpret_cast<double2*>(row + n) = make_double2(v0, v1);
+                        } else {
+                            if (n < g.N) row[n] = v0;
+                            if (n + 1 < g.N) row[n + 1] = v1;
+                        }
+                    }
+                    acc[i][j][0] = acc[i][j][1] = 0.0;
+                }
+            }
+        }
+    }
+    cp_wait<0>();
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC>
+static int launch_persist(const GemmArgs& g, int max_ctas, cudaStream_t s) {
+    using T = TileCfg<BM, BN, BK, WM, WN, ST, BKM>;
+    auto kern = k_gemm_persist<BM, BN, BK, WM, WN, ST, BKM, VEC>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+        attr_done = true;
+    }
+    const long long tm = (g.M + BM - 1) / BM, tn = (g.N + BN - 1) / BN;
+    const long long total = tm * tn * g.Z;
+    if (total > 2147483647LL) throw std::invalid_argument("mode product: too many tiles");
+    const int grid = (int)(total < max_ctas ? total : max_ctas);
+    kern<<<grid, T::NT, T::SMEM, s>>>(g, (int)tm, (int)tn, (int)total);
+    return 1;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC>
 static int launch_cfg(const GemmArgs& g, cudaStream_t s) {
     using T = TileCfg<BM, BN, BK, WM, WN, ST, BKM>;
@@ -274,6 +429,18 @@ template <bool BKM>
 int launch_gemm_family(const GemmArgs& g, bool vec2, int shape, cudaStream_t s) {
     constexpr int BKB = PQ_BK_BIG;
     constexpr int STB = BKB == 32 ? 3 : 4;
+    if (shape == 5) {  // persistent 64x64x16, 3 CTAs per SM
+        static int sms = 0;
+        if (!sms) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            if (sms <= 0) sms = 148;
+        }
+        const int max_ctas = sms * 3;
+        return vec2 ? launch_persist<64, 64, 16, 32, 32, 3, BKM, 2>(g, max_ctas, s)
+                    : launch_persist<64, 64, 16, 32, 32, 3, BKM, 1>(g, max_ctas, s);
+    }
     switch (shape) {
         case 0: return vec2 ? launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 1>(g, s);
         case 1: return vec2 ? launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 1>(g, s);

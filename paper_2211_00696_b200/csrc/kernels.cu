@@ -12,6 +12,7 @@
 #include "kernels.hpp"
 
 #include <cstdio>
+#include <cstdlib>
 #include <stdexcept>
 
 namespace pqb {
@@ -23,6 +24,13 @@ int launch_gemm_nk(const GemmArgs& g, bool vec2, int shape, cudaStream_t s);
 int launch_gemm_kk(const GemmArgs& g, bool vec2, int shape, cudaStream_t s);
 
 static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// PQ_PERSISTENT=1 selects the persistent tiles for large plain products (measured slower than
+// the hardware CTA scheduler on the config-2 pipeline: 191 vs 233 actions/s, so off by default)
+static const bool g_persistent_enabled = [] {
+    const char* e = std::getenv("PQ_PERSISTENT");
+    return e && e[0] == '1';
+}();
 
 int launch_gemm(const GemmArgs& g, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.Z <= 0) return 0;
@@ -36,6 +44,9 @@ int launch_gemm(const GemmArgs& g, cudaStream_t s) {
     auto ctas = [&](int bm, int bn) { return (long long)((g.M + bm - 1) / bm) * ((g.N + bn - 1) / bn) * g.Z; };
     int shape = 3;
     if (ctas(64, 64) < 296 || (g.M <= 128 && g.N <= 128 && ctas(64, 64) < 888)) shape = 4;
+    // large plain products: persistent CTAs with the pipeline running across tiles
+    const bool plain = !g.nterms && !g.accumulate && !g.alpha_z && !g.sq_count;
+    if (shape == 3 && plain && ctas(64, 64) >= 2 * 444 && g_persistent_enabled) shape = 5;
     return g.b_kmajor ? launch_gemm_kk(g, vec2, shape, s) : launch_gemm_nk(g, vec2, shape, s);
 }
 
@@ -538,12 +549,27 @@ __global__ void __launch_bounds__(1024) k_lu_factor_ip(int n, double* __restrict
         if (tid == 0) prow[k] = p;
         if (!pivoted) {
             const double aik = sh[row * ld + k];
-            const double f = aik / sh[p * ld + k];
+            const double akk = sh[p * ld + k];
+            // f = a_ik / a_kk via the reciprocal and one FMA correction (the division's fast path)
+            const double r = 1.0 / akk;
+            double f = aik * r;
+            f = fma(fma(-akk, f, aik), r, f);
             __syncwarp(0xFFu << (tid & 24));
             if (lane8 == 0) sh[row * ld + k] = f;
-            if (f != 0.0)
-                for (int j = k + 1 + lane8; j < n; j += kLuTR)
-                    sh[row * ld + j] = __dsub_rn(sh[row * ld + j], __dmul_rn(f, sh[p * ld + j]));
+            if (f != 0.0) {
+                double* ai = sh + row * ld;
+                const double* ap = sh + p * ld;
+                int j = k + 1 + lane8;
+                for (; j + 3 * kLuTR < n; j += 4 * kLuTR) {  // 4 independent updates in flight
+                    const double x0 = ai[j], x1 = ai[j + kLuTR], x2 = ai[j + 2 * kLuTR], x3 = ai[j + 3 * kLuTR];
+                    const double y0 = ap[j], y1 = ap[j + kLuTR], y2 = ap[j + 2 * kLuTR], y3 = ap[j + 3 * kLuTR];
+                    ai[j] = __dsub_rn(x0, __dmul_rn(f, y0));
+                    ai[j + kLuTR] = __dsub_rn(x1, __dmul_rn(f, y1));
+                    ai[j + 2 * kLuTR] = __dsub_rn(x2, __dmul_rn(f, y2));
+                    ai[j + 3 * kLuTR] = __dsub_rn(x3, __dmul_rn(f, y3));
+                }
+                for (; j < n; j += kLuTR) ai[j] = __dsub_rn(ai[j], __dmul_rn(f, ap[j]));
+            }
         }
         if (k + 1 < n) candidates(k + 1, buf ^ 1);
         __syncthreads();
