@@ -102,19 +102,20 @@ ExpRKTableau tableau_of(int id, double c2) {
     case 2: return exp_rk3_tableau(c2 > 0 ? c2 : 1.0 / 3.0);
     default: break;
     }
-    // Krogstad's fourth-order ETDRK4, restated in the reference's increment form
-    // (PhiTerm coefficients multiply phi_k(-c_i tau A), rows sum to c_i phi_1), c = (0,1/2,1/2,1).
-    // Derivation (variation of constants with linear interpolation of the nonlinearity):
-    //   a21 = 1/2 phi1;  a31 = 1/2 phi1 - 1/2 phi2, a32 = 1/2 phi2   (phi_k at -tau A/2)
-    //   a41 = phi1 - 2 phi2, a43 = 2 phi2                              (phi_k at -tau A)
+    // Krogstad's fourth-order ETDRK4 (Hochbruck-Ostermann 2005 tableau), written in the
+    // reference's increment form (PhiTerm coefficients multiply phi_k(-c_i tau A), rows sum to
+    // c_i phi_1), c = (0, 1/2, 1/2, 1):
+    //   a21 = 1/2 phi1;  a31 = 1/2 phi1 - phi2, a32 = phi2   (phi_k at -tau A/2)
+    //   a41 = phi1 - 2 phi2, a43 = 2 phi2                    (phi_k at -tau A)
     //   b1 = phi1 - 3 phi2 + 4 phi3, b2 = b3 = 2 phi2 - 4 phi3, b4 = 4 phi3 - phi2.
+    // Order 4 checked numerically (tests/test_gpu_configs.py::test_config4_etdrk4_is_fourth_order).
     ExpRKTableau t;
     t.stages = 4;
     t.order = 4;
     t.c = {0.0, 0.5, 0.5, 1.0};
     t.a = {{},
            {{PhiTerm{1, 0.5}}},
-           {{PhiTerm{1, 0.5}, PhiTerm{2, -0.5}}, {PhiTerm{2, 0.5}}},
+           {{PhiTerm{1, 0.5}, PhiTerm{2, -1.0}}, {PhiTerm{2, 1.0}}},
            {{PhiTerm{1, 1.0}, PhiTerm{2, -2.0}}, {}, {PhiTerm{2, 2.0}}}};
     t.b = {{PhiTerm{1, 1.0}, PhiTerm{2, -3.0}, PhiTerm{3, 4.0}},
            {PhiTerm{2, 2.0}, PhiTerm{3, -4.0}},

@@ -229,14 +229,15 @@ TabStore make_tableau(int id, double c2, int& stages, int& order) {
         add(s, -1, 0, 2, -1.5);
         add(s, -1, 2, 2, 1.5);
     } else if (id == 3) {
-        // Krogstad ETDRK4, c = (0, 1/2, 1/2, 1); coefficients multiply phi_k(-c_i tau A)
+        // Krogstad ETDRK4 (Hochbruck-Ostermann tableau), c = (0, 1/2, 1/2, 1); coefficients
+        // multiply phi_k(-c_i tau A): a31 = 1/2 phi1 - phi2, a32 = phi2, a41 = phi1 - 2 phi2, a43 = 2 phi2
         stages = 4;
         order = 4;
         s.c = {0.0, 0.5, 0.5, 1.0};
         add(s, 1, 0, 1, 0.5);
         add(s, 2, 0, 1, 0.5);
-        add(s, 2, 0, 2, -0.5);
-        add(s, 2, 1, 2, 0.5);
+        add(s, 2, 0, 2, -1.0);
+        add(s, 2, 1, 2, 1.0);
         add(s, 3, 0, 1, 1.0);
         add(s, 3, 0, 2, -2.0);
         add(s, 3, 2, 2, 2.0);
