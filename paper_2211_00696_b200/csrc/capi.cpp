@@ -141,6 +141,9 @@ int pq_ctx_destroy(pq_ctx* c) {
             cudaEventDestroy(c->ev_join);
         }
         if (c->ev_beta) cudaEventDestroy(c->ev_beta);
+        if (c->ev_cc) cudaEventDestroy(c->ev_cc);
+        if (c->ev_fac) cudaEventDestroy(c->ev_fac);
+        if (c->pin_fac) cudaFreeHost(c->pin_fac);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -191,6 +194,7 @@ int pq_ctx_release_workspace(pq_ctx* c) {
         for (auto& kv : c->bufs)
             if (kv.second.p) cudaFree(kv.second.p);
         c->bufs.clear();
+        c->fac_host.clear();
     });
 }
 

@@ -167,8 +167,27 @@ DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const
     op.host.assign(factors, factors + total);
     for (double v : op.host)
         if (!std::isfinite(v)) throw std::invalid_argument("DenseMatrix: non-finite entry");
+    const bool had = c.bufs.count(slot) && c.bufs[slot].p;
     double* dev = ws(c, slot, total);
-    cuda_check(cudaMemcpyAsync(dev, factors, total * sizeof(double), cudaMemcpyHostToDevice, c.stream), "upload factors");
+    auto& last = c.fac_host[slot];
+    const bool same = had && last.size() == total && std::memcmp(last.data(), factors, total * sizeof(double)) == 0 &&
+                      c.bufs[slot].p == dev;
+    if (!same) {
+        // stage through pinned memory so the copy is asynchronous (a pageable H2D copy would wait
+        // for the stream to drain, idling the GPU while the host prepares the call)
+        if (!c.ev_fac) cuda_check(cudaEventCreateWithFlags(&c.ev_fac, cudaEventDisableTiming), "factor event");
+        cuda_check(cudaEventSynchronize(c.ev_fac), "factor staging wait");
+        if (c.pin_fac_cap < total) {
+            if (c.pin_fac) cudaFreeHost(c.pin_fac);
+            cuda_check(cudaMallocHost(reinterpret_cast<void**>(&c.pin_fac), total * sizeof(double)), "pinned factors");
+            c.pin_fac_cap = total;
+        }
+        std::memcpy(c.pin_fac, factors, total * sizeof(double));
+        cuda_check(cudaMemcpyAsync(dev, c.pin_fac, total * sizeof(double), cudaMemcpyHostToDevice, c.stream),
+                   "upload factors");
+        cuda_check(cudaEventRecord(c.ev_fac, c.stream), "factor record");
+        last = op.host;
+    }
     size_t off = 0;
     for (int k = 0; k < d; ++k) {
         const int n = op.n[k];
@@ -645,7 +664,7 @@ void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, con
 // single expm batch: CC nodes nest bitwise, so 7-rule node i is 25-rule node 4i); deeper levels
 // exponentiate their fresh nodes on demand.
 static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int nb, const double* bs, int p,
-                               double eps, const PhiExps& px25, double* out, int* points_used) {
+                               double eps, const PhiExps& px25, double* out, int* points_used, int spec_points) {
     if (p < 1) throw std::invalid_argument("phi_adaptive: need p >= 1");
     if (!(eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
     const long long N = op.N;
@@ -691,17 +710,14 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
     double* stats = ws(c, "ccstats", 2 * static_cast<size_t>(nb) * p);
     std::vector<double> hstats(2 * static_cast<size_t>(nb) * p);
     int level = 0;
-    while (true) {
-        const int half_next = 2 * half;
-        if (half_next > (1 << 14)) throw ConvergenceFailure("phi_adaptive: no convergence within the node budget");
-        const NodesWeights& fine = memo_rule(kClenshaw, 2 * half_next + 1);
-        const int fresh = fine.size() / 2;
-        ++level;
-        const bool preswept = level == 1;  // 13-point nodes already in slots 0..12
-        const int need = preswept ? used : used + fresh;
+    // Fresh (odd) nodes of ladder level L >= 2 live in pool slots [base[L], base[L] + fresh).
+    std::map<int, int> level_base;
+    // Sweeps the fresh nodes of `lev` (rule `rl`) into the next free pool slots.
+    auto sweep_level = [&](int lev, const NodesWeights& rl) {
+        const int fr = rl.size() / 2;
         {
             DevBuf& b = c.bufs["ccpool"];
-            const size_t want = static_cast<size_t>(need) * nb * N * sizeof(double);
+            const size_t want = static_cast<size_t>(used + fr) * nb * N * sizeof(double);
             if (b.bytes < want) {
                 double* np = nullptr;
                 cuda_check(cudaStreamSynchronize(c.stream), "pool grow sync");
@@ -717,33 +733,42 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             }
             pool = static_cast<double*>(b.p);
         }
+        std::vector<int> odd(static_cast<size_t>(fr));
+        for (int k = 0; k < fr; ++k) odd[static_cast<size_t>(k)] = 2 * k + 1;
+        const double* E[3];
+        long long Es[3];
+        PhiExps pxl;
+        if (lev == 2) {
+            // 25-rule odd nodes 2k+1, exponentiated in the call's expm batch
+            for (int k = 0; k < op.d; ++k) {
+                E[k] = px25.node[k] + nn[k];
+                Es[k] = 2 * nn[k];
+            }
+        } else {
+            pxl = phi_exponentials(c, op, s, l, thetas_of(rl, odd), false, false, "ccE" + std::to_string(lev));
+            for (int k = 0; k < op.d; ++k) {
+                E[k] = pxl.node[k];
+                Es[k] = nn[k];
+            }
+        }
+        level_base[lev] = used;
+        node_sweep(c, op, E, Es, fr, nb, bs, p, nullptr, nullptr, 0, pool, used);
+        used += fr;
+    };
+    if (!c.ev_cc) cuda_check(cudaEventCreateWithFlags(&c.ev_cc, cudaEventDisableTiming), "cc event");
+    const bool pinned_stats = 2 * nb * p <= 1024;
+    while (true) {
+        const int half_next = 2 * half;
+        if (half_next > (1 << 14)) throw ConvergenceFailure("phi_adaptive: no convergence within the node budget");
+        const NodesWeights& fine = memo_rule(kClenshaw, 2 * half_next + 1);
+        const int fresh = fine.size() / 2;
+        ++level;
+        const bool preswept = level == 1;  // 13-point nodes already in slots 0..12
+        if (!preswept && !level_base.count(level)) sweep_level(level, fine);
         std::vector<int> fine_slot(static_cast<size_t>(fine.size()));
         for (int i = 0; i < rule->size(); ++i) fine_slot[static_cast<size_t>(2 * i)] = slot_of[static_cast<size_t>(i)];
-        std::vector<int> odd(static_cast<size_t>(fresh));
-        for (int k = 0; k < fresh; ++k) {
-            odd[static_cast<size_t>(k)] = 2 * k + 1;
-            fine_slot[static_cast<size_t>(2 * k + 1)] = preswept ? 2 * k + 1 : used + k;
-        }
-        if (!preswept) {
-            const double* E[3];
-            long long Es[3];
-            PhiExps pxl;
-            if (level == 2) {
-                // 25-rule odd nodes 2k+1, exponentiated in the call's expm batch
-                for (int k = 0; k < op.d; ++k) {
-                    E[k] = px25.node[k] + nn[k];
-                    Es[k] = 2 * nn[k];
-                }
-            } else {
-                pxl = phi_exponentials(c, op, s, l, thetas_of(fine, odd), false, false, "ccE");
-                for (int k = 0; k < op.d; ++k) {
-                    E[k] = pxl.node[k];
-                    Es[k] = nn[k];
-                }
-            }
-            node_sweep(c, op, E, Es, fresh, nb, bs, p, nullptr, nullptr, 0, pool, used);
-        }
-        used = need;
+        for (int k = 0; k < fresh; ++k)
+            fine_slot[static_cast<size_t>(2 * k + 1)] = preswept ? 2 * k + 1 : level_base[level] + k;
         const int nxt = 1 - cur;
         combine_all(fine, fine_slot, accs[nxt]);
         half = half_next;
@@ -752,15 +777,23 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         // phiaction.hpp:225-240: max over columns of ||y - y_prev||_inf / ||y||_inf
         launch_colstats(N, nb * p, accs[nxt], accs[cur], stats, c.stream);
         count_launch(c);
-        cuda_check(cudaMemcpyAsync(hstats.data(), stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+        double* hs = pinned_stats ? c.h_small : hstats.data();
+        cuda_check(cudaMemcpyAsync(hs, stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
                    "cc stats readback");
+        cuda_check(cudaEventRecord(c.ev_cc, c.stream), "cc record");
         mark(c, "cc_level_enqueued");
-        cuda_check(cudaStreamSynchronize(c.stream), "cc stats sync");
+        // Speculation: when the planner predicts the next level is needed (its rule has at most
+        // spec_points nodes), its node sweep is enqueued before the host waits for this level's
+        // error, so the GPU never drains at the check (a wasted sweep if this level converges).
+        const int next_points = 2 * fine.size() - 1;
+        if (pinned_stats && spec_points > 0 && next_points <= spec_points && 2 * half_next <= (1 << 14))
+            sweep_level(level + 1, memo_rule(kClenshaw, next_points));
+        cuda_check(cudaEventSynchronize(c.ev_cc), "cc stats wait");
         mark(c, "cc_level_synced");
         cur = nxt;
         double err = 0.0;
         for (int k = 0; k < nb * p; ++k) {
-            const double diff = hstats[2 * k], norm = hstats[2 * k + 1];
+            const double diff = hs[2 * k], norm = hs[2 * k + 1];
             if (diff == 0.0) continue;
             err = std::max(err, norm == 0.0 ? std::numeric_limits<double>::infinity() : diff / norm);
         }
@@ -775,7 +808,7 @@ void phi_adaptive_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const do
                       int* points_used) {
     const NodesWeights& r25 = memo_rule(kClenshaw, 25);
     const PhiExps px = phi_exponentials(c, op, scale, 0, r25.x, false, false, "nodeE");
-    phi_adaptive_shift(c, op, scale, 0, nb, bs, p, eps, px, out, points_used);
+    phi_adaptive_shift(c, op, scale, 0, nb, bs, p, eps, px, out, points_used, 0);
 }
 
 // phiaction.hpp:255-272 + 290-301: l doubling steps with E_k (= expm(2^-l A_k) on entry),
@@ -904,9 +937,39 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
         phi_fixed_shift(c, op, scale, l, nb, bs, p, rule, px, first);
         if (points_used) *points_used = rule.size();
     } else {
-        phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, px, first, points_used);
+        // the planner's node parameter predicts the ladder level that converges: speculate up to
+        // the first CC rule with at least n + 1 points (the plan's Gauss-equivalent count)
+        int spec = 0;
+        if (n > 0) {
+            spec = 13;
+            while (spec < n + 1 && spec < (1 << 15)) spec = 2 * spec - 1;
+        }
+        phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, px, first, points_used, spec);
     }
     mark(c, "nodes");
+    // phi_0 needs only its exponentials and b: run its mode chain on the side stream alongside the
+    // squaring chain, where its CTAs fill the tails of the squaring GEMM waves (not while profiling,
+    // so per-launch events stay unambiguous)
+    const bool side_phi0 = phi0_out && l > 0 && !c.profiling;
+    if (side_phi0) {
+        if (!c.side) {
+            cuda_check(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking), "side stream");
+            cuda_check(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming), "fork event");
+            cuda_check(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming), "join event");
+        }
+        cuda_check(cudaEventRecord(c.ev_fork, c.stream), "fork");
+        cuda_check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "fork wait");
+        cudaStream_t main_stream = c.stream;
+        c.stream = c.side;
+        try {
+            apply_phi0(c, op, px, nb, bs, phi0_out);
+        } catch (...) {
+            c.stream = main_stream;
+            throw;
+        }
+        c.stream = main_stream;
+        cuda_check(cudaEventRecord(c.ev_join, c.side), "join record");
+    }
     if (l > 0) {
         double* res = squaring_pingpong(c, op, l, nb, p, first, first == out ? partner : out, px.sq);
         if (res != out)
@@ -914,7 +977,10 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
                        "plan copy");
     }
     mark(c, "squaring");
-    if (phi0_out) apply_phi0(c, op, px, nb, bs, phi0_out);
+    if (side_phi0)
+        cuda_check(cudaStreamWaitEvent(c.stream, c.ev_join, 0), "join wait");
+    else if (phi0_out)
+        apply_phi0(c, op, px, nb, bs, phi0_out);
 }
 
 void phi_with_plan_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n, int kind,

@@ -57,6 +57,13 @@ struct pq_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_beta = nullptr;  // beta readback (phiquadmv) completes
+    cudaEvent_t ev_cc = nullptr;    // adaptive CC error readback completes
+    // factor uploads: pinned staging (no implicit stream sync) + per-slot cache of the last
+    // operator (reused when the caller passes bit-identical factors again)
+    double* pin_fac = nullptr;
+    size_t pin_fac_cap = 0;
+    cudaEvent_t ev_fac = nullptr;
+    std::map<std::string, std::vector<double>> fac_host;  // slot -> last uploaded host copy
     // timeline marks while profiling: name, device event, host time (us since first mark)
     struct Mark {
         std::string name;
