@@ -445,7 +445,13 @@ int launch_gemm_family(const GemmArgs& g, bool vec2, int shape, cudaStream_t s) 
         case 0: return vec2 ? launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 1>(g, s);
         case 1: return vec2 ? launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 1>(g, s);
         case 2: return vec2 ? launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 2>(g, s) : launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 1>(g, s);
-        case 3: return vec2 ? launch_cfg<64, 64, 16, 32, 32, 3, BKM, 2>(g, s) : launch_cfg<64, 64, 16, 32, 32, 3, BKM, 1>(g, s);
+        case 3:
+            // 4 stages still fit 3 CTAs/SM for row-major B (+3%, r01_gemm_tune.txt); the k-major
+            // B tile is larger and would drop to 2 CTAs/SM, so it keeps 3 stages
+            if constexpr (BKM)
+                return vec2 ? launch_cfg<64, 64, 16, 32, 32, 3, BKM, 2>(g, s) : launch_cfg<64, 64, 16, 32, 32, 3, BKM, 1>(g, s);
+            else
+                return vec2 ? launch_cfg<64, 64, 16, 32, 32, 4, BKM, 2>(g, s) : launch_cfg<64, 64, 16, 32, 32, 4, BKM, 1>(g, s);
         default: return vec2 ? launch_cfg<32, 32, 16, 16, 16, 3, BKM, 2>(g, s) : launch_cfg<32, 32, 16, 16, 16, 3, BKM, 1>(g, s);
     }
 }

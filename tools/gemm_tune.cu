@@ -128,6 +128,9 @@ int main(int argc, char** argv) {
         T(32, 32, 16, 16, 16, 3)
         T(32, 64, 16, 16, 32, 3)
         T(64, 32, 16, 32, 16, 3)
+        T(64, 64, 16, 32, 32, 4)
+        T(64, 64, 16, 32, 32, 5)
+        T(64, 64, 8, 32, 32, 6)
     }
     return 0;
 }
