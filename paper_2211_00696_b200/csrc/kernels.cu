@@ -773,7 +773,48 @@ __global__ void k_sq_combine_any(long long N, int p, int nb, double* __restrict_
     }
 }
 
+// 16-byte variant: each thread owns an adjacent element pair (same arithmetic per element).
+template <int P>
+__global__ void k_sq_combine2(long long N2, int nb, double2* __restrict__ T, const double2* __restrict__ Y,
+                              const double* __restrict__ coef) {
+    const long long total = N2 * nb;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+        const long long m = e / N2, t = e - m * N2;
+        const long long base = m * P * N2 + t;
+        double2 y[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) y[j] = Y[base + j * N2];
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            const double2 ti = T[base + i * N2];
+            const double h = ldexp(1.0, -(i + 1));
+            double vx = __dmul_rn(h, ti.x), vy = __dmul_rn(h, ti.y);
+#pragma unroll
+            for (int j = 0; j <= i; ++j) {
+                const double cj = coef[i * P + j];
+                vx = __dadd_rn(vx, __dmul_rn(cj, y[j].x));
+                vy = __dadd_rn(vy, __dmul_rn(cj, y[j].y));
+            }
+            T[base + i * N2] = make_double2(vx, vy);
+        }
+    }
+}
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
 void launch_sq_combine(long long N, int p, int nb, double* T, const double* Y, const double* coef, cudaStream_t s) {
+    if (N % 2 == 0 && p <= 8 && aligned16(T) && aligned16(Y)) {
+        const long long N2 = N / 2;
+        const unsigned grid2 = grid_for(N2 * nb, 256);
+        double2* T2 = reinterpret_cast<double2*>(T);
+        const double2* Y2 = reinterpret_cast<const double2*>(Y);
+        switch (p) {
+#define PQ_SQC2(PP) \
+    case PP: k_sq_combine2<PP><<<grid2, 256, 0, s>>>(N2, nb, T2, Y2, coef); return;
+            PQ_SQC2(1) PQ_SQC2(2) PQ_SQC2(3) PQ_SQC2(4) PQ_SQC2(5) PQ_SQC2(6) PQ_SQC2(7) PQ_SQC2(8)
+#undef PQ_SQC2
+        }
+    }
     const unsigned grid = grid_for(N * nb, 256);
     switch (p) {
 #define PQ_SQC(PP) \
@@ -796,8 +837,44 @@ __global__ void k_combine_any(long long N, int p, int q, const double* __restric
     }
 }
 
+// 16-byte variant of k_combine (adjacent element pair per thread, same per-element arithmetic).
+template <int P>
+__global__ void k_combine2(long long N2, int q, const double2* __restrict__ V, long long vstride2,
+                           const int* __restrict__ slots, const double* __restrict__ coef, double2* acc,
+                           long long acc_stride2, int zero) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N2; t += (long long)gridDim.x * blockDim.x) {
+        double2 y[P];
+#pragma unroll
+        for (int j = 0; j < P; ++j) y[j] = zero ? make_double2(0.0, 0.0) : acc[j * acc_stride2 + t];
+#pragma unroll 4
+        for (int i = 0; i < q; ++i) {
+            const double2 v = __ldg(V + slots[i] * vstride2 + t);
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const double cij = coef[i * P + j];
+                y[j].x = __dadd_rn(y[j].x, __dmul_rn(cij, v.x));
+                y[j].y = __dadd_rn(y[j].y, __dmul_rn(cij, v.y));
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < P; ++j) acc[j * acc_stride2 + t] = y[j];
+    }
+}
+
 void launch_combine(long long N, int p, int q, const double* V, long long vstride, const int* slots, const double* coef,
                     double* acc, long long acc_stride, int zero, cudaStream_t s) {
+    if (N % 2 == 0 && vstride % 2 == 0 && acc_stride % 2 == 0 && p <= 8 && aligned16(V) && aligned16(acc)) {
+        const long long N2 = N / 2;
+        const unsigned grid2 = grid_for(N2, 256);
+        const double2* V2 = reinterpret_cast<const double2*>(V);
+        double2* A2 = reinterpret_cast<double2*>(acc);
+        switch (p) {
+#define PQ_COMB2(PP) \
+    case PP: k_combine2<PP><<<grid2, 256, 0, s>>>(N2, q, V2, vstride / 2, slots, coef, A2, acc_stride / 2, zero); return;
+            PQ_COMB2(1) PQ_COMB2(2) PQ_COMB2(3) PQ_COMB2(4) PQ_COMB2(5) PQ_COMB2(6) PQ_COMB2(7) PQ_COMB2(8)
+#undef PQ_COMB2
+        }
+    }
     const unsigned grid = grid_for(N, 256);
     switch (p) {
 #define PQ_COMB(PP) \
