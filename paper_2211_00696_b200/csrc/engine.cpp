@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -236,6 +237,9 @@ static GemmArgs square_batch(int n, int count, const double* A, const double* B,
     return g;
 }
 
+static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>& hint, const int* s_dev, int s_max,
+                            double* cur, double* other, double* out);
+
 struct ExpmEntry {
     long long base_off;  // doubles from `base`
     double scale;        // exact multiplier applied after fl(op_scale * a)
@@ -315,9 +319,17 @@ static void expm_core(pq_ctx& c, int n, const double* base, double op_scale, con
         count_launch(c);
     }
     if (!known) std::fill(hint.begin(), hint.end(), s_max);
-    // Squaring rounds cover only the suffix that may still need them: matrices before the first
-    // z with hint_z > r are finished and are flushed to `out` from wherever the ping-pong left them.
-    double* cur = Q;
+    squaring_rounds(c, n, count, hint, s_dev, s_max, Q, other, out);
+}
+
+// Squaring phase of a batched expm (dense.hpp:222-226): entry z is squared s_z <= hint_z times
+// (device counts s_dev decide; the GEMM carries finished entries through).  Rounds cover only
+// the suffix that may still need them: matrices before the first z with hint_z > r are finished
+// and are flushed to `out` from wherever the ping-pong left them.
+static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>& hint, const int* s_dev, int s_max,
+                            double* cur, double* other, double* out) {
+    const size_t nn = static_cast<size_t>(n) * n;
+    cudaStream_t st = c.stream;
     int z_done = 0;
     auto flush = [&](int z_from, int z_to) {
         if (z_to > z_from && cur != out)
@@ -341,6 +353,135 @@ static void expm_core(pq_ctx& c, int n, const double* base, double op_scale, con
     }
     flush(z_done, count);
     check_launch(c);
+}
+
+// The exponentials one phi call needs are all scalar multiples of a few factors,
+// exp(c_z * G_f) with G_f = fl(op_scale * A_f).  Instead of one Pade-13 solve per matrix (an LU
+// each, latency-bound), evaluate a degree-m Taylor polynomial on SHARED powers: with
+// B_f = 2^-e_f G_f (exact, ||B_f||_1 <= 1) and alpha_z = c_z 2^(e_f - s_z) (exact),
+//   exp(c_z G_f) = (sum_k alpha_z^k / k! B_f^k)^(2^s_z),   ||alpha_z B_f||_1 <= theta_m,
+// where theta_m bounds the relative backward error of the truncated series by u = 2^-53 (the
+// same criterion dense.hpp's Pade-13 threshold 5.37 encodes).  The powers B^2..B^m of every
+// factor take ceil(log2 m) batched DMMA launches, the combination is one elementwise pass, and
+// the squarings reuse squaring_rounds.  Against an eigendecomposition ground truth this is as
+// accurate as the reference's Pade-13 ("Exponentials").  Returns false (caller uses
+// expm_core) when a norm is unknown or PQ_EXPM=pade.
+static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, const std::vector<ExpmEntry>& es,
+                        double* out) {
+    static const bool disabled = [] {
+        const char* v = std::getenv("PQ_EXPM");
+        return v && std::string(v) == "pade";
+    }();
+    const int count = static_cast<int>(es.size());
+    if (disabled || count <= 0) return false;
+    std::vector<long long> foff;
+    std::vector<double> fnorm;
+    std::vector<int> fidx(static_cast<size_t>(count));
+    for (int z = 0; z < count; ++z) {
+        const ExpmEntry& e = es[static_cast<size_t>(z)];
+        if (!(e.one_norm >= 0.0) || !std::isfinite(e.scale)) return false;
+        size_t f = 0;
+        while (f < foff.size() && foff[f] != e.base_off) ++f;
+        if (f == foff.size()) {
+            foff.push_back(e.base_off);
+            fnorm.push_back(e.one_norm);
+        }
+        fidx[static_cast<size_t>(z)] = static_cast<int>(f);
+    }
+    const int nf = static_cast<int>(foff.size());
+    std::vector<double> gnorm(static_cast<size_t>(nf)), pow2(static_cast<size_t>(nf)), nu(static_cast<size_t>(nf));
+    for (int f = 0; f < nf; ++f) {
+        // ||fl(op_scale A_f)||_1 <= |op_scale| ||A_f||_1 (1 + n u); the margin keeps the theta test safe
+        const double g = std::abs(op_scale) * fnorm[static_cast<size_t>(f)] * (1.0 + 1e-12);
+        if (!std::isfinite(g)) return false;
+        gnorm[static_cast<size_t>(f)] = g;
+        int ex = 0;
+        if (g > 0.0) std::frexp(g, &ex);  // 2^ex >= g
+        nu[static_cast<size_t>(f)] = std::ldexp(1.0, ex);
+        pow2[static_cast<size_t>(f)] = std::ldexp(1.0, -ex);
+    }
+    // theta_m: largest ||X||_1 with sum_k |c_k| ||X||^(k-1) <= 2^-53 for the series of
+    // log(e^-X T_m(X)) (computed once in exact rational arithmetic; tools/taylor_theta.py)
+    static const int kM[] = {16, 18, 20, 24, 28, 32};
+    static const double kTh[] = {0.7802874256626574, 1.0908637192900361, 1.4382525968043367,
+                                 2.2190488693650896, 3.084000544989162,  4.00756108611804};
+    auto squarings = [&](int z, double th) {
+        const double x = std::abs(es[static_cast<size_t>(z)].scale) * gnorm[static_cast<size_t>(fidx[static_cast<size_t>(z)])];
+        return x > th ? static_cast<int>(std::ceil(std::log2(x / th))) : 0;
+    };
+    // degree: minimise power products + squaring-round batch sizes + a per-launch latency term
+    int best = 0;
+    double best_cost = 0.0;
+    for (int i = 0; i < 6; ++i) {
+        const int m = kM[i];
+        std::vector<int> s(static_cast<size_t>(count));
+        int smax = 0;
+        for (int z = 0; z < count; ++z) smax = std::max(smax, s[static_cast<size_t>(z)] = squarings(z, kTh[i]));
+        double cost = nf * (m - 1.0) + 6.0 * (std::ceil(std::log2(static_cast<double>(m))) + smax);
+        for (int r = 0; r < smax; ++r) {
+            int z0 = 0;
+            while (z0 < count && s[static_cast<size_t>(z0)] <= r) ++z0;
+            cost += count - z0;
+        }
+        if (i == 0 || cost < best_cost) {
+            best = i;
+            best_cost = cost;
+        }
+    }
+    const int m = kM[best];
+    const double th = kTh[best];
+    std::vector<int> hint(static_cast<size_t>(count));
+    std::vector<double> coef(static_cast<size_t>(count) * (m + 1));
+    int s_max = 0;
+    for (int z = 0; z < count; ++z) {
+        const int s = squarings(z, th);
+        hint[static_cast<size_t>(z)] = s;
+        s_max = std::max(s_max, s);
+        const double alpha =
+            std::ldexp(es[static_cast<size_t>(z)].scale * nu[static_cast<size_t>(fidx[static_cast<size_t>(z)])], -s);
+        double* t = coef.data() + static_cast<size_t>(z) * (m + 1);
+        t[0] = 1.0;
+        for (int k = 1; k <= m; ++k) t[k] = t[k - 1] * alpha / k;
+    }
+    std::vector<int> chunks;  // int4 {factor, first entry, count, 0}: runs of one factor, <= kTaylorChunk
+    for (int z = 0; z < count;) {
+        int e = z + 1;
+        while (e < count && e - z < kTaylorChunk && fidx[static_cast<size_t>(e)] == fidx[static_cast<size_t>(z)]) ++e;
+        chunks.insert(chunks.end(), {fidx[static_cast<size_t>(z)], z, e - z, 0});
+        z = e;
+    }
+    const int nchunks = static_cast<int>(chunks.size() / 4);
+    const size_t nn = static_cast<size_t>(n) * n;
+    double* P = ws(c, "taylorP", static_cast<size_t>(nf) * m * nn);
+    double* T = ws(c, "taylorT", static_cast<size_t>(count) * nn);
+    const long long* foff_dev = static_cast<const long long*>(arena_push(c, foff.data(), sizeof(long long) * nf));
+    const double* pow2_dev = static_cast<const double*>(arena_push(c, pow2.data(), sizeof(double) * nf));
+    const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), sizeof(double) * coef.size()));
+    const int* chunk_dev = static_cast<const int*>(arena_push(c, chunks.data(), sizeof(int) * chunks.size()));
+    const int* s_dev = static_cast<const int*>(arena_push(c, hint.data(), sizeof(int) * count));
+    arena_flush(c);
+    cudaStream_t st = c.stream;
+    launch_taylor_base(n, nf, m, base, foff_dev, op_scale, pow2_dev, P, st);
+    count_launch(c);
+    const long long lnn = static_cast<long long>(nn), fs = static_cast<long long>(m) * lnn;
+    for (int h = 1; h < m; h *= 2) {  // P^(h+j) = P^h P^j, j = 1..min(h, m-h), all factors in one launch
+        const int J = std::min(h, m - h);
+        GemmArgs g = square_batch(n, nf * J, P + (h - 1) * lnn, P, P + h * lnn);
+        g.zdiv = J;
+        g.sA1 = fs;
+        g.sA2 = 0;
+        g.sB1 = fs;
+        g.sB2 = lnn;
+        g.sC1 = fs;
+        g.sC2 = lnn;
+        gemm(c, g);
+    }
+    double* first = (s_max % 2 == 0) ? out : T;
+    launch_taylor_combine(n, m, nchunks, chunk_dev, coef_dev, P, first, st);
+    count_launch(c);
+    squaring_rounds(c, n, count, hint, s_dev, s_max, first, first == out ? T : out, out);
+    check_launch(c);
+    return true;
 }
 
 void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_stride, const std::vector<double>& scales,
@@ -407,7 +548,7 @@ static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, con
             for (int f : group) es.push_back({static_cast<long long>(off[f]), 1.0, op.one_norm[f]});
         const size_t nn = static_cast<size_t>(n) * n, ng = group.size();
         double* out = ws(c, tag + "_n" + std::to_string(n), es.size() * nn);
-        expm_core(c, n, base, s, es, out);
+        if (!expm_taylor(c, n, base, s, es, out)) expm_core(c, n, base, s, es, out);
         for (size_t g = 0; g < ng; ++g) {
             px.node[group[g]] = out + g * q * nn;
             px.sq[group[g]] = want_sq ? out + (ng * q + g) * nn : nullptr;

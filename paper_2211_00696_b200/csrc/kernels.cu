@@ -102,6 +102,69 @@ void launch_expm_prep(int n, int count, const double* base, long long base_strid
     k_expm_prep<<<count, thr, 0, s>>>(n, base, base_stride, base_off, op_scale, scale, X, s_out);
 }
 
+// ---- shared-power Taylor exponentials (engine.cpp expm_taylor) ----
+// P[f][0] = 2^-e_f * fl(op_scale * base_f): the normalised first power of factor f.
+__global__ void k_taylor_base(long long nn, int m, const double* __restrict__ base, const long long* __restrict__ f_off,
+                              double op_scale, const double* __restrict__ f_pow2, double* __restrict__ P) {
+    const int f = blockIdx.y;
+    const double* a = base + f_off[f];
+    double* p = P + (long long)f * m * nn;
+    const double sc = f_pow2[f];
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn; e += (long long)gridDim.x * blockDim.x)
+        p[e] = __dmul_rn(sc, __dmul_rn(op_scale, a[e]));
+}
+
+void launch_taylor_base(int n, int nf, int m, const double* base, const long long* f_off, double op_scale,
+                        const double* f_pow2, double* P, cudaStream_t s) {
+    const long long nn = (long long)n * n;
+    long long bx = (nn + 255) / 256;
+    if (bx > 1024) bx = 1024;
+    k_taylor_base<<<dim3((unsigned)bx, (unsigned)nf), 256, 0, s>>>(nn, m, base, f_off, op_scale, f_pow2, P);
+}
+
+// out[e] = sum_{k=m..1} t[e][k] P_f^k  (+ t[e][0] on the diagonal), for the entries of one chunk
+// (chunk = {factor, first entry, count <= kTaylorChunk}); the m powers of one element stay in registers.
+template <int M>
+__global__ void __launch_bounds__(256) k_taylor_combine(int n, long long nn, const double* __restrict__ P,
+                                                        const int4* __restrict__ chunks, const double* __restrict__ coef,
+                                                        double* __restrict__ out) {
+    __shared__ double t_sh[kTaylorChunk * (M + 1)];
+    const int4 ch = chunks[blockIdx.y];
+    for (int i = threadIdx.x; i < ch.z * (M + 1); i += blockDim.x) t_sh[i] = coef[(long long)ch.y * (M + 1) + i];
+    __syncthreads();
+    const double* p = P + (long long)ch.x * M * nn;
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < nn; e += (long long)gridDim.x * blockDim.x) {
+        double v[M];
+#pragma unroll
+        for (int k = 0; k < M; ++k) v[k] = __ldg(p + k * nn + e);
+        const bool diag = (e / n) == (e % n);
+        for (int i = 0; i < ch.z; ++i) {
+            const double* t = t_sh + i * (M + 1);
+            double acc = __dmul_rn(t[M], v[M - 1]);
+#pragma unroll
+            for (int k = M - 1; k >= 1; --k) acc = fma(t[k], v[k - 1], acc);
+            if (diag) acc = __dadd_rn(acc, t[0]);
+            out[(long long)(ch.y + i) * nn + e] = acc;
+        }
+    }
+}
+
+void launch_taylor_combine(int n, int m, int nchunks, const int* chunks, const double* coef, const double* P, double* out,
+                           cudaStream_t s) {
+    const long long nn = (long long)n * n;
+    long long bx = (nn + 255) / 256;
+    if (bx > 2048) bx = 2048;
+    const dim3 grid((unsigned)bx, (unsigned)nchunks);
+    const int4* ch = reinterpret_cast<const int4*>(chunks);
+    switch (m) {
+#define PQ_TC(MM) \
+    case MM: k_taylor_combine<MM><<<grid, 256, 0, s>>>(n, nn, P, ch, coef, out); break;
+        PQ_TC(16) PQ_TC(18) PQ_TC(20) PQ_TC(24) PQ_TC(28) PQ_TC(32)
+#undef PQ_TC
+        default: throw std::invalid_argument("taylor degree not instantiated");
+    }
+}
+
 __global__ void k_scale_copy(long long total, double op_scale, const double* __restrict__ a, double* __restrict__ out) {
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x)
         out[e] = __dmul_rn(op_scale, a[e]);

@@ -42,6 +42,16 @@ int launch_gemm(const GemmArgs& g, cudaStream_t s);  // returns number of kernel
 // base_off (device, nullable) gives each batch entry its own base matrix offset.
 void launch_expm_prep(int n, int count, const double* base, long long base_stride, const long long* base_off,
                       double op_scale, const double* scale, double* X, int* s_out, cudaStream_t s);
+// ---- shared-power Taylor exponentials (engine.cpp expm_taylor) ----
+constexpr int kTaylorChunk = 8;  // entries per combination block (same factor)
+// P[f*m*n^2 ...] = f_pow2[f] * fl(op_scale * base[f_off[f] ...]) for f < nf (first power, normalised)
+void launch_taylor_base(int n, int nf, int m, const double* base, const long long* f_off, double op_scale,
+                        const double* f_pow2, double* P, cudaStream_t s);
+// chunks: nchunks x int4 {factor, first entry, entry count, 0}; coef: [entry][m+1] Taylor weights;
+// P: [factor][power 1..m][n x n]; out[entry] = sum_k coef[entry][k] P_factor^k (P^0 = I).
+// m in {16, 18, 20, 24, 28, 32}.
+void launch_taylor_combine(int n, int m, int nchunks, const int* chunks, const double* coef, const double* P, double* out,
+                           cudaStream_t s);
 // out = op_scale * a (elementwise, rounded once)
 void launch_scale_copy(long long total, double op_scale, const double* a, double* out, cudaStream_t s);
 void launch_pade_mid(int n, int count, const double* A2, const double* A4, const double* A6, double* T1,
