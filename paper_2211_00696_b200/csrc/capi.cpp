@@ -140,6 +140,7 @@ int pq_ctx_destroy(pq_ctx* c) {
             cudaEventDestroy(c->ev_fork);
             cudaEventDestroy(c->ev_join);
         }
+        if (c->ev_late) cudaEventDestroy(c->ev_late);
         if (c->ev_beta) cudaEventDestroy(c->ev_beta);
         if (c->ev_cc) cudaEventDestroy(c->ev_cc);
         if (c->ev_fac) cudaEventDestroy(c->ev_fac);

@@ -240,6 +240,13 @@ static GemmArgs square_batch(int n, int count, const double* A, const double* B,
 static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>& hint, const int* s_dev, int s_max,
                             double* cur, double* other, double* out);
 
+void ensure_side(pq_ctx& c) {
+    if (c.side) return;
+    cuda_check(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking), "side stream");
+    cuda_check(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming), "fork event");
+    cuda_check(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming), "join event");
+}
+
 struct ExpmEntry {
     long long base_off;  // doubles from `base`
     double scale;        // exact multiplier applied after fl(op_scale * a)
@@ -366,8 +373,12 @@ static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>&
 // the squarings reuse squaring_rounds.  Against an eigendecomposition ground truth this is as
 // accurate as the reference's Pade-13 ("Exponentials").  Returns false (caller uses
 // expm_core) when a norm is unknown or PQ_EXPM=pade.
+//
+// Entries [split, count) are "late" (needed only after the node sweep: the squaring chain and
+// phi_0): with late_async their combination and squaring rounds run on the side stream, which
+// records c.ev_late when done; entries [0, split) are finished on c.stream.
 static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, const std::vector<ExpmEntry>& es,
-                        double* out) {
+                        double* out, int split = -1, bool late_async = false) {
     static const bool disabled = [] {
         const char* v = std::getenv("PQ_EXPM");
         return v && std::string(v) == "pade";
@@ -409,20 +420,28 @@ static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, c
         const double x = std::abs(es[static_cast<size_t>(z)].scale) * gnorm[static_cast<size_t>(fidx[static_cast<size_t>(z)])];
         return x > th ? static_cast<int>(std::ceil(std::log2(x / th))) : 0;
     };
+    if (split < 0 || split > count) split = count;
     // degree: minimise power products + squaring-round batch sizes + a per-launch latency term
+    // (rounds of the late range count a quarter: they overlap the node sweep)
+    auto rounds_cost = [&](const std::vector<int>& s, int z_begin, int z_end) {
+        int smax = 0;
+        for (int z = z_begin; z < z_end; ++z) smax = std::max(smax, s[static_cast<size_t>(z)]);
+        double cost = 6.0 * smax;
+        for (int r = 0; r < smax; ++r) {
+            int z0 = z_begin;
+            while (z0 < z_end && s[static_cast<size_t>(z0)] <= r) ++z0;
+            cost += z_end - z0;
+        }
+        return cost;
+    };
     int best = 0;
     double best_cost = 0.0;
     for (int i = 0; i < 6; ++i) {
         const int m = kM[i];
         std::vector<int> s(static_cast<size_t>(count));
-        int smax = 0;
-        for (int z = 0; z < count; ++z) smax = std::max(smax, s[static_cast<size_t>(z)] = squarings(z, kTh[i]));
-        double cost = nf * (m - 1.0) + 6.0 * (std::ceil(std::log2(static_cast<double>(m))) + smax);
-        for (int r = 0; r < smax; ++r) {
-            int z0 = 0;
-            while (z0 < count && s[static_cast<size_t>(z0)] <= r) ++z0;
-            cost += count - z0;
-        }
+        for (int z = 0; z < count; ++z) s[static_cast<size_t>(z)] = squarings(z, kTh[i]);
+        double cost = nf * (m - 1.0) + 6.0 * std::ceil(std::log2(static_cast<double>(m))) + rounds_cost(s, 0, split) +
+                      (late_async ? 0.25 : 1.0) * rounds_cost(s, split, count);
         if (i == 0 || cost < best_cost) {
             best = i;
             best_cost = cost;
@@ -432,36 +451,40 @@ static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, c
     const double th = kTh[best];
     std::vector<int> hint(static_cast<size_t>(count));
     std::vector<double> coef(static_cast<size_t>(count) * (m + 1));
-    int s_max = 0;
     for (int z = 0; z < count; ++z) {
         const int s = squarings(z, th);
         hint[static_cast<size_t>(z)] = s;
-        s_max = std::max(s_max, s);
         const double alpha =
             std::ldexp(es[static_cast<size_t>(z)].scale * nu[static_cast<size_t>(fidx[static_cast<size_t>(z)])], -s);
         double* t = coef.data() + static_cast<size_t>(z) * (m + 1);
         t[0] = 1.0;
         for (int k = 1; k <= m; ++k) t[k] = t[k - 1] * alpha / k;
     }
-    std::vector<int> chunks;  // int4 {factor, first entry, count, 0}: runs of one factor, <= kTaylorChunk
-    for (int z = 0; z < count;) {
-        int e = z + 1;
-        while (e < count && e - z < kTaylorChunk && fidx[static_cast<size_t>(e)] == fidx[static_cast<size_t>(z)]) ++e;
-        chunks.insert(chunks.end(), {fidx[static_cast<size_t>(z)], z, e - z, 0});
-        z = e;
-    }
-    const int nchunks = static_cast<int>(chunks.size() / 4);
+    // int4 {factor, first entry, count, 0}: runs of one factor, <= kTaylorChunk, per range
+    auto chunks_of = [&](int z_begin, int z_end) {
+        std::vector<int> ch;
+        for (int z = z_begin; z < z_end;) {
+            int e = z + 1;
+            while (e < z_end && e - z < kTaylorChunk && fidx[static_cast<size_t>(e)] == fidx[static_cast<size_t>(z)]) ++e;
+            ch.insert(ch.end(), {fidx[static_cast<size_t>(z)], z, e - z, 0});
+            z = e;
+        }
+        return ch;
+    };
+    const std::vector<int> ch_early = chunks_of(0, split), ch_late = chunks_of(split, count);
     const size_t nn = static_cast<size_t>(n) * n;
     double* P = ws(c, "taylorP", static_cast<size_t>(nf) * m * nn);
     double* T = ws(c, "taylorT", static_cast<size_t>(count) * nn);
     const long long* foff_dev = static_cast<const long long*>(arena_push(c, foff.data(), sizeof(long long) * nf));
     const double* pow2_dev = static_cast<const double*>(arena_push(c, pow2.data(), sizeof(double) * nf));
     const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), sizeof(double) * coef.size()));
-    const int* chunk_dev = static_cast<const int*>(arena_push(c, chunks.data(), sizeof(int) * chunks.size()));
+    const int* che_dev = ch_early.empty() ? nullptr
+                                          : static_cast<const int*>(arena_push(c, ch_early.data(), sizeof(int) * ch_early.size()));
+    const int* chl_dev = ch_late.empty() ? nullptr
+                                         : static_cast<const int*>(arena_push(c, ch_late.data(), sizeof(int) * ch_late.size()));
     const int* s_dev = static_cast<const int*>(arena_push(c, hint.data(), sizeof(int) * count));
     arena_flush(c);
-    cudaStream_t st = c.stream;
-    launch_taylor_base(n, nf, m, base, foff_dev, op_scale, pow2_dev, P, st);
+    launch_taylor_base(n, nf, m, base, foff_dev, op_scale, pow2_dev, P, c.stream);
     count_launch(c);
     const long long lnn = static_cast<long long>(nn), fs = static_cast<long long>(m) * lnn;
     for (int h = 1; h < m; h *= 2) {  // P^(h+j) = P^h P^j, j = 1..min(h, m-h), all factors in one launch
@@ -476,10 +499,41 @@ static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, c
         g.sC2 = lnn;
         gemm(c, g);
     }
-    double* first = (s_max % 2 == 0) ? out : T;
-    launch_taylor_combine(n, m, nchunks, chunk_dev, coef_dev, P, first, st);
-    count_launch(c);
-    squaring_rounds(c, n, count, hint, s_dev, s_max, first, first == out ? T : out, out);
+    // combination + squaring rounds of entries [z_begin, z_end) on c.stream
+    auto finish = [&](int z_begin, int z_end, const std::vector<int>& ch, const int* ch_dev) {
+        if (z_end <= z_begin) return;
+        const std::vector<int> h(hint.begin() + z_begin, hint.begin() + z_end);
+        const int s_max = *std::max_element(h.begin(), h.end());
+        double* o = out + static_cast<size_t>(z_begin) * nn;
+        double* t = T + static_cast<size_t>(z_begin) * nn;
+        double* first = (s_max % 2 == 0) ? o : t;
+        // the combination kernel indexes absolute entries: shift the base so entry z_begin lands at `first`
+        launch_taylor_combine(n, m, static_cast<int>(ch.size() / 4), ch_dev, coef_dev, P,
+                              first - static_cast<size_t>(z_begin) * nn, c.stream);
+        count_launch(c);
+        squaring_rounds(c, n, z_end - z_begin, h, s_dev + z_begin, s_max, first, first == o ? t : o, o);
+    };
+    finish(0, split, ch_early, che_dev);
+    if (split < count) {
+        if (late_async) {
+            ensure_side(c);
+            if (!c.ev_late) cuda_check(cudaEventCreateWithFlags(&c.ev_late, cudaEventDisableTiming), "late event");
+            cuda_check(cudaEventRecord(c.ev_fork, c.stream), "late fork");
+            cuda_check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "late fork wait");
+            cudaStream_t main_stream = c.stream;
+            c.stream = c.side;
+            try {
+                finish(split, count, ch_late, chl_dev);
+            } catch (...) {
+                c.stream = main_stream;
+                throw;
+            }
+            c.stream = main_stream;
+            cuda_check(cudaEventRecord(c.ev_late, c.side), "late record");
+        } else {
+            finish(split, count, ch_late, chl_dev);
+        }
+    }
     check_launch(c);
     return true;
 }
@@ -493,21 +547,29 @@ void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_
 
 // All 1-D exponentials one phi call needs, computed in ONE batch per distinct factor size:
 //   node[k] + a*n_k^2 = expm((1 - theta_a) 2^-l fl(s A_k))   (phiaction.hpp:90, :197)
-//   sq[k]             = expm(2^-l fl(s A_k))                  (phiaction.hpp:294-296)
+//   sq[k] + j*n_k^2   = expm(2^(j-l) fl(s A_k)), j < sq_len  (phiaction.hpp:294-296: the reference
+//                       squares E after every doubling step; with sq_chain the whole chain
+//                       E, E^2, E^4, ... is evaluated directly, sq_len = l, else sq_len = 1)
 //   phi0[k]           = expm(fl(s A_k))                       (kron.hpp:125)
 // Bitwise-identical factors are exponentiated once (e.g. the isotropic Laplacians of configs
-// 1, 3, 4, 5): dims sharing a factor share the pointers.
+// 1, 3, 4, 5): dims sharing a factor share the pointers.  With late_async the squaring chain and
+// phi_0 matrices are finished on the side stream (late = true: wait on c.ev_late before use).
 struct PhiExps {
     const double* node[3] = {nullptr, nullptr, nullptr};
     const double* sq[3] = {nullptr, nullptr, nullptr};
     const double* phi0[3] = {nullptr, nullptr, nullptr};
+    int sq_len = 1;
+    bool late = false;
 };
 
 static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, const std::vector<double>& thetas,
-                                bool want_sq, bool want_phi0, const std::string& tag) {
+                                bool want_sq, bool want_phi0, const std::string& tag, bool sq_chain = false,
+                                bool late_async = false) {
     PhiExps px;
     const int q = static_cast<int>(thetas.size());
-    const int per = q + (want_sq ? 1 : 0) + (want_phi0 ? 1 : 0);
+    const int L = want_sq ? (sq_chain ? std::max(l, 1) : 1) : 0;
+    px.sq_len = std::max(L, 1);
+    const int per = q + L + (want_phi0 ? 1 : 0);
     if (per == 0) return px;
     // canonical factors
     int canon[3] = {0, 1, 2};
@@ -535,24 +597,30 @@ static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, con
                 group.push_back(j);
                 done[j] = 1;
             }
-        // batch layout [nodes of every factor][squaring matrices][phi_0 matrices]: the large-norm
-        // phi_0 arguments form the suffix, so only they take expm squaring rounds
+        // batch layout [nodes of every factor][squaring chain of every factor][phi_0 matrices]:
+        // the large-norm late arguments form the suffix, so only they take squaring rounds
         std::vector<ExpmEntry> es;
         for (int f : group) {
             const long long bo = static_cast<long long>(off[f]);
             for (int a = 0; a < q; ++a) es.push_back({bo, std::ldexp(1.0 - thetas[static_cast<size_t>(a)], -l), op.one_norm[f]});
         }
-        if (want_sq)
-            for (int f : group) es.push_back({static_cast<long long>(off[f]), std::ldexp(1.0, -l), op.one_norm[f]});
+        const int split = static_cast<int>(es.size());
+        for (int f : group)
+            for (int j = 0; j < L; ++j) es.push_back({static_cast<long long>(off[f]), std::ldexp(1.0, j - l), op.one_norm[f]});
         if (want_phi0)
             for (int f : group) es.push_back({static_cast<long long>(off[f]), 1.0, op.one_norm[f]});
         const size_t nn = static_cast<size_t>(n) * n, ng = group.size();
         double* out = ws(c, tag + "_n" + std::to_string(n), es.size() * nn);
-        if (!expm_taylor(c, n, base, s, es, out)) expm_core(c, n, base, s, es, out);
+        // the side stream is in order, so waiting on the last ev_late covers every group's late work
+        const bool async = late_async && split < static_cast<int>(es.size());
+        if (expm_taylor(c, n, base, s, es, out, split, async))
+            px.late = px.late || async;
+        else
+            expm_core(c, n, base, s, es, out);
         for (size_t g = 0; g < ng; ++g) {
             px.node[group[g]] = out + g * q * nn;
-            px.sq[group[g]] = want_sq ? out + (ng * q + g) * nn : nullptr;
-            px.phi0[group[g]] = want_phi0 ? out + (ng * q + (want_sq ? ng : 0) + g) * nn : nullptr;
+            px.sq[group[g]] = L > 0 ? out + (ng * q + g * L) * nn : nullptr;
+            px.phi0[group[g]] = want_phi0 ? out + (ng * q + ng * L + g) * nn : nullptr;
         }
     }
     for (int k = 0; k < op.d; ++k) {
@@ -955,10 +1023,13 @@ void phi_adaptive_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const do
 // phiaction.hpp:255-272 + 290-301: l doubling steps with E_k (= expm(2^-l A_k) on entry),
 // squared after each step but the last.  y [nb][p][N] holds phi_j(2^-l A) b on entry; the
 // result lands in y when l is even and in `partner` when l is odd (ping-pong, no copy).
+// With sq_len >= l, E_in[k] already holds the chain E, E^2, ..., E^(2^(l-1)) (phi_exponentials
+// sq_chain) and no matrix squaring is issued here.
 static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int p, double* y, double* partner,
-                                 const double* const* E_in) {
+                                 const double* const* E_in, int sq_len = 1) {
     if (l <= 0) return y;
     const long long N = op.N;
+    const bool chain = sq_len >= l;
     // Distinct exponentials grouped by size, copied into contiguous ping-pong slots so each
     // step's E <- E E is one batched DMMA launch per size (dims sharing an exponential share it).
     struct Group {
@@ -969,7 +1040,7 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
     std::vector<Group> groups;
     int slot_dim[3] = {-1, -1, -1};  // k -> (group, index)
     int slot_idx[3] = {0, 0, 0};
-    for (int k = 0; k < op.d; ++k) {
+    for (int k = 0; k < op.d && !chain; ++k) {
         int same = -1;
         for (int j = 0; j < k; ++j)
             if (E_in[j] == E_in[k]) same = j;
@@ -1025,12 +1096,13 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
     double* nxt = partner;
     for (int step = 0; step < l; ++step) {
         const double* E[3];
-        for (int k = 0; k < op.d; ++k) E[k] = cur_E(k);
+        for (int k = 0; k < op.d; ++k)
+            E[k] = chain ? E_in[k] + static_cast<size_t>(step) * op.n[k] * op.n[k] : cur_E(k);
         mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, Epilogue{});
         launch_sq_combine(N, p, nb, nxt, cur, coef_dev, c.stream);
         count_launch(c);
         std::swap(cur, nxt);
-        if (step < l - 1) {
+        if (step < l - 1 && !chain) {
             for (const Group& G : groups) {
                 const size_t nn = static_cast<size_t>(G.n) * G.n;
                 const int cnt = static_cast<int>(G.dims.size());
@@ -1070,7 +1142,10 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
     if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
     if (p < 1) throw std::invalid_argument(kind == kGauss ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
     const NodesWeights& rule = kind == kGauss ? memo_rule(kGauss, n + 1) : memo_rule(kClenshaw, 25);
-    const PhiExps px = phi_exponentials(c, op, scale, l, rule.x, l > 0, phi0_out != nullptr, "nodeE");
+    // squaring chain and phi_0 exponentials are finished on the side stream during the node sweep
+    // (not while profiling, so per-launch events stay unambiguous)
+    const PhiExps px = phi_exponentials(c, op, scale, l, rule.x, l > 0, phi0_out != nullptr, "nodeE", true,
+                                        !c.profiling);
     mark(c, "exps");
     double* partner = l > 0 ? ws(c, "sqT", static_cast<size_t>(nb) * p * op.N) : nullptr;
     double* first = (l % 2 == 1) ? partner : out;  // the l-step ping-pong then ends in `out`
@@ -1093,11 +1168,7 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
     // so per-launch events stay unambiguous)
     const bool side_phi0 = phi0_out && l > 0 && !c.profiling;
     if (side_phi0) {
-        if (!c.side) {
-            cuda_check(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking), "side stream");
-            cuda_check(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming), "fork event");
-            cuda_check(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming), "join event");
-        }
+        ensure_side(c);
         cuda_check(cudaEventRecord(c.ev_fork, c.stream), "fork");
         cuda_check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "fork wait");
         cudaStream_t main_stream = c.stream;
@@ -1111,8 +1182,9 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
         c.stream = main_stream;
         cuda_check(cudaEventRecord(c.ev_join, c.side), "join record");
     }
+    if (px.late) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_late, 0), "late exps wait");
     if (l > 0) {
-        double* res = squaring_pingpong(c, op, l, nb, p, first, first == out ? partner : out, px.sq);
+        double* res = squaring_pingpong(c, op, l, nb, p, first, first == out ? partner : out, px.sq, px.sq_len);
         if (res != out)
             cuda_check(cudaMemcpyAsync(out, res, sizeof(double) * nb * p * op.N, cudaMemcpyDeviceToDevice, c.stream),
                        "plan copy");

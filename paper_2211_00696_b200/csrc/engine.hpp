@@ -56,6 +56,7 @@ struct pq_ctx {
     // side stream for work independent of the node sweep (phi_0), joined back before returning
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_late = nullptr;  // late exponentials (squaring chain, phi_0) finished on `side`
     cudaEvent_t ev_beta = nullptr;  // beta readback (phiquadmv) completes
     cudaEvent_t ev_cc = nullptr;    // adaptive CC error readback completes
     // factor uploads: pinned staging (no implicit stream sync) + per-slot cache of the last
@@ -144,6 +145,7 @@ int gemm(pq_ctx& c, const GemmArgs& g);
 void prof_collect(pq_ctx& c);  // syncs, folds recorded events into prof_ms/prof_flops
 void mark(pq_ctx& c, const char* name);  // timeline mark (no-op unless profiling)
 void check_launch(pq_ctx& c);
+void ensure_side(pq_ctx& c);  // creates the side stream and its fork/join events on first use
 
 // ---- device building blocks ----
 DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const std::string& slot);
