@@ -96,7 +96,12 @@ void arena_flush(pq_ctx& c) {
     }
 }
 
-void count_launch(pq_ctx& c, int n) { c.launches += static_cast<uint64_t>(n); }
+// Every launch site counts its kernels here, so launch-configuration errors surface at the launch
+// that caused them (cudaGetLastError is a host-side query, no synchronisation).
+void count_launch(pq_ctx& c, int n) {
+    c.launches += static_cast<uint64_t>(n);
+    cuda_check(cudaGetLastError(), "kernel launch");
+}
 
 static cudaEvent_t prof_event(pq_ctx& c) {
     if (c.ev_used == c.ev_pool.size()) {
@@ -915,7 +920,10 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             count_launch(c);
         }
     };
-    combine_all(*rule, slot_of, accs[cur]);
+    // p <= 8: each level is one fused pass (combination + coarse rule + error statistics); the
+    // 7-point result is only ever compared against, so it never goes to memory
+    const bool fused = p <= 8;
+    if (!fused) combine_all(*rule, slot_of, accs[cur]);
     double* stats = ws(c, "ccstats", 2 * static_cast<size_t>(nb) * p);
     std::vector<double> hstats(2 * static_cast<size_t>(nb) * p);
     int level = 0;
@@ -979,13 +987,43 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         for (int k = 0; k < fresh; ++k)
             fine_slot[static_cast<size_t>(2 * k + 1)] = preswept ? 2 * k + 1 : level_base[level] + k;
         const int nxt = 1 - cur;
-        combine_all(fine, fine_slot, accs[nxt]);
+        // phiaction.hpp:225-240: max over columns of ||y - y_prev||_inf / ||y||_inf
+        if (fused) {
+            std::vector<int> idx(static_cast<size_t>(fine.size()));
+            std::iota(idx.begin(), idx.end(), 0);
+            std::vector<double> cf, cc;
+            node_coefs(fine, idx, p, cf);
+            const double* cf_dev = static_cast<const double*>(arena_push(c, cf.data(), cf.size() * sizeof(double)));
+            const double* cc_dev = nullptr;
+            if (level == 1) {  // coarse rule node k = fine node 2k
+                std::vector<int> cidx(static_cast<size_t>(rule->size()));
+                std::iota(cidx.begin(), cidx.end(), 0);
+                std::vector<double> c7;
+                node_coefs(*rule, cidx, p, c7);
+                cc.assign(cf.size(), 0.0);
+                for (int k = 0; k < rule->size(); ++k)
+                    for (int j = 0; j < p; ++j)
+                        cc[static_cast<size_t>(2 * k) * p + j] = c7[static_cast<size_t>(k) * p + j];
+                cc_dev = static_cast<const double*>(arena_push(c, cc.data(), cc.size() * sizeof(double)));
+            }
+            const int* sl_dev = static_cast<const int*>(arena_push(c, fine_slot.data(), fine_slot.size() * sizeof(int)));
+            arena_flush(c);
+            cuda_check(cudaMemsetAsync(stats, 0, sizeof(double) * 2 * nb * p, c.stream), "cc stats zero");
+            for (int m = 0; m < nb; ++m) {
+                launch_combine_stats(N, p, fine.size(), pool + static_cast<long long>(m) * N, static_cast<long long>(nb) * N,
+                                     sl_dev, cf_dev, cc_dev,
+                                     level == 1 ? nullptr : accs[cur] + static_cast<long long>(m) * p * N,
+                                     accs[nxt] + static_cast<long long>(m) * p * N, N, stats + 2 * m * p, c.stream);
+                count_launch(c);
+            }
+        } else {
+            combine_all(fine, fine_slot, accs[nxt]);
+            launch_colstats(N, nb * p, accs[nxt], accs[cur], stats, c.stream);
+            count_launch(c);
+        }
         half = half_next;
         rule = &fine;
         slot_of = std::move(fine_slot);
-        // phiaction.hpp:225-240: max over columns of ||y - y_prev||_inf / ||y||_inf
-        launch_colstats(N, nb * p, accs[nxt], accs[cur], stats, c.stream);
-        count_launch(c);
         double* hs = pinned_stats ? c.h_small : hstats.data();
         cuda_check(cudaMemcpyAsync(hs, stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
                    "cc stats readback");

@@ -11,9 +11,13 @@
 //    for the adaptive CC error (phiaction.hpp:225-239), ETD elementwise terms.
 #include "kernels.hpp"
 
+#include <algorithm>
 #include <cstdio>
+#include <mutex>
+#include <set>
 #include <cstdlib>
 #include <stdexcept>
+#include <type_traits>
 
 namespace pqb {
 
@@ -780,24 +784,6 @@ void launch_fill_identity(int n, int count, double* out, cudaStream_t s) {
 
 // ==================================================================== HBM-bound ============
 
-// acc_j += c_ij v_i over nodes i in ascending order; P register accumulators.
-template <int P>
-__global__ void k_combine(long long N, int q, const double* __restrict__ V, long long vstride,
-                          const int* __restrict__ slots, const double* __restrict__ coef, double* acc,
-                          long long acc_stride, int zero) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
-        double y[P];
-#pragma unroll
-        for (int j = 0; j < P; ++j) y[j] = zero ? 0.0 : acc[j * acc_stride + t];
-        for (int i = 0; i < q; ++i) {
-            const double v = __ldg(V + slots[i] * vstride + t);
-#pragma unroll
-            for (int j = 0; j < P; ++j) y[j] = __dadd_rn(y[j], __dmul_rn(coef[i * P + j], v));
-        }
-#pragma unroll
-        for (int j = 0; j < P; ++j) acc[j * acc_stride + t] = y[j];
-    }
-}
 
 // Doubling combination of one squaring step (phiaction.hpp:260-268), in place over T:
 //   T_i <- 2^-i T_i + sum_{j<=i} (2^-i / (i-j)!) Y_j     (= 2^-i (E y_i + sum_j y_j/(i-j)!))
@@ -900,57 +886,340 @@ __global__ void k_combine_any(long long N, int p, int q, const double* __restric
     }
 }
 
-// 16-byte variant of k_combine (adjacent element pair per thread, same per-element arithmetic).
-template <int P>
-__global__ void k_combine2(long long N2, int q, const double2* __restrict__ V, long long vstride2,
-                           const int* __restrict__ slots, const double* __restrict__ coef, double2* acc,
-                           long long acc_stride2, int zero) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N2; t += (long long)gridDim.x * blockDim.x) {
-        double2 y[P];
+// nonnegative doubles order like their bit patterns
+__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
+    atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
+}
+
+// Streaming node combination shared by the fixed-rule sweep and the adaptive-CC ladder:
+//   acc_j = (zero ? 0 : acc_j) + sum_{i ascending} cf[i][j] V[slots[i]]   (mul then add, as k_combine)
+// MODE 0: plain.  MODE 1: also the coarse rule sum_i cc[i][j] V[slots[i]] from the same reads and
+// per-column stats max|acc_j - coarse_j|, max|acc_j|.  MODE 2: stats against prev_j (read back).
+// W = 2: each thread owns an element pair (16-byte accesses).  Coefficients and slots are staged in
+// shared memory (q <= kCombineSmemNodes) and nodes are consumed four at a time so four independent
+// 16-byte loads per thread are in flight.
+constexpr int kCombineSmemNodes = 128;
+constexpr int kCombineRing = 8;  // cp.async slots per thread in k_node_combine_ring
+constexpr int kCombineBlocksPerSM = 3;
+constexpr int kCombineRing1 = 12;
+template <int P, int W, int MODE, int U = 4, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_node_combine(long long NW, int q, const double* __restrict__ V, long long vs,
+                                                      const int* __restrict__ slots, const double* __restrict__ cf,
+                                                      const double* __restrict__ cc, const double* __restrict__ prev,
+                                                      double* acc, long long as, int zero, double* stats) {
+    using VT = typename std::conditional<W == 2, double2, double>::type;
+    __shared__ double s_cf[kCombineSmemNodes * P];
+    __shared__ double s_cc[MODE == 1 ? kCombineSmemNodes * P : 1];
+    __shared__ int s_sl[kCombineSmemNodes];
+    const bool staged = q <= kCombineSmemNodes;
+    if (staged) {
+        for (int i = threadIdx.x; i < q * P; i += blockDim.x) {
+            s_cf[i] = cf[i];
+            if (MODE == 1) s_cc[i] = cc[i];
+        }
+        for (int i = threadIdx.x; i < q; i += blockDim.x) s_sl[i] = slots[i];
+        __syncthreads();
+    }
+    const double* CF = staged ? s_cf : cf;
+    const double* CC = staged ? s_cc : cc;
+    const int* SL = staged ? s_sl : slots;
+    const VT* Vv = reinterpret_cast<const VT*>(V);
+    VT* A = reinterpret_cast<VT*>(acc);
+    double dmax[MODE ? P : 1], nmax[MODE ? P : 1];
 #pragma unroll
-        for (int j = 0; j < P; ++j) y[j] = zero ? make_double2(0.0, 0.0) : acc[j * acc_stride2 + t];
-#pragma unroll 4
-        for (int i = 0; i < q; ++i) {
-            const double2 v = __ldg(V + slots[i] * vstride2 + t);
+    for (int j = 0; j < (MODE ? P : 1); ++j) dmax[j] = nmax[j] = 0.0;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < NW; t += (long long)gridDim.x * blockDim.x) {
+        double yf[P][W], yc[MODE == 1 ? P : 1][W];
 #pragma unroll
-            for (int j = 0; j < P; ++j) {
-                const double cij = coef[i * P + j];
-                y[j].x = __dadd_rn(y[j].x, __dmul_rn(cij, v.x));
-                y[j].y = __dadd_rn(y[j].y, __dmul_rn(cij, v.y));
+        for (int j = 0; j < P; ++j) {
+            if (zero) {
+#pragma unroll
+                for (int w = 0; w < W; ++w) yf[j][w] = 0.0;
+            } else {
+                const VT a = A[j * as + t];
+#pragma unroll
+                for (int w = 0; w < W; ++w) yf[j][w] = reinterpret_cast<const double*>(&a)[w];
             }
         }
+        if (MODE == 1) {
 #pragma unroll
-        for (int j = 0; j < P; ++j) acc[j * acc_stride2 + t] = y[j];
+            for (int j = 0; j < (MODE == 1 ? P : 1); ++j)
+#pragma unroll
+                for (int w = 0; w < W; ++w) yc[j][w] = 0.0;
+        }
+        auto accumulate = [&](int i, const VT& v) {
+            const double* pv = reinterpret_cast<const double*>(&v);
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const double a = CF[i * P + j];
+#pragma unroll
+                for (int w = 0; w < W; ++w) yf[j][w] = __dadd_rn(yf[j][w], __dmul_rn(a, pv[w]));
+                if (MODE == 1) {
+                    const double b = CC[i * P + j];
+#pragma unroll
+                    for (int w = 0; w < W; ++w) yc[j][w] = __dadd_rn(yc[j][w], __dmul_rn(b, pv[w]));
+                }
+            }
+        };
+        int i = 0;
+        for (; i + U <= q; i += U) {
+            VT v[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) v[u] = __ldg(Vv + SL[i + u] * vs + t);
+#pragma unroll
+            for (int u = 0; u < U; ++u) accumulate(i + u, v[u]);
+        }
+        for (; i < q; ++i) accumulate(i, __ldg(Vv + SL[i] * vs + t));
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            VT o;
+            double* po = reinterpret_cast<double*>(&o);
+#pragma unroll
+            for (int w = 0; w < W; ++w) po[w] = yf[j][w];
+            A[j * as + t] = o;
+            if (MODE) {
+                double cw[W];
+                if (MODE == 2) {
+                    const VT pr = reinterpret_cast<const VT*>(prev)[j * as + t];
+#pragma unroll
+                    for (int w = 0; w < W; ++w) cw[w] = reinterpret_cast<const double*>(&pr)[w];
+                } else {
+#pragma unroll
+                    for (int w = 0; w < W; ++w) cw[w] = yc[MODE == 1 ? j : 0][w];
+                }
+#pragma unroll
+                for (int w = 0; w < W; ++w) {
+                    nmax[MODE ? j : 0] = fmax(nmax[MODE ? j : 0], fabs(yf[j][w]));
+                    dmax[MODE ? j : 0] = fmax(dmax[MODE ? j : 0], fabs(yf[j][w] - cw[w]));
+                }
+            }
+        }
     }
+    if (MODE) {
+        __shared__ double sd[MODE ? P : 1][8], sn[MODE ? P : 1][8];
+#pragma unroll
+        for (int j = 0; j < (MODE ? P : 1); ++j) {
+            for (int o = 16; o > 0; o >>= 1) {
+                dmax[j] = fmax(dmax[j], __shfl_xor_sync(0xffffffffu, dmax[j], o));
+                nmax[j] = fmax(nmax[j], __shfl_xor_sync(0xffffffffu, nmax[j], o));
+            }
+            if ((threadIdx.x & 31) == 0) {
+                sd[j][threadIdx.x >> 5] = dmax[j];
+                sn[j][threadIdx.x >> 5] = nmax[j];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < P) {
+            const int j = threadIdx.x;
+            double d = 0.0, n = 0.0;
+            for (int w = 0; w < (int)blockDim.x / 32; ++w) {
+                d = fmax(d, sd[j][w]);
+                n = fmax(n, sn[j][w]);
+            }
+            // same-address atomics serialise in L2: only blocks that raise the running max issue one
+            if (d > __ldcg(stats + 2 * j)) atomic_max_nonneg(stats + 2 * j, d);
+            if (n > __ldcg(stats + 2 * j + 1)) atomic_max_nonneg(stats + 2 * j + 1, n);
+        }
+    }
+}
+
+// 16-byte variant of k_node_combine fed by a per-thread cp.async ring: thread-private shared
+// memory slots [D][blockDim] keep D x 16 B of node data in flight per thread without spending
+// registers on it and without block barriers (each thread reads only what it copied itself; a
+// slot is refilled after the value read from it has been consumed, in program order).  The ring
+// runs continuously over the flattened (element pair, node) sequence of a persistent thread, so
+// the next pair's first nodes stream in while the current pair finishes.  Same arithmetic and
+// order as k_node_combine.
+__device__ __forceinline__ void ring_copy16(unsigned dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(src));
+}
+__device__ __forceinline__ void ring_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void ring_wait() {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+template <int P, int MODE, int D, int MINB = 1>
+__global__ void __launch_bounds__(256, MINB) k_node_combine_ring(long long NW, int q, const double2* __restrict__ V, long long vs,
+                                                                 const int* __restrict__ slots, const double* __restrict__ cf,
+                                                                 const double* __restrict__ cc, const double2* __restrict__ prev,
+                                                                 double2* acc, long long as, int zero, double* stats) {
+    extern __shared__ __align__(16) double2 ring[];  // [D][blockDim.x]
+    __shared__ double s_cf[kCombineSmemNodes * P];
+    __shared__ double s_cc[MODE == 1 ? kCombineSmemNodes * P : 1];
+    __shared__ int s_sl[kCombineSmemNodes];
+    const bool staged = q <= kCombineSmemNodes;
+    if (staged) {
+        for (int i = threadIdx.x; i < q * P; i += blockDim.x) {
+            s_cf[i] = cf[i];
+            if (MODE == 1) s_cc[i] = cc[i];
+        }
+        for (int i = threadIdx.x; i < q; i += blockDim.x) s_sl[i] = slots[i];
+        __syncthreads();
+    }
+    const double* CF = staged ? s_cf : cf;
+    const double* CC = staged ? s_cc : cc;
+    const int* SL = staged ? s_sl : slots;
+    const unsigned ring0 = static_cast<unsigned>(__cvta_generic_to_shared(ring + threadIdx.x));
+    const unsigned slot_bytes = 16u * blockDim.x;
+    const long long stride = (long long)gridDim.x * blockDim.x;
+    const long long t0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    // issue cursor over (pair, node): pair t_iss, node i_iss
+    long long t_iss = t0;
+    int i_iss = 0, slot_iss = 0;
+    auto issue = [&]() {
+        if (t_iss < NW) {
+            ring_copy16(ring0 + slot_iss * slot_bytes, V + SL[i_iss] * vs + t_iss);
+            if (++i_iss == q) {
+                i_iss = 0;
+                t_iss += stride;
+            }
+        }
+        ring_commit();  // an empty group keeps the wait_group arithmetic uniform
+        slot_iss = slot_iss + 1 == D ? 0 : slot_iss + 1;
+    };
+#pragma unroll 1
+    for (int u = 0; u < D; ++u) issue();
+    double dmax[MODE ? P : 1], nmax[MODE ? P : 1];
+#pragma unroll
+    for (int j = 0; j < (MODE ? P : 1); ++j) dmax[j] = nmax[j] = 0.0;
+    int slot = 0;
+    for (long long t = t0; t < NW; t += stride) {
+        double2 yf[P], yc[MODE == 1 ? P : 1];
+#pragma unroll
+        for (int j = 0; j < P; ++j) yf[j] = zero ? make_double2(0.0, 0.0) : acc[j * as + t];
+        if (MODE == 1) {
+#pragma unroll
+            for (int j = 0; j < (MODE == 1 ? P : 1); ++j) yc[j] = make_double2(0.0, 0.0);
+        }
+        for (int i = 0; i < q; ++i) {
+            ring_wait<D - 1>();  // the oldest group (this node) has landed
+            const double2 v = ring[slot * blockDim.x + threadIdx.x];
+#pragma unroll
+            for (int j = 0; j < P; ++j) {
+                const double a = CF[i * P + j];
+                yf[j].x = __dadd_rn(yf[j].x, __dmul_rn(a, v.x));
+                yf[j].y = __dadd_rn(yf[j].y, __dmul_rn(a, v.y));
+                if (MODE == 1) {
+                    const double b = CC[i * P + j];
+                    yc[j].x = __dadd_rn(yc[j].x, __dmul_rn(b, v.x));
+                    yc[j].y = __dadd_rn(yc[j].y, __dmul_rn(b, v.y));
+                }
+            }
+            issue();  // refills `slot` (slot_iss == slot here)
+            slot = slot + 1 == D ? 0 : slot + 1;
+        }
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            acc[j * as + t] = yf[j];
+            if (MODE) {
+                const double2 cw = MODE == 2 ? prev[j * as + t] : yc[MODE == 1 ? j : 0];
+                nmax[MODE ? j : 0] = fmax(nmax[MODE ? j : 0], fmax(fabs(yf[j].x), fabs(yf[j].y)));
+                dmax[MODE ? j : 0] =
+                    fmax(dmax[MODE ? j : 0], fmax(fabs(yf[j].x - cw.x), fabs(yf[j].y - cw.y)));
+            }
+        }
+    }
+    ring_wait<0>();
+    if (MODE) {
+        __shared__ double sd[MODE ? P : 1][8], sn[MODE ? P : 1][8];
+#pragma unroll
+        for (int j = 0; j < (MODE ? P : 1); ++j) {
+            for (int o = 16; o > 0; o >>= 1) {
+                dmax[j] = fmax(dmax[j], __shfl_xor_sync(0xffffffffu, dmax[j], o));
+                nmax[j] = fmax(nmax[j], __shfl_xor_sync(0xffffffffu, nmax[j], o));
+            }
+            if ((threadIdx.x & 31) == 0) {
+                sd[j][threadIdx.x >> 5] = dmax[j];
+                sn[j][threadIdx.x >> 5] = nmax[j];
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x < P) {
+            const int j = threadIdx.x;
+            double d = 0.0, n = 0.0;
+            for (int w = 0; w < (int)blockDim.x / 32; ++w) {
+                d = fmax(d, sd[j][w]);
+                n = fmax(n, sn[j][w]);
+            }
+            if (d > __ldcg(stats + 2 * j)) atomic_max_nonneg(stats + 2 * j, d);
+            if (n > __ldcg(stats + 2 * j + 1)) atomic_max_nonneg(stats + 2 * j + 1, n);
+        }
+    }
+}
+
+// launches a ring kernel, opting in to > 48 KB of dynamic shared memory once per kernel (the
+// instantiations share one function type, so the flag is keyed by the kernel's address)
+template <class K, class... Args>
+static void ring_launch(K kernel, unsigned grid, size_t smem, cudaStream_t s, Args... args) {
+    static std::mutex mu;
+    static std::set<const void*> opted;
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        if (opted.insert(reinterpret_cast<const void*>(kernel)).second)
+            cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    }
+    kernel<<<grid, 256, smem, s>>>(args...);
+}
+
+// p <= 8 dispatch of k_node_combine; false when p > 8 (callers fall back to the generic kernels)
+static bool node_combine(long long N, int p, int q, const double* V, long long vstride, const int* slots, const double* cf,
+                         const double* cc, const double* prev, double* acc, long long acc_stride, int zero, double* stats,
+                         int mode, cudaStream_t s) {
+    if (p > 8 || p < 1) return false;
+    const bool v2 = N % 2 == 0 && vstride % 2 == 0 && acc_stride % 2 == 0 && aligned16(V) && aligned16(acc) &&
+                    (!prev || aligned16(prev));
+    const int W = v2 ? 2 : 1;
+    const long long NW = N / W;
+    const unsigned grid = grid_for(NW, 256);
+    const long long vs = vstride / W, as = acc_stride / W;
+#define PQ_NC_ARGS NW, q, V, vs, slots, cf, cc, prev, acc, as, zero, stats
+#define PQ_NC(PP)                                                                          \
+    case PP:                                                                               \
+        if (v2) {                                                                          \
+            if (mode == 0) k_node_combine<PP, 2, 0><<<grid, 256, 0, s>>>(PQ_NC_ARGS);      \
+            else if (mode == 1) k_node_combine<PP, 2, 1><<<grid, 256, 0, s>>>(PQ_NC_ARGS); \
+            else k_node_combine<PP, 2, 2><<<grid, 256, 0, s>>>(PQ_NC_ARGS);                \
+        } else {                                                                           \
+            if (mode == 0) k_node_combine<PP, 1, 0><<<grid, 256, 0, s>>>(PQ_NC_ARGS);      \
+            else if (mode == 1) k_node_combine<PP, 1, 1><<<grid, 256, 0, s>>>(PQ_NC_ARGS); \
+            else k_node_combine<PP, 1, 2><<<grid, 256, 0, s>>>(PQ_NC_ARGS);                \
+        }                                                                                  \
+        return true;
+    if (v2) {  // cp.async ring, kCombineRing slots of 16 B per thread, one element pair per thread
+        const size_t ring_bytes = sizeof(double2) * kCombineRing * 256;
+        // persistent: kCombineBlocksPerSM blocks per SM, each thread streaming several pairs
+        long long gb = (NW + 255) / 256;
+        if (gb > 148LL * kCombineBlocksPerSM) gb = 148LL * kCombineBlocksPerSM;
+        const unsigned grid = static_cast<unsigned>(gb);
+        // MODE 1 carries the coarse accumulators too: 2 blocks/SM with a deeper ring
+        const size_t ring_bytes1 = sizeof(double2) * kCombineRing1 * 256;
+        const unsigned grid1 = static_cast<unsigned>(std::min<long long>((NW + 255) / 256, 148LL * 2));
+        const double2* V2 = reinterpret_cast<const double2*>(V);
+        const double2* P2 = reinterpret_cast<const double2*>(prev);
+        double2* A2 = reinterpret_cast<double2*>(acc);
+#define PQ_NR_ARGS NW, q, V2, vs, slots, cf, cc, P2, A2, as, zero, stats
+#define PQ_NR(PP)                                                                                                  \
+    case PP:                                                                                                       \
+        if (mode == 0) k_node_combine_ring<PP, 0, kCombineRing, 3><<<grid, 256, ring_bytes, s>>>(PQ_NR_ARGS);      \
+        else if (mode == 1)                                                                                        \
+            ring_launch(k_node_combine_ring<PP, 1, kCombineRing1, 2>, grid1, ring_bytes1, s, PQ_NR_ARGS);           \
+        else k_node_combine_ring<PP, 2, kCombineRing, 3><<<grid, 256, ring_bytes, s>>>(PQ_NR_ARGS);                \
+        return true;
+        switch (p) { PQ_NR(1) PQ_NR(2) PQ_NR(3) PQ_NR(4) PQ_NR(5) PQ_NR(6) PQ_NR(7) PQ_NR(8) }
+#undef PQ_NR
+#undef PQ_NR_ARGS
+    }
+    switch (p) { PQ_NC(1) PQ_NC(2) PQ_NC(3) PQ_NC(4) PQ_NC(5) PQ_NC(6) PQ_NC(7) PQ_NC(8) }
+#undef PQ_NC
+#undef PQ_NC_ARGS
+    return false;
 }
 
 void launch_combine(long long N, int p, int q, const double* V, long long vstride, const int* slots, const double* coef,
                     double* acc, long long acc_stride, int zero, cudaStream_t s) {
-    if (N % 2 == 0 && vstride % 2 == 0 && acc_stride % 2 == 0 && p <= 8 && aligned16(V) && aligned16(acc)) {
-        const long long N2 = N / 2;
-        const unsigned grid2 = grid_for(N2, 256);
-        const double2* V2 = reinterpret_cast<const double2*>(V);
-        double2* A2 = reinterpret_cast<double2*>(acc);
-        switch (p) {
-#define PQ_COMB2(PP) \
-    case PP: k_combine2<PP><<<grid2, 256, 0, s>>>(N2, q, V2, vstride / 2, slots, coef, A2, acc_stride / 2, zero); return;
-            PQ_COMB2(1) PQ_COMB2(2) PQ_COMB2(3) PQ_COMB2(4) PQ_COMB2(5) PQ_COMB2(6) PQ_COMB2(7) PQ_COMB2(8)
-#undef PQ_COMB2
-        }
-    }
-    const unsigned grid = grid_for(N, 256);
-    switch (p) {
-#define PQ_COMB(PP) \
-    case PP: k_combine<PP><<<grid, 256, 0, s>>>(N, q, V, vstride, slots, coef, acc, acc_stride, zero); break;
-        PQ_COMB(1) PQ_COMB(2) PQ_COMB(3) PQ_COMB(4) PQ_COMB(5) PQ_COMB(6) PQ_COMB(7) PQ_COMB(8)
-#undef PQ_COMB
-        default: k_combine_any<<<grid, 256, 0, s>>>(N, p, q, V, vstride, slots, coef, acc, acc_stride, zero);
-    }
-}
-
-// nonnegative doubles order like their bit patterns
-__device__ __forceinline__ void atomic_max_nonneg(double* addr, double v) {
-    atomicMax(reinterpret_cast<unsigned long long*>(addr), static_cast<unsigned long long>(__double_as_longlong(v)));
+    if (node_combine(N, p, q, V, vstride, slots, coef, nullptr, nullptr, acc, acc_stride, zero, nullptr, 0, s)) return;
+    k_combine_any<<<grid_for(N, 256), 256, 0, s>>>(N, p, q, V, vstride, slots, coef, acc, acc_stride, zero);
 }
 
 __global__ void k_colstats(long long N, const double* __restrict__ y, const double* __restrict__ yp, double* out) {
@@ -982,6 +1251,13 @@ __global__ void k_colstats(long long N, const double* __restrict__ y, const doub
         atomic_max_nonneg(out + 2 * c, dmax);
         atomic_max_nonneg(out + 2 * c + 1, nmax);
     }
+}
+
+// One adaptive-CC ladder level in one pass (phiaction.hpp:175-240): see k_node_combine MODE 1/2.
+bool launch_combine_stats(long long N, int p, int q, const double* V, long long vstride, const int* slots,
+                          const double* cf, const double* cc, const double* prev, double* acc, long long acc_stride,
+                          double* stats, cudaStream_t s) {
+    return node_combine(N, p, q, V, vstride, slots, cf, cc, prev, acc, acc_stride, 1, stats, cc ? 1 : 2, s);
 }
 
 void launch_colstats(long long N, int ncols, const double* y, const double* yp, double* out, cudaStream_t s) {

@@ -75,6 +75,12 @@ void launch_combine(long long N, int p, int q, const double* V, long long vstrid
 // In-place doubling combination of a squaring step: T_i <- 2^-i T_i + sum_{j<=i} coef[i*p+j] Y_j
 // (coef[i][j] = 2^-(i+1)/(i-j)!), columns laid out [nb][p][N].
 void launch_sq_combine(long long N, int p, int nb, double* T, const double* Y, const double* coef, cudaStream_t s);
+// Fused adaptive-CC level (k_combine + coarse rule + k_colstats): acc[j] = sum_i cf[i][j] V[slots[i]];
+// coarse = sum_i cc[i][j] V[slots[i]] (cc != null) or prev[j] (prev != null); stats[2j] max|acc_j -
+// coarse_j|, stats[2j+1] max|acc_j| (atomic max: zero stats first).  False when p > 8.
+bool launch_combine_stats(long long N, int p, int q, const double* V, long long vstride, const int* slots,
+                          const double* cf, const double* cc, const double* prev, double* acc, long long acc_stride,
+                          double* stats, cudaStream_t s);
 // per column c < ncols: out[2c] = max|y_c - yp_c| (yp may be null -> max|y_c|), out[2c+1] = max|y_c|.
 void launch_colstats(long long N, int ncols, const double* y, const double* yp, double* out, cudaStream_t s);
 // out = s1*u + s3*u^3 - au   (Allen-Cahn source minus A u)

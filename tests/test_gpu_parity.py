@@ -139,6 +139,26 @@ def test_adaptive_refuses_unreachable_tolerance(pq):
         pq.phi_adaptive(a, [1.0, 1.0], 2, 1e-30)
 
 
+def test_adaptive_every_p_in_one_process(pq, ref):
+    """Every column count of the fused CC-level kernels (p = 1..8, and p = 9 on the generic path)
+    in one process, then the unreachable-tolerance case: a kernel instantiation that failed to
+    launch once left the ladder with zeroed statistics and a false 'converged'."""
+    rng = np.random.default_rng(606)
+    fs = [rng.uniform(-1, 1, (4, 4)), rng.uniform(-1, 1, (3, 3)), rng.uniform(-1, 1, (2, 2))]
+    b = rng.uniform(-1, 1, 24)
+    for p in [4, 2, 1, 3, 8, 5, 7, 6, 9]:
+        info = {}
+        got = pq.phi_adaptive(pq.KroneckerSum(fs), b, p, 1e-12, info=info)
+        want, pts = ref.phi_adaptive(fs, b, p, 1e-12)
+        assert info["points_used"] == pts, p
+        for j in range(p):
+            assert rel2(got.col(j + 1), want[0][j]) < 1e-11, (p, j)
+    a = pq.KroneckerSum([np.array([[-1.0, 0.2], [0.1, -2.0]])])
+    for p in (2, 4):
+        with pytest.raises(pq.ConvergenceError):
+            pq.phi_adaptive(a, [1.0, 1.0], p, 1e-30)
+
+
 def test_squaring_step(pq, ref):
     rng = np.random.default_rng(9)
     shape = (5, 6, 7)
