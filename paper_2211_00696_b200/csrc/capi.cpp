@@ -141,6 +141,13 @@ int pq_ctx_destroy(pq_ctx* c) {
             cudaEventDestroy(c->ev_join);
         }
         if (c->ev_late) cudaEventDestroy(c->ev_late);
+        if (c->sq2) {
+            cudaStreamSynchronize(c->sq2);
+            cudaStreamDestroy(c->sq2);
+            cudaEventDestroy(c->ev_sqfork);
+        }
+        for (auto e : c->ev_sqA) cudaEventDestroy(e);
+        for (auto e : c->ev_sqB) cudaEventDestroy(e);
         if (c->ev_beta) cudaEventDestroy(c->ev_beta);
         if (c->ev_cc) cudaEventDestroy(c->ev_cc);
         if (c->ev_fac) cudaEventDestroy(c->ev_fac);

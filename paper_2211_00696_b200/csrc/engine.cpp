@@ -245,6 +245,31 @@ static GemmArgs square_batch(int n, int count, const double* A, const double* B,
 static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>& hint, const int* s_dev, int s_max,
                             double* cur, double* other, double* out);
 
+// Two-stream squaring (squaring_pingpong): one RHS, p >= 2, not while profiling (per-launch
+// events must stay unambiguous); PQ_SQ_SPLIT=0 disables it.
+static bool squaring_split_ok(const pq_ctx& c, int nb, int p) {
+    static const bool disabled = [] {
+        const char* v = std::getenv("PQ_SQ_SPLIT");
+        return v && v[0] == '0';
+    }();
+    return !disabled && nb == 1 && p >= 2 && !c.profiling;
+}
+
+// second squaring stream and per-step events for l steps
+static void ensure_sq2(pq_ctx& c, int l) {
+    if (!c.sq2) {
+        cuda_check(cudaStreamCreateWithFlags(&c.sq2, cudaStreamNonBlocking), "sq2 stream");
+        cuda_check(cudaEventCreateWithFlags(&c.ev_sqfork, cudaEventDisableTiming), "sq fork event");
+    }
+    while (static_cast<int>(c.ev_sqA.size()) < l) {
+        cudaEvent_t a, b;
+        cuda_check(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "sq event");
+        cuda_check(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "sq event");
+        c.ev_sqA.push_back(a);
+        c.ev_sqB.push_back(b);
+    }
+}
+
 void ensure_side(pq_ctx& c) {
     if (c.side) return;
     cuda_check(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking), "side stream");
@@ -1130,6 +1155,64 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
     arena_flush(c);
     const int Z1 = nb * p;
     long long Es[3] = {0, 0, 0};
+    if (chain && squaring_split_ok(c, nb, p)) {
+        // Two column halves on two streams, three rotating buffers b_s (step s reads b_s, writes
+        // b_{s+1}).  Lower half [0, h) on c.stream, upper half [h, p) on c.sq2.  The upper
+        // combination of step s reads y_s[j < h]: it waits for the lower combination of step s-1.
+        // The lower chain of step s overwrites b_{s+1} = b_{s-2}, last read by the upper
+        // combination of step s-2.  Everything else is ordered within a stream, so each half's
+        // bandwidth-bound combination runs under the other half's DMMA chain.
+        const int h = p / 2;
+        double* third = ws(c, "sq3", static_cast<size_t>(p) * N);
+        double* b[3];
+        b[0] = y;
+        // rotate so that b_(l mod 3) is `partner` when l mod 3 != 0 (the caller's output then);
+        // for l mod 3 == 0 the result lands in y
+        if (l % 3 == 1) {
+            b[1] = partner;
+            b[2] = third;
+        } else if (l % 3 == 2) {
+            b[1] = third;
+            b[2] = partner;
+        } else {
+            b[1] = partner;
+            b[2] = third;
+        }
+        ensure_sq2(c, l);
+        cuda_check(cudaEventRecord(c.ev_sqfork, c.stream), "sq fork");
+        cuda_check(cudaStreamWaitEvent(c.sq2, c.ev_sqfork, 0), "sq fork wait");
+        const cudaStream_t main_stream = c.stream;
+        try {
+            for (int step = 0; step < l; ++step) {
+                const double* E[3];
+                for (int k = 0; k < op.d; ++k) E[k] = E_in[k] + static_cast<size_t>(step) * op.n[k] * op.n[k];
+                double* cur = b[step % 3];
+                double* nxt = b[(step + 1) % 3];
+                // lower half on the main stream
+                c.stream = main_stream;
+                if (step >= 2) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqB[step - 2], 0), "sq wait B");
+                mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, h, Epilogue{}, "sqchA");
+                launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, 0, h);
+                count_launch(c);
+                cuda_check(cudaEventRecord(c.ev_sqA[step], c.stream), "sq rec A");
+                // upper half on the second stream
+                c.stream = c.sq2;
+                mode_chain(c, op.d, op.n, E, Es, cur + static_cast<size_t>(h) * N, N, nxt + static_cast<size_t>(h) * N, N,
+                           p - h, Epilogue{}, "sqchB");
+                if (step >= 1) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqA[step - 1], 0), "sq wait A");
+                launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, h, p);
+                count_launch(c);
+                cuda_check(cudaEventRecord(c.ev_sqB[step], c.stream), "sq rec B");
+            }
+        } catch (...) {
+            c.stream = main_stream;
+            throw;
+        }
+        c.stream = main_stream;
+        cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqB[l - 1], 0), "sq join");
+        check_launch(c);
+        return b[l % 3];
+    }
     double* cur = y;
     double* nxt = partner;
     for (int step = 0; step < l; ++step) {
@@ -1186,7 +1269,10 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
                                         !c.profiling);
     mark(c, "exps");
     double* partner = l > 0 ? ws(c, "sqT", static_cast<size_t>(nb) * p * op.N) : nullptr;
-    double* first = (l % 2 == 1) ? partner : out;  // the l-step ping-pong then ends in `out`
+    // the squaring then ends in `out`: ping-pong (l odd: start in partner), or the two-stream
+    // three-buffer rotation (l mod 3 != 0: start in partner, squaring_pingpong rotates into out)
+    const bool split_sq = l > 0 && px.sq_len >= l && squaring_split_ok(c, nb, p);
+    double* first = split_sq ? ((l % 3 == 0) ? out : partner) : ((l % 2 == 1) ? partner : out);
     if (kind == kGauss) {
         phi_fixed_shift(c, op, scale, l, nb, bs, p, rule, px, first);
         if (points_used) *points_used = rule.size();

@@ -57,6 +57,10 @@ struct pq_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_late = nullptr;  // late exponentials (squaring chain, phi_0) finished on `side`
+    // two-stream squaring (engine.cpp squaring_pingpong): second stream, fork event, per-step events
+    cudaStream_t sq2 = nullptr;
+    cudaEvent_t ev_sqfork = nullptr;
+    std::vector<cudaEvent_t> ev_sqA, ev_sqB;
     cudaEvent_t ev_beta = nullptr;  // beta readback (phiquadmv) completes
     cudaEvent_t ev_cc = nullptr;    // adaptive CC error readback completes
     // factor uploads: pinned staging (no implicit stream sync) + per-slot cache of the last

@@ -788,33 +788,14 @@ void launch_fill_identity(int n, int count, double* out, cudaStream_t s) {
 // Doubling combination of one squaring step (phiaction.hpp:260-268), in place over T:
 //   T_i <- 2^-i T_i + sum_{j<=i} (2^-i / (i-j)!) Y_j     (= 2^-i (E y_i + sum_j y_j/(i-j)!))
 // for every RHS m (columns [m][i][N]); each element of Y_1..Y_p and T_1..T_p read once.
-template <int P>
-__global__ void k_sq_combine(long long N, int nb, double* __restrict__ T, const double* __restrict__ Y,
-                             const double* __restrict__ coef) {
-    const long long total = N * nb;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-        const long long m = e / N, t = e - m * N;
-        const long long base = m * P * N + t;
-        double y[P];
-#pragma unroll
-        for (int j = 0; j < P; ++j) y[j] = Y[base + j * N];
-#pragma unroll
-        for (int i = 0; i < P; ++i) {
-            double v = __dmul_rn(ldexp(1.0, -(i + 1)), T[base + i * N]);
-#pragma unroll
-            for (int j = 0; j <= i; ++j) v = __dadd_rn(v, __dmul_rn(coef[i * P + j], y[j]));
-            T[base + i * N] = v;
-        }
-    }
-}
 
 __global__ void k_sq_combine_any(long long N, int p, int nb, double* __restrict__ T, const double* __restrict__ Y,
-                                 const double* __restrict__ coef) {
+                                 const double* __restrict__ coef, int i0, int i1) {
     const long long total = N * nb;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
         const long long m = e / N, t = e - m * N;
         const long long base = m * p * N + t;
-        for (int i = 0; i < p; ++i) {
+        for (int i = i0; i < i1; ++i) {
             double v = __dmul_rn(ldexp(1.0, -(i + 1)), T[base + i * N]);
             for (int j = 0; j <= i; ++j) v = __dadd_rn(v, __dmul_rn(coef[i * p + j], Y[base + j * N]));
             T[base + i * N] = v;
@@ -825,16 +806,18 @@ __global__ void k_sq_combine_any(long long N, int p, int nb, double* __restrict_
 // 16-byte variant: each thread owns an adjacent element pair (same arithmetic per element).
 template <int P>
 __global__ void k_sq_combine2(long long N2, int nb, double2* __restrict__ T, const double2* __restrict__ Y,
-                              const double* __restrict__ coef) {
+                              const double* __restrict__ coef, int i0, int i1) {
     const long long total = N2 * nb;
     for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
         const long long m = e / N2, t = e - m * N2;
         const long long base = m * P * N2 + t;
         double2 y[P];
 #pragma unroll
-        for (int j = 0; j < P; ++j) y[j] = Y[base + j * N2];
+        for (int j = 0; j < P; ++j)
+            if (j < i1) y[j] = Y[base + j * N2];
 #pragma unroll
         for (int i = 0; i < P; ++i) {
+            if (i < i0 || i >= i1) continue;
             const double2 ti = T[base + i * N2];
             const double h = ldexp(1.0, -(i + 1));
             double vx = __dmul_rn(h, ti.x), vy = __dmul_rn(h, ti.y);
@@ -851,7 +834,9 @@ __global__ void k_sq_combine2(long long N2, int nb, double2* __restrict__ T, con
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-void launch_sq_combine(long long N, int p, int nb, double* T, const double* Y, const double* coef, cudaStream_t s) {
+void launch_sq_combine(long long N, int p, int nb, double* T, const double* Y, const double* coef, cudaStream_t s,
+                       int i0, int i1) {
+    if (i1 < 0) i1 = p;
     if (N % 2 == 0 && p <= 8 && aligned16(T) && aligned16(Y)) {
         const long long N2 = N / 2;
         const unsigned grid2 = grid_for(N2 * nb, 256);
@@ -859,19 +844,12 @@ void launch_sq_combine(long long N, int p, int nb, double* T, const double* Y, c
         const double2* Y2 = reinterpret_cast<const double2*>(Y);
         switch (p) {
 #define PQ_SQC2(PP) \
-    case PP: k_sq_combine2<PP><<<grid2, 256, 0, s>>>(N2, nb, T2, Y2, coef); return;
+    case PP: k_sq_combine2<PP><<<grid2, 256, 0, s>>>(N2, nb, T2, Y2, coef, i0, i1); return;
             PQ_SQC2(1) PQ_SQC2(2) PQ_SQC2(3) PQ_SQC2(4) PQ_SQC2(5) PQ_SQC2(6) PQ_SQC2(7) PQ_SQC2(8)
 #undef PQ_SQC2
         }
     }
-    const unsigned grid = grid_for(N * nb, 256);
-    switch (p) {
-#define PQ_SQC(PP) \
-    case PP: k_sq_combine<PP><<<grid, 256, 0, s>>>(N, nb, T, Y, coef); break;
-        PQ_SQC(1) PQ_SQC(2) PQ_SQC(3) PQ_SQC(4) PQ_SQC(5) PQ_SQC(6) PQ_SQC(7) PQ_SQC(8)
-#undef PQ_SQC
-        default: k_sq_combine_any<<<grid, 256, 0, s>>>(N, p, nb, T, Y, coef);
-    }
+    k_sq_combine_any<<<grid_for(N * nb, 256), 256, 0, s>>>(N, p, nb, T, Y, coef, i0, i1);
 }
 
 __global__ void k_combine_any(long long N, int p, int q, const double* __restrict__ V, long long vstride,

@@ -74,7 +74,9 @@ void launch_combine(long long N, int p, int q, const double* V, long long vstrid
                     const double* coef, double* acc, long long acc_stride, int zero, cudaStream_t s);
 // In-place doubling combination of a squaring step: T_i <- 2^-i T_i + sum_{j<=i} coef[i*p+j] Y_j
 // (coef[i][j] = 2^-(i+1)/(i-j)!), columns laid out [nb][p][N].
-void launch_sq_combine(long long N, int p, int nb, double* T, const double* Y, const double* coef, cudaStream_t s);
+// Columns i0 <= i < i1 only (default: all p); T_i reads Y_j for j <= i only.
+void launch_sq_combine(long long N, int p, int nb, double* T, const double* Y, const double* coef, cudaStream_t s,
+                       int i0 = 0, int i1 = -1);
 // Fused adaptive-CC level (k_combine + coarse rule + k_colstats): acc[j] = sum_i cf[i][j] V[slots[i]];
 // coarse = sum_i cc[i][j] V[slots[i]] (cc != null) or prev[j] (prev != null); stats[2j] max|acc_j -
 // coarse_j|, stats[2j+1] max|acc_j| (atomic max: zero stats first).  False when p > 8.
