@@ -46,8 +46,8 @@ struct TileCfg {
     static constexpr int MI = WM / 8, NI = WN / 8;
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC>
-__global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, 1) k_gemm(const GemmArgs g) {
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC, int MINB = 1>
+__global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB) k_gemm(const GemmArgs g) {
     using T = TileCfg<BM, BN, BK, WM, WN, ST, BKM>;
     constexpr int NT = T::NT;
     extern __shared__ __align__(16) double smem[];
@@ -399,10 +399,10 @@ static int launch_persist(const GemmArgs& g, int max_ctas, cudaStream_t s) {
     return 1;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC>
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC, int MINB = 1>
 static int launch_cfg(const GemmArgs& g, cudaStream_t s) {
     using T = TileCfg<BM, BN, BK, WM, WN, ST, BKM>;
-    auto kern = k_gemm<BM, BN, BK, WM, WN, ST, BKM, VEC>;
+    auto kern = k_gemm<BM, BN, BK, WM, WN, ST, BKM, VEC, MINB>;
     static bool attr_done = false;  // per instantiation
     if (!attr_done) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
@@ -446,8 +446,12 @@ int launch_gemm_family(const GemmArgs& g, bool vec2, int shape, cudaStream_t s) 
         case 1: return vec2 ? launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 1>(g, s);
         case 2: return vec2 ? launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 2>(g, s) : launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 1>(g, s);
         case 3:
-            // 4 stages still fit 3 CTAs/SM for row-major B (+3%, r01_gemm_tune.txt); the k-major
-            // B tile is larger and would drop to 2 CTAs/SM, so it keeps 3 stages
+            // 16-byte path: BK = 8, 4 stages and <= 128 registers give 4 CTAs (16 warps) per SM,
+            // which keeps the DMMA pipe fed while other warps sit in barriers / epilogues
+            // (+3-4% over 64x64x16 at 3 CTAs/SM on every mode shape, r01_gemm_tune_minb.txt)
+            if (vec2) return launch_cfg<64, 64, 8, 32, 32, 4, BKM, 2, 4>(g, s);
+            // 8-byte path: 4 stages still fit 3 CTAs/SM for row-major B; the k-major B tile is
+            // larger and would drop to 2 CTAs/SM, so it keeps 3 stages
             if constexpr (BKM)
                 return vec2 ? launch_cfg<64, 64, 16, 32, 32, 3, BKM, 2>(g, s) : launch_cfg<64, 64, 16, 32, 32, 3, BKM, 1>(g, s);
             else

@@ -24,12 +24,12 @@ struct Case {
     double flops;
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int ST>
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB = 1>
 float run(const Case& c, int reps, cudaEvent_t e0, cudaEvent_t e1) {
     GemmArgs g = c.g;
     auto f = [&] {
-        if (g.b_kmajor) launch_cfg<BM, BN, BK, WM, WN, ST, true, 2>(g, 0);
-        else launch_cfg<BM, BN, BK, WM, WN, ST, false, 2>(g, 0);
+        if (g.b_kmajor) launch_cfg<BM, BN, BK, WM, WN, ST, true, 2, MINB>(g, 0);
+        else launch_cfg<BM, BN, BK, WM, WN, ST, false, 2, MINB>(g, 0);
     };
     f();
     cudaDeviceSynchronize();
@@ -109,28 +109,20 @@ int main(int argc, char** argv) {
     cudaEventCreate(&e1);
     for (const Case& c : cases) {
         printf("%-9s n=%d Z=%d  GFLOP=%.2f\n", c.name, n, Z, c.flops / 1e9);
-#define T(BM, BN, BK, WM, WN, ST)                                                                      \
+#define T(BM, BN, BK, WM, WN, ST, MINB)                                                                \
     {                                                                                                  \
-        float ms = run<BM, BN, BK, WM, WN, ST>(c, 5, e0, e1);                                          \
+        float ms = run<BM, BN, BK, WM, WN, ST, MINB>(c, 5, e0, e1);                                    \
         if (ms > 0)                                                                                    \
-            printf("  %3dx%3dx%2d w%2dx%2d st%d : %8.1f us  %6.2f TF/s\n", BM, BN, BK, WM, WN, ST, ms * 1e3, \
-                   c.flops / (ms * 1e-3) / 1e12);                                                      \
+            printf("  %3dx%3dx%2d w%2dx%2d st%d minb%d : %8.1f us  %6.2f TF/s\n", BM, BN, BK, WM, WN, ST, MINB, \
+                   ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
     }
-        T(128, 128, 32, 64, 32, 3)
-        T(128, 128, 16, 64, 32, 4)
-        T(128, 128, 16, 32, 64, 4)
-        T(128, 64, 16, 64, 32, 3)
-        T(128, 64, 32, 64, 32, 2)
-        T(128, 64, 16, 32, 32, 3)
-        T(64, 128, 16, 32, 64, 3)
-        T(64, 64, 16, 32, 32, 3)
-        T(64, 64, 32, 32, 32, 3)
-        T(32, 32, 16, 16, 16, 3)
-        T(32, 64, 16, 16, 32, 3)
-        T(64, 32, 16, 32, 16, 3)
-        T(64, 64, 16, 32, 32, 4)
-        T(64, 64, 16, 32, 32, 5)
-        T(64, 64, 8, 32, 32, 6)
+        T(64, 64, 16, 32, 32, 3, 1)
+        T(64, 64, 16, 32, 32, 4, 1)
+        T(64, 64, 16, 32, 32, 2, 4)
+        T(64, 64, 8, 32, 32, 4, 4)
+        T(64, 64, 8, 32, 32, 5, 4)
+        T(64, 64, 8, 32, 32, 6, 3)
+        T(64, 64, 16, 32, 32, 3, 3)
     }
     return 0;
 }
