@@ -289,8 +289,17 @@ def run_ours(args, world, rank, local) -> None:
     }
     if g_ms > 0:
         ach = g_flops / (g_ms / 1e3) / 1e12
+        # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture of
+        # this workload (profiles/r01_gemm_traffic.json); null for workloads without a capture
+        traffic, traffic_src = None, None
+        tpath = Path(__file__).resolve().parent / "profiles" / "r01_gemm_traffic.json"
+        if w.name == "cfg2_advdiff3d_n128_cc_p4" and tpath.exists():
+            t = json.loads(tpath.read_text())
+            traffic = t["mean_dram_bytes_per_launch"]
+            traffic_src = (f"bytes/launch, mean of {len(t['launches'])} mode products in {tpath.name} "
+                           f"(algorithmic {t['algorithmic_bytes_per_launch']:.3g})")
         line["roofline"] = {"bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                            "frac": ach / DMMA_PEAK_TFLOPS, "traffic": None,
+                            "frac": ach / DMMA_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
                             "kernel": "k_gemm (FP64 DMMA mode products + expm products)",
                             "launches": g_launches, "gemm_ms_per_step": g_ms / args.steps,
                             "gemm_share_of_step": (g_ms / args.steps) / (ms_dev / args.steps),

@@ -245,14 +245,16 @@ static GemmArgs square_batch(int n, int count, const double* A, const double* B,
 static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>& hint, const int* s_dev, int s_max,
                             double* cur, double* other, double* out);
 
-// Two-stream squaring (squaring_pingpong): one RHS, p >= 2, not while profiling (per-launch
-// events must stay unambiguous); PQ_SQ_SPLIT=0 disables it.
-static bool squaring_split_ok(const pq_ctx& c, int nb, int p) {
+// Two-stream squaring (squaring_pingpong): one RHS, p >= 2, vectors large enough that a step's
+// GEMMs outweigh the per-step event traffic (config 1, N = 4096: 4330 actions/s without the
+// split, 3368 with it), not while profiling (per-launch events must stay unambiguous);
+// PQ_SQ_SPLIT=0 disables it.
+static bool squaring_split_ok(const pq_ctx& c, int nb, int p, long long N) {
     static const bool disabled = [] {
         const char* v = std::getenv("PQ_SQ_SPLIT");
         return v && v[0] == '0';
     }();
-    return !disabled && nb == 1 && p >= 2 && !c.profiling;
+    return !disabled && nb == 1 && p >= 2 && N >= (1LL << 18) && !c.profiling;
 }
 
 // second squaring stream and per-step events for l steps
@@ -1155,7 +1157,7 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
     arena_flush(c);
     const int Z1 = nb * p;
     long long Es[3] = {0, 0, 0};
-    if (chain && squaring_split_ok(c, nb, p)) {
+    if (chain && squaring_split_ok(c, nb, p, N)) {
         // Two column halves on two streams, three rotating buffers b_s (step s reads b_s, writes
         // b_{s+1}).  Lower half [0, h) on c.stream, upper half [h, p) on c.sq2.  The upper
         // combination of step s reads y_s[j < h]: it waits for the lower combination of step s-1.
@@ -1271,7 +1273,7 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
     double* partner = l > 0 ? ws(c, "sqT", static_cast<size_t>(nb) * p * op.N) : nullptr;
     // the squaring then ends in `out`: ping-pong (l odd: start in partner), or the two-stream
     // three-buffer rotation (l mod 3 != 0: start in partner, squaring_pingpong rotates into out)
-    const bool split_sq = l > 0 && px.sq_len >= l && squaring_split_ok(c, nb, p);
+    const bool split_sq = l > 0 && px.sq_len >= l && squaring_split_ok(c, nb, p, op.N);
     double* first = split_sq ? ((l % 3 == 0) ? out : partner) : ((l % 2 == 1) ? partner : out);
     if (kind == kGauss) {
         phi_fixed_shift(c, op, scale, l, nb, bs, p, rule, px, first);
