@@ -77,8 +77,12 @@ PQ_API int pq_ctx_set_profiling(pq_ctx* ctx, int on);
 PQ_API int pq_ctx_phase_times(pq_ctx* ctx, double* ms6);
 /* With profiling on, every DMMA GEMM launch (mode products and expm products) is bracketed by
  * CUDA events on the context stream.  Returns (synchronising) the number of such launches, their
- * summed device time in ms and their summed algorithmic FLOPs (2*M*N*K per batch entry, dense). */
+ * summed device time in ms and the FLOPs their CTAs executed (negligible exponential blocks
+ * skipped; counted on the device). */
 PQ_API int pq_ctx_gemm_stats(pq_ctx* ctx, int reset, uint64_t* launches, double* ms, double* flops);
+/* Same launches: 2*M*N*K per batch entry, i.e. the dense mode-product work of the reference's
+ * algorithm (kron.hpp:65-108) without any block skipped. */
+PQ_API int pq_ctx_gemm_dense_flops(pq_ctx* ctx, int reset, double* flops);
 /* With profiling on, phase boundaries are marked (device event + host clock).  Returns (and
  * clears, synchronising) a JSON array [{"mark","gpu_us","host_us"}] relative to the first mark. */
 PQ_API int pq_ctx_timeline(pq_ctx* ctx, const char** json);

@@ -132,6 +132,7 @@ int pq_ctx_destroy(pq_ctx* c) {
         cudaFree(c->d_err);
         cudaFree(c->d_int);
         cudaFree(c->d_small);
+        if (c->d_flops) cudaFree(c->d_flops);
         cudaFreeHost(c->h_small);
         for (auto e : c->ev_pool) cudaEventDestroy(e);
         if (c->side) {
@@ -224,6 +225,15 @@ int pq_ctx_gemm_stats(pq_ctx* c, int reset, uint64_t* launches, double* ms, doub
             c->prof_launches = 0;
             c->prof_ms = c->prof_flops = 0.0;
         }
+    });
+}
+
+int pq_ctx_gemm_dense_flops(pq_ctx* c, int reset, double* flops) {
+    return guarded([&] {
+        need_ctx(c);
+        prof_collect(*c);
+        if (flops) *flops = c->prof_flops_dense;
+        if (reset) c->prof_flops_dense = 0.0;
     });
 }
 

@@ -119,9 +119,15 @@ int gemm(pq_ctx& c, const GemmArgs& g) {
         return k;
     }
     if (c.ev_used + 2 > 4096) prof_collect(c);
+    if (!c.d_flops) cuda_check(cudaMalloc(&c.d_flops, sizeof(unsigned long long) * 2048), "flop counters");
+    const size_t slot = c.ev_used / 2;
+    if (slot == 0)
+        cuda_check(cudaMemsetAsync(c.d_flops, 0, sizeof(unsigned long long) * 2048, c.stream), "flop counters zero");
+    GemmArgs gp = g;
+    gp.flop_counter = c.d_flops + slot;
     cudaEvent_t a = prof_event(c), b = prof_event(c);
     cuda_check(cudaEventRecord(a, c.stream), "event record");
-    const int k = launch_gemm(g, c.stream);
+    const int k = launch_gemm(gp, c.stream);
     cuda_check(cudaEventRecord(b, c.stream), "event record");
     count_launch(c, k);
     c.ev_flops.push_back(2.0 * g.M * static_cast<double>(g.N) * g.K * g.Z);
@@ -132,11 +138,16 @@ int gemm(pq_ctx& c, const GemmArgs& g) {
 void prof_collect(pq_ctx& c) {
     if (c.ev_used == 0) return;
     cuda_check(cudaStreamSynchronize(c.stream), "prof sync");
+    std::vector<unsigned long long> executed(c.ev_used / 2);
+    cuda_check(cudaMemcpy(executed.data(), c.d_flops, sizeof(unsigned long long) * executed.size(),
+                          cudaMemcpyDeviceToHost),
+               "flop counters readback");
     for (size_t i = 0; i + 1 < c.ev_used; i += 2) {
         float ms = 0.f;
         cuda_check(cudaEventElapsedTime(&ms, c.ev_pool[i], c.ev_pool[i + 1]), "event elapsed");
         c.prof_ms += ms;
-        c.prof_flops += c.ev_flops[i / 2];
+        c.prof_flops += static_cast<double>(executed[i / 2]);
+        c.prof_flops_dense += c.ev_flops[i / 2];
     }
     c.ev_used = 0;
     c.ev_flops.clear();
@@ -244,6 +255,22 @@ static GemmArgs square_batch(int n, int count, const double* A, const double* B,
 
 static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>& hint, const int* s_dev, int s_max,
                             double* cur, double* other, double* out);
+
+// Negligible-block tables for the exponentials of a phi call (kernels.hpp launch_band_ranges);
+// only the 64x64x8 mode-product tiles read them, so they are built for n >= 64.  PQ_BAND=0
+// disables the skip (every mode product then runs its full K).
+static bool band_enabled(int n) {
+    static const bool disabled = [] {
+        const char* v = std::getenv("PQ_BAND");
+        return v && v[0] == '0';
+    }();
+    return !disabled && n >= 64 && n <= 512;
+}
+static void band_ranges(pq_ctx& c, int n, int count, const double* E, int2* band) {
+    if (!band || count <= 0) return;
+    launch_band_ranges(n, count, E, band, c.stream);
+    count_launch(c);
+}
 
 // Two-stream squaring (squaring_pingpong): one RHS, p >= 2, vectors large enough that a step's
 // GEMMs outweigh the per-step event traffic (config 1, N = 4096: 4330 actions/s without the
@@ -410,7 +437,7 @@ static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>&
 // phi_0): with late_async their combination and squaring rounds run on the side stream, which
 // records c.ev_late when done; entries [0, split) are finished on c.stream.
 static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, const std::vector<ExpmEntry>& es,
-                        double* out, int split = -1, bool late_async = false) {
+                        double* out, int split = -1, bool late_async = false, int2* band = nullptr) {
     static const bool disabled = [] {
         const char* v = std::getenv("PQ_EXPM");
         return v && std::string(v) == "pade";
@@ -544,6 +571,7 @@ static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, c
                               first - static_cast<size_t>(z_begin) * nn, c.stream);
         count_launch(c);
         squaring_rounds(c, n, z_end - z_begin, h, s_dev + z_begin, s_max, first, first == o ? t : o, o);
+        band_ranges(c, n, z_end - z_begin, o, band ? band + static_cast<size_t>(z_begin) * band_row_blocks(n) : nullptr);
     };
     finish(0, split, ch_early, che_dev);
     if (split < count) {
@@ -592,6 +620,10 @@ struct PhiExps {
     const double* phi0[3] = {nullptr, nullptr, nullptr};
     int sq_len = 1;
     bool late = false;
+    // negligible-block tables parallel to node/sq/phi0 (band_row_blocks(n_k) entries per matrix)
+    const int2* node_band[3] = {nullptr, nullptr, nullptr};
+    const int2* sq_band[3] = {nullptr, nullptr, nullptr};
+    const int2* phi0_band[3] = {nullptr, nullptr, nullptr};
 };
 
 static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, const std::vector<double>& thetas,
@@ -643,22 +675,36 @@ static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, con
             for (int f : group) es.push_back({static_cast<long long>(off[f]), 1.0, op.one_norm[f]});
         const size_t nn = static_cast<size_t>(n) * n, ng = group.size();
         double* out = ws(c, tag + "_n" + std::to_string(n), es.size() * nn);
+        const int RB = band_row_blocks(n);
+        int2* band = band_enabled(n)
+                         ? static_cast<int2*>(ws_bytes(c, tag + "_band" + std::to_string(n), sizeof(int2) * es.size() * RB))
+                         : nullptr;
         // the side stream is in order, so waiting on the last ev_late covers every group's late work
         const bool async = late_async && split < static_cast<int>(es.size());
-        if (expm_taylor(c, n, base, s, es, out, split, async))
+        if (expm_taylor(c, n, base, s, es, out, split, async, band)) {
             px.late = px.late || async;
-        else
+        } else {
             expm_core(c, n, base, s, es, out);
+            band_ranges(c, n, static_cast<int>(es.size()), out, band);
+        }
         for (size_t g = 0; g < ng; ++g) {
             px.node[group[g]] = out + g * q * nn;
             px.sq[group[g]] = L > 0 ? out + (ng * q + g * L) * nn : nullptr;
             px.phi0[group[g]] = want_phi0 ? out + (ng * q + ng * L + g) * nn : nullptr;
+            if (band) {
+                px.node_band[group[g]] = band + g * q * RB;
+                px.sq_band[group[g]] = L > 0 ? band + (ng * q + g * L) * RB : nullptr;
+                px.phi0_band[group[g]] = want_phi0 ? band + (ng * q + ng * L + g) * RB : nullptr;
+            }
         }
     }
     for (int k = 0; k < op.d; ++k) {
         px.node[k] = px.node[canon[k]];
         px.sq[k] = px.sq[canon[k]];
         px.phi0[k] = px.phi0[canon[k]];
+        px.node_band[k] = px.node_band[canon[k]];
+        px.sq_band[k] = px.sq_band[canon[k]];
+        px.phi0_band[k] = px.phi0_band[canon[k]];
     }
     return px;
 }
@@ -719,7 +765,8 @@ static GemmArgs mode_gemm(int d, const int* n, int k, const double* E, long long
 }
 
 void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride, const double* x,
-                long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep, const char* tmp_tag) {
+                long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep, const char* tmp_tag,
+                const int2* const* band) {
     long long N = 1;
     for (int k = 0; k < d; ++k) N *= n[k];
     double* tmp[2] = {nullptr, nullptr};
@@ -732,6 +779,16 @@ void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const lo
         double* dst = last ? y : tmp[k % 2];
         const long long dstride = last ? y_stride : N;
         GemmArgs g = mode_gemm(d, n, k, E[k], E_stride[k], src, sstride, dst, dstride, Z1, N);
+        const long long nn = static_cast<long long>(n[k]) * n[k];
+        if (band && band[k] && E_stride[k] % nn == 0) {
+            // which operand holds the exponentials, and how the tile finds its matrix (gemm.cuh)
+            const int RB = band_row_blocks(n[k]);
+            g.band = band[k];
+            g.band_rows = n[k];
+            g.band_stride = (E_stride[k] / nn) * RB;
+            g.band_mode = g.b_kmajor ? 3 : (g.Z == 1 && g.M == Z1 * n[k] && Z1 > 1 ? 1 : 2);
+            if (g.band_mode == 1) g.band_stride = RB;
+        }
         if (last) {
             g.alpha_z = ep.alpha_z;
             g.ext = ep.ext;
@@ -774,7 +831,7 @@ void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, 
 
 static void apply_phi0(pq_ctx& c, const DevOp& op, const PhiExps& px, int nb, const double* b, double* y) {
     long long Es[3] = {0, 0, 0};
-    mode_chain(c, op.d, op.n, px.phi0, Es, b, op.N, y, op.N, nb, Epilogue{}, "phi0");
+    mode_chain(c, op.d, op.n, px.phi0, Es, b, op.N, y, op.N, nb, Epilogue{}, "phi0", px.phi0_band);
 }
 
 // kron.hpp:123-128 (phi_0): expm of every (scaled) factor, then one mode chain per RHS.
@@ -829,7 +886,14 @@ static std::vector<double> thetas_of(const NodesWeights& r, const std::vector<in
 // or stored into pool + (slot0 + a)*nb*N + m*N.
 static void node_sweep(pq_ctx& c, const DevOp& op, const double* const* E, const long long* Es, int q, int nb,
                        const double* bs, int p, const std::vector<double>* coef, double* acc, int zero, double* pool,
-                       int slot0) {
+                       int slot0, const int2* const* band = nullptr) {
+    // band tables follow their exponentials: matrix a of E[k] (stride Es[k]) <-> band[k] + a (Es[k]/n^2) RB
+    auto band_at = [&](int a0, const int2** out) {
+        for (int k = 0; k < op.d; ++k) {
+            const long long nn = static_cast<long long>(op.n[k]) * op.n[k];
+            out[k] = band && band[k] ? band[k] + (a0 * (Es[k] / nn)) * band_row_blocks(op.n[k]) : nullptr;
+        }
+    };
     const long long N = op.N;
     if (q == 0) {
         if (acc && zero) cuda_check(cudaMemsetAsync(acc, 0, sizeof(double) * nb * p * N, c.stream), "zero acc");
@@ -841,9 +905,11 @@ static void node_sweep(pq_ctx& c, const DevOp& op, const double* const* E, const
             for (int a0 = 0; a0 < q; a0 += qc) {
                 const int cnt = std::min(qc, q - a0);
                 const double* Ec[3];
+                const int2* Bc[3];
                 for (int k = 0; k < op.d; ++k) Ec[k] = E[k] + a0 * Es[k];
+                band_at(a0, Bc);
                 mode_chain(c, op.d, op.n, Ec, Es, bs + m * N, 0, pool + (static_cast<long long>(slot0 + a0) * nb + m) * N,
-                           nb * N, cnt, Epilogue{});
+                           nb * N, cnt, Epilogue{}, "chain", Bc);
             }
         return;
     }
@@ -858,8 +924,10 @@ static void node_sweep(pq_ctx& c, const DevOp& op, const double* const* E, const
         for (int a0 = 0; a0 < q; a0 += qc) {
             const int cnt = std::min(qc, q - a0);
             const double* Ec[3];
+            const int2* Bc[3];
             for (int k = 0; k < op.d; ++k) Ec[k] = E[k] + a0 * Es[k];
-            mode_chain(c, op.d, op.n, Ec, Es, bs + m * N, 0, V, N, cnt, Epilogue{});
+            band_at(a0, Bc);
+            mode_chain(c, op.d, op.n, Ec, Es, bs + m * N, 0, V, N, cnt, Epilogue{}, "chain", Bc);
             launch_combine(N, p, cnt, V, N, slot_dev, coef_dev + static_cast<size_t>(a0) * p,
                            acc + static_cast<long long>(m) * p * N, N, (zero && a0 == 0) ? 1 : 0, c.stream);
             count_launch(c);
@@ -878,7 +946,7 @@ static void phi_fixed_shift(pq_ctx& c, const DevOp& op, double s, int l, int nb,
     for (int k = 0; k < op.d; ++k) Es[k] = static_cast<long long>(op.n[k]) * op.n[k];
     (void)s;
     (void)l;
-    node_sweep(c, op, px.node, Es, rule.size(), nb, bs, p, &coef, out, 1, nullptr, 0);
+    node_sweep(c, op, px.node, Es, rule.size(), nb, bs, p, &coef, out, 1, nullptr, 0, px.node_band);
 }
 
 void phi_fixed_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, const NodesWeights& rule,
@@ -896,7 +964,8 @@ void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, con
     node_coefs(rule, nodes, p, coef);
     long long Es[3];
     for (int k = 0; k < op.d; ++k) Es[k] = static_cast<long long>(op.n[k]) * op.n[k];
-    node_sweep(c, op, px.node, Es, static_cast<int>(nodes.size()), nb, bs, p, &coef, acc, zero, nullptr, 0);
+    node_sweep(c, op, px.node, Es, static_cast<int>(nodes.size()), nb, bs, p, &coef, acc, zero, nullptr, 0,
+               px.node_band);
 }
 
 // phiaction.hpp:156-245 (Alg. 2): nested CC ladder, node vectors kept in a device pool, all sums
@@ -929,7 +998,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             E[k] = px25.node[k];
             Es[k] = 2 * nn[k];
         }
-        node_sweep(c, op, E, Es, 13, nb, bs, p, nullptr, nullptr, 0, pool, 0);
+        node_sweep(c, op, E, Es, 13, nb, bs, p, nullptr, nullptr, 0, pool, 0, px25.node_band);
     }
     double* accs[2] = {out, ws(c, "ccacc", col)};
     int cur = 0;
@@ -980,6 +1049,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         std::vector<int> odd(static_cast<size_t>(fr));
         for (int k = 0; k < fr; ++k) odd[static_cast<size_t>(k)] = 2 * k + 1;
         const double* E[3];
+        const int2* B[3] = {nullptr, nullptr, nullptr};
         long long Es[3];
         PhiExps pxl;
         if (lev == 2) {
@@ -987,16 +1057,18 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             for (int k = 0; k < op.d; ++k) {
                 E[k] = px25.node[k] + nn[k];
                 Es[k] = 2 * nn[k];
+                B[k] = px25.node_band[k] ? px25.node_band[k] + band_row_blocks(op.n[k]) : nullptr;
             }
         } else {
             pxl = phi_exponentials(c, op, s, l, thetas_of(rl, odd), false, false, "ccE" + std::to_string(lev));
             for (int k = 0; k < op.d; ++k) {
                 E[k] = pxl.node[k];
                 Es[k] = nn[k];
+                B[k] = pxl.node_band[k];
             }
         }
         level_base[lev] = used;
-        node_sweep(c, op, E, Es, fr, nb, bs, p, nullptr, nullptr, 0, pool, used);
+        node_sweep(c, op, E, Es, fr, nb, bs, p, nullptr, nullptr, 0, pool, used, B);
         used += fr;
     };
     if (!c.ev_cc) cuda_check(cudaEventCreateWithFlags(&c.ev_cc, cudaEventDisableTiming), "cc event");
@@ -1091,7 +1163,7 @@ void phi_adaptive_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const do
 // With sq_len >= l, E_in[k] already holds the chain E, E^2, ..., E^(2^(l-1)) (phi_exponentials
 // sq_chain) and no matrix squaring is issued here.
 static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int p, double* y, double* partner,
-                                 const double* const* E_in, int sq_len = 1) {
+                                 const double* const* E_in, int sq_len = 1, const int2* const* band_in = nullptr) {
     if (l <= 0) return y;
     const long long N = op.N;
     const bool chain = sq_len >= l;
@@ -1187,20 +1259,24 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
         try {
             for (int step = 0; step < l; ++step) {
                 const double* E[3];
-                for (int k = 0; k < op.d; ++k) E[k] = E_in[k] + static_cast<size_t>(step) * op.n[k] * op.n[k];
+                const int2* Bd[3] = {nullptr, nullptr, nullptr};
+                for (int k = 0; k < op.d; ++k) {
+                    E[k] = E_in[k] + static_cast<size_t>(step) * op.n[k] * op.n[k];
+                    if (band_in && band_in[k]) Bd[k] = band_in[k] + step * band_row_blocks(op.n[k]);
+                }
                 double* cur = b[step % 3];
                 double* nxt = b[(step + 1) % 3];
                 // lower half on the main stream
                 c.stream = main_stream;
                 if (step >= 2) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqB[step - 2], 0), "sq wait B");
-                mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, h, Epilogue{}, "sqchA");
+                mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, h, Epilogue{}, "sqchA", Bd);
                 launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, 0, h);
                 count_launch(c);
                 cuda_check(cudaEventRecord(c.ev_sqA[step], c.stream), "sq rec A");
                 // upper half on the second stream
                 c.stream = c.sq2;
                 mode_chain(c, op.d, op.n, E, Es, cur + static_cast<size_t>(h) * N, N, nxt + static_cast<size_t>(h) * N, N,
-                           p - h, Epilogue{}, "sqchB");
+                           p - h, Epilogue{}, "sqchB", Bd);
                 if (step >= 1) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqA[step - 1], 0), "sq wait A");
                 launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, h, p);
                 count_launch(c);
@@ -1219,9 +1295,12 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
     double* nxt = partner;
     for (int step = 0; step < l; ++step) {
         const double* E[3];
-        for (int k = 0; k < op.d; ++k)
+        const int2* Bd[3] = {nullptr, nullptr, nullptr};
+        for (int k = 0; k < op.d; ++k) {
             E[k] = chain ? E_in[k] + static_cast<size_t>(step) * op.n[k] * op.n[k] : cur_E(k);
-        mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, Epilogue{});
+            if (chain && band_in && band_in[k]) Bd[k] = band_in[k] + step * band_row_blocks(op.n[k]);
+        }
+        mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, Epilogue{}, "chain", Bd);
         launch_sq_combine(N, p, nb, nxt, cur, coef_dev, c.stream);
         count_launch(c);
         std::swap(cur, nxt);
@@ -1310,7 +1389,8 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
     }
     if (px.late) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_late, 0), "late exps wait");
     if (l > 0) {
-        double* res = squaring_pingpong(c, op, l, nb, p, first, first == out ? partner : out, px.sq, px.sq_len);
+        double* res =
+            squaring_pingpong(c, op, l, nb, p, first, first == out ? partner : out, px.sq, px.sq_len, px.sq_band);
         if (res != out)
             cuda_check(cudaMemcpyAsync(out, res, sizeof(double) * nb * p * op.N, cudaMemcpyDeviceToDevice, c.stream),
                        "plan copy");

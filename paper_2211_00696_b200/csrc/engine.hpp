@@ -82,7 +82,9 @@ struct pq_ctx {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<double> ev_flops;
-    double prof_ms = 0.0, prof_flops = 0.0;
+    double prof_ms = 0.0, prof_flops = 0.0;  // prof_flops: executed (negligible blocks skipped)
+    double prof_flops_dense = 0.0;            // 2 M N K Z of the same launches
+    unsigned long long* d_flops = nullptr;    // per-launch executed-flop counters (profiling)
     uint64_t prof_launches = 0;
 };
 
@@ -157,9 +159,11 @@ DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const
 void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_stride,
                 const std::vector<double>& scales, double base_one_norm, double* out);
 // y[z1] = (E_0[z1] (x) ... (x) E_{d-1}[z1]) x[z1] for z1 < Z1, epilogue fused into the last mode.
+// band (nullable, per dim): negligible-block tables of E[k]'s matrices (launch_band_ranges),
+// matrix a of E[k] at band[k] + a (E_stride[k]/n_k^2) ceil(n_k/64).
 void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride,
                 const double* x, long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep,
-                const char* tmp_tag = "chain");
+                const char* tmp_tag = "chain", const int2* const* band = nullptr);
 void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, double* y);
 void exp_action_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* b, double* y);
 double max_inf_norm_dev(pq_ctx& c, const double* v, long long N, int ncols);  // syncs

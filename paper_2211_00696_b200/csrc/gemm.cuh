@@ -139,21 +139,43 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
 #pragma unroll
         for (int j = 0; j < T::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    const int KT = (g.K + BK - 1) / BK;
+    int kt_lo = 0, KT = (g.K + BK - 1) / BK;
+    if constexpr (BM == 64 && BN == 64 && BK == 8) {
+        // negligible-block skip: this tile's exponential row block only touches slices [lo, hi)
+        if (g.band) {
+            int e, rb;
+            if (g.band_mode == 1) {
+                e = m0 / g.band_rows;
+                rb = (m0 % g.band_rows) >> 6;
+            } else {
+                e = z1;
+                rb = (g.band_mode == 2 ? m0 : n0) >> 6;
+            }
+            const int2 r = g.band[(long long)e * g.band_stride + rb];
+            kt_lo = r.x;
+            KT = min(KT, r.y);
+        }
+    }
+    const int NKT = KT > kt_lo ? KT - kt_lo : 0;
+    if (g.flop_counter && tid == 0) {
+        const long long rows = min(BM, g.M - m0), cols = min(BN, g.N - n0);
+        const long long kexec = NKT > 0 ? min(KT * BK, g.K) - kt_lo * BK : 0;
+        atomicAdd(g.flop_counter, static_cast<unsigned long long>(2 * rows * cols * kexec));
+    }
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
-        if (s < KT) load_stage(s, s);
+        if (s < NKT) load_stage(s, kt_lo + s);
         cp_commit();
     }
     const double* tA0 = sA + (wm * WM + gid) * T::SA + tig;
     const double* tB0 = BKM ? sB + (wn * WN + gid) * T::SB + tig : sB + tig * T::SB + wn * WN + gid;
 #pragma unroll 1
-    for (int kt = 0; kt < KT; ++kt) {
+    for (int kt = 0; kt < NKT; ++kt) {
         cp_wait<ST - 2>();
         __syncthreads();
         {
             const int nk = kt + ST - 1;
-            if (nk < KT) load_stage(nk % ST, nk);
+            if (nk < NKT) load_stage(nk % ST, kt_lo + nk);
             cp_commit();
         }
         const int st = kt % ST;

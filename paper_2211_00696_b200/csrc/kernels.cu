@@ -49,7 +49,7 @@ int launch_gemm(const GemmArgs& g, cudaStream_t s) {
     int shape = 3;
     if (ctas(64, 64) < 296 || (g.M <= 128 && g.N <= 128 && ctas(64, 64) < 888)) shape = 4;
     // large plain products: persistent CTAs with the pipeline running across tiles
-    const bool plain = !g.nterms && !g.accumulate && !g.alpha_z && !g.sq_count;
+    const bool plain = !g.nterms && !g.accumulate && !g.alpha_z && !g.sq_count && !g.flop_counter;
     if (shape == 3 && plain && ctas(64, 64) >= 2 * 444 && g_persistent_enabled) shape = 5;
     return g.b_kmajor ? launch_gemm_kk(g, vec2, shape, s) : launch_gemm_nk(g, vec2, shape, s);
 }
@@ -769,6 +769,61 @@ __global__ void k_imax(const int* v, int count, int* out) {
     if (threadIdx.x == 0) *out = m;
 }
 void launch_imax(const int* v, int count, int* out, cudaStream_t s) { k_imax<<<1, 32, 0, s>>>(v, count, out); }
+
+// One CTA per matrix: global max, then one warp per (64-row block, 8-column slice) pair.
+__global__ void k_band_ranges(int n, const double* __restrict__ E, int2* __restrict__ out) {
+    const int z = blockIdx.x;
+    const double* e = E + (long long)z * n * n;
+    const long long nn = (long long)n * n;
+    __shared__ double red[32];
+    __shared__ double gmax_sh;
+    __shared__ unsigned char need[8 * 64];  // [row block][slice], n <= 512
+    double m = 0.0;
+    bool bad = false;
+    for (long long i = threadIdx.x; i < nn; i += blockDim.x) {
+        const double v = fabs(e[i]);
+        if (!(v <= 1.7976931348623157e308)) bad = true;  // NaN / Inf
+        m = fmax(m, v);
+    }
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    bad = __syncthreads_or(bad);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double g = 0.0;
+        for (int w = 0; w < (int)blockDim.x / 32; ++w) g = fmax(g, red[w]);
+        gmax_sh = g;
+    }
+    __syncthreads();
+    const double thr = ldexp(gmax_sh, -64);
+    const int RB = (n + 63) / 64, NS = (n + 7) / 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    for (int pr = warp; pr < RB * NS; pr += nw) {
+        const int rb = pr / NS, sl = pr % NS;
+        double bm = 0.0;
+        for (int t = lane; t < 64 * 8; t += 32) {
+            const int r = rb * 64 + t / 8, c = sl * 8 + t % 8;
+            if (r < n && c < n) bm = fmax(bm, fabs(e[(long long)r * n + c]));
+        }
+        for (int o = 16; o > 0; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+        if (lane == 0) need[rb * 64 + sl] = bad || bm > thr;
+    }
+    __syncthreads();
+    for (int rb = threadIdx.x; rb < RB; rb += blockDim.x) {
+        int lo = NS, hi = 0;
+        for (int sl = 0; sl < NS; ++sl)
+            if (need[rb * 64 + sl]) {
+                lo = min(lo, sl);
+                hi = sl + 1;
+            }
+        out[(long long)z * RB + rb] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
+    }
+}
+void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s) {
+    if (count <= 0) return;
+    if (n > 512) throw std::invalid_argument("band ranges: n > 512");
+    k_band_ranges<<<count, 256, 0, s>>>(n, E, out);
+}
 
 __global__ void k_identity(int n, long long total, double* out) {
     const long long nn = (long long)n * n;

@@ -76,10 +76,14 @@ class Context:
         check(lib.pq_ctx_set_profiling(self.handle, 1 if on else 0))
 
     def gemm_stats(self, reset: bool = True) -> tuple:
-        """(launches, device ms, algorithmic FLOPs) of the DMMA GEMM launches recorded while profiling."""
-        n, ms, fl = C.c_uint64(), C.c_double(), C.c_double()
+        """(launches, device ms, executed FLOPs, dense FLOPs) of the DMMA GEMM launches recorded while
+        profiling; executed < dense when negligible exponential blocks were skipped."""
+        n, ms, fl, dense = C.c_uint64(), C.c_double(), C.c_double(), C.c_double()
+        check(lib.pq_ctx_gemm_dense_flops(self.handle, 0, C.byref(dense)))
         check(lib.pq_ctx_gemm_stats(self.handle, 1 if reset else 0, C.byref(n), C.byref(ms), C.byref(fl)))
-        return int(n.value), ms.value, fl.value
+        if reset:
+            check(lib.pq_ctx_gemm_dense_flops(self.handle, 1, None))
+        return int(n.value), ms.value, fl.value, dense.value
 
     def set_workspace_limit(self, nbytes: int) -> None:
         check(lib.pq_ctx_set_workspace_limit(self.handle, nbytes))
