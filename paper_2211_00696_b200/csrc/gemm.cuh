@@ -140,26 +140,46 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
         for (int j = 0; j < T::NI; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
     int kt_lo = 0, KT = (g.K + BK - 1) / BK;
-    if constexpr (BM == 64 && BN == 64 && BK == 8) {
-        // negligible-block skip: this tile's exponential row block only touches slices [lo, hi)
+    int w_lo = 0, w_hi = KT;  // this warp's DMMA slices (absolute)
+    if constexpr (BK == 8 && (BM == 32 || BM == 64) && (BN == 32 || BN == 64) && WM <= 32 && WN <= 32) {
+        // negligible-block skip: the CTA streams the union of the 32-row exponential blocks its
+        // tile covers, each warp multiplies only inside its own block's slices
         if (g.band) {
-            int e, rb;
-            if (g.band_mode == 1) {
-                e = m0 / g.band_rows;
-                rb = (m0 % g.band_rows) >> 6;
-            } else {
+            int e, r0, te, wr;
+            if (g.band_mode == 3) {  // exponential = B (k-major): its rows are the tile's columns
                 e = z1;
-                rb = (g.band_mode == 2 ? m0 : n0) >> 6;
+                r0 = n0;
+                te = BN;
+                wr = n0 + wn * WN;
+            } else {
+                e = g.band_mode == 1 ? m0 / g.band_rows : z1;
+                r0 = g.band_mode == 1 ? m0 % g.band_rows : m0;
+                te = BM;
+                wr = r0 + wm * WM;
             }
-            const int2 r = g.band[(long long)e * g.band_stride + rb];
-            kt_lo = r.x;
-            KT = min(KT, r.y);
+            const int2* br = g.band + (long long)e * g.band_stride;
+            const int nb = (g.band_rows + 31) >> 5;
+            int lo = 1 << 30, hi = 0;
+            for (int b = r0 >> 5; b < min((r0 + te + 31) >> 5, nb); ++b) {
+                const int2 v = br[b];
+                if (v.y > v.x) {
+                    lo = min(lo, v.x);
+                    hi = max(hi, v.y);
+                }
+            }
+            kt_lo = hi > lo ? lo : 0;
+            KT = min(KT, hi > lo ? hi : 0);
+            const int wb = wr >> 5;
+            const int2 mine = wb < nb ? br[wb] : make_int2(0, 0);
+            w_lo = mine.x;
+            w_hi = mine.y;
         }
     }
     const int NKT = KT > kt_lo ? KT - kt_lo : 0;
-    if (g.flop_counter && tid == 0) {
-        const long long rows = min(BM, g.M - m0), cols = min(BN, g.N - n0);
-        const long long kexec = NKT > 0 ? min(KT * BK, g.K) - kt_lo * BK : 0;
+    if (g.flop_counter && lane == 0) {
+        const long long rows = max(0, min(WM, g.M - (m0 + wm * WM))), cols = max(0, min(WN, g.N - (n0 + wn * WN)));
+        const int lo = max(kt_lo, w_lo), hi = min(KT, w_hi);
+        const long long kexec = hi > lo ? min(hi * BK, g.K) - lo * BK : 0;
         atomicAdd(g.flop_counter, static_cast<unsigned long long>(2 * rows * cols * kexec));
     }
 #pragma unroll
@@ -179,6 +199,8 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
             cp_commit();
         }
         const int st = kt % ST;
+        const int kabs = kt_lo + kt;
+        if (kabs < w_lo || kabs >= w_hi) continue;  // warp-uniform: this warp's rows need no DMMA here
         const double* tA = tA0 + st * T::ASZ;
         const double* tB = tB0 + st * T::BSZ;
 #pragma unroll
@@ -467,6 +489,10 @@ int launch_gemm_family(const GemmArgs& g, bool vec2, int shape, cudaStream_t s) 
         case 0: return vec2 ? launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 1>(g, s);
         case 1: return vec2 ? launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 1>(g, s);
         case 2: return vec2 ? launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 2>(g, s) : launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 1>(g, s);
+        case 6:  // negligible-block skip, exponential = A: 32-row tiles stream only their block's slices
+            return launch_cfg<32, 64, 8, 16, 32, 4, BKM, 2, 6>(g, s);
+        case 7:  // negligible-block skip, exponential = B (k-major): 32-column tiles
+            return launch_cfg<64, 32, 8, 32, 16, 4, BKM, 2, 6>(g, s);
         case 3:
             // 16-byte path: BK = 8, 4 stages and <= 128 registers give 4 CTAs (16 warps) per SM,
             // which keeps the DMMA pipe fed while other warps sit in barriers / epilogues

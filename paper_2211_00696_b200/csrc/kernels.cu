@@ -17,6 +17,7 @@
 #include <set>
 #include <cstdlib>
 #include <stdexcept>
+#include <string>
 #include <type_traits>
 
 namespace pqb {
@@ -31,6 +32,10 @@ static bool al16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) =
 
 // PQ_PERSISTENT=1 selects the persistent tiles for large plain products (measured slower than
 // the hardware CTA scheduler on the config-2 pipeline: 191 vs 233 actions/s, so off by default)
+static const bool g_band_tile32 = [] {
+    const char* e = std::getenv("PQ_BAND_TILE");
+    return !(e && std::string(e) == "64");
+}();
 static const bool g_persistent_enabled = [] {
     const char* e = std::getenv("PQ_PERSISTENT");
     return e && e[0] == '1';
@@ -51,6 +56,9 @@ int launch_gemm(const GemmArgs& g, cudaStream_t s) {
     // large plain products: persistent CTAs with the pipeline running across tiles
     const bool plain = !g.nterms && !g.accumulate && !g.alpha_z && !g.sq_count && !g.flop_counter;
     if (shape == 3 && plain && ctas(64, 64) >= 2 * 444 && g_persistent_enabled) shape = 5;
+    // negligible-block skip (g.band): 32-extent tiles along the exponential's rows, so each CTA
+    // streams exactly the k-slices its 32-row block needs (PQ_BAND_TILE=64 keeps 64x64 tiles)
+    if (shape == 3 && vec2 && g.band && g_band_tile32) shape = g.band_mode == 3 ? 7 : 6;
     return g.b_kmajor ? launch_gemm_kk(g, vec2, shape, s) : launch_gemm_nk(g, vec2, shape, s);
 }
 
@@ -770,14 +778,14 @@ __global__ void k_imax(const int* v, int count, int* out) {
 }
 void launch_imax(const int* v, int count, int* out, cudaStream_t s) { k_imax<<<1, 32, 0, s>>>(v, count, out); }
 
-// One CTA per matrix: global max, then one warp per (64-row block, 8-column slice) pair.
+// One CTA per matrix: global max, then one warp per (32-row block, 8-column slice) pair.
 __global__ void k_band_ranges(int n, const double* __restrict__ E, int2* __restrict__ out) {
     const int z = blockIdx.x;
     const double* e = E + (long long)z * n * n;
     const long long nn = (long long)n * n;
     __shared__ double red[32];
     __shared__ double gmax_sh;
-    __shared__ unsigned char need[8 * 64];  // [row block][slice], n <= 512
+    __shared__ unsigned char need[16 * 64];  // [32-row block][slice], n <= 512
     double m = 0.0;
     bool bad = false;
     for (long long i = threadIdx.x; i < nn; i += blockDim.x) {
@@ -796,13 +804,13 @@ __global__ void k_band_ranges(int n, const double* __restrict__ E, int2* __restr
     }
     __syncthreads();
     const double thr = ldexp(gmax_sh, -64);
-    const int RB = (n + 63) / 64, NS = (n + 7) / 8;
+    const int RB = (n + 31) / 32, NS = (n + 7) / 8;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     for (int pr = warp; pr < RB * NS; pr += nw) {
         const int rb = pr / NS, sl = pr % NS;
         double bm = 0.0;
-        for (int t = lane; t < 64 * 8; t += 32) {
-            const int r = rb * 64 + t / 8, c = sl * 8 + t % 8;
+        for (int t = lane; t < 32 * 8; t += 32) {
+            const int r = rb * 32 + t / 8, c = sl * 8 + t % 8;
             if (r < n && c < n) bm = fmax(bm, fabs(e[(long long)r * n + c]));
         }
         for (int o = 16; o > 0; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));

@@ -34,9 +34,11 @@ struct GemmArgs {
     const int* sq_count = nullptr;    // expm squaring: z with sq_round >= sq_count[z] copies A
     int sq_round = 0;
     // Negligible-block skip for mode products (64x64x8 tiles only): band[e*band_stride + rb] =
-    // {first, last+1} 8-wide k-slices of 64-row block rb of exponential e that hold any entry above
-    // 2^-64 max|E| (launch_band_ranges).  band_mode 1: A = exponentials stacked along M
-    // (e = m0 / band_rows); 2: A = exponential z1; 3: B (k-major) = exponential z1, rb from n0.
+    // {first, last+1} 8-wide k-slices of 32-row block rb of exponential e that hold any entry above
+    // 2^-64 max|E| (launch_band_ranges).  The CTA streams the union of its two 32-row blocks; each
+    // warp issues DMMAs only inside its own block's range.  band_mode 1: A = exponentials stacked
+    // along M (e = m0 / band_rows); 2: A = exponential z1; 3: B (k-major) = exponential z1, rows
+    // from n0.
     const int2* band = nullptr;
     long long band_stride = 0;
     int band_mode = 0, band_rows = 0;
@@ -73,12 +75,12 @@ void launch_lu_solve(int n, int count, double* P, double* Q, int* err, cudaStrea
 // n <= 128: shared-memory factorisation of P (L\U over P, pivots in piv[count*n]) + a batched
 // triangular solve of Q over 32-column slices.  Q <- P^{-1} Q.
 void launch_lu_factor_solve(int n, int count, double* P, double* Q, int* piv, int* err, cudaStream_t s);
-// Per matrix z < count (n x n, stride n*n) and 64-row block rb: out[z*ceil(n/64) + rb] = {first,
+// Per matrix z < count (n x n, stride n*n) and 32-row block rb: out[z*ceil(n/32) + rb] = {first,
 // last+1} of the 8-wide column slices whose block max |E| exceeds 2^-64 max|E_z| (NaN/Inf count as
 // needed; an all-negligible row block gives an empty range).  Dropping the rest changes a mode
 // product by at most n 2^-64 of its max-norm -- below half an ulp in practice.
 void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s);
-inline int band_row_blocks(int n) { return (n + 63) / 64; }
+inline int band_row_blocks(int n) { return (n + 31) / 32; }
 // max over z of s_z -> *out (device int)
 void launch_imax(const int* v, int count, int* out, cudaStream_t s);
 
