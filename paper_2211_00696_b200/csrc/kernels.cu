@@ -778,59 +778,50 @@ __global__ void k_imax(const int* v, int count, int* out) {
 }
 void launch_imax(const int* v, int count, int* out, cudaStream_t s) { k_imax<<<1, 32, 0, s>>>(v, count, out); }
 
-// One CTA per matrix: global max, then one warp per (32-row block, 8-column slice) pair.
-__global__ void k_band_ranges(int n, const double* __restrict__ E, int2* __restrict__ out) {
-    const int z = blockIdx.x;
+// One CTA per (matrix, 32-row block), one pass over the block's rows: one warp per 8-column
+// slice computes the slice max; the threshold is 2^-64 x the block's own max (a lower bound of the
+// matrix max, so the skip is at least as conservative as the matrix-relative criterion).
+__global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __restrict__ E, int2* __restrict__ out) {
+    const int z = blockIdx.x, rb = blockIdx.y;
     const double* e = E + (long long)z * n * n;
-    const long long nn = (long long)n * n;
-    __shared__ double red[32];
-    __shared__ double gmax_sh;
-    __shared__ unsigned char need[16 * 64];  // [32-row block][slice], n <= 512
-    double m = 0.0;
-    bool bad = false;
-    for (long long i = threadIdx.x; i < nn; i += blockDim.x) {
-        const double v = fabs(e[i]);
-        if (!(v <= 1.7976931348623157e308)) bad = true;  // NaN / Inf
-        m = fmax(m, v);
+    __shared__ double smax[64];  // slices of this block, n <= 512
+    const int NS = (n + 7) / 8;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int sl = warp; sl < NS; sl += blockDim.x >> 5) {
+        double bm = 0.0;
+        int bad = 0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int t = lane + 32 * u;
+            const int r = rb * 32 + t / 8, c = sl * 8 + t % 8;
+            if (r < n && c < n) {
+                const double v = fabs(__ldg(e + (long long)r * n + c));
+                bad |= !(v <= 1.7976931348623157e308);  // NaN / Inf
+                bm = fmax(bm, v);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
+        bad = __any_sync(0xffffffffu, bad);
+        if (lane == 0) smax[sl] = bad ? __longlong_as_double(0x7ff0000000000000LL) : bm;
     }
-    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-    bad = __syncthreads_or(bad);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
     __syncthreads();
     if (threadIdx.x == 0) {
         double g = 0.0;
-        for (int w = 0; w < (int)blockDim.x / 32; ++w) g = fmax(g, red[w]);
-        gmax_sh = g;
-    }
-    __syncthreads();
-    const double thr = ldexp(gmax_sh, -64);
-    const int RB = (n + 31) / 32, NS = (n + 7) / 8;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    for (int pr = warp; pr < RB * NS; pr += nw) {
-        const int rb = pr / NS, sl = pr % NS;
-        double bm = 0.0;
-        for (int t = lane; t < 32 * 8; t += 32) {
-            const int r = rb * 32 + t / 8, c = sl * 8 + t % 8;
-            if (r < n && c < n) bm = fmax(bm, fabs(e[(long long)r * n + c]));
-        }
-        for (int o = 16; o > 0; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-        if (lane == 0) need[rb * 64 + sl] = bad || bm > thr;
-    }
-    __syncthreads();
-    for (int rb = threadIdx.x; rb < RB; rb += blockDim.x) {
+        for (int sl = 0; sl < NS; ++sl) g = fmax(g, smax[sl]);
+        const double thr = ldexp(g, -64);
         int lo = NS, hi = 0;
         for (int sl = 0; sl < NS; ++sl)
-            if (need[rb * 64 + sl]) {
+            if (smax[sl] > thr || !(g <= 1.7976931348623157e308)) {
                 lo = min(lo, sl);
                 hi = sl + 1;
             }
-        out[(long long)z * RB + rb] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
+        out[(long long)z * gridDim.y + rb] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
     }
 }
 void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s) {
     if (count <= 0) return;
     if (n > 512) throw std::invalid_argument("band ranges: n > 512");
-    k_band_ranges<<<count, 256, 0, s>>>(n, E, out);
+    k_band_ranges<<<dim3(count, (n + 31) / 32), 256, 0, s>>>(n, E, out);
 }
 
 __global__ void k_identity(int n, long long total, double* out) {

@@ -76,9 +76,9 @@ void launch_lu_solve(int n, int count, double* P, double* Q, int* err, cudaStrea
 // triangular solve of Q over 32-column slices.  Q <- P^{-1} Q.
 void launch_lu_factor_solve(int n, int count, double* P, double* Q, int* piv, int* err, cudaStream_t s);
 // Per matrix z < count (n x n, stride n*n) and 32-row block rb: out[z*ceil(n/32) + rb] = {first,
-// last+1} of the 8-wide column slices whose block max |E| exceeds 2^-64 max|E_z| (NaN/Inf count as
-// needed; an all-negligible row block gives an empty range).  Dropping the rest changes a mode
-// product by at most n 2^-64 of its max-norm -- below half an ulp in practice.
+// last+1} of the 8-wide column slices whose max |E| exceeds 2^-64 x the row block's max (<= max|E_z|;
+// NaN/Inf count as needed; an all-zero row block gives an empty range).  Dropping the rest changes
+// a mode product by at most n 2^-64 of its max-norm -- below half an ulp in practice.
 void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s);
 inline int band_row_blocks(int n) { return (n + 31) / 32; }
 // max over z of s_z -> *out (device int)
