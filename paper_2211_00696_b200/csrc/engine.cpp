@@ -259,12 +259,14 @@ static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>&
 // Negligible-block tables for the exponentials of a phi call (kernels.hpp launch_band_ranges);
 // only the 64x64x8 mode-product tiles read them, so they are built for n >= 64.  PQ_BAND=0
 // disables the skip (every mode product then runs its full K).
-static bool band_enabled(int n) {
+static bool band_enabled(int n, long long N) {
     static const bool disabled = [] {
         const char* v = std::getenv("PQ_BAND");
         return v && v[0] == '0';
     }();
-    return !disabled && n >= 64 && n <= 512;
+    // tiny operators are launch-latency bound: the table launches would cost more than they save
+    // (config 1, N = 4096: 4568 actions/s without, 3665 with)
+    return !disabled && n >= 64 && n <= 512 && N >= (1LL << 18);
 }
 static void band_ranges(pq_ctx& c, int n, int count, const double* E, int2* band) {
     if (!band || count <= 0) return;
@@ -676,7 +678,7 @@ static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, con
         const size_t nn = static_cast<size_t>(n) * n, ng = group.size();
         double* out = ws(c, tag + "_n" + std::to_string(n), es.size() * nn);
         const int RB = band_row_blocks(n);
-        int2* band = band_enabled(n)
+        int2* band = band_enabled(n, op.N)
                          ? static_cast<int2*>(ws_bytes(c, tag + "_band" + std::to_string(n), sizeof(int2) * es.size() * RB))
                          : nullptr;
         // the side stream is in order, so waiting on the last ev_late covers every group's late work

@@ -141,21 +141,23 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
 
     int kt_lo = 0, KT = (g.K + BK - 1) / BK;
     int w_lo = 0, w_hi = KT;  // this warp's DMMA slices (absolute)
-    if constexpr (BK == 8 && (BM == 32 || BM == 64) && (BN == 32 || BN == 64) && WM <= 32 && WN <= 32) {
+    if constexpr (BK == 8) {
         // negligible-block skip: the CTA streams the union of the 32-row exponential blocks its
         // tile covers, each warp multiplies only inside its own block's slices
         if (g.band) {
-            int e, r0, te, wr;
+            int e, r0, te, wr, we;
             if (g.band_mode == 3) {  // exponential = B (k-major): its rows are the tile's columns
                 e = z1;
                 r0 = n0;
                 te = BN;
                 wr = n0 + wn * WN;
+                we = WN;
             } else {
                 e = g.band_mode == 1 ? m0 / g.band_rows : z1;
                 r0 = g.band_mode == 1 ? m0 % g.band_rows : m0;
                 te = BM;
                 wr = r0 + wm * WM;
+                we = WM;
             }
             const int2* br = g.band + (long long)e * g.band_stride;
             const int nb = (g.band_rows + 31) >> 5;
@@ -169,10 +171,15 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
             }
             kt_lo = hi > lo ? lo : 0;
             KT = min(KT, hi > lo ? hi : 0);
-            const int wb = wr >> 5;
-            const int2 mine = wb < nb ? br[wb] : make_int2(0, 0);
-            w_lo = mine.x;
-            w_hi = mine.y;
+            if (we <= 32) {  // the warp lies in one 32-row block: multiply only inside its range
+                const int wb = wr >> 5;
+                const int2 mine = wb < nb ? br[wb] : make_int2(0, 0);
+                w_lo = mine.x;
+                w_hi = mine.y;
+            } else {
+                w_lo = kt_lo;
+                w_hi = KT;
+            }
         }
     }
     const int NKT = KT > kt_lo ? KT - kt_lo : 0;

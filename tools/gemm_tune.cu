@@ -3,6 +3,7 @@
 // Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2211_00696_b200/csrc \
 //          -o tools/gemm_tune tools/gemm_tune.cu
 #include <cstdio>
+#include <algorithm>
 #include <vector>
 
 #include "gemm.cuh"
@@ -70,30 +71,53 @@ int main(int argc, char** argv) {
     cudaMemset(coef, 0, 64 * 64 * 8);
     cudaMemset(alpha, 0, 64 * 8);
     const double fl = 2.0 * N * n * Z;
+    // optional negligible-block band: each 32-row block rb needs slices [4rb - w, 4rb + 4 + w)
+    const int bw = argc > 4 ? atoi(argv[4]) : -1;
+    int2* band = nullptr;
+    double band_frac = 1.0;
+    if (bw >= 0) {
+        const int RB = (n + 31) / 32, NS = (n + 7) / 8;
+        std::vector<int2> hb(RB * Z);
+        long long kept = 0;
+        for (int z = 0; z < Z; ++z)
+            for (int rb = 0; rb < RB; ++rb) {
+                const int lo = std::max(0, 4 * rb - bw), hi = std::min(NS, 4 * rb + 4 + bw);
+                hb[z * RB + rb] = make_int2(lo, hi);
+                kept += hi - lo;
+            }
+        band_frac = (double)kept / (RB * NS * Z);
+        CK(cudaMalloc(&band, sizeof(int2) * hb.size()));
+        cudaMemcpy(band, hb.data(), sizeof(int2) * hb.size(), cudaMemcpyHostToDevice);
+        printf("band half-width %d slices: %.2f of the K work kept\n", bw, band_frac);
+    }
     std::vector<Case> cases;
     {  // mode 0, stacked nodes: (Z n x n) . (n x n^2)
         GemmArgs g;
         g.A = E; g.lda = n; g.B = X; g.ldb = (long long)n * n; g.C = Y; g.ldc = (long long)n * n;
         g.M = Z * n; g.N = n * n; g.K = n; g.Z = 1;
-        cases.push_back({"mode0", g, fl});
+        if (band) { g.band = band; g.band_mode = 1; g.band_rows = n; g.band_stride = (n + 31) / 32; }
+        cases.push_back({"mode0", g, fl * band_frac});
     }
     {  // mode 1: batch (Z * n) of (n x n) . (n x n)
         GemmArgs g;
         g.A = E; g.lda = n; g.B = X; g.ldb = n; g.C = Y; g.ldc = n;
         g.M = n; g.N = n; g.K = n; g.Z = Z * n; g.zdiv = n;
         g.sA1 = (long long)n * n; g.sB1 = N; g.sB2 = (long long)n * n; g.sC1 = N; g.sC2 = (long long)n * n;
-        cases.push_back({"mode1", g, fl});
+        if (band) { g.band = band; g.band_mode = 2; g.band_rows = n; g.band_stride = (n + 31) / 32; }
+        cases.push_back({"mode1", g, fl * band_frac});
     }
     {  // mode 2 (last): X (n^2 x n) . E^T, batch Z
         GemmArgs g;
         g.A = X; g.lda = n; g.B = E; g.b_kmajor = 1; g.ldb = n; g.C = Y; g.ldc = n;
         g.M = n * n; g.N = n; g.K = n; g.Z = Z;
         g.sA1 = N; g.sB1 = (long long)n * n; g.sC1 = N;
-        cases.push_back({"mode2", g, fl});
+        if (band) { g.band = band; g.band_mode = 3; g.band_rows = n; g.band_stride = (n + 31) / 32; }
+        cases.push_back({"mode2", g, fl * band_frac});
     }
     {  // mode 2 + squaring epilogue (p = 4 groups: 1..4 extra addends)
         GemmArgs g = cases.back().g;
         g.sB1 = 0;
+        g.band = nullptr;
         g.alpha_z = alpha; g.ext = EXT; g.ext_s = N; g.ext_group = 4; g.coef = coef; g.cld = 4; g.nterms = nterms;
         cases.push_back({"mode2+sq", g, fl});
     }
@@ -117,12 +141,12 @@ int main(int argc, char** argv) {
                    ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
     }
         T(64, 64, 8, 32, 32, 4, 4)
-        T(64, 64, 8, 32, 32, 3, 4)
-        T(64, 64, 8, 32, 32, 3, 5)
-        T(64, 64, 8, 32, 32, 4, 5)
-        T(64, 64, 16, 32, 32, 2, 5)
         T(32, 64, 8, 16, 32, 4, 6)
         T(64, 32, 8, 32, 16, 4, 6)
+        T(32, 128, 8, 16, 64, 4, 4)
+        T(128, 32, 8, 64, 16, 4, 4)
+        T(32, 128, 8, 32, 32, 4, 4)
+        T(128, 32, 8, 32, 32, 4, 4)
     }
     return 0;
 }
