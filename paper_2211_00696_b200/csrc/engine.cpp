@@ -205,6 +205,7 @@ DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const
         cuda_check(cudaEventRecord(c.ev_fac, c.stream), "factor record");
         last = op.host;
     }
+    op.serial = ++c.op_serial;
     size_t off = 0;
     for (int k = 0; k < d; ++k) {
         const int n = op.n[k];
@@ -429,23 +430,93 @@ static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>&
 // B_f = 2^-e_f G_f (exact, ||B_f||_1 <= 1) and alpha_z = c_z 2^(e_f - s_z) (exact),
 //   exp(c_z G_f) = (sum_k alpha_z^k / k! B_f^k)^(2^s_z),   ||alpha_z B_f||_1 <= theta_m,
 // where theta_m bounds the relative backward error of the truncated series by u = 2^-53 (the
-// same criterion dense.hpp's Pade-13 threshold 5.37 encodes).  The powers B^2..B^m of every
-// factor take ceil(log2 m) batched DMMA launches, the combination is one elementwise pass, and
-// the squarings reuse squaring_rounds.  Against an eigendecomposition ground truth this is as
-// accurate as the reference's Pade-13 ("Exponentials").  Returns false (caller uses
-// expm_core) when a norm is unknown or PQ_EXPM=pade.
-//
-// Entries [split, count) are "late" (needed only after the node sweep: the squaring chain and
-// phi_0): with late_async their combination and squaring rounds run on the side stream, which
-// records c.ev_late when done; entries [0, split) are finished on c.stream.
-static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, const std::vector<ExpmEntry>& es,
-                        double* out, int split = -1, bool late_async = false, int2* band = nullptr) {
+// same criterion dense.hpp's Pade-13 threshold 5.37 encodes; tools/taylor_theta.py computes it
+// in exact rational arithmetic).  m = 32 (theta_32 = 4.0076): the powers B^2..B^32 of every factor
+// take five batched DMMA launches that do not depend on the plan, so phiquadmv enqueues them
+// before it waits for beta (taylor_prefetch); the combination is one elementwise pass and the
+// squarings reuse squaring_rounds.  Against an eigendecomposition ground truth this is as
+// accurate as the reference's Pade-13.
+constexpr int kTaylorM = 32;
+constexpr double kTaylorTheta = 4.00756108611804;
+
+static bool taylor_disabled() {
     static const bool disabled = [] {
         const char* v = std::getenv("PQ_EXPM");
         return v && std::string(v) == "pade";
     }();
+    return disabled;
+}
+
+// per canonical factor: gnorm >= ||fl(op_scale A_f)||_1, 2^-e_f and 2^e_f with 2^e_f >= gnorm
+struct TaylorFactors {
+    std::vector<long long> foff;
+    std::vector<double> gnorm, pow2, nu;
+};
+static bool taylor_factors(double op_scale, const std::vector<long long>& foff, const std::vector<double>& fnorm,
+                           TaylorFactors& tf) {
+    tf.foff = foff;
+    const size_t nf = foff.size();
+    tf.gnorm.assign(nf, 0.0);
+    tf.pow2.assign(nf, 1.0);
+    tf.nu.assign(nf, 1.0);
+    for (size_t f = 0; f < nf; ++f) {
+        // ||fl(op_scale A_f)||_1 <= |op_scale| ||A_f||_1 (1 + n u); the margin keeps the theta test safe
+        const double g = std::abs(op_scale) * fnorm[f] * (1.0 + 1e-12);
+        if (!std::isfinite(g)) return false;
+        tf.gnorm[f] = g;
+        int ex = 0;
+        if (g > 0.0) std::frexp(g, &ex);  // 2^ex >= g
+        tf.nu[f] = std::ldexp(1.0, ex);
+        tf.pow2[f] = std::ldexp(1.0, -ex);
+    }
+    return true;
+}
+
+// B_f^k, k = 1..kTaylorM, stored [f][k-1][n x n] in ws "taylorP<n>"; reused within one API call
+// (same DevOp serial, scale and factor set), recomputed otherwise.
+static const double* taylor_powers(pq_ctx& c, int n, const double* base, double op_scale, const TaylorFactors& tf,
+                                   uint64_t serial) {
+    const int nf = static_cast<int>(tf.foff.size());
+    const size_t nn = static_cast<size_t>(n) * n;
+    double* P = ws(c, "taylorP" + std::to_string(n), static_cast<size_t>(nf) * kTaylorM * nn);
+    pq_ctx::PowCache& pc = c.pow_cache[n];
+    if (serial != 0 && pc.serial == serial && pc.P == P && pc.base == base && pc.foff == tf.foff && pc.scale == op_scale)
+        return P;
+    const long long* foff_dev = static_cast<const long long*>(arena_push(c, tf.foff.data(), sizeof(long long) * nf));
+    const double* pow2_dev = static_cast<const double*>(arena_push(c, tf.pow2.data(), sizeof(double) * nf));
+    arena_flush(c);
+    launch_taylor_base(n, nf, kTaylorM, base, foff_dev, op_scale, pow2_dev, P, c.stream);
+    count_launch(c);
+    const long long lnn = static_cast<long long>(nn), fs = static_cast<long long>(kTaylorM) * lnn;
+    for (int h = 1; h < kTaylorM; h *= 2) {  // P^(h+j) = P^h P^j, j = 1..min(h, m-h), all factors in one launch
+        const int J = std::min(h, kTaylorM - h);
+        GemmArgs g = square_batch(n, nf * J, P + (h - 1) * lnn, P, P + h * lnn);
+        g.zdiv = J;
+        g.sA1 = fs;
+        g.sA2 = 0;
+        g.sB1 = fs;
+        g.sB2 = lnn;
+        g.sC1 = fs;
+        g.sC2 = lnn;
+        gemm(c, g);
+    }
+    pc.P = P;
+    pc.base = base;
+    pc.foff = tf.foff;
+    pc.scale = op_scale;
+    pc.serial = serial;
+    return P;
+}
+
+// Entries [split, count) are "late" (needed only after the node sweep: the squaring chain and
+// phi_0): with late_async their combination and squaring rounds run on the side stream, which
+// records c.ev_late when done; entries [0, split) are finished on c.stream.  Returns false
+// (caller uses expm_core) when a norm is unknown or PQ_EXPM=pade.
+static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, const std::vector<ExpmEntry>& es,
+                        double* out, int split = -1, bool late_async = false, int2* band = nullptr,
+                        uint64_t serial = 0) {
     const int count = static_cast<int>(es.size());
-    if (disabled || count <= 0) return false;
+    if (taylor_disabled() || count <= 0) return false;
     std::vector<long long> foff;
     std::vector<double> fnorm;
     std::vector<int> fidx(static_cast<size_t>(count));
@@ -460,63 +531,18 @@ static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, c
         }
         fidx[static_cast<size_t>(z)] = static_cast<int>(f);
     }
-    const int nf = static_cast<int>(foff.size());
-    std::vector<double> gnorm(static_cast<size_t>(nf)), pow2(static_cast<size_t>(nf)), nu(static_cast<size_t>(nf));
-    for (int f = 0; f < nf; ++f) {
-        // ||fl(op_scale A_f)||_1 <= |op_scale| ||A_f||_1 (1 + n u); the margin keeps the theta test safe
-        const double g = std::abs(op_scale) * fnorm[static_cast<size_t>(f)] * (1.0 + 1e-12);
-        if (!std::isfinite(g)) return false;
-        gnorm[static_cast<size_t>(f)] = g;
-        int ex = 0;
-        if (g > 0.0) std::frexp(g, &ex);  // 2^ex >= g
-        nu[static_cast<size_t>(f)] = std::ldexp(1.0, ex);
-        pow2[static_cast<size_t>(f)] = std::ldexp(1.0, -ex);
-    }
-    // theta_m: largest ||X||_1 with sum_k |c_k| ||X||^(k-1) <= 2^-53 for the series of
-    // log(e^-X T_m(X)) (computed once in exact rational arithmetic; tools/taylor_theta.py)
-    static const int kM[] = {16, 18, 20, 24, 28, 32};
-    static const double kTh[] = {0.7802874256626574, 1.0908637192900361, 1.4382525968043367,
-                                 2.2190488693650896, 3.084000544989162,  4.00756108611804};
-    auto squarings = [&](int z, double th) {
-        const double x = std::abs(es[static_cast<size_t>(z)].scale) * gnorm[static_cast<size_t>(fidx[static_cast<size_t>(z)])];
-        return x > th ? static_cast<int>(std::ceil(std::log2(x / th))) : 0;
-    };
+    TaylorFactors tf;
+    if (!taylor_factors(op_scale, foff, fnorm, tf)) return false;
     if (split < 0 || split > count) split = count;
-    // degree: minimise power products + squaring-round batch sizes + a per-launch latency term
-    // (rounds of the late range count a quarter: they overlap the node sweep)
-    auto rounds_cost = [&](const std::vector<int>& s, int z_begin, int z_end) {
-        int smax = 0;
-        for (int z = z_begin; z < z_end; ++z) smax = std::max(smax, s[static_cast<size_t>(z)]);
-        double cost = 6.0 * smax;
-        for (int r = 0; r < smax; ++r) {
-            int z0 = z_begin;
-            while (z0 < z_end && s[static_cast<size_t>(z0)] <= r) ++z0;
-            cost += z_end - z0;
-        }
-        return cost;
-    };
-    int best = 0;
-    double best_cost = 0.0;
-    for (int i = 0; i < 6; ++i) {
-        const int m = kM[i];
-        std::vector<int> s(static_cast<size_t>(count));
-        for (int z = 0; z < count; ++z) s[static_cast<size_t>(z)] = squarings(z, kTh[i]);
-        double cost = nf * (m - 1.0) + 6.0 * std::ceil(std::log2(static_cast<double>(m))) + rounds_cost(s, 0, split) +
-                      (late_async ? 0.25 : 1.0) * rounds_cost(s, split, count);
-        if (i == 0 || cost < best_cost) {
-            best = i;
-            best_cost = cost;
-        }
-    }
-    const int m = kM[best];
-    const double th = kTh[best];
+    constexpr int m = kTaylorM;
     std::vector<int> hint(static_cast<size_t>(count));
     std::vector<double> coef(static_cast<size_t>(count) * (m + 1));
     for (int z = 0; z < count; ++z) {
-        const int s = squarings(z, th);
+        const size_t f = static_cast<size_t>(fidx[static_cast<size_t>(z)]);
+        const double x = std::abs(es[static_cast<size_t>(z)].scale) * tf.gnorm[f];
+        const int s = x > kTaylorTheta ? static_cast<int>(std::ceil(std::log2(x / kTaylorTheta))) : 0;
         hint[static_cast<size_t>(z)] = s;
-        const double alpha =
-            std::ldexp(es[static_cast<size_t>(z)].scale * nu[static_cast<size_t>(fidx[static_cast<size_t>(z)])], -s);
+        const double alpha = std::ldexp(es[static_cast<size_t>(z)].scale * tf.nu[f], -s);
         double* t = coef.data() + static_cast<size_t>(z) * (m + 1);
         t[0] = 1.0;
         for (int k = 1; k <= m; ++k) t[k] = t[k - 1] * alpha / k;
@@ -534,10 +560,8 @@ static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, c
     };
     const std::vector<int> ch_early = chunks_of(0, split), ch_late = chunks_of(split, count);
     const size_t nn = static_cast<size_t>(n) * n;
-    double* P = ws(c, "taylorP", static_cast<size_t>(nf) * m * nn);
+    const double* P = taylor_powers(c, n, base, op_scale, tf, serial);
     double* T = ws(c, "taylorT", static_cast<size_t>(count) * nn);
-    const long long* foff_dev = static_cast<const long long*>(arena_push(c, foff.data(), sizeof(long long) * nf));
-    const double* pow2_dev = static_cast<const double*>(arena_push(c, pow2.data(), sizeof(double) * nf));
     const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), sizeof(double) * coef.size()));
     const int* che_dev = ch_early.empty() ? nullptr
                                           : static_cast<const int*>(arena_push(c, ch_early.data(), sizeof(int) * ch_early.size()));
@@ -545,21 +569,6 @@ static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, c
                                          : static_cast<const int*>(arena_push(c, ch_late.data(), sizeof(int) * ch_late.size()));
     const int* s_dev = static_cast<const int*>(arena_push(c, hint.data(), sizeof(int) * count));
     arena_flush(c);
-    launch_taylor_base(n, nf, m, base, foff_dev, op_scale, pow2_dev, P, c.stream);
-    count_launch(c);
-    const long long lnn = static_cast<long long>(nn), fs = static_cast<long long>(m) * lnn;
-    for (int h = 1; h < m; h *= 2) {  // P^(h+j) = P^h P^j, j = 1..min(h, m-h), all factors in one launch
-        const int J = std::min(h, m - h);
-        GemmArgs g = square_batch(n, nf * J, P + (h - 1) * lnn, P, P + h * lnn);
-        g.zdiv = J;
-        g.sA1 = fs;
-        g.sA2 = 0;
-        g.sB1 = fs;
-        g.sB2 = lnn;
-        g.sC1 = fs;
-        g.sC2 = lnn;
-        gemm(c, g);
-    }
     // combination + squaring rounds of entries [z_begin, z_end) on c.stream
     auto finish = [&](int z_begin, int z_end, const std::vector<int>& ch, const int* ch_dev) {
         if (z_end <= z_begin) return;
@@ -683,7 +692,7 @@ static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, con
                          : nullptr;
         // the side stream is in order, so waiting on the last ev_late covers every group's late work
         const bool async = late_async && split < static_cast<int>(es.size());
-        if (expm_taylor(c, n, base, s, es, out, split, async, band)) {
+        if (expm_taylor(c, n, base, s, es, out, split, async, band, op.serial)) {
             px.late = px.late || async;
         } else {
             expm_core(c, n, base, s, es, out);
@@ -709,6 +718,39 @@ static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, con
         px.phi0_band[k] = px.phi0_band[canon[k]];
     }
     return px;
+}
+
+// Canonical factors grouped by size exactly as phi_exponentials batches them, so the prefetched
+// powers carry the same factor set (and cache key) as the exponentials that use them.
+void taylor_prefetch(pq_ctx& c, const DevOp& op, double scale) {
+    if (taylor_disabled()) return;
+    size_t off[3] = {0, 0, 0};
+    for (int k = 1; k < op.d; ++k) off[k] = off[k - 1] + static_cast<size_t>(op.n[k - 1]) * op.n[k - 1];
+    int canon[3] = {0, 1, 2};
+    for (int k = 0; k < op.d; ++k) {
+        canon[k] = k;
+        for (int j = 0; j < k; ++j)
+            if (canon[j] == j && op.n[j] == op.n[k] &&
+                std::memcmp(op.host.data() + off[j], op.host.data() + off[k], sizeof(double) * op.n[k] * op.n[k]) == 0) {
+                canon[k] = j;
+                break;
+            }
+    }
+    std::vector<int> done(3, 0);
+    for (int k = 0; k < op.d; ++k) {
+        if (canon[k] != k || done[k]) continue;
+        const int n = op.n[k];
+        std::vector<long long> foff;
+        std::vector<double> fnorm;
+        for (int j = k; j < op.d; ++j)
+            if (canon[j] == j && op.n[j] == n) {
+                foff.push_back(static_cast<long long>(off[j]));
+                fnorm.push_back(op.one_norm[j]);
+                done[j] = 1;
+            }
+        TaylorFactors tf;
+        if (taylor_factors(scale, foff, fnorm, tf)) taylor_powers(c, n, op.F[0], scale, tf, op.serial);
+    }
 }
 
 // ------------------------------------------------------------------ mode products --------
@@ -1429,6 +1471,9 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
                    "beta readback");
         cuda_check(cudaEventRecord(c.ev_beta, c.stream), "beta record");
     }
+    // the exponentials' shared Taylor powers do not depend on the plan: enqueue them before the
+    // host waits for beta, so the GPU computes them while the host plans
+    taylor_prefetch(c, op, 1.0);
     if (nb > 0 && nb <= 512) {
         cuda_check(cudaEventSynchronize(c.ev_beta), "beta wait");
         for (int m = 0; m < nb; ++m) beta = std::max(beta, c.h_small[2 * m + 1]);

@@ -61,6 +61,17 @@ struct pq_ctx {
     cudaStream_t sq2 = nullptr;
     cudaEvent_t ev_sqfork = nullptr;
     std::vector<cudaEvent_t> ev_sqA, ev_sqB;
+    // Taylor powers of the current call's factors (engine.cpp taylor_powers), per factor size;
+    // valid only for the DevOp serial they were computed for (never reused across calls)
+    struct PowCache {
+        const double* P = nullptr;
+        const double* base = nullptr;
+        std::vector<long long> foff;
+        double scale = 0.0;
+        uint64_t serial = 0;
+    };
+    std::map<int, PowCache> pow_cache;
+    uint64_t op_serial = 0;  // incremented per operator upload (one per API call)
     cudaEvent_t ev_beta = nullptr;  // beta readback (phiquadmv) completes
     cudaEvent_t ev_cc = nullptr;    // adaptive CC error readback completes
     // factor uploads: pinned staging (no implicit stream sync) + per-slot cache of the last
@@ -101,6 +112,7 @@ struct DevOp {
     double one_norm[3] = {0, 0, 0};                    // host: 1-norms of the unscaled factors
     double inf_norm[3] = {0, 0, 0};                    // host: inf-norms of the unscaled factors
     std::vector<double> host;                          // host copy (concatenated), for host math
+    uint64_t serial = 0;                               // upload serial (per API call)
 };
 
 // Epilogue applied at the last mode of a mode chain (see GemmArgs).
@@ -181,6 +193,9 @@ struct PlanInfo {
     int l = 0, n = 0, points = 0, mode = 0, planned = 0;
     double alpha = 0, beta = 0, cost = 0;
 };
+// Enqueues the Taylor powers of op's factors at `scale` (they do not depend on the plan), so they
+// run while the host waits for beta and plans; phi_exponentials of the same call reuses them.
+void taylor_prefetch(pq_ctx& c, const DevOp& op, double scale);
 void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l,
                    int l, double c1, double c2, double* out, PlanInfo* info, double* phi0_out = nullptr);
 void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p,
