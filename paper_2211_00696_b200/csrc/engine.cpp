@@ -1117,6 +1117,15 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
     };
     if (!c.ev_cc) cuda_check(cudaEventCreateWithFlags(&c.ev_cc, cudaEventDisableTiming), "cc event");
     const bool pinned_stats = 2 * nb * p <= 1024;
+    // a level whose combination runs on c.sq2 (while the speculative sweep of the next level runs
+    // on the main stream): the main stream joins on ev_cc before it reads that level's sums
+    bool join_pending = false;
+    const cudaStream_t main_stream = c.stream;
+    struct RestoreStream {  // an exception thrown while a level runs on c.sq2 leaves c.stream intact
+        pq_ctx& c;
+        cudaStream_t s;
+        ~RestoreStream() { c.stream = s; }
+    } restore{c, main_stream};
     while (true) {
         const int half_next = 2 * half;
         if (half_next > (1 << 14)) throw ConvergenceFailure("phi_adaptive: no convergence within the node budget");
@@ -1130,6 +1139,20 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         for (int k = 0; k < fresh; ++k)
             fine_slot[static_cast<size_t>(2 * k + 1)] = preswept ? 2 * k + 1 : level_base[level] + k;
         const int nxt = 1 - cur;
+        const int next_points = 2 * fine.size() - 1;
+        const bool will_spec =
+            pinned_stats && spec_points > 0 && next_points <= spec_points && 2 * half_next <= (1 << 14);
+        if (join_pending) {
+            cuda_check(cudaStreamWaitEvent(main_stream, c.ev_cc, 0), "cc join");
+            join_pending = false;
+        }
+        const bool offload = fused && will_spec && !c.profiling;
+        if (offload) {
+            ensure_sq2(c, 0);
+            cuda_check(cudaEventRecord(c.ev_sqfork, main_stream), "cc fork");
+            cuda_check(cudaStreamWaitEvent(c.sq2, c.ev_sqfork, 0), "cc fork wait");
+            c.stream = c.sq2;
+        }
         // phiaction.hpp:225-240: max over columns of ||y - y_prev||_inf / ||y||_inf
         if (fused) {
             std::vector<int> idx(static_cast<size_t>(fine.size()));
@@ -1171,13 +1194,15 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         cuda_check(cudaMemcpyAsync(hs, stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
                    "cc stats readback");
         cuda_check(cudaEventRecord(c.ev_cc, c.stream), "cc record");
+        if (offload) {
+            c.stream = main_stream;
+            join_pending = true;
+        }
         mark(c, "cc_level_enqueued");
         // Speculation: when the planner predicts the next level is needed (its rule has at most
         // spec_points nodes), its node sweep is enqueued before the host waits for this level's
         // error, so the GPU never drains at the check (a wasted sweep if this level converges).
-        const int next_points = 2 * fine.size() - 1;
-        if (pinned_stats && spec_points > 0 && next_points <= spec_points && 2 * half_next <= (1 << 14))
-            sweep_level(level + 1, memo_rule(kClenshaw, next_points));
+        if (will_spec) sweep_level(level + 1, memo_rule(kClenshaw, next_points));
         cuda_check(cudaEventSynchronize(c.ev_cc), "cc stats wait");
         mark(c, "cc_level_synced");
         cur = nxt;
@@ -1189,6 +1214,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         }
         if (err <= eps) break;
     }
+    if (join_pending) cuda_check(cudaStreamWaitEvent(main_stream, c.ev_cc, 0), "cc join");
     if (accs[cur] != out)
         cuda_check(cudaMemcpyAsync(out, accs[cur], col * sizeof(double), cudaMemcpyDeviceToDevice, c.stream), "cc copy");
     if (points_used) *points_used = rule->size();
