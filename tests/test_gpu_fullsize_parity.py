@@ -1,0 +1,57 @@
+"""SURVEY.md 8(d) parity plan at the sizes it names, against the compiled reference (oracle/_ref,
+unmodified headers) run on the GPU box's host cores:
+
+* configs 1 and 2 at FULL size through phiquadmv (the reference plans (l, n) itself; the GPU must
+  reproduce the plan, the CC point count, every phi_j column and phi_0);
+* config 5's full pipeline at n = 96 (variable-coefficient factor, GL, p = 6, l from the planner);
+* config 4 (ETDRK4, Allen-Cahn) at n = 32, 10 steps.
+
+Tolerance: relative 2-norm <= 1e-11 per column (BASELINE.json north_star).  These exercise the
+sm_100a paths the small cases cannot: 64x64-class mode-product tiles with the negligible-block
+skip, the shared-power Taylor exponentials with squaring rounds, the two-stream squaring and
+the fused CC ladder at the headline shape.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import rel2
+
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+THREADS = os.cpu_count() or 1
+
+
+def _phiquadmv_vs_reference(pq, ref, w):
+    a = pq.KroneckerSum(w.factors)
+    b = w.rhs(0)
+    info = pq.PhiInfo()
+    phi0, cols = pq.phi_0p(a, [b], pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode)), info)
+    want, rinfo = ref.phiquadmv(w.factors, b[None, :], w.p, w.eps, w.mode, threads=THREADS)
+    assert (info.l, info.n, info.points) == (rinfo["l"], rinfo["n"], rinfo["points"])
+    errs = [rel2(cols[0, j], want[0][j]) for j in range(w.p)]
+    assert max(errs) <= 1e-11, errs
+    e0 = rel2(phi0[0], ref.exp_action(w.factors, b))
+    assert e0 <= 1e-11, e0
+
+
+@pytest.mark.parametrize("cfg", [1, 2])
+def test_fullsize_phiquadmv_vs_reference(pq, ref, cfg):
+    from paper_2211_00696_b200.workloads import config
+    _phiquadmv_vs_reference(pq, ref, config(cfg))
+
+
+def test_config5_pipeline_n96_vs_reference(pq, ref):
+    from paper_2211_00696_b200.workloads import config
+    _phiquadmv_vs_reference(pq, ref, config(5, n=96))
+
+
+def test_config4_etdrk4_n32_vs_reference(pq, ref):
+    from paper_2211_00696_b200.workloads import allen_cahn_u0, config
+    w = config(4, n=32)
+    u0 = allen_cahn_u0(w.N)
+    res = pq.integrate(pq.KroneckerSum(w.A), ("cubic", 1.0, -1.0), u0, 0.0, 10 * w.tau, 10, pq.etdrk4_tableau(),
+                       pq.PhiRequest(eps=w.eps))
+    want, calls = ref.integrate(w.A, 1, u0, 0.0, 10 * w.tau, 10, 3, eps=w.eps)
+    assert res.phi_calls == calls
+    assert rel2(res.u, want) <= 1e-11
