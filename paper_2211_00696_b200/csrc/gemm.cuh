@@ -7,6 +7,7 @@
 // 64-bit address arithmetic) and the epilogue is compact (the extra-addend loop is not
 // unrolled) so the whole kernel stays inside the instruction cache.
 #pragma once
+#include <cstdlib>
 #include <stdexcept>
 
 #include "kernels.hpp"
@@ -64,6 +65,9 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
     const int wm = warp / T::NWN, wn = warp % T::NWN;
     const int gid = lane >> 2, tig = lane & 3;
 
+    // programmatic dependent launch: everything above is index math; global data written by the
+    // preceding kernel (operands, band tables, squaring counts) is read only after this wait
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (g.sq_count && g.sq_round >= g.sq_count[z]) {
         // expm squaring already finished for this matrix: carry it through unchanged.
         for (int e = tid; e < BM * BN; e += NT) {
@@ -141,7 +145,7 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
 
     int kt_lo = 0, KT = (g.K + BK - 1) / BK;
     int w_lo = 0, w_hi = KT;  // this warp's DMMA slices (absolute)
-    if constexpr (BK == 8) {
+    if constexpr (BK == 8 || BK == 16) {
         // negligible-block skip: the CTA streams the union of the 32-row exponential blocks its
         // tile covers, each warp multiplies only inside its own block's slices
         if (g.band) {
@@ -169,13 +173,15 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
                     hi = max(hi, v.y);
                 }
             }
-            kt_lo = hi > lo ? lo : 0;
-            KT = min(KT, hi > lo ? hi : 0);
+            // the table counts 8-column slices; a BK-wide stage covers BK/8 of them
+            constexpr int SH = BK == 16 ? 1 : 0;
+            kt_lo = hi > lo ? (lo >> SH) : 0;
+            KT = min(KT, hi > lo ? ((hi + (1 << SH) - 1) >> SH) : 0);
             if (we <= 32) {  // the warp lies in one 32-row block: multiply only inside its range
                 const int wb = wr >> 5;
                 const int2 mine = wb < nb ? br[wb] : make_int2(0, 0);
-                w_lo = mine.x;
-                w_hi = mine.y;
+                w_lo = mine.x >> SH;
+                w_hi = (mine.y + (1 << SH) - 1) >> SH;
             } else {
                 w_lo = kt_lo;
                 w_hi = KT;
@@ -224,6 +230,9 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
         }
     }
     cp_wait<0>();
+    // this CTA no longer needs the SM for DMMA work: let the next kernel in the stream launch its
+    // CTAs (they stop at griddepcontrol.wait until this grid has completed)
+    asm volatile("griddepcontrol.launch_dependents;");
 
     // ---- epilogue (registers -> global) ----
     const double alpha = g.alpha_z ? g.alpha_z[z1] : g.alpha;
@@ -450,6 +459,16 @@ static int launch_persist(const GemmArgs& g, int max_ctas, cudaStream_t s) {
     return 1;
 }
 
+// Programmatic dependent launch for the mode products (PQ_PDL=0 disables): the next GEMM's CTAs
+// are scheduled while this one drains its last wave.
+static bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PQ_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC, int MINB = 1>
 static int launch_cfg(const GemmArgs& g, cudaStream_t s) {
     using T = TileCfg<BM, BN, BK, WM, WN, ST, BKM>;
@@ -466,7 +485,17 @@ static int launch_cfg(const GemmArgs& g, cudaStream_t s) {
     for (int z0 = 0; z0 < g.Z; z0 += 65535) {
         a.z_off = z0;
         const int zc = g.Z - z0 < 65535 ? g.Z - z0 : 65535;
-        kern<<<dim3((unsigned)gx, (unsigned)gy, (unsigned)zc), T::NT, T::SMEM, s>>>(a);
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3((unsigned)gx, (unsigned)gy, (unsigned)zc);
+        cfg.blockDim = dim3(T::NT);
+        cfg.dynamicSmemBytes = T::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kern, a);
         ++launches;
     }
     return launches;
