@@ -543,9 +543,16 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
     mark(*c, "uploaded");
     PlanInfo pi;
     double* d0 = out0 ? stage_out(*c, out0, static_cast<size_t>(nb) * N, space, "hout0") : nullptr;
-    phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi, d0);
+    // pinned host phi_0 buffer: copied out by the engine as soon as phi_0 exists (overlaps the squaring)
+    double* h0 = nullptr;
+    if (out0 && space == PQ_HOST) {
+        cudaPointerAttributes at{};
+        if (cudaPointerGetAttributes(&at, out0) == cudaSuccess && at.type == cudaMemoryTypeHost) h0 = out0;
+        cudaGetLastError();  // a pageable pointer is not an error
+    }
+    phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi, d0, h0);
     mark(*c, "computed");
-    if (out0) finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
+    if (out0 && !h0) finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
     finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
     finish(*c, space);
     if (info) {

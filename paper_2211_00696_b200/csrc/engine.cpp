@@ -1410,7 +1410,8 @@ void squaring_steps_dev(pq_ctx& c, const DevOp& op, double scale, int nb, int p,
 
 // phiaction.hpp:277-303, plus (when phi0_out) kron.hpp:123-128 phi_0 from the same expm batch.
 static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n,
-                         int kind, double eps, double* out, int* points_used, double* phi0_out) {
+                         int kind, double eps, double* out, int* points_used, double* phi0_out,
+                         double* phi0_host = nullptr) {
     if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
     if (p < 1) throw std::invalid_argument(kind == kGauss ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
     const NodesWeights& rule = kind == kGauss ? memo_rule(kGauss, n + 1) : memo_rule(kClenshaw, 25);
@@ -1450,6 +1451,9 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
         c.stream = c.side;
         try {
             apply_phi0(c, op, px, nb, bs, phi0_out);
+            if (phi0_host)  // pinned destination: the D2H overlaps the squaring
+                cuda_check(cudaMemcpyAsync(phi0_host, phi0_out, sizeof(double) * nb * op.N, cudaMemcpyDeviceToHost, c.side),
+                           "phi_0 D2H");
         } catch (...) {
             c.stream = main_stream;
             throw;
@@ -1466,10 +1470,14 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
                        "plan copy");
     }
     mark(c, "squaring");
-    if (side_phi0)
+    if (side_phi0) {
         cuda_check(cudaStreamWaitEvent(c.stream, c.ev_join, 0), "join wait");
-    else if (phi0_out)
+    } else if (phi0_out) {
         apply_phi0(c, op, px, nb, bs, phi0_out);
+        if (phi0_host)
+            cuda_check(cudaMemcpyAsync(phi0_host, phi0_out, sizeof(double) * nb * op.N, cudaMemcpyDeviceToHost, c.stream),
+                       "phi_0 D2H");
+    }
 }
 
 void phi_with_plan_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n, int kind,
@@ -1479,7 +1487,7 @@ void phi_with_plan_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const d
 
 // phiaction.hpp:307-346 (+ phi_0 when phi0_out).
 void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l, int l,
-                   double c1, double c2, double* out, PlanInfo* info, double* phi0_out) {
+                   double c1, double c2, double* out, PlanInfo* info, double* phi0_out, double* phi0_host) {
     if (p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
     double alpha = 0.0;
     for (int k = 0; k < op.d; ++k) alpha += op.inf_norm[k];
@@ -1530,7 +1538,7 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
     }
     mark(c, "planned");
     int points = 0;
-    phi_call_dev(c, op, 1.0, nb, bs, p, l, n, mode, eps, out, &points, phi0_out);
+    phi_call_dev(c, op, 1.0, nb, bs, p, l, n, mode, eps, out, &points, phi0_out, phi0_host);
     if (info) {
         info->l = l;
         info->n = n;
