@@ -143,12 +143,12 @@ int main(int argc, char** argv) {
         T(64, 64, 8, 32, 32, 4, 4)
         T(32, 64, 8, 16, 32, 4, 6)
         T(64, 32, 8, 32, 16, 4, 6)
-        T(32, 64, 16, 16, 32, 3, 6)
-        T(64, 32, 16, 32, 16, 3, 6)
-        T(32, 64, 8, 16, 32, 4, 8)
-        T(64, 32, 8, 32, 16, 4, 8)
-        T(32, 64, 8, 16, 32, 6, 6)
-        T(64, 32, 8, 32, 16, 6, 6)
+        T(32, 128, 8, 16, 64, 4, 4)
+        T(32, 128, 8, 32, 32, 4, 4)
+        T(32, 128, 8, 16, 32, 4, 3)
+        T(128, 32, 8, 32, 16, 4, 3)
+        T(128, 32, 8, 64, 16, 4, 4)
+        T(32, 256, 8, 32, 64, 3, 2)
     }
     return 0;
 }
