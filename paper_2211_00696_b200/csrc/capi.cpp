@@ -110,6 +110,8 @@ int pq_ctx_create(int device, pq_ctx** out) {
         c->device = device;
         cuda_check(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking), "cudaStreamCreate");
         c->own_stream = true;
+        const char* tr = std::getenv("PQ_TRACE");
+        c->trace = tr && tr[0] == '1';
         cuda_check(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc(err)");
         cuda_check(cudaMemset(c->d_err, 0, sizeof(int)), "memset(err)");
         cuda_check(cudaMalloc(&c->d_int, 64 * sizeof(int)), "cudaMalloc(int)");
@@ -203,7 +205,7 @@ int pq_ctx_release_workspace(pq_ctx* c) {
         for (auto& kv : c->bufs)
             if (kv.second.p) cudaFree(kv.second.p);
         c->bufs.clear();
-        c->fac_host.clear();
+        c->fac_cache.clear();
     });
 }
 

@@ -59,6 +59,7 @@ double* ws(pq_ctx& c, const std::string& name, size_t count) {
 }
 
 void arena_begin(pq_ctx& c) {
+    c.deferred.clear();  // never carry side-stream work from an earlier (failed) call
     ParamArena& a = c.arena;
     if (!a.host) {
         a.cap = size_t(8) << 20;
@@ -76,8 +77,16 @@ const void* arena_push(pq_ctx& c, const void* data, size_t bytes) {
     ParamArena& a = c.arena;
     const size_t off = (a.used + 15) & ~size_t(15);
     if (off + bytes > a.cap) {
+        if (bytes > a.cap) throw std::invalid_argument("parameter table larger than the 8 MB staging arena");
+        // wrap around: every table pushed so far may still be read by enqueued work on any of the
+        // context's streams (and by deferred side-stream work not yet enqueued), so enqueue that,
+        // let all of it finish, then rewind
         arena_flush(c);
-        arena_begin(c);
+        run_deferred(c);
+        cuda_check(cudaStreamSynchronize(c.stream), "arena wrap");
+        if (c.side) cuda_check(cudaStreamSynchronize(c.side), "arena wrap");
+        if (c.sq2) cuda_check(cudaStreamSynchronize(c.sq2), "arena wrap");
+        a.used = a.flushed = 0;
         return arena_push(c, data, bytes);
     }
     std::memcpy(a.host + off, data, bytes);
@@ -154,7 +163,7 @@ void prof_collect(pq_ctx& c) {
 }
 
 void mark(pq_ctx& c, const char* name) {
-    if (!c.profiling) return;
+    if (!c.profiling && !c.trace) return;
     static const auto t0 = std::chrono::steady_clock::now();
     cudaEvent_t e;
     cuda_check(cudaEventCreate(&e), "mark event");
@@ -181,15 +190,15 @@ DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const
         op.N *= shape[k];
         total += static_cast<size_t>(shape[k]) * shape[k];
     }
-    op.host.assign(factors, factors + total);
-    for (double v : op.host)
-        if (!std::isfinite(v)) throw std::invalid_argument("DenseMatrix: non-finite entry");
-    const bool had = c.bufs.count(slot) && c.bufs[slot].p;
     double* dev = ws(c, slot, total);
-    auto& last = c.fac_host[slot];
-    const bool same = had && last.size() == total && std::memcmp(last.data(), factors, total * sizeof(double)) == 0 &&
-                      c.bufs[slot].p == dev;
+    pq_ctx::FacCache& fc = c.fac_cache[slot];
+    bool same = fc.host && fc.d == d && fc.dev == dev && fc.host->size() == total &&
+                std::memcmp(fc.host->data(), factors, total * sizeof(double)) == 0;
+    for (int k = 0; k < d && same; ++k) same = fc.n[k] == shape[k];
     if (!same) {
+        auto host = std::make_shared<std::vector<double>>(factors, factors + total);
+        for (double v : *host)
+            if (!std::isfinite(v)) throw std::invalid_argument("DenseMatrix: non-finite entry");
         // stage through pinned memory so the copy is asynchronous (a pageable H2D copy would wait
         // for the stream to drain, idling the GPU while the host prepares the call)
         if (!c.ev_fac) cuda_check(cudaEventCreateWithFlags(&c.ev_fac, cudaEventDisableTiming), "factor event");
@@ -203,29 +212,53 @@ DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const
         cuda_check(cudaMemcpyAsync(dev, c.pin_fac, total * sizeof(double), cudaMemcpyHostToDevice, c.stream),
                    "upload factors");
         cuda_check(cudaEventRecord(c.ev_fac, c.stream), "factor record");
-        last = op.host;
+        // dense.hpp:122-141 (host copies; the planner's alpha uses the inf-norms)
+        size_t off = 0;
+        size_t offs[3] = {0, 0, 0};
+        for (int k = 0; k < d; ++k) {
+            const int n = shape[k];
+            offs[k] = off;
+            const double* f = host->data() + off;
+            std::vector<double> col(static_cast<size_t>(n), 0.0);
+            double best_row = 0.0;
+            for (int i = 0; i < n; ++i) {
+                double rs = 0.0;
+                for (int j = 0; j < n; ++j) {
+                    const double a = std::abs(f[static_cast<size_t>(i) * n + j]);
+                    rs += a;
+                    col[static_cast<size_t>(j)] += a;
+                }
+                if (rs > best_row) best_row = rs;
+            }
+            fc.inf_norm[k] = best_row;
+            fc.one_norm[k] = *std::max_element(col.begin(), col.end());
+            off += static_cast<size_t>(n) * n;
+        }
+        // bit-identical factors (the isotropic Laplacians of configs 1, 3, 4, 5) are exponentiated once
+        for (int k = 0; k < d; ++k) {
+            fc.canon[k] = k;
+            for (int j = 0; j < k; ++j)
+                if (fc.canon[j] == j && shape[j] == shape[k] &&
+                    std::memcmp(host->data() + offs[j], host->data() + offs[k],
+                                sizeof(double) * shape[k] * shape[k]) == 0) {
+                    fc.canon[k] = j;
+                    break;
+                }
+        }
+        fc.d = d;
+        for (int k = 0; k < 3; ++k) fc.n[k] = k < d ? shape[k] : 0;
+        fc.host = host;
+        fc.dev = dev;
     }
+    op.host = fc.host;
     op.serial = ++c.op_serial;
     size_t off = 0;
     for (int k = 0; k < d; ++k) {
-        const int n = op.n[k];
-        const double* f = op.host.data() + off;
         op.F[k] = dev + off;
-        // dense.hpp:122-141 (host copies; the planner's alpha uses the inf-norms)
-        std::vector<double> col(static_cast<size_t>(n), 0.0);
-        double best_row = 0.0;
-        for (int i = 0; i < n; ++i) {
-            double rs = 0.0;
-            for (int j = 0; j < n; ++j) {
-                const double a = std::abs(f[static_cast<size_t>(i) * n + j]);
-                rs += a;
-                col[static_cast<size_t>(j)] += a;
-            }
-            if (rs > best_row) best_row = rs;
-        }
-        op.inf_norm[k] = best_row;
-        op.one_norm[k] = *std::max_element(col.begin(), col.end());
-        off += static_cast<size_t>(n) * n;
+        op.inf_norm[k] = fc.inf_norm[k];
+        op.one_norm[k] = fc.one_norm[k];
+        op.canon[k] = fc.canon[k];
+        off += static_cast<size_t>(op.n[k]) * op.n[k];
     }
     return op;
 }
@@ -569,13 +602,16 @@ static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, c
                                          : static_cast<const int*>(arena_push(c, ch_late.data(), sizeof(int) * ch_late.size()));
     const int* s_dev = static_cast<const int*>(arena_push(c, hint.data(), sizeof(int) * count));
     arena_flush(c);
-    // combination + squaring rounds of entries [z_begin, z_end) on c.stream
-    auto finish = [&](int z_begin, int z_end, const std::vector<int>& ch, const int* ch_dev) {
+    // combination + squaring rounds of entries [z_begin, z_end) on c.stream; the ping-pong partner
+    // of entry z is tbase + (z - z_begin) n^2 (the late range has its own scratch, see below)
+    auto finish = [c_ = &c, n, nn, out, P, coef_dev, s_dev, band, hint](int z_begin, int z_end, const std::vector<int>& ch,
+                                                                         const int* ch_dev, double* tbase) {
+        pq_ctx& c = *c_;
         if (z_end <= z_begin) return;
         const std::vector<int> h(hint.begin() + z_begin, hint.begin() + z_end);
         const int s_max = *std::max_element(h.begin(), h.end());
         double* o = out + static_cast<size_t>(z_begin) * nn;
-        double* t = T + static_cast<size_t>(z_begin) * nn;
+        double* t = tbase;
         double* first = (s_max % 2 == 0) ? o : t;
         // the combination kernel indexes absolute entries: shift the base so entry z_begin lands at `first`
         launch_taylor_combine(n, m, static_cast<int>(ch.size() / 4), ch_dev, coef_dev, P,
@@ -584,29 +620,42 @@ static bool expm_taylor(pq_ctx& c, int n, const double* base, double op_scale, c
         squaring_rounds(c, n, z_end - z_begin, h, s_dev + z_begin, s_max, first, first == o ? t : o, o);
         band_ranges(c, n, z_end - z_begin, o, band ? band + static_cast<size_t>(z_begin) * band_row_blocks(n) : nullptr);
     };
-    finish(0, split, ch_early, che_dev);
+    finish(0, split, ch_early, che_dev, T);
     if (split < count) {
         if (late_async) {
+            // the late entries depend only on the powers already enqueued: fork here, but enqueue
+            // their work after the first node sweep (run_deferred), so it does not delay the sweep
             ensure_side(c);
             if (!c.ev_late) cuda_check(cudaEventCreateWithFlags(&c.ev_late, cudaEventDisableTiming), "late event");
-            cuda_check(cudaEventRecord(c.ev_fork, c.stream), "late fork");
-            cuda_check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "late fork wait");
-            cudaStream_t main_stream = c.stream;
-            c.stream = c.side;
-            try {
-                finish(split, count, ch_late, chl_dev);
-            } catch (...) {
+            if (!c.ev_latefork) cuda_check(cudaEventCreateWithFlags(&c.ev_latefork, cudaEventDisableTiming), "late fork");
+            cuda_check(cudaEventRecord(c.ev_latefork, c.stream), "late fork");
+            double* tl = ws(c, "taylorTlate", static_cast<size_t>(count - split) * nn);
+            c.deferred.push_back([c_ = &c, finish, split, count, ch_late, chl_dev, tl] {
+                pq_ctx& c = *c_;
+                cuda_check(cudaStreamWaitEvent(c.side, c.ev_latefork, 0), "late fork wait");
+                const cudaStream_t main_stream = c.stream;
+                c.stream = c.side;
+                try {
+                    finish(split, count, ch_late, chl_dev, tl);
+                } catch (...) {
+                    c.stream = main_stream;
+                    throw;
+                }
                 c.stream = main_stream;
-                throw;
-            }
-            c.stream = main_stream;
-            cuda_check(cudaEventRecord(c.ev_late, c.side), "late record");
+                cuda_check(cudaEventRecord(c.ev_late, c.side), "late record");
+            });
         } else {
-            finish(split, count, ch_late, chl_dev);
+            finish(split, count, ch_late, chl_dev, T + static_cast<size_t>(split) * nn);
         }
     }
     check_launch(c);
     return true;
+}
+
+void run_deferred(pq_ctx& c) {
+    std::vector<std::function<void()>> work;
+    work.swap(c.deferred);
+    for (auto& w : work) w();
 }
 
 void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_stride, const std::vector<double>& scales,
@@ -646,20 +695,11 @@ static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, con
     px.sq_len = std::max(L, 1);
     const int per = q + L + (want_phi0 ? 1 : 0);
     if (per == 0) return px;
-    // canonical factors
+    // canonical factors (upload_op: bit-identical factors share one exponential)
     int canon[3] = {0, 1, 2};
     size_t off[3] = {0, 0, 0};
     for (int k = 1; k < op.d; ++k) off[k] = off[k - 1] + static_cast<size_t>(op.n[k - 1]) * op.n[k - 1];
-    for (int k = 0; k < op.d; ++k) {
-        canon[k] = k;
-        for (int j = 0; j < k; ++j)
-            if (canon[j] == j && op.n[j] == op.n[k] &&
-                std::memcmp(op.host.data() + off[j], op.host.data() + off[k],
-                            sizeof(double) * op.n[k] * op.n[k]) == 0) {
-                canon[k] = j;
-                break;
-            }
-    }
+    for (int k = 0; k < op.d; ++k) canon[k] = op.canon[k];
     // one batch per distinct n over the canonical factors with that n
     std::vector<int> done(3, 0);
     const double* base = op.F[0];  // factors are contiguous on the device
@@ -727,15 +767,7 @@ void taylor_prefetch(pq_ctx& c, const DevOp& op, double scale) {
     size_t off[3] = {0, 0, 0};
     for (int k = 1; k < op.d; ++k) off[k] = off[k - 1] + static_cast<size_t>(op.n[k - 1]) * op.n[k - 1];
     int canon[3] = {0, 1, 2};
-    for (int k = 0; k < op.d; ++k) {
-        canon[k] = k;
-        for (int j = 0; j < k; ++j)
-            if (canon[j] == j && op.n[j] == op.n[k] &&
-                std::memcmp(op.host.data() + off[j], op.host.data() + off[k], sizeof(double) * op.n[k] * op.n[k]) == 0) {
-                canon[k] = j;
-                break;
-            }
-    }
+    for (int k = 0; k < op.d; ++k) canon[k] = op.canon[k];
     std::vector<int> done(3, 0);
     for (int k = 0; k < op.d; ++k) {
         if (canon[k] != k || done[k]) continue;
@@ -991,6 +1023,7 @@ static void phi_fixed_shift(pq_ctx& c, const DevOp& op, double s, int l, int nb,
     (void)s;
     (void)l;
     node_sweep(c, op, px.node, Es, rule.size(), nb, bs, p, &coef, out, 1, nullptr, 0, px.node_band);
+    run_deferred(c);  // the late exponentials' side-stream work, now that the sweep is enqueued
 }
 
 void phi_fixed_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, const NodesWeights& rule,
@@ -1043,6 +1076,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             Es[k] = 2 * nn[k];
         }
         node_sweep(c, op, E, Es, 13, nb, bs, p, nullptr, nullptr, 0, pool, 0, px25.node_band);
+        run_deferred(c);  // the late exponentials' side-stream work, now that the sweep is enqueued
     }
     double* accs[2] = {out, ws(c, "ccacc", col)};
     int cur = 0;
@@ -1461,6 +1495,7 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
         c.stream = main_stream;
         cuda_check(cudaEventRecord(c.ev_join, c.side), "join record");
     }
+    run_deferred(c);  // (no-op unless the node phase did not flush it)
     if (px.late) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_late, 0), "late exps wait");
     if (l > 0) {
         double* res =

@@ -7,7 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -53,10 +55,15 @@ struct pq_ctx {
     double* d_small = nullptr;   // device scratch for reductions
     int* d_int = nullptr;        // device int scratch (expm squaring counts)
     bool profiling = false;
+    bool trace = false;  // PQ_TRACE=1: phase marks without profiling's stream serialisation
     // side stream for work independent of the node sweep (phi_0), joined back before returning
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_late = nullptr;  // late exponentials (squaring chain, phi_0) finished on `side`
+    cudaEvent_t ev_latefork = nullptr;  // main-stream point the late exponentials depend on
+    // side-stream work enqueued only after the first node sweep is on the main stream (so the
+    // host's enqueue time for it does not delay the sweep); run_deferred() flushes it
+    std::vector<std::function<void()>> deferred;
     // two-stream squaring (engine.cpp squaring_pingpong): second stream, fork event, per-step events
     cudaStream_t sq2 = nullptr;
     cudaEvent_t ev_sqfork = nullptr;
@@ -79,7 +86,16 @@ struct pq_ctx {
     double* pin_fac = nullptr;
     size_t pin_fac_cap = 0;
     cudaEvent_t ev_fac = nullptr;
-    std::map<std::string, std::vector<double>> fac_host;  // slot -> last uploaded host copy
+    // slot -> the last uploaded operator: validated host copy, device pointer, norms, canonical map
+    struct FacCache {
+        int d = 0;
+        int n[3] = {0, 0, 0};
+        std::shared_ptr<const std::vector<double>> host;
+        const double* dev = nullptr;
+        double one_norm[3] = {0, 0, 0}, inf_norm[3] = {0, 0, 0};
+        int canon[3] = {0, 1, 2};
+    };
+    std::map<std::string, FacCache> fac_cache;
     // timeline marks while profiling: name, device event, host time (us since first mark)
     struct Mark {
         std::string name;
@@ -111,7 +127,8 @@ struct DevOp {
     const double* F[3] = {nullptr, nullptr, nullptr};  // device, row-major n_k x n_k (unscaled)
     double one_norm[3] = {0, 0, 0};                    // host: 1-norms of the unscaled factors
     double inf_norm[3] = {0, 0, 0};                    // host: inf-norms of the unscaled factors
-    std::vector<double> host;                          // host copy (concatenated), for host math
+    std::shared_ptr<const std::vector<double>> host;   // host copy (concatenated), for host math
+    int canon[3] = {0, 1, 2};                          // first dim holding a bit-identical factor
     uint64_t serial = 0;                               // upload serial (per API call)
 };
 
@@ -164,6 +181,7 @@ void prof_collect(pq_ctx& c);  // syncs, folds recorded events into prof_ms/prof
 void mark(pq_ctx& c, const char* name);  // timeline mark (no-op unless profiling)
 void check_launch(pq_ctx& c);
 void ensure_side(pq_ctx& c);  // creates the side stream and its fork/join events on first use
+void run_deferred(pq_ctx& c);
 
 // ---- device building blocks ----
 DevOp upload_op(pq_ctx& c, int d, const int* shape, const double* factors, const std::string& slot);

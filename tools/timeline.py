@@ -1,7 +1,12 @@
 #!/usr/bin/env python
-"""Device/host timeline of one phi_0..phi_p call (engine marks, pq_ctx_timeline)."""
+"""Device/host timeline of one phi_0..phi_p call (engine marks, pq_ctx_timeline).
+
+usage: python tools/timeline.py [config] [--trace]
+  default: marks under profiling mode (every GEMM bracketed by events, side streams serialised);
+  --trace: PQ_TRACE=1 marks only, normal scheduling (the production overlap is kept)."""
 import ctypes as C
 import json
+import os
 import sys
 from pathlib import Path
 
@@ -13,7 +18,11 @@ def main():
     import paper_2211_00696_b200 as pq
     from paper_2211_00696_b200 import _lib as L
     from paper_2211_00696_b200.workloads import config
-    cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+    args = [x for x in sys.argv[1:] if not x.startswith("--")]
+    trace = "--trace" in sys.argv
+    if trace:
+        os.environ["PQ_TRACE"] = "1"
+    cfg = int(args[0]) if args else 2
     w = config(cfg)
     a = pq.KroneckerSum(w.factors)
     ctx = pq.Context(0)
@@ -35,7 +44,8 @@ def main():
     for _ in range(3):
         step()
     torch.cuda.synchronize()
-    ctx.set_profiling(True)
+    if not trace:
+        ctx.set_profiling(True)
     for it in range(2):
         step()
         js = C.c_char_p()
