@@ -442,6 +442,16 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, 1)
     cp_wait<0>();
 }
 
+// Programmatic dependent launch for the mode products (PQ_PDL=0 disables): the next GEMM's CTAs
+// are scheduled while this one drains its last wave.
+static bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("PQ_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC>
 static int launch_persist(const GemmArgs& g, int max_ctas, cudaStream_t s) {
     using T = TileCfg<BM, BN, BK, WM, WN, ST, BKM>;
@@ -459,15 +469,6 @@ static int launch_persist(const GemmArgs& g, int max_ctas, cudaStream_t s) {
     return 1;
 }
 
-// Programmatic dependent launch for the mode products (PQ_PDL=0 disables): the next GEMM's CTAs
-// are scheduled while this one drains its last wave.
-static bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("PQ_PDL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
 
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC, int MINB = 1>
 static int launch_cfg(const GemmArgs& g, cudaStream_t s) {

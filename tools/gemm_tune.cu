@@ -140,15 +140,8 @@ int main(int argc, char** argv) {
             printf("  %3dx%3dx%2d w%2dx%2d st%d minb%d : %8.1f us  %6.2f TF/s\n", BM, BN, BK, WM, WN, ST, MINB, \
                    ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
     }
-        T(64, 64, 8, 32, 32, 4, 4)
-        T(32, 64, 8, 16, 32, 4, 6)
-        T(64, 32, 8, 32, 16, 4, 6)
-        T(32, 128, 8, 16, 64, 4, 4)
         T(32, 128, 8, 32, 32, 4, 4)
-        T(32, 128, 8, 16, 32, 4, 3)
-        T(128, 32, 8, 32, 16, 4, 3)
-        T(128, 32, 8, 64, 16, 4, 4)
-        T(32, 256, 8, 32, 64, 3, 2)
+        T(64, 32, 8, 32, 16, 4, 6)
     }
     return 0;
 }
