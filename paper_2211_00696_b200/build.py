@@ -19,6 +19,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libpq_b200.so"
+CLI = PKG / "phiquad_cli"  # the reference CLI's wire format on this engine (cli/phiquad_cli.cpp)
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -80,6 +81,11 @@ def build(verbose: bool = False) -> Path:
                 "-L", str(CUDA / "lib64"), "-lcudart_static", "-ldl", "-lrt", "-lpthread",
                 "-Wl,--exclude-libs,ALL", "-Wl,-soname,libpq_b200.so"]
         run(link)
+    cli_src = PKG / "cli" / "phiquad_cli.cpp"
+    headers = list((ROOT / "include" / "phiquad").glob("*.hpp"))
+    if not CLI.exists() or any(p.stat().st_mtime > CLI.stat().st_mtime for p in [cli_src, LIB, *headers]):
+        run([os.environ.get("CXX", "g++"), "-std=c++20", "-O2", "-pthread", "-I", str(ROOT / "include"), str(cli_src),
+             "-L", str(PKG), "-lpq_b200", "-Wl,-rpath,$ORIGIN", "-o", str(CLI)])
     return LIB
 
 
