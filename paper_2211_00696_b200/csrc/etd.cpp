@@ -2,6 +2,7 @@
 // The state u, the stage increments D_j and every phi call stay in HBM; per stage the host only
 // enqueues kernels.  Plans are cached per (sigma, p) with beta = 1 exactly as PhiEngine does.
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -159,6 +160,24 @@ void apply_phi_group(DevPhiEngine& eng, double sigma, const std::vector<std::vec
         arena_flush(c);
         launch_combine(N, 1, static_cast<int>(slots.size()), D, N, sl, cf, gk, N, 1, c.stream);
         count_launch(c);
+    }
+    // with l = 0 (no squaring) and a Gauss rule, sum_k phi_k(A) g_k is one
+    // exp-action per node on the mixed vector sum_k theta^(k-1)/(k-1)! g_k (phi_lincomb,
+    // phiaction.hpp:355-389) instead of kmax exp-actions per node and a kmax x kmax column block
+    // of which only the diagonal is used.  Same plan, same phi-call count; the sum is rounded in a
+    // different order (within the 1e-11 parity bar).  PQ_ETD_LINCOMB=0 keeps the per-column path.
+    static const bool lincomb = [] {
+        const char* v = std::getenv("PQ_ETD_LINCOMB");
+        return !(v && v[0] == '0');
+    }();
+    const Plan& plan = eng.plan_for(sigma, kmax);
+    if (lincomb && plan.l == 0 && eng.base.mode == kGauss) {
+        ++eng.calls;
+        double* s = ws(c, "etd_lin", static_cast<size_t>(N));
+        phi_lincomb_dev(c, eng.op, -sigma * eng.tau, kmax, g, memo_rule(kGauss, plan.n + 1), s);
+        launch_axpy(N, eng.tau, s, u, c.stream);
+        count_launch(c);
+        return;
     }
     double* cols = ws(c, "etd_cols", static_cast<size_t>(kmax) * kmax * N);
     eng.apply(sigma, kmax, kmax, g, cols);
