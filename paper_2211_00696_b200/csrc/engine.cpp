@@ -660,6 +660,24 @@ void run_deferred(pq_ctx& c) {
 
 void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_stride, const std::vector<double>& scales,
                 double base_one_norm, double* out) {
+    // Large dense matrices (the dense phi oracle's augmented matrix): the
+    // per-matrix LU of the Pade solve runs in one CTA and is impractical beyond n ~ 512, so they
+    // take the shared-power Taylor path (DMMA products + squarings over the whole GPU; as accurate,
+    // DESIGN.md 3a).  Its degree/scaling choice needs the 1-norm on the host.
+    if (n > 512 && base_stride == 0) {
+        if (base_one_norm < 0.0) {
+            std::vector<double> h(static_cast<size_t>(n) * n), col(static_cast<size_t>(n), 0.0);
+            cuda_check(cudaMemcpyAsync(h.data(), base, sizeof(double) * h.size(), cudaMemcpyDeviceToHost, c.stream),
+                       "expm norm readback");
+            cuda_check(cudaStreamSynchronize(c.stream), "expm norm sync");
+            for (int i = 0; i < n; ++i)
+                for (int j = 0; j < n; ++j) col[static_cast<size_t>(j)] += std::abs(h[static_cast<size_t>(i) * n + j]);
+            base_one_norm = *std::max_element(col.begin(), col.end());
+        }
+        std::vector<ExpmEntry> es;
+        for (int z = 0; z < count; ++z) es.push_back({0, scales[static_cast<size_t>(z)], base_one_norm});
+        if (expm_taylor(c, n, base, 1.0, es, out)) return;
+    }
     std::vector<ExpmEntry> es;
     for (int z = 0; z < count; ++z) es.push_back({z * base_stride, scales[static_cast<size_t>(z)], base_one_norm});
     expm_core(c, n, base, 1.0, es, out);
