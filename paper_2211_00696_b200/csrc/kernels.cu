@@ -348,204 +348,10 @@ __global__ void __launch_bounds__(1024) k_lu_solve(int n, double* __restrict__ P
 // never stored, since the right-hand sides are eliminated alongside.
 constexpr int kLuTR = 8;  // threads per row
 
-__global__ void __launch_bounds__(1024) k_lu_smem(int n, int w, int slices, const double* __restrict__ Pg,
-                                                  double* __restrict__ Qg, int* __restrict__ err) {
-    extern __shared__ __align__(16) double sh[];
-    const int z = blockIdx.x / slices, sl = blockIdx.x % slices;
-    const int c0 = sl * w, wc = min(w, n - c0);  // this CTA's Q columns [c0, c0 + wc)
-    const int ld = n + w + 8;                    // padded row: P | Q slice
-    const double* P = Pg + (long long)z * n * n;
-    double* Q = Qg + (long long)z * n * n;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int e = tid; e < n * n; e += nt) sh[(e / n) * ld + e % n] = P[e];
-    for (int e = tid; e < n * wc; e += nt) sh[(e / wc) * ld + n + e % wc] = Q[(long long)(e / wc) * n + c0 + e % wc];
-    __shared__ int piv_sh;
-    __syncthreads();
-    const int row = tid / kLuTR, lane8 = tid % kLuTR;
-    const int width = n + wc;
-    for (int k = 0; k < n; ++k) {
-        if (tid < 32) {  // warp 0: first maximal |a_ik|, i >= k
-            double best = -1.0;
-            int bi = n;
-            for (int i = k + tid; i < n; i += 32) {
-                const double v = fabs(sh[i * ld + k]);
-                if (v > best) {
-                    best = v;
-                    bi = i;
-                }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ov > best || (ov == best && oi < bi)) {
-                    best = ov;
-                    bi = oi;
-                }
-            }
-            if (tid == 0) {
-                if (best == 0.0) {
-                    atomicExch(err, 1);
-                    bi = -1;
-                }
-                piv_sh = bi;
-            }
-        }
-        __syncthreads();
-        const int piv = piv_sh;
-        if (piv < 0) return;
-        if (piv != k && row == k) {
-            for (int j = lane8; j < width; j += kLuTR) {
-                const double t = sh[k * ld + j];
-                sh[k * ld + j] = sh[piv * ld + j];
-                sh[piv * ld + j] = t;
-            }
-        }
-        __syncthreads();
-        if (row > k && row < n) {
-            const double f = sh[row * ld + k] / sh[k * ld + k];
-            if (f != 0.0)
-                for (int j = k + 1 + lane8; j < width; j += kLuTR)
-                    sh[row * ld + j] = __dsub_rn(sh[row * ld + j], __dmul_rn(f, sh[k * ld + j]));
-        }
-        __syncthreads();
-    }
-    for (int k = n - 1; k >= 0; --k) {
-        if (row == k) {
-            const double akk = sh[k * ld + k];
-            for (int j = n + lane8; j < width; j += kLuTR) sh[k * ld + j] = sh[k * ld + j] / akk;
-        }
-        __syncthreads();
-        if (row < k) {
-            const double aik = sh[row * ld + k];
-            if (aik != 0.0)
-                for (int j = n + lane8; j < width; j += kLuTR)
-                    sh[row * ld + j] = __dsub_rn(sh[row * ld + j], __dmul_rn(aik, sh[k * ld + j]));
-        }
-        __syncthreads();
-    }
-    for (int e = tid; e < n * wc; e += nt) Q[(long long)(e / wc) * n + c0 + e % wc] = sh[(e / wc) * ld + n + e % wc];
-}
 
-// --- factor-then-solve path for n <= 128 -------------------------------------------------
-// (1) k_lu_factor: one CTA per matrix factors P = L U with partial pivoting entirely in shared
-//     memory (the reference's elimination, dense.hpp:156-173, on P only), writes L\U back over P
-//     and the pivot rows to piv[z][k].
-// (2) k_lu_trsm: CTA (z, 32-column slice of Q) applies the row swaps and the forward elimination
-//     in the reference's per-element order (b_ij -= f_ik b_kj, k ascending), then a
-//     column-oriented back substitution, Q slice staged in shared memory.
-__global__ void __launch_bounds__(1024) k_lu_factor(int n, double* __restrict__ Pg, int* __restrict__ piv,
-                                                    int* __restrict__ err) {
-    extern __shared__ __align__(16) double sh[];
-    const int ld = n + 1;  // odd stride: column reads (pivot search) spread over the banks
-    double* P = Pg + (long long)blockIdx.x * n * n;
-    int* pv = piv + (long long)blockIdx.x * n;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int e = tid; e < n * n; e += nt) sh[(e / n) * ld + e % n] = P[e];
-    __shared__ int piv_sh;
-    __syncthreads();
-    const int row = tid / kLuTR, lane8 = tid % kLuTR;
-    for (int k = 0; k < n; ++k) {
-        if (tid < 32) {
-            double best = -1.0;
-            int bi = n;
-            for (int i = k + tid; i < n; i += 32) {
-                const double v = fabs(sh[i * ld + k]);
-                if (v > best) {
-                    best = v;
-                    bi = i;
-                }
-            }
-            for (int o = 16; o > 0; o >>= 1) {
-                const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                if (ov > best || (ov == best && oi < bi)) {
-                    best = ov;
-                    bi = oi;
-                }
-            }
-            if (tid == 0) {
-                if (best == 0.0) {
-                    atomicExch(err, 1);
-                    bi = -1;
-                }
-                piv_sh = bi;
-                pv[k] = bi;
-            }
-        }
-        __syncthreads();
-        const int p = piv_sh;
-        if (p < 0) return;
-        if (p != k)
-            for (int j = tid; j < n; j += nt) {
-                const double t = sh[k * ld + j];
-                sh[k * ld + j] = sh[p * ld + j];
-                sh[p * ld + j] = t;
-            }
-        __syncthreads();
-        if (row > k && row < n) {
-            const double aik = sh[row * ld + k];
-            const double f = aik / sh[k * ld + k];
-            __syncwarp(0xFFu << (tid & 24));  // the row's 8 lanes have read a_ik
-            if (lane8 == 0) sh[row * ld + k] = f;  // L entry (0 when the reference skips the row)
-            if (f != 0.0)
-                for (int j = k + 1 + lane8; j < n; j += kLuTR)
-                    sh[row * ld + j] = __dsub_rn(sh[row * ld + j], __dmul_rn(f, sh[k * ld + j]));
-        }
-        __syncthreads();
-    }
-    for (int e = tid; e < n * n; e += nt) P[e] = sh[(e / n) * ld + e % n];
-}
 
 constexpr int kTrsmW = 32;  // RHS columns per CTA
 
-__global__ void __launch_bounds__(256) k_lu_trsm(int n, const double* __restrict__ LUg, const int* __restrict__ piv,
-                                                 double* __restrict__ Qg, int slices) {
-    extern __shared__ __align__(16) double sb[];  // n x kTrsmW slice of Q
-    __shared__ double colk[128];
-    const int z = blockIdx.x / slices, sl = blockIdx.x % slices;
-    const int c0 = sl * kTrsmW, wc = min(kTrsmW, n - c0);
-    const double* LU = LUg + (long long)z * n * n;
-    const int* pv = piv + (long long)z * n;
-    double* Q = Qg + (long long)z * n * n;
-    const int tid = threadIdx.x, nt = blockDim.x;
-    for (int e = tid; e < n * kTrsmW; e += nt) {
-        const int i = e / kTrsmW, j = e % kTrsmW;
-        sb[e] = j < wc ? Q[(long long)i * n + c0 + j] : 0.0;
-    }
-    __syncthreads();
-    const int j = tid % kTrsmW, rg = tid / kTrsmW, nrg = nt / kTrsmW;  // column j, row group
-    // forward: at step k swap rows k <-> piv[k], then b_ij -= l_ik b_kj for i > k
-    for (int k = 0; k < n; ++k) {
-        const int p = pv[k];
-        if (p != k && rg == 0) {
-            const double t = sb[k * kTrsmW + j];
-            sb[k * kTrsmW + j] = sb[p * kTrsmW + j];
-            sb[p * kTrsmW + j] = t;
-        }
-        for (int i = k + 1 + tid; i < n; i += nt) colk[i] = LU[(long long)i * n + k];
-        __syncthreads();
-        const double bk = sb[k * kTrsmW + j];
-        for (int i = k + 1 + rg; i < n; i += nrg) {
-            const double f = colk[i];
-            if (f != 0.0) sb[i * kTrsmW + j] = __dsub_rn(sb[i * kTrsmW + j], __dmul_rn(f, bk));
-        }
-        __syncthreads();
-    }
-    // back substitution, column oriented: x_k = b_k / u_kk ; b_i -= u_ik x_k (i < k)
-    for (int k = n - 1; k >= 0; --k) {
-        for (int i = tid; i <= k; i += nt) colk[i] = LU[(long long)i * n + k];
-        __syncthreads();
-        const double xk = sb[k * kTrsmW + j] / colk[k];
-        for (int i = rg; i < k; i += nrg) sb[i * kTrsmW + j] = __dsub_rn(sb[i * kTrsmW + j], __dmul_rn(colk[i], xk));
-        __syncthreads();
-        if (rg == 0) sb[k * kTrsmW + j] = xk;
-    }
-    __syncthreads();
-    for (int e = tid; e < n * kTrsmW; e += nt) {
-        const int i = e / kTrsmW, jj = e % kTrsmW;
-        if (jj < wc) Q[(long long)i * n + c0 + jj] = sb[e];
-    }
-}
 
 // --- implicit-pivoting factorisation (n <= 128), one barrier per pivot --------------------
 // Rows stay where they are; each thread-row tracks its current position in the reference's
@@ -753,20 +559,6 @@ void launch_lu_factor_solve(int n, int count, double* P, double* Q, int* piv, in
 }
 
 void launch_lu_solve(int n, int count, double* P, double* Q, int* err, cudaStream_t s) {
-    if (n <= 128) {
-        int slices = 1;
-        while ((long long)n * (n + (n + slices - 1) / slices + 8) * 8 > 220 * 1024) ++slices;
-        const int w = (n + slices - 1) / slices;
-        const int smem = n * (n + w + 8) * 8;
-        static int attr = 0;  // opt-in size already granted
-        if (smem > attr) {
-            cudaFuncSetAttribute(k_lu_smem, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-            attr = 220 * 1024;
-        }
-        const int thr = ((n * kLuTR + 31) / 32) * 32;
-        k_lu_smem<<<count * slices, thr, smem, s>>>(n, w, slices, P, Q, err);
-        return;
-    }
     k_lu_solve<<<count, 1024, 0, s>>>(n, P, Q, err);
 }
 
@@ -824,17 +616,6 @@ void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream
     k_band_ranges<<<dim3(count, (n + 31) / 32), 256, 0, s>>>(n, E, out);
 }
 
-__global__ void k_identity(int n, long long total, double* out) {
-    const long long nn = (long long)n * n;
-    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
-        const long long r = e % nn;
-        out[e] = (r / n) == (r % n) ? 1.0 : 0.0;
-    }
-}
-void launch_fill_identity(int n, int count, double* out, cudaStream_t s) {
-    const long long total = (long long)count * n * n;
-    k_identity<<<grid_for(total, 256), 256, 0, s>>>(n, total, out);
-}
 
 // ==================================================================== HBM-bound ============
 

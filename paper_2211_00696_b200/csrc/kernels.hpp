@@ -109,7 +109,5 @@ void launch_cubic_minus(long long N, double s1, double s3, const double* u, cons
 void launch_axpy(long long N, double c, const double* x, double* y, cudaStream_t s);
 // y = x - au  (generic source already evaluated)
 void launch_sub(long long N, const double* x, const double* au, double* y, cudaStream_t s);
-// y = y + c * x  for a strided batch of cnt columns sharing c (used for U += tau phi_k)
-void launch_fill_identity(int n, int count, double* out, cudaStream_t s);
 
 }  // namespace pqb
