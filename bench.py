@@ -48,6 +48,60 @@ def load_peaks() -> dict:
         return {}
 
 
+class NvmlSampler:
+    """SM clock and clock-event reasons polled through NVML every ~2 ms on a host thread, strictly
+    inside the timed region (a short region holds no nvidia-smi sample at its 200 ms period)."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, device: int):
+        self.device, self.rows, self.max_mhz, self.ok = device, [], None, False
+        self.stop = None
+
+    def __enter__(self):
+        import threading
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+            self.stop = threading.Event()
+
+            def poll():
+                while not self.stop.is_set():
+                    try:
+                        self.rows.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM),
+                                          nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+                    except Exception:
+                        pass
+                    self.stop.wait(0.002)
+
+            self.thread = threading.Thread(target=poll, daemon=True)
+            self.thread.start()
+            self.ok = True
+        except Exception:
+            self.ok = False
+        return self
+
+    def __exit__(self, *exc):
+        if self.ok:
+            self.stop.set()
+            self.thread.join(timeout=2)
+
+    def summary(self) -> dict:
+        if not self.ok or not self.rows:
+            return None
+        import pynvml as nv
+        reasons = sorted({name for _, bits in self.rows for name, const in self.REASONS
+                          if hasattr(nv, const) and bits & getattr(nv, const)})
+        return {"sm_mhz": statistics.median(r[0] for r in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": "NVML, 2 ms, timed region"}
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
 
@@ -248,9 +302,9 @@ def run_ours(args, world, rank, local) -> None:
         step_device()
     torch.cuda.synchronize()
 
-    with ClockSampler(local) as clk:
+    with ClockSampler(local) as clk, NvmlSampler(local) as nvml:
         ms_dev, launches = timed(step_device, args.steps)
-    clocks = clk.summary()
+    clocks = nvml.summary() or clk.summary()
     ms_dev_max = max_over_ranks(ms_dev, world)
     units = world * nb * args.steps
     value = units / (ms_dev_max / 1e3)
