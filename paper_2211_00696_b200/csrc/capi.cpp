@@ -546,16 +546,21 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
     PlanInfo pi;
     double* d0 = out0 ? stage_out(*c, out0, static_cast<size_t>(nb) * N, space, "hout0") : nullptr;
     // pinned host phi_0 buffer: copied out by the engine as soon as phi_0 exists (overlaps the squaring)
-    double* h0 = nullptr;
-    if (out0 && space == PQ_HOST) {
+    auto pinned = [&](double* ptr) {
+        if (!ptr || space != PQ_HOST) return false;
         cudaPointerAttributes at{};
-        if (cudaPointerGetAttributes(&at, out0) == cudaSuccess && at.type == cudaMemoryTypeHost) h0 = out0;
+        const bool yes = cudaPointerGetAttributes(&at, ptr) == cudaSuccess && at.type == cudaMemoryTypeHost;
         cudaGetLastError();  // a pageable pointer is not an error
-    }
-    phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi, d0, h0);
+        return yes;
+    };
+    double* h0 = pinned(out0) ? out0 : nullptr;
+    double* hc = pinned(out) ? out : nullptr;
+    bool cols_copied = false;
+    phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi, d0, h0,
+                  hc, &cols_copied);
     mark(*c, "computed");
     if (out0 && !h0) finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
-    finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
+    if (!cols_copied) finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
     finish(*c, space);
     if (info) {
         info->l = pi.l;

@@ -1284,8 +1284,11 @@ void phi_adaptive_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const do
 // result lands in y when l is even and in `partner` when l is odd (ping-pong, no copy).
 // With sq_len >= l, E_in[k] already holds the chain E, E^2, ..., E^(2^(l-1)) (phi_exponentials
 // sq_chain) and no matrix squaring is issued here.
+// host_out (pinned, two-stream path only): each column half is copied to the host as soon as its
+// last step is done; *copied reports whether that happened.
 static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int p, double* y, double* partner,
-                                 const double* const* E_in, int sq_len = 1, const int2* const* band_in = nullptr) {
+                                 const double* const* E_in, int sq_len = 1, const int2* const* band_in = nullptr,
+                                 double* host_out = nullptr, bool* copied = nullptr) {
     if (l <= 0) return y;
     const long long N = op.N;
     const bool chain = sq_len >= l;
@@ -1409,6 +1412,16 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
             throw;
         }
         c.stream = main_stream;
+        if (host_out) {  // lower half is final on the main stream now, the upper half on sq2
+            const double* res = b[l % 3];
+            cuda_check(cudaMemcpyAsync(host_out, res, sizeof(double) * h * N, cudaMemcpyDeviceToHost, main_stream),
+                       "phi lower D2H");
+            cuda_check(cudaMemcpyAsync(host_out + static_cast<size_t>(h) * N, res + static_cast<size_t>(h) * N,
+                                       sizeof(double) * (p - h) * N, cudaMemcpyDeviceToHost, c.sq2),
+                       "phi upper D2H");
+            cuda_check(cudaEventRecord(c.ev_sqB[l - 1], c.sq2), "sq rec B (copy)");
+            if (copied) *copied = true;
+        }
         cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqB[l - 1], 0), "sq join");
         check_launch(c);
         return b[l % 3];
@@ -1463,7 +1476,7 @@ void squaring_steps_dev(pq_ctx& c, const DevOp& op, double scale, int nb, int p,
 // phiaction.hpp:277-303, plus (when phi0_out) kron.hpp:123-128 phi_0 from the same expm batch.
 static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n,
                          int kind, double eps, double* out, int* points_used, double* phi0_out,
-                         double* phi0_host = nullptr) {
+                         double* phi0_host = nullptr, double* out_host = nullptr, bool* out_copied = nullptr) {
     if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
     if (p < 1) throw std::invalid_argument(kind == kGauss ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
     const NodesWeights& rule = kind == kGauss ? memo_rule(kGauss, n + 1) : memo_rule(kClenshaw, 25);
@@ -1516,8 +1529,8 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
     run_deferred(c);  // (no-op unless the node phase did not flush it)
     if (px.late) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_late, 0), "late exps wait");
     if (l > 0) {
-        double* res =
-            squaring_pingpong(c, op, l, nb, p, first, first == out ? partner : out, px.sq, px.sq_len, px.sq_band);
+        double* res = squaring_pingpong(c, op, l, nb, p, first, first == out ? partner : out, px.sq, px.sq_len,
+                                        px.sq_band, split_sq ? out_host : nullptr, out_copied);
         if (res != out)
             cuda_check(cudaMemcpyAsync(out, res, sizeof(double) * nb * p * op.N, cudaMemcpyDeviceToDevice, c.stream),
                        "plan copy");
@@ -1540,7 +1553,8 @@ void phi_with_plan_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const d
 
 // phiaction.hpp:307-346 (+ phi_0 when phi0_out).
 void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l, int l,
-                   double c1, double c2, double* out, PlanInfo* info, double* phi0_out, double* phi0_host) {
+                   double c1, double c2, double* out, PlanInfo* info, double* phi0_out, double* phi0_host,
+                   double* out_host, bool* out_copied) {
     if (p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
     double alpha = 0.0;
     for (int k = 0; k < op.d; ++k) alpha += op.inf_norm[k];
@@ -1591,7 +1605,7 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
     }
     mark(c, "planned");
     int points = 0;
-    phi_call_dev(c, op, 1.0, nb, bs, p, l, n, mode, eps, out, &points, phi0_out, phi0_host);
+    phi_call_dev(c, op, 1.0, nb, bs, p, l, n, mode, eps, out, &points, phi0_out, phi0_host, out_host, out_copied);
     if (info) {
         info->l = l;
         info->n = n;

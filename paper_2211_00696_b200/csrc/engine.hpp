@@ -215,10 +215,12 @@ struct PlanInfo {
 // run while the host waits for beta and plans; phi_exponentials of the same call reuses them.
 void taylor_prefetch(pq_ctx& c, const DevOp& op, double scale);
 // phi0_host (optional, pinned host memory): phi_0 is also copied there as soon as it is computed,
-// on the side stream while the squaring runs (joined before the call returns).
+// on the side stream while the squaring runs (joined before the call returns).  out_host
+// (optional, pinned): the phi columns are copied there per column half as each half finishes
+// (two-stream squaring only; *out_copied says whether it happened).
 void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l,
                    int l, double c1, double c2, double* out, PlanInfo* info, double* phi0_out = nullptr,
-                   double* phi0_host = nullptr);
+                   double* phi0_host = nullptr, double* out_host = nullptr, bool* out_copied = nullptr);
 void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p,
                            const NodesWeights& rule, const std::vector<int>& nodes, int zero, double* acc);
 void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const double* bs, const NodesWeights& rule,
