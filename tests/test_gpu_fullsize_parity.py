@@ -55,3 +55,27 @@ def test_config4_etdrk4_n32_vs_reference(pq, ref):
     want, calls = ref.integrate(w.A, 1, u0, 0.0, 10 * w.tau, 10, 3, eps=w.eps)
     assert res.phi_calls == calls
     assert rel2(res.u, want) <= 1e-11
+
+
+@pytest.mark.parametrize("shape,nb", [((72, 65, 64), 1), ((96, 81, 40), 1), ((72, 65, 64), 2)])
+def test_unaligned_shapes_vs_reference(pq, ref, shape, nb):
+    """N >= 2^18 (negligible-block skip, two-stream squaring, side-stream exponentials) with factor
+    sizes that are not multiples of 32 / 64 and an odd size (8-byte operand path, partial row
+    blocks, band ranges at 16-column granularity), advection-diffusion factors, CC adaptive."""
+    rng = np.random.default_rng(sum(shape))
+    fs = []
+    for k, n in enumerate(shape):
+        h = 1.0 / (n + 1)
+        lap = (2.0 * np.eye(n) - np.eye(n, k=1) - np.eye(n, k=-1)) / h**2
+        adv = (np.eye(n, k=1) - np.eye(n, k=-1)) / (2 * h)
+        fs.append(-2e-3 * ((1.0, 0.5, 0.2)[k] * lap + (8.0, -3.0, 1.0)[k] * adv))
+    bs = rng.standard_normal((nb, int(np.prod(shape))))
+    a = pq.KroneckerSum(fs)
+    info = pq.PhiInfo()
+    phi0, cols = pq.phi_0p(a, list(bs), pq.PhiRequest(p=4, eps=1e-10, mode=pq.QuadKind.clenshaw_curtis), info)
+    want, rinfo = ref.phiquadmv(fs, bs, 4, 1e-10, 1, threads=THREADS)
+    assert (info.l, info.n, info.points) == (rinfo["l"], rinfo["n"], rinfo["points"])
+    for m in range(nb):
+        errs = [rel2(cols[m, j], want[m][j]) for j in range(4)]
+        assert max(errs) <= 1e-11, (m, errs)
+        assert rel2(phi0[m], ref.exp_action(fs, bs[m])) <= 1e-11
