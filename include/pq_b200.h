@@ -176,6 +176,15 @@ PQ_API int pq_phi_nodes_partial(pq_ctx* ctx, int d, const int* shape, const doub
 /* l modified-squaring steps on y [nb][p][N] with E = expm(2^-l A_k) (phiaction.hpp:290-301). */
 PQ_API int pq_squaring_chain(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb, int p, int l,
                       double* y);
+/* Building blocks of the distributed squaring (paper_2211_00696_b200/sharded.py):
+ * one mode product y[b] = (I (x) .. E .. (x) I) x[b] along `mode` of a d-way tensor of the given
+ * shape, for nb columns of length prod(shape) (kron.hpp:65-87 accumulate_mode_apply, one mode),
+ * and one modified-squaring combination in place, T_i <- 2^-i (T_i + sum_{j<=i} Y_j/(i-j)!) for
+ * the p columns of each of nb right-hand sides laid out [nb][p][N] (phiaction.hpp:260-268; T holds
+ * E y_i on entry, Y the old y).  Device pointers only. */
+PQ_API int pq_mode_product(pq_ctx* ctx, int d, const int* shape, int mode, const double* E, int nb,
+                           const double* x, double* y);
+PQ_API int pq_squaring_combine(pq_ctx* ctx, long long n, int p, int nb, double* t, const double* y);
 
 /* exponential integrators (integrators.hpp) ----------------------------------------------- */
 /* Increment-form tableau (ExpRKTableau, integrators.hpp:32-38) flattened into terms: a term

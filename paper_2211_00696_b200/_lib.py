@@ -61,6 +61,8 @@ SIGNATURES = {
     "pq_ctx_phase_times": (C.c_int, [vp, dp]),
     "pq_ctx_gemm_stats": (C.c_int, [vp, C.c_int, C.POINTER(C.c_uint64), dp, dp]),
     "pq_ctx_gemm_dense_flops": (C.c_int, [vp, C.c_int, dp]),
+    "pq_mode_product": (C.c_int, [vp, C.c_int, ip, C.c_int, vp, C.c_int, vp, vp]),
+    "pq_squaring_combine": (C.c_int, [vp, C.c_longlong, C.c_int, C.c_int, vp, vp]),
     "pq_ctx_timeline": (C.c_int, [vp, C.POINTER(C.c_char_p)]),
     "pq_gauss_legendre": (C.c_int, [C.c_int, dp, dp]),
     "pq_clenshaw_curtis": (C.c_int, [C.c_int, dp, dp]),

@@ -623,6 +623,43 @@ int pq_phi_nodes_partial(pq_ctx* c, int d, const int* shape, const double* facto
     });
 }
 
+int pq_mode_product(pq_ctx* c, int d, const int* shape, int mode, const double* E, int nb, const double* x, double* y) {
+    return guarded([&] {
+        need_ctx(c);
+        const long long N = dim_of(d, shape);
+        need(mode >= 0 && mode < d, "mode_product: mode out of range");
+        need(nb >= 1, "mode_product: need at least one column");
+        need(E && x && y && x != y, "mode_product: null or aliased pointers");
+        int n[3] = {1, 1, 1};
+        for (int k = 0; k < d; ++k) n[k] = shape[k];
+        gemm(*c, mode_gemm_public(d, n, mode, E, x, y, nb, N));
+        check_launch(*c);
+    });
+}
+
+int pq_squaring_combine(pq_ctx* c, long long n, int p, int nb, double* t, const double* y) {
+    return guarded([&] {
+        need_ctx(c);
+        need(n >= 1 && p >= 1 && nb >= 1, "squaring_combine: bad extents");
+        need(t && y, "squaring_combine: null pointers");
+        std::vector<double> inv(static_cast<size_t>(p), 1.0);
+        double f = 1.0;
+        for (int k = 1; k < p; ++k) {
+            f *= k;
+            inv[static_cast<size_t>(k)] = 1.0 / f;
+        }
+        std::vector<double> coef(static_cast<size_t>(p) * p, 0.0);
+        for (int i = 0; i < p; ++i)
+            for (int j = 0; j <= i; ++j)
+                coef[static_cast<size_t>(i) * p + j] = std::ldexp(1.0, -(i + 1)) * inv[static_cast<size_t>(i - j)];
+        arena_begin(*c);
+        const double* cd = static_cast<const double*>(arena_push(*c, coef.data(), coef.size() * sizeof(double)));
+        arena_flush(*c);
+        launch_sq_combine(n, p, nb, t, y, cd, c->stream);
+        count_launch(*c);
+    });
+}
+
 int pq_squaring_chain(pq_ctx* c, int d, const int* shape, const double* factors, int nb, int p, int l, double* y) {
     return guarded([&] {
         need_ctx(c);

@@ -858,6 +858,11 @@ static GemmArgs mode_gemm(int d, const int* n, int k, const double* E, long long
     return g;
 }
 
+GemmArgs mode_gemm_public(int d, const int* n, int mode, const double* E, const double* x, double* y, int nb,
+                          long long N) {
+    return mode_gemm(d, n, mode, E, 0, x, N, y, N, nb, N);
+}
+
 void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride, const double* x,
                 long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep, const char* tmp_tag,
                 const int2* const* band) {

@@ -195,6 +195,9 @@ void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const lo
                 const double* x, long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep,
                 const char* tmp_tag = "chain", const int2* const* band = nullptr);
 void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, double* y);
+// one mode product of nb columns (no band table): the GEMM the mode chain issues for `mode`
+GemmArgs mode_gemm_public(int d, const int* n, int mode, const double* E, const double* x, double* y, int nb,
+                          long long N);
 void exp_action_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* b, double* y);
 double max_inf_norm_dev(pq_ctx& c, const double* v, long long N, int ncols);  // syncs
 
