@@ -79,3 +79,19 @@ def test_unaligned_shapes_vs_reference(pq, ref, shape, nb):
         errs = [rel2(cols[m, j], want[m][j]) for j in range(4)]
         assert max(errs) <= 1e-11, (m, errs)
         assert rel2(phi0[m], ref.exp_action(fs, bs[m])) <= 1e-11
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+def test_many_columns_large_n_vs_reference(pq, ref, mode):
+    """p = 12 > 8 at N = 262144: the generic (non-templated) combination kernels together with the
+    two-stream squaring, the band tiles and both rules."""
+    from paper_2211_00696_b200.workloads import config
+    w = config(2, n=64)
+    b = w.rhs(0)
+    info = pq.PhiInfo()
+    phi0, cols = pq.phi_0p(pq.KroneckerSum(w.factors), [b], pq.PhiRequest(p=12, eps=1e-10, mode=pq.QuadKind(mode)),
+                           info)
+    want, rinfo = ref.phiquadmv(w.factors, b[None, :], 12, 1e-10, mode, threads=THREADS)
+    assert (info.l, info.n, info.points) == (rinfo["l"], rinfo["n"], rinfo["points"])
+    errs = [rel2(cols[0, j], want[0][j]) for j in range(12)]
+    assert max(errs) <= 1e-11, errs
