@@ -12,6 +12,7 @@ report all seven criteria (planner table, CC point counts 49/97, full pipeline v
 oracle at p = 20 both rules, a-priori bound never undercut, algebraic identities on 100 random
 systems, ETD convergence orders, speed vs the dense reference) as PASS."""
 import os
+import re
 import subprocess
 from pathlib import Path
 
@@ -54,3 +55,27 @@ def test_reference_acceptance_gate_on_b200():
     verdicts = [ln for ln in r.stdout.splitlines() if ln.startswith("criterion ") and ": " in ln and "note" not in ln]
     assert len(verdicts) == 7 and all(": PASS" in ln for ln in verdicts), r.stdout
     assert "acceptance: all 7 criteria passed" in r.stdout
+
+
+def _numbers(line):
+    return [float(x) for x in re.findall(r"[-+]?\d+\.?\d*(?:[eE][-+]?\d+)?", line)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("demo", ["demo_heat3d", "demo_phi_action"])
+def test_reference_demos_on_b200(demo):
+    """The reference's demos (proj/demos), built against the drop-in headers: every line matches the
+    reference build's output (tests/golden/<demo>_ref_output.txt, `make -C tests/cpp demos_golden`)
+    exactly, except the reported error figures, which must stay <= max(1e-11, 2x the reference's)."""
+    r = _run(demo, timeout=300)
+    assert r.returncode == 0, r.stdout + r.stderr
+    got = r.stdout.splitlines()
+    want = (ROOT / "tests" / "golden" / f"{demo}_ref_output.txt").read_text().splitlines()
+    assert len(got) == len(want)
+    for g, w in zip(got, want):
+        if re.search(r"=\s*[-+]?[\d.]+e[-+]\d+\s*$", w):  # an error figure (scientific notation)
+            gv, wv = _numbers(g)[-1], _numbers(w)[-1]
+            assert g.rsplit("=", 1)[0] == w.rsplit("=", 1)[0]
+            assert gv <= max(1e-11, 2 * wv), (g, w)
+        else:
+            assert g == w
