@@ -905,6 +905,28 @@ void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const lo
     check_launch(c);
 }
 
+// Negligible-block tables of the unscaled factors (scaling does not move them); the factors of
+// the benchmark operators are tridiagonal, so a 32-row block needs ~5 of 16 k-slices.  Exact:
+// the dropped blocks hold only entries below 2^-64 of the block's max (for these factors, zeros,
+// which the reference skips too, kron.hpp:81).  Cached per operator upload.
+static void factor_bands(pq_ctx& c, const DevOp& op, const int2** out) {
+    for (int k = 0; k < op.d; ++k) out[k] = nullptr;
+    bool any = false;
+    for (int k = 0; k < op.d; ++k) any = any || band_enabled(op.n[k], op.N);
+    if (!any) return;
+    if (c.fac_band_serial != op.serial || op.serial == 0) {
+        for (int k = 0; k < op.d; ++k) {
+            c.fac_band[k] = nullptr;
+            if (!band_enabled(op.n[k], op.N)) continue;
+            int2* b = static_cast<int2*>(ws_bytes(c, "facband" + std::to_string(k), sizeof(int2) * band_row_blocks(op.n[k])));
+            band_ranges(c, op.n[k], 1, op.F[k], b);
+            c.fac_band[k] = b;
+        }
+        c.fac_band_serial = op.serial;
+    }
+    for (int k = 0; k < op.d; ++k) out[k] = c.fac_band[k];
+}
+
 // kron.hpp:111-119: y = sum_k mode_k(A_k) x (factor scaled by `scale` first when != 1).
 void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, double* y) {
     const double* F[3] = {op.F[0], op.F[1], op.F[2]};
@@ -920,9 +942,17 @@ void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, 
             off += static_cast<size_t>(op.n[k]) * op.n[k];
         }
     }
+    const int2* fb[3];
+    factor_bands(c, op, fb);
     for (int k = 0; k < op.d; ++k) {
         GemmArgs g = mode_gemm(op.d, op.n, k, F[k], 0, x, 0, y, 0, 1, op.N);
         g.accumulate = k > 0;
+        if (fb[k]) {
+            g.band = fb[k];
+            g.band_rows = op.n[k];
+            g.band_stride = 0;
+            g.band_mode = g.b_kmajor ? 3 : 2;
+        }
         gemm(c, g);
     }
     check_launch(c);
@@ -1662,8 +1692,12 @@ void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const doub
             count_launch(c);
         }
         const double* Ec[3];
-        for (int k = 0; k < op.d; ++k) Ec[k] = px.node[k] + a0 * Es[k];
-        mode_chain(c, op.d, op.n, Ec, Es, M, N, V, N, cnt, Epilogue{});
+        const int2* Bc[3];
+        for (int k = 0; k < op.d; ++k) {
+            Ec[k] = px.node[k] + a0 * Es[k];
+            Bc[k] = px.node_band[k] ? px.node_band[k] + a0 * band_row_blocks(op.n[k]) : nullptr;
+        }
+        mode_chain(c, op.d, op.n, Ec, Es, M, N, V, N, cnt, Epilogue{}, "chain", Bc);
         launch_combine(N, 1, cnt, V, N, vsl, w_dev + a0, out, N, a0 == 0 ? 1 : 0, c.stream);
         count_launch(c);
     }

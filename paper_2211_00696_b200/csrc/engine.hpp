@@ -79,6 +79,9 @@ struct pq_ctx {
     };
     std::map<int, PowCache> pow_cache;
     uint64_t op_serial = 0;  // incremented per operator upload (one per API call)
+    // negligible-block tables of the operator's own factors (kron_matvec), per upload serial
+    uint64_t fac_band_serial = 0;
+    const int2* fac_band[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev_beta = nullptr;  // beta readback (phiquadmv) completes
     cudaEvent_t ev_cc = nullptr;    // adaptive CC error readback completes
     // factor uploads: pinned staging (no implicit stream sync) + per-slot cache of the last

@@ -95,3 +95,28 @@ def test_many_columns_large_n_vs_reference(pq, ref, mode):
     assert (info.l, info.n, info.points) == (rinfo["l"], rinfo["n"], rinfo["points"])
     errs = [rel2(cols[0, j], want[0][j]) for j in range(12)]
     assert max(errs) <= 1e-11, errs
+
+
+def test_kron_matvec_large_vs_reference(pq, ref):
+    """kron_matvec at N = 2^18 takes the factor band tables (tridiagonal factors: ~1/3 of the
+    k-slices); dropping all-zero blocks is exact, so the result must match the reference's
+    zero-skipping loop (kron.hpp:81) to rounding."""
+    from paper_2211_00696_b200.workloads import config
+    w = config(2, n=64)
+    x = w.rhs(0)
+    got = pq.kron_matvec(pq.KroneckerSum(w.factors), x)
+    want = ref.kron_matvec(w.factors, x)
+    assert rel2(got, want) <= 1e-13
+
+
+def test_config4_etdrk4_n64_vs_reference(pq, ref):
+    """ETDRK4 at N = 2^18: the band-skipped phi_lincomb stage groups (l = 0, Gauss) and the
+    band-skipped A u products against the reference's erk_step loop."""
+    from paper_2211_00696_b200.workloads import allen_cahn_u0, config
+    w = config(4, n=64)
+    u0 = allen_cahn_u0(w.N)
+    res = pq.integrate(pq.KroneckerSum(w.A), ("cubic", 1.0, -1.0), u0, 0.0, 4 * w.tau, 4, pq.etdrk4_tableau(),
+                       pq.PhiRequest(eps=w.eps))
+    want, calls = ref.integrate(w.A, 1, u0, 0.0, 4 * w.tau, 4, 3, eps=w.eps)
+    assert res.phi_calls == calls
+    assert rel2(res.u, want) <= 1e-11
