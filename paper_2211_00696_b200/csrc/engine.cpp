@@ -1683,13 +1683,38 @@ void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const doub
     const int qc = node_chunk(c, N, q, 4);
     double* M = ws(c, "lincMix", static_cast<size_t>(qc) * N);
     double* V = ws(c, "lincV", static_cast<size_t>(qc) * N);
+    // mixing coefficients transposed per group of <= 8 nodes: input j, output node a -> [j][a - g0]
+    constexpr int kMixOut = 8;
+    std::vector<double> mixT;
+    std::vector<size_t> mix_off;
+    for (int g0 = 0; g0 < q; g0 += kMixOut) {
+        const int gc = std::min(kMixOut, q - g0);
+        mix_off.push_back(mixT.size());
+        for (int j = 0; j < p; ++j)
+            for (int a = 0; a < gc; ++a) mixT.push_back(mix[static_cast<size_t>(g0 + a) * p + j]);
+    }
+    const double* mixT_dev = static_cast<const double*>(arena_push(c, mixT.data(), mixT.size() * sizeof(double)));
+    arena_flush(c);
     for (int a0 = 0; a0 < q; a0 += qc) {
         const int cnt = std::min(qc, q - a0);
-        for (int a = 0; a < cnt; ++a) {
-            // mix_i = sum_j c_ij b_j, one output column (p = 1) over the p inputs as "nodes"
-            launch_combine(N, 1, p, bs, N, bsl, mix_dev + static_cast<size_t>(a0 + a) * p, M + static_cast<long long>(a) * N,
-                           N, 1, c.stream);
-            count_launch(c);
+        // mix_a = sum_j c_aj b_j (ascending j) for up to 8 nodes per streaming pass: the p inputs
+        // are read once per group instead of once per node
+        for (int a = 0; a < cnt;) {
+            const int node = a0 + a, g = node / kMixOut, in_g = node % kMixOut;
+            const int gc = std::min(kMixOut, q - g * kMixOut);
+            const int take = std::min(gc - in_g, cnt - a);
+            if (in_g == 0 && take == gc) {
+                launch_combine(N, gc, p, bs, N, bsl, mixT_dev + mix_off[static_cast<size_t>(g)], M + static_cast<long long>(a) * N,
+                               N, 1, c.stream);
+                count_launch(c);
+            } else {
+                for (int t = 0; t < take; ++t) {  // a chunk boundary inside a group: one node at a time
+                    launch_combine(N, 1, p, bs, N, bsl, mix_dev + static_cast<size_t>(node + t) * p,
+                                   M + static_cast<long long>(a + t) * N, N, 1, c.stream);
+                    count_launch(c);
+                }
+            }
+            a += take;
         }
         const double* Ec[3];
         const int2* Bc[3];
