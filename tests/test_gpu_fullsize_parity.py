@@ -120,3 +120,17 @@ def test_config4_etdrk4_n64_vs_reference(pq, ref):
     want, calls = ref.integrate(w.A, 1, u0, 0.0, 4 * w.tau, 4, 3, eps=w.eps)
     assert res.phi_calls == calls
     assert rel2(res.u, want) <= 1e-11
+
+
+def test_config3_fullsize_one_rhs_vs_reference(pq, ref):
+    """Config 3 at FULL size (n = 256, N = 16.8 M, one RHS; '1 RHS full size'),
+    pinned (l, n) = (1, 9) Gauss so the reference finishes in ~2 minutes on the box's cores: the
+    full node phase (10 nodes) plus one modified-squaring step, every phi column to 1e-11."""
+    from paper_2211_00696_b200.workloads import config
+    w = config(3)
+    b = w.rhs(0)
+    got = pq.phi_with_plan(pq.KroneckerSum(w.factors), [b], 3, 1, 9, pq.QuadKind.gauss_legendre, w.eps)
+    want, pts = ref.phi_with_plan(w.factors, b[None, :], 3, 1, 9, 0, w.eps, threads=THREADS)
+    assert pts == 0 or pts == 10
+    errs = [rel2(np.asarray(got[0].col(j + 1)), want[0][j]) for j in range(3)]
+    assert max(errs) <= 1e-11, errs
