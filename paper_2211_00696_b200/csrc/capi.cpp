@@ -177,6 +177,14 @@ int pq_ctx_set_stream(pq_ctx* c, void* stream) {
             cuda_check(cudaEventCreateWithFlags(&c->arena.done, cudaEventDisableTiming), "event");
             cuda_check(cudaEventRecord(c->arena.done, c->stream), "record");
         }
+        // helper streams follow the new stream's priority: recreated on next use
+        for (cudaStream_t* h : {&c->side, &c->sq2}) {
+            if (*h) {
+                cuda_check(cudaStreamSynchronize(*h), "sync helper stream");
+                cudaStreamDestroy(*h);
+                *h = nullptr;
+            }
+        }
     });
 }
 

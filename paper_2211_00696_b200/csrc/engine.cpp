@@ -320,11 +320,22 @@ static bool squaring_split_ok(const pq_ctx& c, int nb, int p, long long N) {
     return !disabled && nb == 1 && p >= 2 && N >= (1LL << 18) && !c.profiling;
 }
 
+// helper streams inherit the priority of the context's stream, so a caller that runs its
+// context on a high-priority stream (bench.py's overlapped end-to-end leg) keeps it end to end
+void make_helper_stream(pq_ctx& c, cudaStream_t* s, const char* what) {
+    int prio = 0;
+    if (cudaStreamGetPriority(c.stream, &prio) != cudaSuccess) {
+        cudaGetLastError();
+        prio = 0;
+    }
+    cuda_check(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, prio), what);
+}
+
 // second squaring stream and per-step events for l steps
 static void ensure_sq2(pq_ctx& c, int l) {
     if (!c.sq2) {
-        cuda_check(cudaStreamCreateWithFlags(&c.sq2, cudaStreamNonBlocking), "sq2 stream");
-        cuda_check(cudaEventCreateWithFlags(&c.ev_sqfork, cudaEventDisableTiming), "sq fork event");
+        make_helper_stream(c, &c.sq2, "sq2 stream");
+        if (!c.ev_sqfork) cuda_check(cudaEventCreateWithFlags(&c.ev_sqfork, cudaEventDisableTiming), "sq fork event");
     }
     while (static_cast<int>(c.ev_sqA.size()) < l) {
         cudaEvent_t a, b;
@@ -337,9 +348,9 @@ static void ensure_sq2(pq_ctx& c, int l) {
 
 void ensure_side(pq_ctx& c) {
     if (c.side) return;
-    cuda_check(cudaStreamCreateWithFlags(&c.side, cudaStreamNonBlocking), "side stream");
-    cuda_check(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming), "fork event");
-    cuda_check(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming), "join event");
+    make_helper_stream(c, &c.side, "side stream");
+    if (!c.ev_fork) cuda_check(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming), "fork event");
+    if (!c.ev_join) cuda_check(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming), "join event");
 }
 
 struct ExpmEntry {

@@ -38,3 +38,59 @@ def test_pinned_host_outputs_equal_device_outputs(pq, n):
     assert np.array_equal(o0_pin.numpy(), o0_dev.cpu().numpy())
     assert np.array_equal(o_pin.numpy(), o_dev.cpu().numpy())
     ctx.close()
+
+
+def test_two_host_callers_concurrently_match_sequential(pq):
+    """bench.py's end-to-end leg runs two host threads, each with its own context, stream and
+    pinned buffers, calling pq_phi_0p at once (the reference API is re-entrant).  Every result
+    must equal the same call made alone, bitwise, across several overlapped rounds."""
+    import threading
+    import torch
+    from paper_2211_00696_b200.workloads import config
+    w = config(2, n=64)
+    a = pq.KroneckerSum(w.factors)
+    req = pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode))
+    d, sh, fac = a._abi()
+    rc = req._c()
+    rhs = [w.rhs(10 + k) for k in range(2)]
+
+    def make():
+        ctx = pq.Context(0)
+        st = torch.cuda.Stream()
+        ctx.set_stream(st.cuda_stream)
+        return ctx, st
+
+    def call(ctx, b, o0, o):
+        info = pq._lib.PhiInfoC()
+        pq._lib.check(pq._lib.lib.pq_phi_0p(ctx.handle, d, sh, fac, 1, C.c_void_p(b.data_ptr()), C.byref(rc),
+                                            C.c_void_p(o0.data_ptr()), C.c_void_p(o.data_ptr()), C.byref(info),
+                                            pq._lib.PQ_HOST))
+
+    callers = [make() for _ in range(2)]
+    bufs = [(torch.from_numpy(rhs[k].copy()).pin_memory(), torch.empty((1, w.N), dtype=torch.float64).pin_memory(),
+             torch.empty((1, w.p, w.N), dtype=torch.float64).pin_memory()) for k in range(2)]
+    want = []
+    for k in range(2):
+        call(callers[k][0], *bufs[k])
+        want.append((bufs[k][1].numpy().copy(), bufs[k][2].numpy().copy()))
+    errors = []
+
+    def worker(k):
+        try:
+            for _ in range(3):
+                bufs[k][1].fill_(float("nan"))
+                bufs[k][2].fill_(float("nan"))
+                call(callers[k][0], *bufs[k])
+                if not (np.array_equal(bufs[k][1].numpy(), want[k][0]) and np.array_equal(bufs[k][2].numpy(), want[k][1])):
+                    errors.append(f"caller {k}: result differs from the sequential call")
+        except Exception as e:  # pragma: no cover
+            errors.append(repr(e))
+
+    ths = [threading.Thread(target=worker, args=(k,)) for k in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors
+    for ctx, _ in callers:
+        ctx.close()
