@@ -121,20 +121,27 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
     }
     b_kstep = BKM ? 1 : g.ldb;
 
-    auto load_stage = [&](int stage, int kt) {
-        const int k0 = kt * BK;
+    // consecutive k slices are loaded in order: the source pointers advance by one slice per call
+    // (no per-slice 64-bit multiply in the issue path)
+    const long long b_step = static_cast<long long>(BK) * b_kstep;
+    int k_next = 0;
+    auto load_next = [&](int stage) {
+        const int k0 = k_next;
 #pragma unroll
         for (int it = 0; it < A_IT; ++it) {
             if (A_CH % NT != 0 && tid + it * NT >= A_CH) continue;
             const bool ok = a_ok[it] && k0 + a_k[it] < g.K;
-            cp_async<VEC>(a_dst[it] + 8u * stage * T::ASZ, ok ? a_src[it] + k0 : A, ok);
+            cp_async<VEC>(a_dst[it] + 8u * stage * T::ASZ, ok ? a_src[it] : A, ok);
+            a_src[it] += BK;
         }
 #pragma unroll
         for (int it = 0; it < B_IT; ++it) {
             if (B_CH % NT != 0 && tid + it * NT >= B_CH) continue;
             const bool ok = b_ok[it] && k0 + b_k[it] < g.K;
-            cp_async<VEC>(b_dst[it] + 8u * stage * T::BSZ, ok ? b_src[it] + (long long)k0 * b_kstep : B, ok);
+            cp_async<VEC>(b_dst[it] + 8u * stage * T::BSZ, ok ? b_src[it] : B, ok);
+            b_src[it] += b_step;
         }
+        k_next += BK;
     };
 
     double acc[T::MI][T::NI][2];
@@ -195,9 +202,14 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
         const long long kexec = hi > lo ? min(hi * BK, g.K) - lo * BK : 0;
         atomicAdd(g.flop_counter, static_cast<unsigned long long>(2 * rows * cols * kexec));
     }
+    k_next = kt_lo * BK;
+#pragma unroll
+    for (int it = 0; it < A_IT; ++it) a_src[it] += k_next;
+#pragma unroll
+    for (int it = 0; it < B_IT; ++it) b_src[it] += static_cast<long long>(k_next) * b_kstep;
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
-        if (s < NKT) load_stage(s, kt_lo + s);
+        if (s < NKT) load_next(s);
         cp_commit();
     }
     const double* tA0 = sA + (wm * WM + gid) * T::SA + tig;
@@ -208,7 +220,7 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
         __syncthreads();
         {
             const int nk = kt + ST - 1;
-            if (nk < NKT) load_stage(nk % ST, kt_lo + nk);
+            if (nk < NKT) load_next(nk % ST);
             cp_commit();
         }
         const int st = kt % ST;
