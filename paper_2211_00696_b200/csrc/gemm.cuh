@@ -541,10 +541,12 @@ int launch_gemm_family(const GemmArgs& g, bool vec2, int shape, cudaStream_t s) 
         case 1: return vec2 ? launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 1>(g, s);
         case 2: return vec2 ? launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 2>(g, s) : launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 1>(g, s);
         case 6:  // negligible-block skip, exponential = A: 32-row tiles stream only their block's slices
-            // (32x128 with four 32x32 warps: +3% over 32x64 on the node-sweep band shapes, +4.5% dense)
-            return launch_cfg<32, 128, 8, 32, 32, 4, BKM, 2, 4>(g, s);
-        case 7:  // negligible-block skip, exponential = B (k-major): 32-column tiles
-            return launch_cfg<64, 32, 8, 32, 16, 4, BKM, 2, 6>(g, s);
+            // (32x128 with four 32x32 warps: +3% over 32x64 on the node-sweep band shapes, +4.5% dense;
+            // 16-wide k slices in 2 stages: +2.5-4% over 8-wide in 4 once the load issue path lost its
+            // per-slice 64-bit multiplies, tools/gemm_tune.cu, profiles/r01_gemm_tune_bk16.txt)
+            return launch_cfg<32, 128, 16, 32, 32, 2, BKM, 2, 4>(g, s);
+        case 7:  // negligible-block skip, exponential = B (k-major): 32-column tiles (BK 16: +3-6%)
+            return launch_cfg<64, 32, 16, 32, 16, 2, BKM, 2, 6>(g, s);
         case 3:
             // 16-byte path: BK = 8, 4 stages and <= 128 registers give 4 CTAs (16 warps) per SM,
             // which keeps the DMMA pipe fed while other warps sit in barriers / epilogues

@@ -141,7 +141,12 @@ int main(int argc, char** argv) {
                    ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
     }
         T(32, 128, 8, 32, 32, 4, 4)
+        T(32, 128, 8, 32, 32, 3, 4)
+        T(32, 128, 16, 32, 32, 2, 4)
+        T(64, 64, 8, 32, 32, 4, 4)
         T(64, 32, 8, 32, 16, 4, 6)
+        T(64, 32, 16, 32, 16, 2, 6)
+        T(64, 32, 8, 32, 16, 3, 6)
     }
     return 0;
 }
