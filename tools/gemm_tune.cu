@@ -1,12 +1,13 @@
 // Tile-configuration sweep for the FP64 DMMA mode-product GEMM (gemm.cuh) on the exact shapes of
 // the phi pipeline at n = 128 (config 2) and n = 256 / 512 (configs 3 / 5).
-// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2211_00696_b200/csrc \
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I paper_2211_00696_b200/csrc -I tools \
 //          -o tools/gemm_tune tools/gemm_tune.cu
 #include <cstdio>
 #include <algorithm>
 #include <vector>
 
 #include "gemm.cuh"
+#include "gemm_ws_experiment.cuh"
 
 using namespace pqb;
 
@@ -31,6 +32,30 @@ float run(const Case& c, int reps, cudaEvent_t e0, cudaEvent_t e1) {
     auto f = [&] {
         if (g.b_kmajor) launch_cfg<BM, BN, BK, WM, WN, ST, true, 2, MINB>(g, 0);
         else launch_cfg<BM, BN, BK, WM, WN, ST, false, 2, MINB>(g, 0);
+    };
+    f();
+    cudaDeviceSynchronize();
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) f();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+        printf("  launch error %s\n", cudaGetErrorString(err));
+        return -1;
+    }
+    return ms / reps;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB>
+float run_ws(const Case& c, int reps, cudaEvent_t e0, cudaEvent_t e1) {
+    GemmArgs g = c.g;
+    if (!ws_ok<BM, BN, BK>(g)) return -1;
+    auto f = [&] {
+        if (g.b_kmajor) launch_ws<BM, BN, BK, WM, WN, ST, true, MINB>(g, 0);
+        else launch_ws<BM, BN, BK, WM, WN, ST, false, MINB>(g, 0);
     };
     f();
     cudaDeviceSynchronize();
@@ -140,13 +165,23 @@ int main(int argc, char** argv) {
             printf("  %3dx%3dx%2d w%2dx%2d st%d minb%d : %8.1f us  %6.2f TF/s\n", BM, BN, BK, WM, WN, ST, MINB, \
                    ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
     }
-        T(32, 128, 8, 32, 32, 4, 4)
-        T(32, 128, 8, 32, 32, 3, 4)
+#define TW(BM, BN, BK, WM, WN, ST, MINB)                                                               \
+    {                                                                                                  \
+        float ms = run_ws<BM, BN, BK, WM, WN, ST, MINB>(c, 5, e0, e1);                                 \
+        if (ms > 0)                                                                                    \
+            printf("  WS %3dx%3dx%2d w%2dx%2d st%d minb%d : %8.1f us  %6.2f TF/s\n", BM, BN, BK, WM, WN, ST, MINB, \
+                   ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
+    }
         T(32, 128, 16, 32, 32, 2, 4)
-        T(64, 64, 8, 32, 32, 4, 4)
-        T(64, 32, 8, 32, 16, 4, 6)
+        TW(32, 128, 16, 32, 32, 2, 3)
+        TW(32, 128, 16, 32, 32, 3, 3)
+        TW(32, 128, 16, 32, 32, 2, 4)
+        TW(32, 128, 8, 32, 32, 4, 3)
         T(64, 32, 16, 32, 16, 2, 6)
-        T(64, 32, 8, 32, 16, 3, 6)
+        TW(64, 32, 16, 32, 16, 2, 4)
+        TW(64, 32, 16, 32, 16, 3, 4)
+        TW(64, 32, 16, 32, 16, 4, 4)
+        TW(64, 32, 8, 32, 16, 4, 5)
     }
     return 0;
 }
