@@ -73,6 +73,16 @@ float run_ws(const Case& c, int reps, cudaEvent_t e0, cudaEvent_t e1) {
     return ms / reps;
 }
 
+__global__ void fill_rand(double* p, long long n, unsigned seed) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+        unsigned long long x = (i + 1) * 6364136223846793005ull + seed * 1442695040888963407ull;
+        x ^= x >> 33;
+        x *= 0xff51afd7ed558ccdull;
+        x ^= x >> 33;
+        p[i] = (double)(x >> 11) * (1.0 / 9007199254740992.0) - 0.5;
+    }
+}
+
 int main(int argc, char** argv) {
     const int n = argc > 1 ? atoi(argv[1]) : 128;
     const int Z = argc > 2 ? atoi(argv[2]) : 12;  // nodes (or columns)
@@ -84,6 +94,12 @@ int main(int argc, char** argv) {
     CK(cudaMalloc(&E, sizeof(double) * n * n * Z));
     cudaMemset(X, 0, sizeof(double) * N * Z);
     cudaMemset(E, 0, sizeof(double) * n * n * Z);
+    if (argc > 5 && atoi(argv[5]) == 1) {  // random operands instead of zeros (data-dependent power)
+        fill_rand<<<1024, 256>>>(X, N * Z, 1);
+        fill_rand<<<1024, 256>>>(E, (long long)n * n * Z, 2);
+        cudaDeviceSynchronize();
+        printf("random operands\n");
+    }
     cudaMemset(EXT, 0, sizeof(double) * N * Z);
     double *coef, *alpha;
     int* nterms;
