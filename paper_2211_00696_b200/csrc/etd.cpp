@@ -343,9 +343,63 @@ static int run_etd(pq_ctx* c, int d, const int* shape, const double* factors, co
                                    space == PQ_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->stream),
                    "u0");
         DevPhiEngine eng{*c, op, tau, *base, {}, 0};
-        for (int s = 0; s < m; ++s) {
+        // After one eager step (workspaces, plans, exponential caches, kernel attributes all set),
+        // two steps u_a -> u_b -> u_a are captured into one CUDA graph and replayed for the rest of
+        // the run: the step is device-only for device-side sources (the sources here do not depend
+        // on t), so the replay removes the host enqueue of ~60 launches per step.  Any capture
+        // failure falls back to eager steps.  PQ_ETD_GRAPH=0 disables.
+        static const bool graphs_on = [] {
+            const char* e = std::getenv("PQ_ETD_GRAPH");
+            return !(e && e[0] == '0');
+        }();
+        bool try_graph = graphs_on && src.s.kind != PQ_SOURCE_CALLBACK && !c->profiling && !c->trace;
+        cudaGraphExec_t pair = nullptr;
+        int pair_calls = 0;
+        for (int s = 0; s < m;) {
+            if (s >= 1 && try_graph && !pair && m - s >= 2) {
+                try_graph = false;
+                arena_begin(*c);  // a fresh parameter arena: no wrap-around (and its syncs) while capturing
+                const int calls0 = eng.calls;
+                cudaGraph_t graph = nullptr;
+                bool ok = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+                if (ok) {
+                    try {
+                        erk_step_dev(eng, src, t0 + s * tau, ua, tb, ub);
+                        erk_step_dev(eng, src, t0 + (s + 1) * tau, ub, tb, ua);
+                    } catch (...) {
+                        ok = false;
+                    }
+                    const cudaError_t e = cudaStreamEndCapture(c->stream, &graph);
+                    ok = ok && e == cudaSuccess && graph && cudaGraphInstantiate(&pair, graph, 0) == cudaSuccess;
+                    if (graph) cudaGraphDestroy(graph);
+                }
+                if (!ok) {
+                    cudaGetLastError();
+                    if (pair) cudaGraphExecDestroy(pair);
+                    pair = nullptr;
+                    eng.calls = calls0;  // nothing captured ran: redo these steps eagerly
+                    continue;
+                }
+                pair_calls = eng.calls - calls0;
+                cuda_check(cudaGraphLaunch(pair, c->stream), "graph launch");
+                s += 2;
+                continue;
+            }
+            if (pair && m - s >= 2) {
+                cuda_check(cudaGraphLaunch(pair, c->stream), "graph launch");
+                eng.calls += pair_calls;
+                s += 2;
+                continue;
+            }
             erk_step_dev(eng, src, t0 + s * tau, ua, tb, ub);
             std::swap(ua, ub);
+            ++s;
+        }
+        if (pair) {
+            cuda_check(cudaStreamSynchronize(c->stream), "graph drain");
+            cudaGraphExecDestroy(pair);
+            // events recorded while capturing are not real records: re-arm the arena's
+            if (c->arena.done) cuda_check(cudaEventRecord(c->arena.done, c->stream), "arena record");
         }
         cuda_check(cudaMemcpyAsync(u_out, ua, N * sizeof(double),
                                    space == PQ_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream),
