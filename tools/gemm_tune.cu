@@ -189,6 +189,9 @@ int main(int argc, char** argv) {
                    ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
     }
         T(32, 128, 16, 32, 32, 2, 4)
+        T(32, 256, 16, 32, 32, 2, 2)
+        T(32, 256, 16, 32, 64, 2, 2)
+        T(32, 128, 16, 32, 64, 2, 4)
         TW(32, 128, 16, 32, 32, 2, 3)
         TW(32, 128, 16, 32, 32, 3, 3)
         TW(32, 128, 16, 32, 32, 2, 4)
