@@ -189,6 +189,7 @@ int main(int argc, char** argv) {
                    ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
     }
         T(32, 128, 16, 32, 32, 2, 4)
+        T(32, 128, 16, 32, 32, 2, 5)
         T(32, 128, 16, 32, 32, 3, 3)
         T(32, 128, 16, 32, 32, 3, 4)
         T(32, 256, 16, 32, 32, 2, 2)
@@ -199,6 +200,8 @@ int main(int argc, char** argv) {
         TW(32, 128, 16, 32, 32, 2, 4)
         TW(32, 128, 8, 32, 32, 4, 3)
         T(64, 32, 16, 32, 16, 2, 6)
+        T(64, 32, 16, 32, 16, 2, 7)
+        T(64, 32, 16, 32, 16, 2, 8)
         T(64, 32, 16, 32, 16, 3, 5)
         T(64, 32, 16, 32, 16, 3, 6)
         TW(64, 32, 16, 32, 16, 2, 4)
