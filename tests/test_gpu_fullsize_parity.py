@@ -134,3 +134,22 @@ def test_config3_fullsize_one_rhs_vs_reference(pq, ref):
     assert pts == 0 or pts == 10
     errs = [rel2(np.asarray(got[0].col(j + 1)), want[0][j]) for j in range(3)]
     assert max(errs) <= 1e-11, errs
+
+
+@pytest.mark.parametrize("mode,p,nb", [(1, 1, 1), (1, 8, 1), (1, 3, 2), (0, 6, 1), (0, 9, 1), (0, 2, 3)])
+def test_rule_p_nb_combinations_large_n_vs_reference(pq, ref, mode, p, nb):
+    """N = 2^18 (band tiles, side-stream exponentials; the two-stream squaring only for nb = 1,
+    p >= 2) across the combination-kernel boundaries: p = 1, p = 8 (largest templated), p = 9
+    (generic), several RHS sharing one plan (beta = max over RHS), both rules."""
+    from paper_2211_00696_b200.workloads import config
+    w = config(2, n=64)
+    bs = np.stack([w.rhs(20 + k) for k in range(nb)])
+    info = pq.PhiInfo()
+    phi0, cols = pq.phi_0p(pq.KroneckerSum(w.factors), list(bs), pq.PhiRequest(p=p, eps=1e-10, mode=pq.QuadKind(mode)),
+                           info)
+    want, rinfo = ref.phiquadmv(w.factors, bs, p, 1e-10, mode, threads=THREADS)
+    assert (info.l, info.n, info.points) == (rinfo["l"], rinfo["n"], rinfo["points"])
+    for m in range(nb):
+        errs = [rel2(cols[m, j], want[m][j]) for j in range(p)]
+        assert max(errs) <= 1e-11, (m, errs)
+        assert rel2(phi0[m], ref.exp_action(w.factors, bs[m])) <= 1e-11
