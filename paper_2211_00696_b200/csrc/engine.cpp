@@ -291,7 +291,8 @@ static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>&
                             double* cur, double* other, double* out);
 
 // Negligible-block tables for the exponentials of a phi call (kernels.hpp launch_band_ranges);
-// only the 64x64x8 mode-product tiles read them, so they are built for n >= 64.  PQ_BAND=0
+// only the band mode-product tiles (vec2 paths of the 64x64 family) read them, so they are built
+// for n >= 64.  PQ_BAND=0
 // disables the skip (every mode product then runs its full K).
 static bool band_enabled(int n, long long N) {
     static const bool disabled = [] {

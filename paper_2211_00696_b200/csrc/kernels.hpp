@@ -33,7 +33,8 @@ struct GemmArgs {
     int accumulate = 0;
     const int* sq_count = nullptr;    // expm squaring: z with sq_round >= sq_count[z] copies A
     int sq_round = 0;
-    // Negligible-block skip for mode products (64x64x8 tiles only): band[e*band_stride + rb] =
+    // Negligible-block skip for mode products (the 32x128x16 / 64x32x16 band tiles, launch_gemm
+    // shapes 6 / 7): band[e*band_stride + rb] =
     // {first, last+1} 8-wide k-slices of 32-row block rb of exponential e that hold any entry above
     // 2^-64 max|E| (launch_band_ranges).  The CTA streams the union of its two 32-row blocks; each
     // warp issues DMMAs only inside its own block's range.  band_mode 1: A = exponentials stacked
