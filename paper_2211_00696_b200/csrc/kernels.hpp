@@ -36,7 +36,7 @@ struct GemmArgs {
     // Negligible-block skip for mode products (the 32x128x16 / 64x32x16 band tiles, launch_gemm
     // shapes 6 / 7): band[e*band_stride + rb] =
     // {first, last+1} 8-wide k-slices of 32-row block rb of exponential e that hold any entry above
-    // 2^-64 max|E| (launch_band_ranges).  The CTA streams the union of its two 32-row blocks; each
+    // 2^-64 max|E| (launch_band_ranges).  The CTA streams the union of the 32-row blocks it covers; each
     // warp issues DMMAs only inside its own block's range.  band_mode 1: A = exponentials stacked
     // along M (e = m0 / band_rows); 2: A = exponential z1; 3: B (k-major) = exponential z1, rows
     // from n0.
