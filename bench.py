@@ -158,10 +158,21 @@ def dist_init():
     if world > 1:
         import torch
         import torch.distributed as dist
-        torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if _backend() == "gloo":
+            # plumbing check only (tests/test_gpu_bench_contract.py): ranks share the visible GPUs; the
+            # RHS-sharded data path has no collective, gloo carries the barrier and the max-over-ranks
+            local = local % torch.cuda.device_count()
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     return world, rank, local
+
+
+def _backend() -> str:
+    return os.environ.get("PQ_BENCH_BACKEND", "nccl")
 
 
 def max_over_ranks(x: float, world: int) -> float:
@@ -169,7 +180,7 @@ def max_over_ranks(x: float, world: int) -> float:
         return x
     import torch
     import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    t = torch.tensor([x], dtype=torch.float64, device="cpu" if _backend() == "gloo" else "cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 

@@ -33,3 +33,22 @@ def test_bench_line_contract():
     assert ro["achieved"] > 0 and ro["peak"] > 0
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     assert d["gpu_launches"] > 0
+
+
+def test_bench_two_ranks_plumbing():
+    """The N > 1 launch the driver uses (torch.distributed.run, one process per rank), with gloo
+    carrying the barrier / max-over-ranks so both ranks can share the one GPU of this box: the RHS
+    shards have no data-path collective, so this checks the rank plumbing and the aggregate line."""
+    import os
+    env = dict(os.environ, PQ_BENCH_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29517", str(ROOT / "bench.py"),
+                        "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "1", "--e2e-callers", "1"],
+                       capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
+    assert "x2" in d["config"]["parallelism"]
+    assert d["e2e"]["value"] > 0
