@@ -149,6 +149,10 @@ int pq_ctx_destroy(pq_ctx* c) {
             cudaStreamDestroy(c->sq2);
             cudaEventDestroy(c->ev_sqfork);
         }
+        if (c->sqhi) {
+            cudaStreamSynchronize(c->sqhi);
+            cudaStreamDestroy(c->sqhi);
+        }
         for (auto e : c->ev_sqA) cudaEventDestroy(e);
         for (auto e : c->ev_sqB) cudaEventDestroy(e);
         if (c->ev_beta) cudaEventDestroy(c->ev_beta);
@@ -178,7 +182,7 @@ int pq_ctx_set_stream(pq_ctx* c, void* stream) {
             cuda_check(cudaEventRecord(c->arena.done, c->stream), "record");
         }
         // helper streams follow the new stream's priority: recreated on next use
-        for (cudaStream_t* h : {&c->side, &c->sq2}) {
+        for (cudaStream_t* h : {&c->side, &c->sq2, &c->sqhi}) {
             if (*h) {
                 cuda_check(cudaStreamSynchronize(*h), "sync helper stream");
                 cudaStreamDestroy(*h);

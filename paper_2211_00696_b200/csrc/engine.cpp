@@ -332,6 +332,30 @@ void make_helper_stream(pq_ctx& c, cudaStream_t* s, const char* what) {
     cuda_check(cudaStreamCreateWithPriority(s, cudaStreamNonBlocking, prio), what);
 }
 
+// Rotating buffers of the two-stream squaring.  Three suffice for the data dependencies; when the
+// results go to pinned host memory the lower half gets l + 1 (no reuse, so it never waits for the
+// upper half and finishes -- and starts its D2H -- while the upper half still computes), as long
+// as the extra buffers stay under 2 GB (config 2: 5 x 67 MB).
+static int squaring_ring(int nb, int p, long long N, int l, bool host_out) {
+    const int R = std::max(3, l + 1);
+    if (!host_out || R == 3) return 3;
+    const double extra = static_cast<double>(R - 3) * nb * p * static_cast<double>(N) * sizeof(double);
+    return extra <= 2.0e9 ? R : 3;
+}
+
+// stream for the run-ahead lower half: one priority level above the context's stream
+static void ensure_sqhi(pq_ctx& c) {
+    if (c.sqhi) return;
+    int prio = 0, least = 0, greatest = 0;
+    if (cudaStreamGetPriority(c.stream, &prio) != cudaSuccess) {
+        cudaGetLastError();
+        prio = 0;
+    }
+    cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
+    cuda_check(cudaStreamCreateWithPriority(&c.sqhi, cudaStreamNonBlocking, std::max(greatest, prio - 1)),
+               "sqhi stream");
+}
+
 // second squaring stream and per-step events for l steps
 static void ensure_sq2(pq_ctx& c, int l) {
     if (!c.sq2) {
@@ -1409,25 +1433,26 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
         // combination of step s-2.  Everything else is ordered within a stream, so each half's
         // bandwidth-bound combination runs under the other half's DMMA chain.
         const int h = p / 2;
-        double* third = ws(c, "sq3", static_cast<size_t>(p) * N);
-        double* b[3];
+        // R rotating buffers (squaring_ring): the lower chain of step s overwrites b_{s+1} =
+        // b_{s+1-R}, last read by the upper combination of step s+1-R
+        const int R = squaring_ring(nb, p, N, l, host_out != nullptr);
+        double* scratch = ws(c, "sq3", static_cast<size_t>(R - 2) * p * N);
+        std::vector<double*> b(static_cast<size_t>(R), nullptr);
         b[0] = y;
-        // rotate so that b_(l mod 3) is `partner` when l mod 3 != 0 (the caller's output then);
-        // for l mod 3 == 0 the result lands in y
-        if (l % 3 == 1) {
-            b[1] = partner;
-            b[2] = third;
-        } else if (l % 3 == 2) {
-            b[1] = third;
-            b[2] = partner;
-        } else {
-            b[1] = partner;
-            b[2] = third;
-        }
+        // b_(l mod R) is `partner` when l mod R != 0 (the caller's output then); for l mod R == 0
+        // the result lands in y.  The other slots are scratch.
+        const int fin = (l % R == 0) ? 1 : l % R;
+        b[static_cast<size_t>(fin)] = partner;
+        for (int r = 1, k = 0; r < R; ++r)
+            if (r != fin) b[static_cast<size_t>(r)] = scratch + static_cast<size_t>(k++) * p * N;
         ensure_sq2(c, l);
+        const bool ahead = host_out != nullptr;  // lower half on the higher-priority stream
+        if (ahead) ensure_sqhi(c);
         cuda_check(cudaEventRecord(c.ev_sqfork, c.stream), "sq fork");
         cuda_check(cudaStreamWaitEvent(c.sq2, c.ev_sqfork, 0), "sq fork wait");
+        if (ahead) cuda_check(cudaStreamWaitEvent(c.sqhi, c.ev_sqfork, 0), "sq fork wait (lower)");
         const cudaStream_t main_stream = c.stream;
+        const cudaStream_t lower_stream = ahead ? c.sqhi : main_stream;
         try {
             for (int step = 0; step < l; ++step) {
                 const double* E[3];
@@ -1436,11 +1461,11 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
                     E[k] = E_in[k] + static_cast<size_t>(step) * op.n[k] * op.n[k];
                     if (band_in && band_in[k]) Bd[k] = band_in[k] + step * band_row_blocks(op.n[k]);
                 }
-                double* cur = b[step % 3];
-                double* nxt = b[(step + 1) % 3];
-                // lower half on the main stream
-                c.stream = main_stream;
-                if (step >= 2) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqB[step - 2], 0), "sq wait B");
+                double* cur = b[static_cast<size_t>(step % R)];
+                double* nxt = b[static_cast<size_t>((step + 1) % R)];
+                // lower half on the main stream (or the run-ahead stream)
+                c.stream = lower_stream;
+                if (step + 1 >= R) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqB[step + 1 - R], 0), "sq wait B");
                 mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, h, Epilogue{}, "sqchA", Bd);
                 launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, 0, h);
                 count_launch(c);
@@ -1459,10 +1484,14 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
             throw;
         }
         c.stream = main_stream;
-        if (host_out) {  // lower half is final on the main stream now, the upper half on sq2
-            const double* res = b[l % 3];
-            cuda_check(cudaMemcpyAsync(host_out, res, sizeof(double) * h * N, cudaMemcpyDeviceToHost, main_stream),
+        if (host_out) {  // lower half is final on its stream now, the upper half on sq2
+            const double* res = b[static_cast<size_t>(l % R)];
+            cuda_check(cudaMemcpyAsync(host_out, res, sizeof(double) * h * N, cudaMemcpyDeviceToHost, lower_stream),
                        "phi lower D2H");
+            if (ahead) {
+                cuda_check(cudaEventRecord(c.ev_sqA[l - 1], lower_stream), "sq rec A (copy)");
+                cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqA[l - 1], 0), "sq join (lower)");
+            }
             cuda_check(cudaMemcpyAsync(host_out + static_cast<size_t>(h) * N, res + static_cast<size_t>(h) * N,
                                        sizeof(double) * (p - h) * N, cudaMemcpyDeviceToHost, c.sq2),
                        "phi upper D2H");
@@ -1471,7 +1500,7 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
         }
         cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqB[l - 1], 0), "sq join");
         check_launch(c);
-        return b[l % 3];
+        return b[static_cast<size_t>(l % R)];
     }
     double* cur = y;
     double* nxt = partner;
@@ -1536,7 +1565,8 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
     // the squaring then ends in `out`: ping-pong (l odd: start in partner), or the two-stream
     // three-buffer rotation (l mod 3 != 0: start in partner, squaring_pingpong rotates into out)
     const bool split_sq = l > 0 && px.sq_len >= l && squaring_split_ok(c, nb, p, op.N);
-    double* first = split_sq ? ((l % 3 == 0) ? out : partner) : ((l % 2 == 1) ? partner : out);
+    const int ring = squaring_ring(nb, p, op.N, l, out_host != nullptr);
+    double* first = split_sq ? ((l % ring == 0) ? out : partner) : ((l % 2 == 1) ? partner : out);
     if (kind == kGauss) {
         phi_fixed_shift(c, op, scale, l, nb, bs, p, rule, px, first);
         if (points_used) *points_used = rule.size();
