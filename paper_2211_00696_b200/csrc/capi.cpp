@@ -149,12 +149,11 @@ int pq_ctx_destroy(pq_ctx* c) {
             cudaStreamDestroy(c->sq2);
             cudaEventDestroy(c->ev_sqfork);
         }
-        if (c->sqhi) {
-            cudaStreamSynchronize(c->sqhi);
-            cudaStreamDestroy(c->sqhi);
+        for (auto s : c->sqs) {
+            cudaStreamSynchronize(s);
+            cudaStreamDestroy(s);
         }
-        for (auto e : c->ev_sqA) cudaEventDestroy(e);
-        for (auto e : c->ev_sqB) cudaEventDestroy(e);
+        for (auto e : c->ev_sqg) cudaEventDestroy(e);
         if (c->ev_beta) cudaEventDestroy(c->ev_beta);
         if (c->ev_cc) cudaEventDestroy(c->ev_cc);
         if (c->ev_fac) cudaEventDestroy(c->ev_fac);
@@ -182,7 +181,12 @@ int pq_ctx_set_stream(pq_ctx* c, void* stream) {
             cuda_check(cudaEventRecord(c->arena.done, c->stream), "record");
         }
         // helper streams follow the new stream's priority: recreated on next use
-        for (cudaStream_t* h : {&c->side, &c->sq2, &c->sqhi}) {
+        for (cudaStream_t s : c->sqs) {
+            cuda_check(cudaStreamSynchronize(s), "sync helper stream");
+            cudaStreamDestroy(s);
+        }
+        c->sqs.clear();
+        for (cudaStream_t* h : {&c->side, &c->sq2}) {
             if (*h) {
                 cuda_check(cudaStreamSynchronize(*h), "sync helper stream");
                 cudaStreamDestroy(*h);
@@ -574,6 +578,7 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
     if (out0 && !h0) finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
     if (!cols_copied) finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
     finish(*c, space);
+    mark(*c, "returned");
     if (info) {
         info->l = pi.l;
         info->n = pi.n;

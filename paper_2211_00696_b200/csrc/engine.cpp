@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
@@ -343,31 +344,30 @@ static int squaring_ring(int nb, int p, long long N, int l, bool host_out) {
     return extra <= 2.0e9 ? R : 3;
 }
 
-// stream for the run-ahead lower half: one priority level above the context's stream
-static void ensure_sqhi(pq_ctx& c) {
-    if (c.sqhi) return;
+// helper streams of the per-column squaring cascade: descending priority from the top of the
+// device's range down to the context stream's own level (equal where the range runs out)
+static void ensure_sq_cascade(pq_ctx& c, int G) {
+    if (static_cast<int>(c.sqs.size()) >= G) return;
     int prio = 0, least = 0, greatest = 0;
     if (cudaStreamGetPriority(c.stream, &prio) != cudaSuccess) {
         cudaGetLastError();
         prio = 0;
     }
     cuda_check(cudaDeviceGetStreamPriorityRange(&least, &greatest), "priority range");
-    cuda_check(cudaStreamCreateWithPriority(&c.sqhi, cudaStreamNonBlocking, std::max(greatest, prio - 1)),
-               "sqhi stream");
+    while (static_cast<int>(c.sqs.size()) < G) {
+        const int g = static_cast<int>(c.sqs.size());
+        cudaStream_t s;
+        cuda_check(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, std::max(greatest, prio - (G - 1 - g))),
+                   "sq cascade stream");
+        c.sqs.push_back(s);
+    }
 }
 
-// second squaring stream and per-step events for l steps
-static void ensure_sq2(pq_ctx& c, int l) {
+// second squaring stream and its fork event
+static void ensure_sq2(pq_ctx& c) {
     if (!c.sq2) {
         make_helper_stream(c, &c.sq2, "sq2 stream");
         if (!c.ev_sqfork) cuda_check(cudaEventCreateWithFlags(&c.ev_sqfork, cudaEventDisableTiming), "sq fork event");
-    }
-    while (static_cast<int>(c.ev_sqA.size()) < l) {
-        cudaEvent_t a, b;
-        cuda_check(cudaEventCreateWithFlags(&a, cudaEventDisableTiming), "sq event");
-        cuda_check(cudaEventCreateWithFlags(&b, cudaEventDisableTiming), "sq event");
-        c.ev_sqA.push_back(a);
-        c.ev_sqB.push_back(b);
     }
 }
 
@@ -1271,7 +1271,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         }
         const bool offload = fused && will_spec && !c.profiling;
         if (offload) {
-            ensure_sq2(c, 0);
+            ensure_sq2(c);
             cuda_check(cudaEventRecord(c.ev_sqfork, main_stream), "cc fork");
             cuda_check(cudaStreamWaitEvent(c.sq2, c.ev_sqfork, 0), "cc fork wait");
             c.stream = c.sq2;
@@ -1426,16 +1426,26 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
     const int Z1 = nb * p;
     long long Es[3] = {0, 0, 0};
     if (chain && squaring_split_ok(c, nb, p, N)) {
-        // Two column halves on two streams, three rotating buffers b_s (step s reads b_s, writes
-        // b_{s+1}).  Lower half [0, h) on c.stream, upper half [h, p) on c.sq2.  The upper
-        // combination of step s reads y_s[j < h]: it waits for the lower combination of step s-1.
-        // The lower chain of step s overwrites b_{s+1} = b_{s-2}, last read by the upper
-        // combination of step s-2.  Everything else is ordered within a stream, so each half's
-        // bandwidth-bound combination runs under the other half's DMMA chain.
-        const int h = p / 2;
-        // R rotating buffers (squaring_ring): the lower chain of step s overwrites b_{s+1} =
-        // b_{s+1-R}, last read by the upper combination of step s+1-R
+        // Column groups on their own streams, R rotating buffers b_s (step s reads b_s, writes
+        // b_{s+1}).  Column i of step s needs columns j <= i of step s-1 (phiaction.hpp:260-268), so
+        // group g's combination of step s waits for every lower group's combination of step s-1,
+        // and group g's chain of step s overwrites b_{s+1} = b_{s+1-R}, last read by the higher
+        // groups' combinations of step s+1-R.  Everything else is ordered within a stream, so one
+        // group's bandwidth-bound combination runs under the others' DMMA chains.
+        //  * device-resident: two halves, lower on the context stream, upper on c.sq2, R = 3;
+        //  * pinned host results (squaring_ring > 3): groups on helper streams with descending
+        //    priority and no buffer reuse, so the lowest columns finish first and their D2H runs
+        //    under the later columns.  Two groups by default; PQ_SQ_GROUPS=3|4 splits further (one
+        //    column per group at p = 4: same e2e within noise, twice the launches).
         const int R = squaring_ring(nb, p, N, l, host_out != nullptr);
+        const bool cascade = host_out != nullptr && R > 3;
+        static const int max_groups = [] {
+            const char* e = std::getenv("PQ_SQ_GROUPS");
+            return e ? std::max(2, std::min(4, std::atoi(e))) : 2;
+        }();
+        const int G = cascade ? std::min(p, max_groups) : 2;
+        std::vector<int> lo(static_cast<size_t>(G) + 1);
+        for (int g = 0; g <= G; ++g) lo[static_cast<size_t>(g)] = cascade ? (g * p) / G : (g == 0 ? 0 : g == 1 ? p / 2 : p);
         double* scratch = ws(c, "sq3", static_cast<size_t>(R - 2) * p * N);
         std::vector<double*> b(static_cast<size_t>(R), nullptr);
         b[0] = y;
@@ -1445,14 +1455,23 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
         b[static_cast<size_t>(fin)] = partner;
         for (int r = 1, k = 0; r < R; ++r)
             if (r != fin) b[static_cast<size_t>(r)] = scratch + static_cast<size_t>(k++) * p * N;
-        ensure_sq2(c, l);
-        const bool ahead = host_out != nullptr;  // lower half on the higher-priority stream
-        if (ahead) ensure_sqhi(c);
-        cuda_check(cudaEventRecord(c.ev_sqfork, c.stream), "sq fork");
-        cuda_check(cudaStreamWaitEvent(c.sq2, c.ev_sqfork, 0), "sq fork wait");
-        if (ahead) cuda_check(cudaStreamWaitEvent(c.sqhi, c.ev_sqfork, 0), "sq fork wait (lower)");
+        ensure_sq2(c);
+        if (cascade) ensure_sq_cascade(c, G);
+        while (static_cast<int>(c.ev_sqg.size()) < G * l) {
+            cudaEvent_t e;
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "sq event");
+            c.ev_sqg.push_back(e);
+        }
+        auto ev = [&](int g, int st) { return c.ev_sqg[static_cast<size_t>(st) * G + g]; };
         const cudaStream_t main_stream = c.stream;
-        const cudaStream_t lower_stream = ahead ? c.sqhi : main_stream;
+        std::vector<cudaStream_t> gs(static_cast<size_t>(G));
+        for (int g = 0; g < G; ++g)
+            gs[static_cast<size_t>(g)] = cascade ? c.sqs[static_cast<size_t>(g)] : (g == 0 ? main_stream : c.sq2);
+        cuda_check(cudaEventRecord(c.ev_sqfork, main_stream), "sq fork");
+        for (int g = 0; g < G; ++g)
+            if (gs[static_cast<size_t>(g)] != main_stream)
+                cuda_check(cudaStreamWaitEvent(gs[static_cast<size_t>(g)], c.ev_sqfork, 0), "sq fork wait");
+        static const char* tags[4] = {"sqch0", "sqch1", "sqch2", "sqch3"};
         try {
             for (int step = 0; step < l; ++step) {
                 const double* E[3];
@@ -1463,42 +1482,46 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
                 }
                 double* cur = b[static_cast<size_t>(step % R)];
                 double* nxt = b[static_cast<size_t>((step + 1) % R)];
-                // lower half on the main stream (or the run-ahead stream)
-                c.stream = lower_stream;
-                if (step + 1 >= R) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqB[step + 1 - R], 0), "sq wait B");
-                mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, h, Epilogue{}, "sqchA", Bd);
-                launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, 0, h);
-                count_launch(c);
-                cuda_check(cudaEventRecord(c.ev_sqA[step], c.stream), "sq rec A");
-                // upper half on the second stream
-                c.stream = c.sq2;
-                mode_chain(c, op.d, op.n, E, Es, cur + static_cast<size_t>(h) * N, N, nxt + static_cast<size_t>(h) * N, N,
-                           p - h, Epilogue{}, "sqchB", Bd);
-                if (step >= 1) cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqA[step - 1], 0), "sq wait A");
-                launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, h, p);
-                count_launch(c);
-                cuda_check(cudaEventRecord(c.ev_sqB[step], c.stream), "sq rec B");
+                for (int g = 0; g < G; ++g) {
+                    const int c0 = lo[static_cast<size_t>(g)], c1 = lo[static_cast<size_t>(g) + 1];
+                    c.stream = gs[static_cast<size_t>(g)];
+                    if (step + 1 >= R)
+                        for (int h = g + 1; h < G; ++h)
+                            cuda_check(cudaStreamWaitEvent(c.stream, ev(h, step + 1 - R), 0), "sq wait (reuse)");
+                    mode_chain(c, op.d, op.n, E, Es, cur + static_cast<size_t>(c0) * N, N, nxt + static_cast<size_t>(c0) * N,
+                               N, c1 - c0, Epilogue{}, tags[g], Bd);
+                    if (step >= 1)
+                        for (int h = 0; h < g; ++h)
+                            cuda_check(cudaStreamWaitEvent(c.stream, ev(h, step - 1), 0), "sq wait (columns)");
+                    launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, c0, c1);
+                    count_launch(c);
+                    cuda_check(cudaEventRecord(ev(g, step), c.stream), "sq rec");
+                }
             }
         } catch (...) {
             c.stream = main_stream;
             throw;
         }
         c.stream = main_stream;
-        if (host_out) {  // lower half is final on its stream now, the upper half on sq2
-            const double* res = b[static_cast<size_t>(l % R)];
-            cuda_check(cudaMemcpyAsync(host_out, res, sizeof(double) * h * N, cudaMemcpyDeviceToHost, lower_stream),
-                       "phi lower D2H");
-            if (ahead) {
-                cuda_check(cudaEventRecord(c.ev_sqA[l - 1], lower_stream), "sq rec A (copy)");
-                cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqA[l - 1], 0), "sq join (lower)");
+        const double* res = b[static_cast<size_t>(l % R)];
+        for (int g = 0; g < G; ++g) {
+            const int c0 = lo[static_cast<size_t>(g)], c1 = lo[static_cast<size_t>(g) + 1];
+            const cudaStream_t st = gs[static_cast<size_t>(g)];
+            c.stream = st;
+            mark(c, "sq_group_done");
+            if (host_out) {  // this group's columns are final on its stream now
+                cuda_check(cudaMemcpyAsync(host_out + static_cast<size_t>(c0) * N, res + static_cast<size_t>(c0) * N,
+                                           sizeof(double) * (c1 - c0) * N, cudaMemcpyDeviceToHost, st),
+                           "phi columns D2H");
+                mark(c, "sq_group_copied");
             }
-            cuda_check(cudaMemcpyAsync(host_out + static_cast<size_t>(h) * N, res + static_cast<size_t>(h) * N,
-                                       sizeof(double) * (p - h) * N, cudaMemcpyDeviceToHost, c.sq2),
-                       "phi upper D2H");
-            cuda_check(cudaEventRecord(c.ev_sqB[l - 1], c.sq2), "sq rec B (copy)");
-            if (copied) *copied = true;
+            c.stream = main_stream;
+            if (st != main_stream) {
+                cuda_check(cudaEventRecord(ev(g, l - 1), st), "sq rec (final)");
+                cuda_check(cudaStreamWaitEvent(main_stream, ev(g, l - 1), 0), "sq join");
+            }
         }
-        cuda_check(cudaStreamWaitEvent(c.stream, c.ev_sqB[l - 1], 0), "sq join");
+        if (host_out && copied) *copied = true;
         check_launch(c);
         return b[static_cast<size_t>(l % R)];
     }

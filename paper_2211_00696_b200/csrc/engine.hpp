@@ -66,11 +66,11 @@ struct pq_ctx {
     std::vector<std::function<void()>> deferred;
     // two-stream squaring (engine.cpp squaring_pingpong): second stream, fork event, per-step events
     cudaStream_t sq2 = nullptr;
-    // lower column half of a two-stream squaring whose results go to pinned host memory: one
-    // priority level above `stream`, so that half runs ahead and its D2H overlaps the upper half
-    cudaStream_t sqhi = nullptr;
+    // per-column squaring streams when the results go to pinned host memory (descending priority:
+    // column 1 runs ahead and its D2H overlaps the later columns) and their per-(group, step) events
+    std::vector<cudaStream_t> sqs;
+    std::vector<cudaEvent_t> ev_sqg;
     cudaEvent_t ev_sqfork = nullptr;
-    std::vector<cudaEvent_t> ev_sqA, ev_sqB;
     // Taylor powers of the current call's factors (engine.cpp taylor_powers), per factor size;
     // valid only for the DevOp serial they were computed for (never reused across calls)
     struct PowCache {

@@ -9,11 +9,13 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n", [16, 64])
-def test_pinned_host_outputs_equal_device_outputs(pq, n):
+@pytest.mark.parametrize("cfg,n", [(2, 16), (2, 64), (2, 128), (3, 64), (5, 64)])
+def test_pinned_host_outputs_equal_device_outputs(pq, cfg, n):
+    """(2, 64), (2, 128): the per-column squaring cascade (p = 4 groups); (3, 64): p = 3 groups;
+    (5, 64): p = 6 columns in 4 uneven groups; (2, 16): below the split threshold."""
     import torch
     from paper_2211_00696_b200.workloads import config
-    w = config(2, n=n)
+    w = config(cfg, n=n)
     a = pq.KroneckerSum(w.factors)
     req = pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode))
     b = w.rhs(5)

@@ -20,6 +20,7 @@ d, sh, fac = a._abi()
 rc = req._c()
 N = w.N
 NC = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+DIR = sys.argv[2] if len(sys.argv) > 2 else "both"  # both | h2d | d2h
 REPS = 8
 
 
@@ -54,8 +55,12 @@ ncopy = [0]
 def copier():
     while not stop.is_set():
         with torch.cuda.stream(cst):
-            db.copy_(hb, non_blocking=True)
-            ho.copy_(do, non_blocking=True)
+            if DIR in ("both", "h2d"):
+                db.copy_(hb, non_blocking=True)
+                if DIR == "h2d":
+                    do.copy_(ho, non_blocking=True)
+            if DIR in ("both", "d2h"):
+                ho.copy_(do, non_blocking=True)
         cst.synchronize()
         ncopy[0] += 1
 
@@ -87,5 +92,5 @@ t2 = time.perf_counter()
 n1 = ncopy[0]
 stop.set()
 th.join()
-print(json.dumps({"callers": NC, "device_actions_per_s_alone": alone, "device_actions_per_s_with_copier": with_copies,
+print(json.dumps({"callers": NC, "copies": DIR, "device_actions_per_s_alone": alone, "device_actions_per_s_with_copier": with_copies,
                   "copier_actions_per_s_during": (n1 - n0) / (t2 - t1)}))

@@ -3,7 +3,8 @@
 
 usage: python tools/timeline.py [config] [--trace]
   default: marks under profiling mode (every GEMM bracketed by events, side streams serialised);
-  --trace: PQ_TRACE=1 marks only, normal scheduling (the production overlap is kept)."""
+  --trace: PQ_TRACE=1 marks only, normal scheduling (the production overlap is kept).
+  --host: the end-to-end call (pinned host b in, phi_0..phi_p to pinned host memory, PQ_HOST)."""
 import ctypes as C
 import json
 import os
@@ -37,9 +38,14 @@ def main():
     rc = req._c()
     info = L.PhiInfoC()
 
+    space = L.PQ_DEVICE
+    if "--host" in sys.argv:
+        b, out0, out = b.cpu().pin_memory(), out0.cpu().pin_memory(), out.cpu().pin_memory()
+        space = L.PQ_HOST
+
     def step():
         L.check(L.lib.pq_phi_0p(ctx.handle, d, sh, fac, 1, C.c_void_p(b.data_ptr()), C.byref(rc),
-                                C.c_void_p(out0.data_ptr()), C.c_void_p(out.data_ptr()), C.byref(info), L.PQ_DEVICE))
+                                C.c_void_p(out0.data_ptr()), C.c_void_p(out.data_ptr()), C.byref(info), space))
 
     for _ in range(3):
         step()
