@@ -33,12 +33,21 @@ def test_pinned_host_outputs_equal_device_outputs(pq, cfg, n):
     b_pin = torch.from_numpy(b.copy()).pin_memory()
     o0_pin = torch.full((1, w.N), np.nan, dtype=torch.float64).pin_memory()
     o_pin = torch.full((1, w.p, w.N), np.nan, dtype=torch.float64).pin_memory()
-    pq._lib.check(pq._lib.lib.pq_phi_0p(ctx.handle, d, sh, fac, 1, C.c_void_p(b_pin.data_ptr()), C.byref(rc),
-                                        C.c_void_p(o0_pin.data_ptr()), C.c_void_p(o_pin.data_ptr()), C.byref(info),
-                                        pq._lib.PQ_HOST))
-    # read immediately: the call must have completed every copy it issued
-    assert np.array_equal(o0_pin.numpy(), o0_dev.cpu().numpy())
-    assert np.array_equal(o_pin.numpy(), o_dev.cpu().numpy())
+    # three calls on the same context (warm workspaces and helper streams), the third into fresh
+    # output buffers
+    for k in range(3):
+        if k == 2:
+            o0_pin = torch.full((1, w.N), np.nan, dtype=torch.float64).pin_memory()
+            o_pin = torch.full((1, w.p, w.N), np.nan, dtype=torch.float64).pin_memory()
+        else:
+            o0_pin.fill_(np.nan)
+            o_pin.fill_(np.nan)
+        pq._lib.check(pq._lib.lib.pq_phi_0p(ctx.handle, d, sh, fac, 1, C.c_void_p(b_pin.data_ptr()), C.byref(rc),
+                                            C.c_void_p(o0_pin.data_ptr()), C.c_void_p(o_pin.data_ptr()),
+                                            C.byref(info), pq._lib.PQ_HOST))
+        # read immediately: the call must have completed every copy it issued
+        assert np.array_equal(o0_pin.numpy(), o0_dev.cpu().numpy()), k
+        assert np.array_equal(o_pin.numpy(), o_dev.cpu().numpy()), k
     ctx.close()
 
 
