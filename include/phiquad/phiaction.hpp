@@ -152,27 +152,70 @@ inline std::vector<PhiColumns> phi_with_plan(const KroneckerSum& a, const std::v
     return detail::scatter(out, static_cast<int>(bs.size()), p, dim);
 }
 
-inline std::vector<PhiColumns> phiquadmv_multi(const KroneckerSum& a, const std::vector<std::vector<double>>& bs,
-                                               const PhiRequest& req, PhiInfo* info = nullptr) {
+namespace detail {
+
+// The result columns, allocated (and value-initialised, as std::vector must) by several threads:
+// first-touching tens of MB from one thread costs more than the device computation at these sizes
+// (config 2: 67 MB, ~24 ms single-threaded on the B200 box's host vs ~3.4 ms for the phi call).
+inline std::vector<PhiColumns> alloc_columns(int nb, int p, int dim) {
+    std::vector<PhiColumns> out(static_cast<size_t>(nb));
+    for (auto& pc : out) {
+        pc.dim = dim;
+        pc.cols.resize(static_cast<size_t>(p));
+    }
+    const int count = nb * p;
+    const int threads = static_cast<long long>(dim) * count >= (1LL << 20) ? std::min(count, 8) : 1;
+    parallel_for(count, threads, [&](int k) {
+        out[static_cast<size_t>(k / p)].cols[static_cast<size_t>(k % p)] = std::vector<double>(static_cast<size_t>(dim));
+    });
+    return out;
+}
+
+// phiquadmv on the caller's vectors in place: b_m read from its own storage, phi_j written straight
+// into the PhiColumns vectors (pq_phiquadmv_cols) -- no flattening or scattering copies
+inline std::vector<PhiColumns> phiquadmv_ptrs(const KroneckerSum& a, const std::vector<const double*>& bs,
+                                              const PhiRequest& req, PhiInfo* info) {
     if (req.p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
     const int dim = a.dim();
-    const auto flat = detail::gather(bs, dim, "phiquadmv");
+    const int nb = static_cast<int>(bs.size());
     const auto f = detail::flatten(a);
     const pq_phi_request r = detail::abi_request(req);
     pq_phi_info pi{};
-    std::vector<double> out(bs.size() * static_cast<size_t>(req.p) * dim);
-    b200::check(pq_phiquadmv(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
-                             flat.data(), &r, out.data(), &pi, PQ_HOST));
+    std::vector<PhiColumns> out = alloc_columns(nb, req.p, dim);
+    std::vector<double*> cols;
+    cols.reserve(static_cast<size_t>(nb) * req.p);
+    for (auto& pc : out)
+        for (auto& c : pc.cols) cols.push_back(c.data());
+    b200::check(pq_phiquadmv_cols(b200::context(), a.order(), f.shape.data(), f.data.data(), nb, bs.data(), &r,
+                                  cols.data(), &pi, PQ_HOST));
     if (info)
         *info = PhiInfo{pi.l,     pi.n,    pi.points,          pi.mode == PQ_GAUSS_LEGENDRE ? QuadKind::gauss_legendre
                                                                                          : QuadKind::clenshaw_curtis,
                         pi.alpha, pi.beta, pi.planned != 0, pi.plan_cost};
-    return detail::scatter(out, static_cast<int>(bs.size()), req.p, dim);
+    return out;
+}
+
+}  // namespace detail
+
+inline std::vector<PhiColumns> phiquadmv_multi(const KroneckerSum& a, const std::vector<std::vector<double>>& bs,
+                                               const PhiRequest& req, PhiInfo* info = nullptr) {
+    if (req.p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
+    if (bs.empty()) throw std::invalid_argument("phiquadmv: need at least one right-hand side");
+    std::vector<const double*> ptrs;
+    for (const auto& b : bs) {
+        if (static_cast<long long>(b.size()) != static_cast<long long>(a.dim()))
+            throw std::invalid_argument("phiquadmv: vector length mismatch");
+        ptrs.push_back(b.data());
+    }
+    return detail::phiquadmv_ptrs(a, ptrs, req, info);
 }
 
 inline PhiColumns phiquadmv(const KroneckerSum& a, const std::vector<double>& b, const PhiRequest& req,
                             PhiInfo* info = nullptr) {
-    return std::move(phiquadmv_multi(a, {b}, req, info).front());
+    if (req.p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
+    if (static_cast<long long>(b.size()) != static_cast<long long>(a.dim()))
+        throw std::invalid_argument("phiquadmv: vector length mismatch");
+    return std::move(detail::phiquadmv_ptrs(a, {b.data()}, req, info).front());
 }
 
 /// sum_j phi_j(A) b_j in one quadrature sweep (no scaling/squaring).

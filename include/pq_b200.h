@@ -157,6 +157,12 @@ PQ_API int pq_phi_with_plan(pq_ctx* ctx, int d, const int* shape, const double* 
  * reads beta back from the device, i.e. synchronises once before planning). */
 PQ_API int pq_phiquadmv(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb, const double* bs,
                  const pq_phi_request* req, double* out, pq_phi_info* info, int space);
+/* phiaction.hpp:307 phiquadmv_multi with the caller's vectors as they are: RHS m at bs[m], and
+ * phi_{j+1}(A) b_m written to cols[m*p + j] (each N doubles).  The drop-in headers call this so a
+ * std::vector RHS and the PhiColumns vectors are read / written in place (no flattening copies). */
+PQ_API int pq_phiquadmv_cols(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb,
+                             const double* const* bs, const pq_phi_request* req, double* const* cols,
+                             pq_phi_info* info, int space);
 /* phiquadmv plus phi_0 = exp_action for every RHS: out0 [nb][N], out [nb][p][N] — the
  * "phi_0..phi_p action" the benchmark counts. */
 PQ_API int pq_phi_0p(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb, const double* bs,

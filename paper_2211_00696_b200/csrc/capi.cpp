@@ -544,8 +544,11 @@ int pq_phi_with_plan(pq_ctx* c, int d, const int* shape, const double* factors, 
     });
 }
 
+// b_list / col_list (pq_phiquadmv_cols): RHS m at b_list[m], phi_{j+1} of RHS m to col_list[m p + j]
+// instead of the contiguous bs / out
 static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
-                          const pq_phi_request* req, double* out0, double* out, pq_phi_info* info, int space) {
+                          const pq_phi_request* req, double* out0, double* out, pq_phi_info* info, int space,
+                          const double* const* b_list = nullptr, double* const* col_list = nullptr) {
     need_ctx(c);
     need(req != nullptr, "phiquadmv: null request");
     need(req->p >= 1, "phiquadmv: need p >= 1");
@@ -556,8 +559,27 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
     mark(*c, "call");
     arena_begin(*c);
     DevOp op = upload_op(*c, d, shape, factors, "factors");
-    const double* db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
-    double* dout = stage_out(*c, out, static_cast<size_t>(nb) * p * N, space, "hout");
+    const double* db = nullptr;
+    if (b_list) {
+        for (int m = 0; m < nb; ++m) need(b_list[m] != nullptr, "phiquadmv: null right-hand side");
+        if (space == PQ_DEVICE && nb == 1) {
+            db = b_list[0];
+        } else {
+            double* g = ws(*c, "hin_b", static_cast<size_t>(nb) * N);
+            for (int m = 0; m < nb; ++m)
+                cuda_check(cudaMemcpyAsync(g + static_cast<size_t>(m) * N, b_list[m], N * sizeof(double),
+                                           space == PQ_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                                           c->stream),
+                           "gather b");
+            db = g;
+        }
+    } else {
+        db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
+    }
+    if (col_list)
+        for (int k = 0; k < nb * p; ++k) need(col_list[k] != nullptr, "phiquadmv: null output column");
+    double* dout = col_list ? ws(*c, "hout", static_cast<size_t>(nb) * p * N)
+                            : stage_out(*c, out, static_cast<size_t>(nb) * p * N, space, "hout");
     mark(*c, "uploaded");
     PlanInfo pi;
     double* d0 = out0 ? stage_out(*c, out0, static_cast<size_t>(nb) * N, space, "hout0") : nullptr;
@@ -576,7 +598,14 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
                   hc, &cols_copied);
     mark(*c, "computed");
     if (out0 && !h0) finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
-    if (!cols_copied) finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
+    if (col_list) {
+        for (int k = 0; k < nb * p; ++k)
+            cuda_check(cudaMemcpyAsync(col_list[k], dout + static_cast<size_t>(k) * N, N * sizeof(double),
+                                       space == PQ_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream),
+                       "scatter columns");
+    } else if (!cols_copied) {
+        finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
+    }
     finish(*c, space);
     mark(*c, "returned");
     if (info) {
@@ -594,6 +623,14 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
 int pq_phiquadmv(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
                  const pq_phi_request* req, double* out, pq_phi_info* info, int space) {
     return guarded([&] { run_phiquadmv(c, d, shape, factors, nb, bs, req, nullptr, out, info, space); });
+}
+
+int pq_phiquadmv_cols(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* const* bs,
+                      const pq_phi_request* req, double* const* cols, pq_phi_info* info, int space) {
+    return guarded([&] {
+        need(bs != nullptr && cols != nullptr, "phiquadmv: null vector list");
+        run_phiquadmv(c, d, shape, factors, nb, nullptr, req, nullptr, nullptr, info, space, bs, cols);
+    });
 }
 
 int pq_phi_0p(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,

@@ -105,3 +105,44 @@ def test_two_host_callers_concurrently_match_sequential(pq):
     assert not errors, errors
     for ctx, _ in callers:
         ctx.close()
+
+
+@pytest.mark.parametrize("space", ["host", "device"])
+def test_phiquadmv_cols_equals_contiguous(pq, space):
+    """pq_phiquadmv_cols (the drop-in headers' entry: each RHS and each result column at its own
+    address) returns bitwise what pq_phiquadmv returns in one contiguous buffer, nb = 2."""
+    import torch
+    from paper_2211_00696_b200.workloads import config
+    w = config(2, n=32)
+    a = pq.KroneckerSum(w.factors)
+    req = pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode))
+    ctx = pq.Context(0)
+    d, sh, fac = a._abi()
+    rc = req._c()
+    nb, N, p = 2, w.N, w.p
+    bs = np.stack([w.rhs(20), w.rhs(21)])
+    want = np.empty((nb, p, N))
+    info = pq._lib.PhiInfoC()
+    pq._lib.check(pq._lib.lib.pq_phiquadmv(ctx.handle, d, sh, fac, nb, C.c_void_p(bs.ctypes.data), C.byref(rc),
+                                           C.c_void_p(want.ctypes.data), C.byref(info), pq._lib.PQ_HOST))
+    if space == "host":
+        b_sep = [np.ascontiguousarray(bs[m]) for m in range(nb)]
+        cols = [np.full(N, np.nan) for _ in range(nb * p)]
+        bptr = [x.ctypes.data for x in b_sep]
+        cptr = [x.ctypes.data for x in cols]
+        sp = pq._lib.PQ_HOST
+    else:
+        b_sep = [torch.from_numpy(bs[m].copy()).cuda() for m in range(nb)]
+        cols = [torch.full((N,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(nb * p)]
+        bptr = [x.data_ptr() for x in b_sep]
+        cptr = [x.data_ptr() for x in cols]
+        sp = pq._lib.PQ_DEVICE
+    barr = (C.c_void_p * nb)(*bptr)
+    carr = (C.c_void_p * (nb * p))(*cptr)
+    info2 = pq._lib.PhiInfoC()
+    pq._lib.check(pq._lib.lib.pq_phiquadmv_cols(ctx.handle, d, sh, fac, nb, barr, C.byref(rc), carr, C.byref(info2), sp))
+    torch.cuda.synchronize()
+    got = np.stack([np.asarray(c.cpu() if space == "device" else c) for c in cols]).reshape(nb, p, N)
+    assert np.array_equal(got, want)
+    assert (info2.l, info2.n, info2.points) == (info.l, info.n, info.points)
+    ctx.close()
