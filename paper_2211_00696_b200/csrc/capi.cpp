@@ -9,6 +9,7 @@
 #include <map>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "engine.hpp"
@@ -41,6 +42,43 @@ long long dim_of(int d, const int* shape) {
         n *= shape[k];
     }
     return n;
+}
+
+// Pageable host results go through context-owned pinned buffers: the engine's early, overlapped
+// result copies (phi_0 during the squaring, the run-ahead column half) need pinned destinations, and
+// a pageable cudaMemcpy is a staged synchronous copy after the compute.  The bounce is copied to the
+// caller's memory by several host threads once the call has finished.
+static double* pinned_bounce(pq_ctx& c, const char* name, size_t count) {
+    auto& slot = c.pin_bounce[name];
+    const size_t bytes = count * sizeof(double);
+    if (slot.second < bytes) {
+        if (slot.first) cuda_check(cudaFreeHost(slot.first), "cudaFreeHost(bounce)");
+        slot = {nullptr, 0};
+        cuda_check(cudaMallocHost(reinterpret_cast<void**>(&slot.first), bytes), "cudaMallocHost(bounce)");
+        slot.second = bytes;
+    }
+    return slot.first;
+}
+
+// dst[k] <- src + k*count for each k, split over up to 8 host threads in 4 MB pieces
+static void host_scatter(double* const* dst, const double* src, int parts, size_t count) {
+    const size_t piece = size_t(1) << 19;  // doubles (4 MB)
+    const size_t per = (count + piece - 1) / piece, total = per * static_cast<size_t>(parts);
+    auto work = [&](size_t t0, size_t step) {
+        for (size_t t = t0; t < total; t += step) {
+            const size_t k = t / per, o = (t % per) * piece, len = std::min(piece, count - o);
+            std::memcpy(dst[k] + o, src + k * count + o, len * sizeof(double));
+        }
+    };
+    const size_t threads = std::min<size_t>(8, total);
+    if (threads <= 1) {
+        work(0, 1);
+        return;
+    }
+    std::vector<std::thread> team;
+    for (size_t w = 1; w < threads; ++w) team.emplace_back(work, w, threads);
+    work(0, threads);
+    for (auto& t : team) t.join();
 }
 
 // Device view of a caller vector: device pointers pass through; host data is staged.
@@ -158,6 +196,7 @@ int pq_ctx_destroy(pq_ctx* c) {
         if (c->ev_cc) cudaEventDestroy(c->ev_cc);
         if (c->ev_fac) cudaEventDestroy(c->ev_fac);
         if (c->pin_fac) cudaFreeHost(c->pin_fac);
+        for (auto& kv : c->pin_bounce) cudaFreeHost(kv.second.first);
         if (c->own_stream) cudaStreamDestroy(c->stream);
         delete c;
     });
@@ -564,6 +603,8 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
         for (int m = 0; m < nb; ++m) need(b_list[m] != nullptr, "phiquadmv: null right-hand side");
         if (space == PQ_DEVICE && nb == 1) {
             db = b_list[0];
+        } else if (space == PQ_HOST && nb == 1) {
+            db = stage_in(*c, b_list[0], static_cast<size_t>(N), space, "hin_b");
         } else {
             double* g = ws(*c, "hin_b", static_cast<size_t>(nb) * N);
             for (int m = 0; m < nb; ++m)
@@ -593,20 +634,70 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
     };
     double* h0 = pinned(out0) ? out0 : nullptr;
     double* hc = pinned(out) ? out : nullptr;
+    double* bounce0 = nullptr;
+    double* bounce = nullptr;
+    if (space == PQ_HOST) {
+        if (out0 && !h0) h0 = bounce0 = pinned_bounce(*c, "phi0", static_cast<size_t>(nb) * N);
+        if (col_list || (out && !hc)) hc = bounce = pinned_bounce(*c, "cols", static_cast<size_t>(nb) * p * N);
+    }
     bool cols_copied = false;
+    c->early.clear();
     phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi, d0, h0,
                   hc, &cols_copied);
+    // bounced results that are already on their way: move each to the caller's memory as soon as
+    // its copy lands, while the device finishes the rest of the call
+    bool done0 = false;
+    std::vector<char> done_col(static_cast<size_t>(nb) * p, 0);
+    auto drain = [&](const pq_ctx::EarlyCopy& e) {
+        if (bounce0 && e.host == bounce0) {
+            cuda_check(cudaEventSynchronize(e.ev), "early copy wait");
+            host_scatter(&out0, bounce0, 1, static_cast<size_t>(nb) * N);
+            done0 = true;
+        } else if (bounce && e.host >= bounce && e.host < bounce + static_cast<size_t>(nb) * p * N) {
+            const size_t k0 = static_cast<size_t>(e.host - bounce) / N, kc = e.count / N;
+            if (k0 * N != static_cast<size_t>(e.host - bounce) || kc * N != e.count) return;  // not whole columns
+            cuda_check(cudaEventSynchronize(e.ev), "early copy wait");
+            if (col_list) {
+                host_scatter(col_list + k0, bounce + k0 * N, static_cast<int>(kc), static_cast<size_t>(N));
+            } else {
+                double* dst = out + k0 * N;
+                host_scatter(&dst, bounce + k0 * N, 1, kc * N);
+            }
+            for (size_t k = k0; k < k0 + kc; ++k) done_col[k] = 1;
+        }
+    };
+    if (bounce0 || bounce)
+        for (size_t i = 0; i + 1 < c->early.size(); ++i) drain(c->early[i]);  // the last one ends the call anyway
     mark(*c, "computed");
     if (out0 && !h0) finish_out(*c, out0, d0, static_cast<size_t>(nb) * N, space);
-    if (col_list) {
+    if (bounce && !cols_copied)
+        cuda_check(cudaMemcpyAsync(bounce, dout, static_cast<size_t>(nb) * p * N * sizeof(double), cudaMemcpyDeviceToHost,
+                                   c->stream),
+                   "D2H (bounce)");
+    if (col_list && space == PQ_DEVICE) {
         for (int k = 0; k < nb * p; ++k)
             cuda_check(cudaMemcpyAsync(col_list[k], dout + static_cast<size_t>(k) * N, N * sizeof(double),
-                                       space == PQ_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream),
+                                       cudaMemcpyDeviceToDevice, c->stream),
                        "scatter columns");
-    } else if (!cols_copied) {
+    } else if (!bounce && !cols_copied) {
         finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
     }
     finish(*c, space);
+    if (bounce0 && !done0) host_scatter(&out0, bounce0, 1, static_cast<size_t>(nb) * N);
+    if (bounce) {
+        for (int k = 0; k < nb * p; ++k) {
+            if (done_col[static_cast<size_t>(k)]) continue;
+            int k1 = k;
+            while (k1 + 1 < nb * p && !done_col[static_cast<size_t>(k1) + 1]) ++k1;
+            if (col_list) {
+                host_scatter(col_list + k, bounce + static_cast<size_t>(k) * N, k1 - k + 1, static_cast<size_t>(N));
+            } else {
+                double* dst = out + static_cast<size_t>(k) * N;
+                host_scatter(&dst, bounce + static_cast<size_t>(k) * N, 1, static_cast<size_t>(k1 - k + 1) * N);
+            }
+            k = k1;
+        }
+    }
     mark(*c, "returned");
     if (info) {
         info->l = pi.l;

@@ -163,6 +163,17 @@ void prof_collect(pq_ctx& c) {
     c.ev_flops.clear();
 }
 
+void note_early_copy(pq_ctx& c, cudaStream_t s, double* host, size_t count) {
+    const size_t i = c.early.size();
+    if (c.ev_early.size() <= i) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "early copy event");
+        c.ev_early.push_back(e);
+    }
+    cuda_check(cudaEventRecord(c.ev_early[i], s), "early copy record");
+    c.early.push_back({c.ev_early[i], host, count});
+}
+
 void mark(pq_ctx& c, const char* name) {
     if (!c.profiling && !c.trace) return;
     static const auto t0 = std::chrono::steady_clock::now();
@@ -1513,6 +1524,7 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
                 cuda_check(cudaMemcpyAsync(host_out + static_cast<size_t>(c0) * N, res + static_cast<size_t>(c0) * N,
                                            sizeof(double) * (c1 - c0) * N, cudaMemcpyDeviceToHost, st),
                            "phi columns D2H");
+                note_early_copy(c, st, host_out + static_cast<size_t>(c0) * N, static_cast<size_t>(c1 - c0) * N);
                 mark(c, "sq_group_copied");
             }
             c.stream = main_stream;
@@ -1616,9 +1628,11 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
         c.stream = c.side;
         try {
             apply_phi0(c, op, px, nb, bs, phi0_out);
-            if (phi0_host)  // pinned destination: the D2H overlaps the squaring
+            if (phi0_host) {  // pinned destination: the D2H overlaps the squaring
                 cuda_check(cudaMemcpyAsync(phi0_host, phi0_out, sizeof(double) * nb * op.N, cudaMemcpyDeviceToHost, c.side),
                            "phi_0 D2H");
+                note_early_copy(c, c.side, phi0_host, static_cast<size_t>(nb) * op.N);
+            }
         } catch (...) {
             c.stream = main_stream;
             throw;

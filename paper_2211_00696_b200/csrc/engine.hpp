@@ -91,6 +91,18 @@ struct pq_ctx {
     // operator (reused when the caller passes bit-identical factors again)
     double* pin_fac = nullptr;
     size_t pin_fac_cap = 0;
+    // result copies into pinned host memory issued before the end of a call, each followed by an
+    // event (note_early_copy): a caller bouncing pageable results can consume them while the device
+    // still computes the rest
+    struct EarlyCopy {
+        cudaEvent_t ev;
+        double* host;
+        size_t count;
+    };
+    std::vector<EarlyCopy> early;
+    std::vector<cudaEvent_t> ev_early;
+    // pinned bounce buffers for pageable host results (capi.cpp run_phiquadmv): name -> (ptr, bytes)
+    std::map<std::string, std::pair<double*, size_t>> pin_bounce;
     cudaEvent_t ev_fac = nullptr;
     // slot -> the last uploaded operator: validated host copy, device pointer, norms, canonical map
     struct FacCache {
@@ -184,6 +196,7 @@ void count_launch(pq_ctx& c, int n = 1);
 // launch_gemm + launch counting + (when profiling) per-launch events and algorithmic flops
 int gemm(pq_ctx& c, const GemmArgs& g);
 void prof_collect(pq_ctx& c);  // syncs, folds recorded events into prof_ms/prof_flops
+void note_early_copy(pq_ctx& c, cudaStream_t s, double* host, size_t count);  // after an early D2H on s
 void mark(pq_ctx& c, const char* name);  // timeline mark (no-op unless profiling)
 void check_launch(pq_ctx& c);
 void ensure_side(pq_ctx& c);  // creates the side stream and its fork/join events on first use
