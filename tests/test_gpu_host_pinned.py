@@ -9,10 +9,12 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.mark.parametrize("memory", ["pinned", "pageable"])
 @pytest.mark.parametrize("cfg,n", [(2, 16), (2, 64), (2, 128), (3, 64), (5, 64)])
-def test_pinned_host_outputs_equal_device_outputs(pq, cfg, n):
-    """(2, 64), (2, 128): the per-column squaring cascade (p = 4 groups); (3, 64): p = 3 groups;
-    (5, 64): p = 6 columns in 4 uneven groups; (2, 16): below the split threshold."""
+def test_pinned_host_outputs_equal_device_outputs(pq, cfg, n, memory):
+    """(2, 64), (2, 128), (3, 64), (5, 64): the two-group squaring with the run-ahead lower half
+    (uneven halves at p = 3); (2, 16): below the split threshold.  Pageable buffers go through the
+    engine's pinned bounce, with the early copies drained while the call runs (capi.cpp)."""
     import torch
     from paper_2211_00696_b200.workloads import config
     w = config(cfg, n=n)
@@ -35,10 +37,16 @@ def test_pinned_host_outputs_equal_device_outputs(pq, cfg, n):
     o_pin = torch.full((1, w.p, w.N), np.nan, dtype=torch.float64).pin_memory()
     # three calls on the same context (warm workspaces and helper streams), the third into fresh
     # output buffers
+    def fresh(shape):
+        t = torch.full(shape, np.nan, dtype=torch.float64)
+        return t.pin_memory() if memory == "pinned" else t
+
+    if memory == "pageable":
+        b_pin = torch.from_numpy(b.copy())
     for k in range(3):
-        if k == 2:
-            o0_pin = torch.full((1, w.N), np.nan, dtype=torch.float64).pin_memory()
-            o_pin = torch.full((1, w.p, w.N), np.nan, dtype=torch.float64).pin_memory()
+        if k == 2 or memory == "pageable":
+            o0_pin = fresh((1, w.N))
+            o_pin = fresh((1, w.p, w.N))
         else:
             o0_pin.fill_(np.nan)
             o_pin.fill_(np.nan)
