@@ -69,6 +69,23 @@ inline std::vector<PhiColumns> scatter(const std::vector<double>& flat, int nb, 
     return out;
 }
 
+// The result columns, allocated (and value-initialised, as std::vector must) by several threads:
+// first-touching tens of MB from one thread costs more than the device computation at these sizes
+// (config 2: 67 MB, ~24 ms single-threaded on the B200 box's host vs ~3.4 ms for the phi call).
+inline std::vector<PhiColumns> alloc_columns(int nb, int p, int dim) {
+    std::vector<PhiColumns> out(static_cast<size_t>(nb));
+    for (auto& pc : out) {
+        pc.dim = dim;
+        pc.cols.resize(static_cast<size_t>(p));
+    }
+    const int count = nb * p;
+    const int threads = static_cast<long long>(dim) * count >= (1LL << 20) ? std::min(count, 8) : 1;
+    parallel_for(count, threads, [&](int k) {
+        out[static_cast<size_t>(k / p)].cols[static_cast<size_t>(k % p)] = std::vector<double>(static_cast<size_t>(dim));
+    });
+    return out;
+}
+
 inline pq_phi_request abi_request(const PhiRequest& r) {
     pq_phi_request c{};
     c.p = r.p;
@@ -142,34 +159,30 @@ inline std::vector<PhiColumns> phi_with_plan(const KroneckerSum& a, const std::v
     (void)threads;
     if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
     const int dim = a.dim();
-    const auto flat = detail::gather(bs, dim, mode == QuadKind::gauss_legendre ? "phi_fixed" : "phi_adaptive");
+    std::vector<const double*> ptrs;
+    for (const auto& b : bs) {
+        if (static_cast<int>(b.size()) != dim)
+            throw std::invalid_argument(std::string(mode == QuadKind::gauss_legendre ? "phi_fixed" : "phi_adaptive") +
+                                        ": vector length mismatch");
+        ptrs.push_back(b.data());
+    }
     const auto f = detail::flatten(a);
-    std::vector<double> out(bs.size() * static_cast<size_t>(std::max(p, 0)) * dim);
+    const int nb = static_cast<int>(bs.size());
+    std::vector<PhiColumns> out;
+    std::vector<double*> cols;
+    if (p >= 1) {
+        out = detail::alloc_columns(nb, p, dim);
+        for (auto& pc : out)
+            for (auto& c : pc.cols) cols.push_back(c.data());
+    }
     int pts = 0;
-    b200::check(pq_phi_with_plan(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
-                                 flat.data(), p, l, n, abi_kind(mode), eps, out.data(), &pts, PQ_HOST));
+    b200::check(pq_phi_with_plan_cols(b200::context(), a.order(), f.shape.data(), f.data.data(), nb, ptrs.data(), p, l,
+                                      n, abi_kind(mode), eps, cols.data(), &pts, PQ_HOST));
     if (points_used) *points_used = pts;
-    return detail::scatter(out, static_cast<int>(bs.size()), p, dim);
+    return out;
 }
 
 namespace detail {
-
-// The result columns, allocated (and value-initialised, as std::vector must) by several threads:
-// first-touching tens of MB from one thread costs more than the device computation at these sizes
-// (config 2: 67 MB, ~24 ms single-threaded on the B200 box's host vs ~3.4 ms for the phi call).
-inline std::vector<PhiColumns> alloc_columns(int nb, int p, int dim) {
-    std::vector<PhiColumns> out(static_cast<size_t>(nb));
-    for (auto& pc : out) {
-        pc.dim = dim;
-        pc.cols.resize(static_cast<size_t>(p));
-    }
-    const int count = nb * p;
-    const int threads = static_cast<long long>(dim) * count >= (1LL << 20) ? std::min(count, 8) : 1;
-    parallel_for(count, threads, [&](int k) {
-        out[static_cast<size_t>(k / p)].cols[static_cast<size_t>(k % p)] = std::vector<double>(static_cast<size_t>(dim));
-    });
-    return out;
-}
 
 // phiquadmv on the caller's vectors in place: b_m read from its own storage, phi_j written straight
 // into the PhiColumns vectors (pq_phiquadmv_cols) -- no flattening or scattering copies

@@ -153,6 +153,11 @@ PQ_API int pq_squaring_step(pq_ctx* ctx, int d, const int* shape, const double* 
 PQ_API int pq_phi_with_plan(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb,
                      const double* bs, int p, int l, int n, int kind, double eps, double* out,
                      int* points_used, int space);
+/* phiaction.hpp:277 phi_with_plan with the caller's vectors as they are: RHS m at bs[m], phi_{j+1}
+ * of RHS m to cols[m*p + j] (the drop-in headers' phi_with_plan and PhiEngine::apply). */
+PQ_API int pq_phi_with_plan_cols(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb,
+                                 const double* const* bs, int p, int l, int n, int kind, double eps,
+                                 double* const* cols, int* points_used, int space);
 /* phiaction.hpp:307 phiquadmv_multi (plans from alpha = infnorm_bound, beta = max ||b||_inf;
  * reads beta back from the device, i.e. synchronises once before planning). */
 PQ_API int pq_phiquadmv(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb, const double* bs,

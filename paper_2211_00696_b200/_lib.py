@@ -89,6 +89,8 @@ SIGNATURES = {
                                    C.c_double, vp, ip, C.c_int]),
     "pq_phiquadmv": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, vp, C.POINTER(PhiRequestC), vp,
                                C.POINTER(PhiInfoC), C.c_int]),
+    "pq_phi_with_plan_cols": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, C.POINTER(vp), C.c_int, C.c_int, C.c_int,
+                                        C.c_int, C.c_double, C.POINTER(vp), ip, C.c_int]),
     "pq_phiquadmv_cols": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, C.POINTER(vp), C.POINTER(PhiRequestC),
                                     C.POINTER(vp), C.POINTER(PhiInfoC), C.c_int]),
     "pq_phi_0p": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, vp, C.POINTER(PhiRequestC), vp, vp,

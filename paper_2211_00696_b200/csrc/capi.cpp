@@ -583,6 +583,43 @@ int pq_phi_with_plan(pq_ctx* c, int d, const int* shape, const double* factors, 
     });
 }
 
+int pq_phi_with_plan_cols(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* const* bs,
+                          int p, int l, int n, int kind, double eps, double* const* cols, int* points_used, int space) {
+    return guarded([&] {
+        need_ctx(c);
+        need(l >= 0, "phi_with_plan: need l >= 0");
+        check_kind(kind);
+        need(p >= 1, kind == PQ_GAUSS_LEGENDRE ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
+        if (kind == PQ_GAUSS_LEGENDRE) need(n + 1 >= 1, "gauss_legendre: need at least one point");
+        const long long N = dim_of(d, shape);
+        if (nb == 0) return;
+        need(bs != nullptr && cols != nullptr, "phi_with_plan: null vector list");
+        for (int m = 0; m < nb; ++m) need(bs[m] != nullptr, "phi_with_plan: null right-hand side");
+        for (int k = 0; k < nb * p; ++k) need(cols[k] != nullptr, "phi_with_plan: null output column");
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        double* db = ws(*c, "hin_b", static_cast<size_t>(nb) * N);
+        for (int m = 0; m < nb; ++m)
+            cuda_check(cudaMemcpyAsync(db + static_cast<size_t>(m) * N, bs[m], N * sizeof(double),
+                                       space == PQ_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c->stream),
+                       "gather b");
+        double* dout = ws(*c, "hout", static_cast<size_t>(nb) * p * N);
+        phi_with_plan_dev(*c, op, 1.0, nb, db, p, l, n, kind, eps, dout, points_used);
+        const size_t total = static_cast<size_t>(nb) * p * N;
+        if (space == PQ_HOST) {  // one D2H into a pinned bounce, then host threads fill the columns
+            double* bnc = pinned_bounce(*c, "cols", total);
+            cuda_check(cudaMemcpyAsync(bnc, dout, total * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
+            finish(*c, space);
+            host_scatter(cols, bnc, nb * p, static_cast<size_t>(N));
+        } else {
+            for (int k = 0; k < nb * p; ++k)
+                cuda_check(cudaMemcpyAsync(cols[k], dout + static_cast<size_t>(k) * N, N * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, c->stream),
+                           "scatter columns");
+        }
+    });
+}
+
 // b_list / col_list (pq_phiquadmv_cols): RHS m at b_list[m], phi_{j+1} of RHS m to col_list[m p + j]
 // instead of the contiguous bs / out
 static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,

@@ -154,3 +154,31 @@ def test_phiquadmv_cols_equals_contiguous(pq, space):
     assert np.array_equal(got, want)
     assert (info2.l, info2.n, info2.points) == (info.l, info.n, info.points)
     ctx.close()
+
+
+@pytest.mark.parametrize("kind", [0, 1])
+def test_phi_with_plan_cols_equals_contiguous(pq, kind):
+    """pq_phi_with_plan_cols (drop-in phi_with_plan / PhiEngine::apply) returns bitwise what
+    pq_phi_with_plan returns contiguously; nb = 2 pageable host vectors, both rules."""
+    from paper_2211_00696_b200.workloads import config
+    w = config(2, n=32)
+    a = pq.KroneckerSum(w.factors)
+    ctx = pq.Context(0)
+    d, sh, fac = a._abi()
+    nb, N, p, l, n = 2, w.N, w.p, 3, 8
+    mode = pq._lib.PQ_GAUSS_LEGENDRE if kind == 0 else pq._lib.PQ_CLENSHAW_CURTIS
+    bs = np.stack([w.rhs(30), w.rhs(31)])
+    want = np.empty((nb, p, N))
+    pts = C.c_int(0)
+    pq._lib.check(pq._lib.lib.pq_phi_with_plan(ctx.handle, d, sh, fac, nb, C.c_void_p(bs.ctypes.data), p, l, n, mode,
+                                               w.eps, C.c_void_p(want.ctypes.data), C.byref(pts), pq._lib.PQ_HOST))
+    b_sep = [np.ascontiguousarray(bs[m]) for m in range(nb)]
+    cols = [np.full(N, np.nan) for _ in range(nb * p)]
+    barr = (C.c_void_p * nb)(*[x.ctypes.data for x in b_sep])
+    carr = (C.c_void_p * (nb * p))(*[x.ctypes.data for x in cols])
+    pts2 = C.c_int(0)
+    pq._lib.check(pq._lib.lib.pq_phi_with_plan_cols(ctx.handle, d, sh, fac, nb, barr, p, l, n, mode, w.eps, carr,
+                                                    C.byref(pts2), pq._lib.PQ_HOST))
+    assert np.array_equal(np.stack(cols).reshape(nb, p, N), want)
+    assert pts2.value == pts.value
+    ctx.close()
