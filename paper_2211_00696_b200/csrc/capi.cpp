@@ -48,6 +48,8 @@ long long dim_of(int d, const int* shape) {
 // result copies (phi_0 during the squaring, the run-ahead column half) need pinned destinations, and
 // a pageable cudaMemcpy is a staged synchronous copy after the compute.  The bounce is copied to the
 // caller's memory by several host threads once the call has finished.
+constexpr size_t kBounceMin = size_t(1) << 20;  // doubles (8 MB)
+
 static double* pinned_bounce(pq_ctx& c, const char* name, size_t count) {
     auto& slot = c.pin_bounce[name];
     const size_t bytes = count * sizeof(double);
@@ -606,7 +608,7 @@ int pq_phi_with_plan_cols(pq_ctx* c, int d, const int* shape, const double* fact
         double* dout = ws(*c, "hout", static_cast<size_t>(nb) * p * N);
         phi_with_plan_dev(*c, op, 1.0, nb, db, p, l, n, kind, eps, dout, points_used);
         const size_t total = static_cast<size_t>(nb) * p * N;
-        if (space == PQ_HOST) {  // one D2H into a pinned bounce, then host threads fill the columns
+        if (space == PQ_HOST && total >= kBounceMin) {  // one D2H into a pinned bounce, host threads fill the columns
             double* bnc = pinned_bounce(*c, "cols", total);
             cuda_check(cudaMemcpyAsync(bnc, dout, total * sizeof(double), cudaMemcpyDeviceToHost, c->stream), "D2H");
             finish(*c, space);
@@ -614,8 +616,10 @@ int pq_phi_with_plan_cols(pq_ctx* c, int d, const int* shape, const double* fact
         } else {
             for (int k = 0; k < nb * p; ++k)
                 cuda_check(cudaMemcpyAsync(cols[k], dout + static_cast<size_t>(k) * N, N * sizeof(double),
-                                           cudaMemcpyDeviceToDevice, c->stream),
+                                           space == PQ_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice,
+                                           c->stream),
                            "scatter columns");
+            finish(*c, space);
         }
     });
 }
@@ -673,7 +677,9 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
     double* hc = pinned(out) ? out : nullptr;
     double* bounce0 = nullptr;
     double* bounce = nullptr;
-    if (space == PQ_HOST) {
+    // (only for results of 8 MB and more: below that the direct copies cost less than the bounce's
+    // host threads and first-use cudaMallocHost)
+    if (space == PQ_HOST && static_cast<size_t>(nb) * p * N >= kBounceMin) {
         if (out0 && !h0) h0 = bounce0 = pinned_bounce(*c, "phi0", static_cast<size_t>(nb) * N);
         if (col_list || (out && !hc)) hc = bounce = pinned_bounce(*c, "cols", static_cast<size_t>(nb) * p * N);
     }
@@ -711,10 +717,10 @@ static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* fact
         cuda_check(cudaMemcpyAsync(bounce, dout, static_cast<size_t>(nb) * p * N * sizeof(double), cudaMemcpyDeviceToHost,
                                    c->stream),
                    "D2H (bounce)");
-    if (col_list && space == PQ_DEVICE) {
+    if (col_list && !bounce) {
         for (int k = 0; k < nb * p; ++k)
             cuda_check(cudaMemcpyAsync(col_list[k], dout + static_cast<size_t>(k) * N, N * sizeof(double),
-                                       cudaMemcpyDeviceToDevice, c->stream),
+                                       space == PQ_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream),
                        "scatter columns");
     } else if (!bounce && !cols_copied) {
         finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
