@@ -4,23 +4,33 @@
 Default workload = BASELINE configs[1] (config 2): 3D advection-diffusion, n = 128 per dim
 (N = 2,097,152 DOF, fp64), p = 4, eps = 1e-10, adaptive Clenshaw-Curtis.  One "step" = one
 complete phi_0..phi_4 evaluation for one right-hand side (planner + node exponentials + node
-sweep + combine + l squaring steps + phi_0 exp-action), through the engine's C ABI.
+sweep + combine + l squaring steps + phi_0 exp-action), through the engine's C ABI.  Every step
+gets a FRESH seeded right-hand side (seed 1000 + i for step i, warm-up steps first), so nothing
+the host memoises per b survives from one step to the next.
 
-  value : actions/s with b already resident in HBM (device pointers), summed over ranks
+  value : actions/s with the step's b already resident in HBM (device pointers), all ranks
   e2e   : same metric through the public host-buffer call (pinned host b in, all p+1 result
           vectors back to pinned host memory inside the timed region)
-  roofline: FP64 DMMA GEMM launches (the mode products and expm products, >95% of the flops),
-          algorithmic flops / CUDA-event launch time vs the measured DMMA peak
-  cpu_baseline: the compiled reference (oracle/_ref) on a bounded sample
+  roofline: FP64 DMMA GEMM launches (mode products + expm products): EXECUTED flops / CUDA-event
+          launch time vs the measured DMMA peak; the dense-equivalent rate is reported beside it
+  cpu_baseline: the compiled reference (oracle/_ref) on this host: one complete call (config 2)
 
-Multi-GPU (torchrun, one process per GPU): every rank evaluates its own right-hand side
-(seed 1000 + rank) — independent units, no data-path collective (weak scaling); timing is the
-max over ranks of the device time.  `--impl reference` times the reference CPU implementation.
+`--impl reference` times the reference's own CPU path (oracle/_ref: the unmodified reference
+headers) with all host threads: for configs 1 and 2 every step is one COMPLETE reference
+phiquadmv + exp_action call on that step's right-hand side (no extrapolation); it never loads
+libpq_b200.so.  Config 4 (`--config 4`, ETDRK4 Allen-Cahn) reports ETDRK4 time steps/s.
+
+Multi-GPU (torchrun, one process per GPU): `--shard rhs` (default for N > 1 until the node
+sharded path is selected with `--shard nodes`): every rank evaluates its own right-hand sides --
+independent units, no data-path collective (weak scaling); timing is the max over ranks of the
+device time.
 """
 from __future__ import annotations
 
 import argparse
+import importlib.util
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -38,6 +48,17 @@ sys.path.insert(0, str(ROOT))
 # m8n8k4 f64 (SASS DMMA.8x8x4) register-only loop; MEASURED_PEAKS.json has no FP64 entry.
 DMMA_PEAK_TFLOPS = 36.95
 FP64_COPY_GBS = 6288.3
+METRIC = "phi_0..p(tau A)v actions/sec at N=n^d DOF"
+
+
+def load_workloads():
+    """paper_2211_00696_b200/workloads.py loaded by path: importing it through the package would
+    run the package __init__, which loads libpq_b200.so (the reference arm must not)."""
+    spec = importlib.util.spec_from_file_location("_pq_workloads", ROOT / "paper_2211_00696_b200" / "workloads.py")
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod  # dataclasses resolve their module through sys.modules
+    spec.loader.exec_module(mod)
+    return mod
 
 
 def load_peaks() -> dict:
@@ -191,88 +212,192 @@ def barrier(world: int) -> None:
         dist.barrier()
 
 
+
+
+# ------------------------------------------------------------------ shared config -----------
+
+def bench_config(w, args, world: int) -> dict:
+    """The `config` object BOTH arms print (identical dict for the same flags)."""
+    cfg = {"workload": w.name, "N": w.N, "d": w.d, "n": w.n, "p": w.p, "eps": w.eps, "tau": w.tau,
+           "rule": "cc" if w.mode else "gauss", "rhs_per_step": w.nb if args.config == 3 else 1,
+           "rhs": "fresh seeded N(0,1) b per step: seed 1000 + i (warm-up steps first), numpy PCG64",
+           "l2": "flushed between steps (256 MiB write, untimed)",
+           "parallelism": f"{args.shard}-sharded x{world}"}
+    if args.config == 4:
+        cfg.update({"rhs_per_step": 1, "rhs": "u0 ~ U[-0.9, 0.9] seed 2024; one step = one ETDRK4 time step (dt = tau)",
+                    "steps_per_integration": args.etd_steps})
+    return cfg
+
+
+def step_seeds(args, rank: int, nb: int) -> list:
+    """RHS seed indices per bench step (warm-up first), for this rank."""
+    per = args.warmup + args.steps
+    return [[(rank * per + i) * nb + k for k in range(nb)] for i in range(per)]
+
+
 # ------------------------------------------------------------------ CPU reference ------------
 
-def reference_sample(w, threads: int) -> dict:
-    """Bounded sample of the reference's own CPU path on this host (oracle/_ref, unmodified
-    reference headers): one reference exp_action (phi_0 = 3 Pade-13 expm + one exp-action, the
-    unit every phi column is built from), extrapolated to a full phi_0..phi_p call with the
-    reference's own structure: its node sweep runs `threads` nodes in parallel (ceil(q_level/T)
-    waves per CC level), its l*p squaring exp-actions and phi_0 are serial."""
-    from oracle.ref import Ref
-    ref = Ref()
-    b = w.rhs(0)
-    t0 = time.perf_counter()
-    ref.exp_action(w.factors, b)
-    t_ea = time.perf_counter() - t0
-    import math
-    alpha = ref.infnorm_bound(w.factors)
-    beta = float(np.max(np.abs(b)))
-    l, n, _ = ref.setup_quadrature(w.eps, w.p, alpha, beta, w.mode, 0.0, 1.0, w.d)
-    if w.mode == 1:
-        levels = [7, 6, 12]          # CC ladder 7 -> 13 -> 25 (the GPU run reports points_used = 25)
-    else:
-        levels = [n + 1]
-    waves = sum(math.ceil(q / max(1, threads)) for q in levels)
-    serial_units = waves + l * w.p + 1
-    t_call = serial_units * t_ea
-    return {"t_exp_action_s": t_ea, "plan_l": l, "plan_n": n, "waves": waves, "serial_exp_actions": serial_units,
-            "t_call_s": t_call}
-
-
-def reference_full_call(w, threads: int) -> dict:
-    """One complete reference phi_0..phi_p call on this host (oracle/_ref, unmodified reference
-    headers): phiquadmv (planner, node sweep over `threads` threads, serial squaring) plus
-    exp_action for phi_0 -- measured, not extrapolated.  ~23 s at config 2 on 16 cores."""
-    from oracle.ref import Ref
-    ref = Ref()
-    b = w.rhs(0)
+def reference_phi_call(ref, w, b, threads: int) -> dict:
+    """One complete reference phi_0..phi_p call (oracle/_ref, unmodified reference headers):
+    phiquadmv (planner, node sweep over `threads` threads, serial squaring, phiaction.hpp:307-346)
+    plus exp_action for phi_0 (kron.hpp:123-128) -- measured, not extrapolated."""
     t0 = time.perf_counter()
     _, info = ref.phiquadmv(w.factors, b[None, :], w.p, w.eps, w.mode, threads=threads)
     ref.exp_action(w.factors, b)
     return {"t_call_s": time.perf_counter() - t0, "plan": [info["l"], info["n"], info["points"]]}
 
 
+def reference_extrapolated(ref, w, b, threads: int) -> dict:
+    """Configs 3 and 5 only (a complete reference call takes 10 min .. hours): one reference
+    exp_action on the operator, scaled by the reference's own structure -- node-sweep waves over
+    `threads` threads + l*p serial squaring exp-actions + phi_0.  Labelled as an extrapolation."""
+    t0 = time.perf_counter()
+    ref.exp_action(w.factors, b)
+    t_ea = time.perf_counter() - t0
+    alpha = ref.infnorm_bound(w.factors)
+    beta = float(np.max(np.abs(b)))
+    l, n, _ = ref.setup_quadrature(w.eps, w.p, alpha, beta, w.mode, 0.0, 1.0, w.d)
+    waves = math.ceil((n + 1) / max(1, threads))
+    units = waves + l * w.p + 1
+    return {"t_call_s": units * t_ea, "t_exp_action_s": t_ea, "plan": [l, n, n + 1], "units": units}
+
+
 def run_reference(args, world, rank) -> None:
-    from paper_2211_00696_b200.workloads import config
     if rank != 0:
         return
-    w = config(args.config)
+    from oracle.ref import Ref
+    W = load_workloads()
+    w = W.config(args.config)
+    ref = Ref()
     threads = os.cpu_count() or 1
-    samples = []
-    for i in range(args.warmup + args.steps):
-        s = reference_sample(w, threads)
-        if i >= args.warmup:
-            samples.append(s)
-    t_call = statistics.median([s["t_call_s"] for s in samples])
-    v = 1.0 / t_call
-    s0 = samples[-1]
+    cfg = bench_config(w, args, world)
+    if args.config == 4:
+        # bounded sample: one reference integrate over `ref_etd_steps` ETDRK4 steps per bench step
+        u0 = W.allen_cahn_u0(w.N)
+        m = args.ref_etd_steps
+        times = []
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            ref.integrate(w.A, 1, u0, 0.0, m * w.tau, m, 3, eps=w.eps, threads=threads)
+            if i >= args.warmup:
+                times.append(time.perf_counter() - t0)
+        v = args.steps * m / sum(times)
+        sample = (f"per bench step: reference integrate (integrators.hpp:193) of {m} ETDRK4 steps (Allen-Cahn, "
+                  f"n={w.n}, tableau as ExpRKTableau, {threads} threads), measured; value = time steps/s")
+        unit = "ETDRK4 steps/s"
+        ms = sum(times) / len(times) * 1e3
+    else:
+        seeds = step_seeds(args, 0, 1)
+        times, plans = [], set()
+        full = args.config in (1, 2)
+        for i, s in enumerate(seeds):
+            b = w.rhs(s[0])
+            r = reference_phi_call(ref, w, b, threads) if full else reference_extrapolated(ref, w, b, threads)
+            if i >= args.warmup:
+                times.append(r["t_call_s"])
+                plans.add(tuple(r["plan"]))
+        nb = w.nb if args.config == 3 else 1
+        v = args.steps * nb / sum(times) if full else nb / statistics.median(times)
+        unit = "actions/s"
+        ms = sum(times) / len(times) * 1e3
+        sample = (f"every bench step one COMPLETE reference phiquadmv + exp_action call on that step's fresh b "
+                  f"({threads} threads for the node sweep; squaring serial as in the reference), measured; "
+                  f"plans (l, n, points) seen: {sorted(plans)}" if full else
+                  f"extrapolated: one reference exp_action per step scaled to {r['units']} serial exp-actions "
+                  f"(node waves at {threads} threads + l*p + phi_0) per RHS, x{nb} RHS")
     line = {
-        "impl": "reference", "metric": "phi_0..p(tau A)v actions/sec at N=n^d DOF", "value": v,
-        "unit": "actions/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": t_call * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic (seeded N(0,1) RHS, BASELINE operator)",
-        "config": {"workload": w.name, "N": w.N, "p": w.p, "eps": w.eps, "rule": "cc" if w.mode else "gauss"},
-        "cpu_baseline": {"value": v, "unit": "actions/s", "cores": threads, "kind": "reference",
-                         "sample": (f"per step: one reference exp_action on the {w.name} operator "
-                                    f"({s0['t_exp_action_s']:.2f} s, threads={threads}); call time extrapolated "
-                                    f"as {s0['serial_exp_actions']} serial exp-actions = {s0['waves']} node-sweep "
-                                    f"waves + l*p={s0['plan_l']}*{w.p} squaring + 1 phi_0")},
-        "e2e": {"value": v, "unit": "actions/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC if args.config != 4 else "ETDRK4 time steps/s (config 4)",
+        "value": v, "unit": unit, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak" if args.shard == "rhs" else "strong",
+        "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded inputs, BASELINE operator built in fp64)", "config": cfg,
+        "cpu_baseline": {"value": v, "unit": unit, "cores": threads, "kind": "reference", "sample": sample},
+        "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ------------------------------------------------------------------ GPU arm ------------------
 
-def run_ours(args, world, rank, local) -> None:
+def roofline_line(ctx, steps: int, ms_step_dev: float, w, kstats=None) -> dict:
+    """DMMA roofline of the GEMM launches recorded while profiling (ctx.gemm_stats), plus the HBM
+    roofline of the streaming kernels (ctx.kernel_stats) when available."""
+    g_launches, g_ms, g_flops, g_flops_dense = ctx.gemm_stats(reset=True)
+    if g_ms <= 0:
+        return None
+    ach = g_flops / (g_ms / 1e3) / 1e12
+    dense = g_flops_dense / (g_ms / 1e3) / 1e12
+    traffic, traffic_src = None, None
+    tpath = ROOT / "profiles" / "r02_gemm_traffic.json"
+    if not tpath.exists():
+        tpath = ROOT / "profiles" / "r01_gemm_traffic.json"
+    if w.name == "cfg2_advdiff3d_n128_cc_p4" and tpath.exists():
+        t = json.loads(tpath.read_text())
+        traffic = t["mean_dram_bytes_per_launch"]
+        traffic_src = (f"DRAM bytes/launch, mean of {len(t['launches'])} node-sweep mode products in {tpath.name} "
+                       f"(ncu --set full; algorithmic {t['algorithmic_bytes_per_launch']:.3g})")
+    ro = {"bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+          "frac": ach / DMMA_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
+          "kernel": "k_gemm (FP64 DMMA mode products + expm products), all launches of the step",
+          "achieved_note": ("EXECUTED flops: each CTA adds 2*rows*cols*k_issued to a device counter; exponential "
+                            "blocks below 2^-64 max|E| are skipped (DESIGN.md 3b) and not counted"),
+          "dense_equiv_tflops": dense, "dense_equiv_frac": dense / DMMA_PEAK_TFLOPS,
+          "dense_equiv_note": "2*M*N*K of the same launches (the reference's dense mode products) / the same time",
+          "launches_per_step": g_launches / steps, "gemm_ms_per_step": g_ms / steps,
+          "gemm_share_of_step": (g_ms / steps) / ms_step_dev if ms_step_dev > 0 else None,
+          "peak_source": "measured DMMA loop, profiles/fp64_peak_r01.jsonl (MEASURED_PEAKS.json has no FP64 entry)"}
+    if kstats:
+        hbm = load_peaks().get("hbm_gbs") or FP64_COPY_GBS
+        rows = {}
+        for name, s in sorted(kstats.items()):
+            if s["ms"] <= 0:
+                continue
+            gbs = s["bytes"] / (s["ms"] / 1e3) / 1e9
+            rows[name] = {"launches_per_step": s["launches"] / steps, "ms_per_step": s["ms"] / steps,
+                          "GB/s": gbs, "frac": gbs / hbm}
+        ro["hbm_kernels"] = {"peak_GBps": hbm, "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy, burst)",
+                             "kernels": rows, "bytes_note": "algorithmic bytes: every vector read/written once"}
+    return ro
+
+
+def cpu_baseline_line(w, args) -> dict:
+    threads = os.cpu_count() or 1
+    try:
+        from oracle.ref import Ref
+        ref = Ref()
+        if w.N <= 4_000_000 and args.config in (1, 2):
+            s = reference_phi_call(ref, w, w.rhs(0), threads)
+            sample = (f"one complete reference phi_0..phi_{w.p} call on this workload (phiquadmv + exp_action, "
+                      f"{threads} threads for the node sweep, squaring serial as in the reference), measured: "
+                      f"{s['t_call_s']:.1f} s, plan (l, n, points) = {tuple(s['plan'])}")
+        else:
+            s = reference_extrapolated(ref, w, w.rhs(0), threads)
+            sample = (f"one reference exp_action on this operator ({s['t_exp_action_s']:.2f} s), extrapolated to "
+                      f"{s['units']} serial exp-actions per phi_0..phi_{w.p} call")
+        return {"value": 1.0 / s["t_call_s"], "unit": "actions/s", "cores": threads, "kind": "reference",
+                "sample": sample}
+    except Exception as e:  # oracle missing on this box: say so
+        return {"value": None, "unit": "actions/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+
+
+def _pool(host_rows: list, nbytes_each: int, budget: int):
+    """How many distinct per-step inputs to keep: all of them when they fit `budget` bytes, else
+    cycle through as many as fit (at least 2, so consecutive steps never share b)."""
+    return max(2, min(len(host_rows), budget // max(1, nbytes_each)))
+
+
+def run_ours_phi(args, world, rank, local) -> None:
+    import ctypes as C
+    import threading
+
     import torch
     import paper_2211_00696_b200 as pq
-    from paper_2211_00696_b200.workloads import config
 
+    W = load_workloads()
     torch.cuda.set_device(local)
-    w = config(args.config)
-    nb = 1 if args.config != 3 else w.nb
+    w = W.config(args.config)
+    nb = w.nb if args.config == 3 else 1
+    N = w.N
     a = pq.KroneckerSum(w.factors)
     ctx = pq.Context(local)
     # one dedicated stream shared by torch (inputs, L2 flush, events) and the engine
@@ -280,33 +405,37 @@ def run_ours(args, world, rank, local) -> None:
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     req = pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode))
-    N = w.N
-    bs_host = np.stack([w.rhs(rank * nb + k) for k in range(nb)])
-    b_dev = torch.from_numpy(bs_host).cuda()
-    # pinned host buffers for the end-to-end leg
-    b_pin = torch.from_numpy(bs_host).pin_memory()
+    seeds = step_seeds(args, rank, nb)
+    per_step = nb * N * 8
+    free = torch.cuda.mem_get_info()[0]
+    npool = _pool(seeds, per_step, min(8 << 30, free // 6))
+    hosts = [np.stack([w.rhs(s) for s in seeds[i]]) for i in range(len(seeds))]
+    b_dev = [torch.from_numpy(hosts[i]).cuda() for i in range(npool)]
+    npin = _pool(seeds, per_step, 4 << 30)
+    b_pin = [torch.from_numpy(hosts[i]).pin_memory() for i in range(npin)]
     out0_pin = torch.empty((nb, N), dtype=torch.float64).pin_memory()
     out_pin = torch.empty((nb, w.p, N), dtype=torch.float64).pin_memory()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
 
     d, sh, fac = a._abi()
     rc = req._c()
-    import ctypes as C
     out0 = torch.empty((nb, N), dtype=torch.float64, device="cuda")
     out = torch.empty((nb, w.p, N), dtype=torch.float64, device="cuda")
     info = pq._lib.PhiInfoC()
+    plans = set()
 
-    def step_device():
-        pq._lib.check(pq._lib.lib.pq_phi_0p(ctx.handle, d, sh, fac, nb, C.c_void_p(b_dev.data_ptr()), C.byref(rc),
-                                  C.c_void_p(out0.data_ptr()), C.c_void_p(out.data_ptr()), C.byref(info),
-                                  pq._lib.PQ_DEVICE))
+    def step_device(i):
+        pq._lib.check(pq._lib.lib.pq_phi_0p(ctx.handle, d, sh, fac, nb, C.c_void_p(b_dev[i % npool].data_ptr()),
+                                            C.byref(rc), C.c_void_p(out0.data_ptr()), C.c_void_p(out.data_ptr()),
+                                            C.byref(info), pq._lib.PQ_DEVICE))
+        plans.add((info.l, info.n, info.points))
 
-    def step_host():
-        pq._lib.check(pq._lib.lib.pq_phi_0p(ctx.handle, d, sh, fac, nb, C.c_void_p(b_pin.data_ptr()), C.byref(rc),
-                                  C.c_void_p(out0_pin.data_ptr()), C.c_void_p(out_pin.data_ptr()), C.byref(info),
-                                  pq._lib.PQ_HOST))
+    def host_call(cx, i, bufs, inf):
+        pq._lib.check(pq._lib.lib.pq_phi_0p(cx.handle, d, sh, fac, nb, C.c_void_p(b_pin[i % npin].data_ptr()),
+                                            C.byref(rc), C.c_void_p(bufs[0].data_ptr()),
+                                            C.c_void_p(bufs[1].data_ptr()), C.byref(inf), pq._lib.PQ_HOST))
 
-    def timed(fn, k):
+    def timed(fn, first, k):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
         barrier(world)
         torch.cuda.synchronize()
@@ -314,54 +443,50 @@ def run_ours(args, world, rank, local) -> None:
         for i in range(k):
             flush.zero_()                       # L2 flush between steps (untimed)
             evs[i][0].record(stream)
-            fn()
+            fn(first + i)
             evs[i][1].record(stream)
         torch.cuda.synchronize()
         barrier(world)
-        launches = ctx.launches - l0
-        ms = sum(e0.elapsed_time(e1) for e0, e1 in evs)
-        return ms, launches
+        return sum(e0.elapsed_time(e1) for e0, e1 in evs), ctx.launches - l0
 
     free0 = torch.cuda.mem_get_info()[0]
-    for _ in range(args.warmup):
-        step_device()
+    for i in range(args.warmup):
+        step_device(i)
     torch.cuda.synchronize()
     ctx_bytes = max(1, free0 - torch.cuda.mem_get_info()[0])  # one context's workspace at this size
 
     with ClockSampler(local) as clk, NvmlSampler(local) as nvml:
-        ms_dev, launches = timed(step_device, args.steps)
+        ms_dev, launches = timed(step_device, args.warmup, args.steps)
     clocks = nvml.summary() or clk.summary()
     ms_dev_max = max_over_ranks(ms_dev, world)
     units = world * nb * args.steps
     value = units / (ms_dev_max / 1e3)
 
-    # roofline pass: same K steps with the DMMA GEMM launches bracketed by events
+    # roofline pass: the same K steps (same b's) with every DMMA GEMM and streaming kernel bracketed
     ctx.set_profiling(True)
     ctx.gemm_stats(reset=True)
-    for _ in range(args.steps):
+    ctx.kernel_stats(reset=True)
+    for i in range(args.steps):
         flush.zero_()
-        step_device()
-    g_launches, g_ms, g_flops, g_flops_dense = ctx.gemm_stats(reset=True)
+        step_device(args.warmup + i)
+    kst = ctx.kernel_stats(reset=True)
+    roof = roofline_line(ctx, args.steps, ms_dev / args.steps, w, kst)
     ctx.set_profiling(False)
 
     # end-to-end through the host-buffer call (H2D of b, D2H of phi_0..phi_p inside the region)
-    for _ in range(max(1, min(args.warmup, 2))):
-        step_host()
-    ms_e2e, _ = timed(step_host, args.steps)
+    for i in range(max(1, min(args.warmup, 2))):
+        host_call(ctx, i, (out0_pin, out_pin), info)
+    torch.cuda.synchronize()
+    ms_e2e, _ = timed(lambda i: host_call(ctx, i, (out0_pin, out_pin), info), args.warmup, args.steps)
     ms_e2e_max = max_over_ranks(ms_e2e, world)
     e2e_single = units / (ms_e2e_max / 1e3)
 
     # ... and with several host callers (the reference API is re-entrant; each caller has its own
-    # context, stream and pinned buffers), so one call's PCIe transfers and host-side syncs run
-    # under another call's DMMA work (tools/e2e_diag.py: 2 callers 3.34, 3: 3.13, 4: 2.94 ms per
-    # action vs 3.78 for one).  The K steps are split between the callers; the region spans from
-    # one start event to the last caller's end event.  Inputs are larger than L2 (b arrives by H2D,
-    # the workspaces are GB), so no flush between the overlapped calls.
-    import threading
-    # as many callers as the remaining HBM holds workspaces for (config 5: ~56 GB each -> fewer)
+    # context, stream and pinned result buffers), so one call's PCIe transfers and host-side syncs
+    # run under another call's DMMA work.  The K steps (each its own fresh b) are split between the
+    # callers; the region spans from one start event to the last caller's end event.  Inputs are
+    # larger than L2 (b arrives by H2D, the workspaces are GB), so no flush between the calls.
     ncall = max(1, min(args.e2e_callers, 1 + int(0.8 * torch.cuda.mem_get_info()[0] // ctx_bytes)))
-    # staggered stream priorities (numerically lower = higher): equal-priority callers tend to fall
-    # into lockstep (all compute, then all copy)
     pr = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
     lo_prio, hi_prio = max(pr), min(pr)
     prios = [hi_prio + (lo_prio - hi_prio) * k // max(1, ncall - 1) for k in range(ncall)]
@@ -370,29 +495,20 @@ def run_ours(args, world, rank, local) -> None:
         st = torch.cuda.Stream(priority=prios[k])
         cx = ctx if k == 0 else pq.Context(local)
         cx.set_stream(st.cuda_stream)
-        pins = (b_pin, out0_pin, out_pin) if k == 0 else (
-            torch.from_numpy(bs_host).pin_memory(), torch.empty((nb, N), dtype=torch.float64).pin_memory(),
-            torch.empty((nb, w.p, N), dtype=torch.float64).pin_memory())
-        callers.append((cx, st, pins))
-    info2 = pq._lib.PhiInfoC()
-
-    def host_call(cx, bufs, inf):
-        pq._lib.check(pq._lib.lib.pq_phi_0p(cx.handle, d, sh, fac, nb, C.c_void_p(bufs[0].data_ptr()), C.byref(rc),
-                                  C.c_void_p(bufs[1].data_ptr()), C.c_void_p(bufs[2].data_ptr()), C.byref(inf),
-                                  pq._lib.PQ_HOST))
-
-    for cx, st, bufs in callers:  # warm the second context (workspaces, caches)
-        host_call(cx, bufs, info2)
+        bufs = (out0_pin, out_pin) if k == 0 else (torch.empty((nb, N), dtype=torch.float64).pin_memory(),
+                                                   torch.empty((nb, w.p, N), dtype=torch.float64).pin_memory())
+        callers.append((cx, st, bufs))
+    for k, (cx, st, bufs) in enumerate(callers):  # warm the other contexts (workspaces, caches)
+        host_call(cx, k, bufs, pq._lib.PhiInfoC())
     torch.cuda.synchronize()
 
     def e2e_callers(k):
-        counts = [k // ncall + (1 if i < k % ncall else 0) for i in range(ncall)]
         start = torch.cuda.Event(enable_timing=True)
         ends = [torch.cuda.Event(enable_timing=True) for _ in callers]
+        mine = [[args.warmup + j for j in range(k) if j % ncall == i] for i in range(ncall)]
         errs = []
         barrier(world)
         torch.cuda.synchronize()
-        l0 = sum(cx.launches for cx, _, _ in callers)
         start.record(callers[0][1])
         for _, st, _ in callers[1:]:
             st.wait_event(start)
@@ -401,8 +517,8 @@ def run_ours(args, world, rank, local) -> None:
             cx, st, bufs = callers[i]
             try:
                 inf = pq._lib.PhiInfoC()
-                for _ in range(counts[i]):
-                    host_call(cx, bufs, inf)
+                for j in mine[i]:
+                    host_call(cx, j, bufs, inf)
                 ends[i].record(st)
             except Exception as e:  # pragma: no cover - surfaced below
                 errs.append(e)
@@ -416,73 +532,130 @@ def run_ours(args, world, rank, local) -> None:
             raise errs[0]
         torch.cuda.synchronize()
         barrier(world)
-        ms = max(start.elapsed_time(e) for e, c in zip(ends, counts) if c > 0)
-        return ms, sum(cx.launches for cx, _, _ in callers) - l0
+        return max(start.elapsed_time(e) for e, m in zip(ends, mine) if m)
 
-    ms_e2e2, _ = e2e_callers(args.steps)
-    ms_e2e2_max = max_over_ranks(ms_e2e2, world)
+    ms_e2e2_max = max_over_ranks(e2e_callers(args.steps), world)
     e2e_value = units / (ms_e2e2_max / 1e3)
 
-    fac_bytes = sum(f.size for f in w.factors) * 8
     line = {
-        "metric": "phi_0..p(tau A)v actions/sec at N=n^d DOF", "value": value, "unit": "actions/s",
+        "metric": METRIC, "value": value, "unit": "actions/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev_max / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded N(0,1) RHS per rank, BASELINE operator built in fp64)",
-        "config": {"workload": w.name, "N": N, "d": w.d, "n": w.n, "p": w.p, "eps": w.eps, "tau": w.tau,
-                   "rule": "cc" if w.mode else "gauss", "rhs_per_rank": nb,
-                   "plan": {"l": info.l, "n": info.n, "points": info.points},
-                   "l2": "flushed between steps (256 MiB write, untimed)", "parallelism": f"rhs-sharded x{world}"},
+        "data": "synthetic (fresh seeded N(0,1) RHS per step and rank, BASELINE operator built in fp64)",
+        "config": bench_config(w, args, world),
+        "plans": sorted(list(p) for p in plans),
         "gpu_launches": launches,
         "clocks": clocks,
-        "roofline": None, "cpu_baseline": None,
-        "e2e": {"value": e2e_value, "unit": "actions/s", "h2d_bytes_per_step": int(nb * N * 8 + fac_bytes),
+        "roofline": roof, "cpu_baseline": None,
+        "e2e": {"value": e2e_value, "unit": "actions/s", "h2d_bytes_per_step": int(nb * N * 8),
                 "d2h_bytes_per_step": int(nb * (w.p + 1) * N * 8), "callers": ncall,
                 "single_caller_value": e2e_single,
+                "distinct_rhs": {"device": npool, "pinned_host": npin},
                 "note": ("pq_phi_0p with pinned host b in and all p+1 vectors back every step; concurrent "
                          "host threads with their own contexts/streams overlap one call's PCIe transfers with "
-                         "another's compute; single_caller_value = one synchronous caller")},
+                         "another's compute; single_caller_value = one synchronous caller; the operator's "
+                         "factors are uploaded once (bit-identical factors are not re-copied) and not counted")},
     }
-    if g_ms > 0:
-        ach = g_flops / (g_ms / 1e3) / 1e12
-        # DRAM bytes per launch of the dominant kernel from the committed ncu --set full capture of
-        # this workload (profiles/r01_gemm_traffic.json); null for workloads without a capture
-        traffic, traffic_src = None, None
-        tpath = Path(__file__).resolve().parent / "profiles" / "r01_gemm_traffic.json"
-        if w.name == "cfg2_advdiff3d_n128_cc_p4" and tpath.exists():
-            t = json.loads(tpath.read_text())
-            traffic = t["mean_dram_bytes_per_launch"]
-            traffic_src = (f"bytes/launch, mean of {len(t['launches'])} mode products in {tpath.name} "
-                           f"(algorithmic {t['algorithmic_bytes_per_launch']:.3g})")
-        alg = g_flops_dense / (g_ms / 1e3) / 1e12
-        line["roofline"] = {"bound": "tensor", "achieved": alg, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                            "frac": alg / DMMA_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
-                            "executed_tflops": ach, "executed_frac": ach / DMMA_PEAK_TFLOPS,
-                            "kernel": "k_gemm (FP64 DMMA mode products + expm products)",
-                            "launches": g_launches, "gemm_ms_per_step": g_ms / args.steps,
-                            "flops_note": ("achieved = ALGORITHMIC flops (dense 2*M*N*K per mode product, SURVEY 8(d); "
-                                           "skipped work not credited) / GEMM time, which exceeds the DMMA peak because "
-                                           "the tiles skip exponential blocks below 2^-64 max|E| (DESIGN.md 3b); "
-                                           "executed_* = the FLOPs the DMMA tiles actually issued (device counters)"),
-                            "gemm_share_of_step": (g_ms / args.steps) / (ms_dev / args.steps),
-                            "peak_source": "measured DMMA loop, profiles/fp64_peak_r01.jsonl"}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_line(w, args)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_ours_etd(args, world, rank, local) -> None:
+    """Config 4: ETDRK4 on Allen-Cahn (n = 128, dt = 1e-3).  One bench step = one integrate() of
+    `--etd-steps` time steps (the whole config-4 run at the default 100) from u0 resident in HBM;
+    value = ETDRK4 time steps per second (all ranks: independent runs, weak)."""
+    import ctypes as C
+
+    import torch
+    import paper_2211_00696_b200 as pq
+
+    W = load_workloads()
+    torch.cuda.set_device(local)
+    w = W.config(4)
+    N, m = w.N, args.etd_steps
+    a = pq.KroneckerSum(w.A)
+    ctx = pq.Context(local)
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    ctx.set_stream(stream.cuda_stream)
+    u0h = W.allen_cahn_u0(N, seed=2024 + rank)
+    u0 = torch.from_numpy(u0h).cuda()
+    u0_pin = torch.from_numpy(u0h).pin_memory()
+    u_out = torch.empty(N, dtype=torch.float64, device="cuda")
+    u_pin = torch.empty(N, dtype=torch.float64).pin_memory()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    tab = pq.etdrk4_tableau()
+    tc, tkeep = tab._c()
+    src, skeep = pq.phiquad._source(("cubic", 1.0, -1.0))
+    base = pq.PhiRequest(eps=w.eps)._c()
+    d, sh, fac = a._abi()
+    calls = C.c_int()
+
+    def run(space):
+        ui, uo = (u0, u_out) if space == pq._lib.PQ_DEVICE else (u0_pin, u_pin)
+        pq._lib.check(pq._lib.lib.pq_integrate(ctx.handle, d, sh, fac, C.byref(src), C.c_void_p(ui.data_ptr()),
+                                               0.0, m * w.tau, m, C.byref(tc), C.byref(base),
+                                               C.c_void_p(uo.data_ptr()), C.byref(calls), space))
+
+    def timed(space, k):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        barrier(world)
+        torch.cuda.synchronize()
+        l0 = ctx.launches
+        for i in range(k):
+            flush.zero_()
+            evs[i][0].record(stream)
+            run(space)
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+        return sum(e0.elapsed_time(e1) for e0, e1 in evs), ctx.launches - l0
+
+    for _ in range(args.warmup):
+        run(pq._lib.PQ_DEVICE)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk, NvmlSampler(local) as nvml:
+        ms_dev, launches = timed(pq._lib.PQ_DEVICE, args.steps)
+    clocks = nvml.summary() or clk.summary()
+    ms_max = max_over_ranks(ms_dev, world)
+    value = world * args.steps * m / (ms_max / 1e3)
+    ctx.set_profiling(True)
+    ctx.gemm_stats(reset=True)
+    ctx.kernel_stats(reset=True)
+    for _ in range(args.steps):
+        flush.zero_()
+        run(pq._lib.PQ_DEVICE)
+    kst = ctx.kernel_stats(reset=True)
+    roof = roofline_line(ctx, args.steps * m, ms_dev / (args.steps * m), w, kst)
+    ctx.set_profiling(False)
+    run(pq._lib.PQ_HOST)
+    ms_e2e, _ = timed(pq._lib.PQ_HOST, args.steps)
+    e2e = world * args.steps * m / (max_over_ranks(ms_e2e, world) / 1e3)
+    line = {
+        "metric": "ETDRK4 time steps/s (config 4)", "value": value, "unit": "ETDRK4 steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (u0 ~ U[-0.9,0.9] seeded, Allen-Cahn operator built in fp64)",
+        "config": bench_config(w, args, world), "phi_calls_per_integration": calls.value,
+        "gpu_launches": launches, "clocks": clocks, "roofline": roof, "cpu_baseline": None,
+        "e2e": {"value": e2e, "unit": "ETDRK4 steps/s", "h2d_bytes_per_step": N * 8, "d2h_bytes_per_step": N * 8,
+                "note": "pq_integrate with pinned host u0 in and u back every bench step"},
+    }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
+            from oracle.ref import Ref
+            ref = Ref()
             threads = os.cpu_count() or 1
-            if w.N <= 4_000_000:  # a full reference call fits the 10-30 s budget (config 2: ~23 s)
-                s = reference_full_call(w, threads)
-                sample = (f"one complete reference phi_0..phi_{w.p} call on this workload (phiquadmv + exp_action, "
-                          f"{threads} threads for the node sweep, squaring serial as in the reference), measured: "
-                          f"{s['t_call_s']:.1f} s, plan (l, n, points) = {tuple(s['plan'])}")
-            else:
-                s = reference_sample(w, threads)
-                sample = (f"one reference exp_action on this operator ({s['t_exp_action_s']:.2f} s), extrapolated to "
-                          f"{s['serial_exp_actions']} serial exp-actions per phi_0..phi_{w.p} call "
-                          f"(node waves {s['waves']} at {threads} threads + l*p + phi_0; l={s['plan_l']})")
-            line["cpu_baseline"] = {"value": 1.0 / s["t_call_s"], "unit": "actions/s", "cores": threads,
-                                    "kind": "reference", "sample": sample}
-        except Exception as e:  # oracle missing on this box: say so
-            line["cpu_baseline"] = {"value": None, "unit": "actions/s", "cores": 0, "kind": "reference",
+            k = args.ref_etd_steps
+            t0 = time.perf_counter()
+            ref.integrate(w.A, 1, u0h, 0.0, k * w.tau, k, 3, eps=w.eps, threads=threads)
+            t = time.perf_counter() - t0
+            line["cpu_baseline"] = {"value": k / t, "unit": "ETDRK4 steps/s", "cores": threads, "kind": "reference",
+                                    "sample": f"reference integrate of {k} ETDRK4 steps, measured ({t:.1f} s)"}
+        except Exception as e:
+            line["cpu_baseline"] = {"value": None, "unit": "ETDRK4 steps/s", "cores": 0, "kind": "reference",
                                     "sample": f"unavailable: {e}"}
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -494,17 +667,23 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 5])
+    ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--shard", default="rhs", choices=["rhs"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-callers", type=int, default=4, help="concurrent host callers in the e2e leg")
+    ap.add_argument("--etd-steps", type=int, default=100, help="config 4: ETDRK4 steps per bench step")
+    ap.add_argument("--ref-etd-steps", type=int, default=2, help="config 4: reference ETDRK4 steps per sample")
     args = ap.parse_args()
-    world, rank, local = dist_init() if args.impl == "ours" else (int(os.environ.get("WORLD_SIZE", "1")),
-                                                                    int(os.environ.get("RANK", "0")), 0)
     if args.impl == "reference":
+        world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
         run_reference(args, world, rank)
+        return
+    world, rank, local = dist_init()
+    if args.config == 4:
+        run_ours_etd(args, world, rank, local)
     else:
-        run_ours(args, world, rank, local)
-    if world > 1 and args.impl == "ours":
+        run_ours_phi(args, world, rank, local)
+    if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()
 

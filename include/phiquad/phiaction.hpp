@@ -157,24 +157,26 @@ inline std::vector<PhiColumns> phi_with_plan(const KroneckerSum& a, const std::v
                                              int l, int n, QuadKind mode, double eps, int threads = 1,
                                              int* points_used = nullptr) {
     (void)threads;
+    // argument checks in the reference's order (phiaction.hpp:281-290 -> cached_rule -> phi_fixed_multi /
+    // phi_adaptive_multi); the C ABI repeats them, the vector lengths are only known here
     if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
+    const bool gauss = mode == QuadKind::gauss_legendre;
+    if (gauss && n + 1 < 1) throw std::invalid_argument("gauss_legendre: need at least one point");
+    if (p < 1) throw std::invalid_argument(gauss ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
+    if (!gauss && !(eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
     const int dim = a.dim();
     std::vector<const double*> ptrs;
     for (const auto& b : bs) {
         if (static_cast<int>(b.size()) != dim)
-            throw std::invalid_argument(std::string(mode == QuadKind::gauss_legendre ? "phi_fixed" : "phi_adaptive") +
-                                        ": vector length mismatch");
+            throw std::invalid_argument(std::string(gauss ? "phi_fixed" : "phi_adaptive") + ": vector length mismatch");
         ptrs.push_back(b.data());
     }
     const auto f = detail::flatten(a);
     const int nb = static_cast<int>(bs.size());
-    std::vector<PhiColumns> out;
+    std::vector<PhiColumns> out = detail::alloc_columns(nb, p, dim);
     std::vector<double*> cols;
-    if (p >= 1) {
-        out = detail::alloc_columns(nb, p, dim);
-        for (auto& pc : out)
-            for (auto& c : pc.cols) cols.push_back(c.data());
-    }
+    for (auto& pc : out)
+        for (auto& c : pc.cols) cols.push_back(c.data());
     int pts = 0;
     b200::check(pq_phi_with_plan_cols(b200::context(), a.order(), f.shape.data(), f.data.data(), nb, ptrs.data(), p, l,
                                       n, abi_kind(mode), eps, cols.data(), &pts, PQ_HOST));
@@ -212,23 +214,24 @@ inline std::vector<PhiColumns> phiquadmv_ptrs(const KroneckerSum& a, const std::
 
 inline std::vector<PhiColumns> phiquadmv_multi(const KroneckerSum& a, const std::vector<std::vector<double>>& bs,
                                                const PhiRequest& req, PhiInfo* info = nullptr) {
+    // reference order (phiaction.hpp:307-346): p, then the pinned l, then phi_with_plan's checks --
+    // eps for the adaptive rule and the vector lengths in phi_fixed_multi / phi_adaptive_multi
     if (req.p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
-    if (bs.empty()) throw std::invalid_argument("phiquadmv: need at least one right-hand side");
+    if (req.l.has_value() && *req.l < 0) throw std::invalid_argument("phiquadmv: need l >= 0");
+    const bool gauss = req.mode == QuadKind::gauss_legendre;
+    if (!gauss && !(req.eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
     std::vector<const double*> ptrs;
     for (const auto& b : bs) {
         if (static_cast<long long>(b.size()) != static_cast<long long>(a.dim()))
-            throw std::invalid_argument("phiquadmv: vector length mismatch");
+            throw std::invalid_argument(std::string(gauss ? "phi_fixed" : "phi_adaptive") + ": vector length mismatch");
         ptrs.push_back(b.data());
     }
-    return detail::phiquadmv_ptrs(a, ptrs, req, info);
+    return detail::phiquadmv_ptrs(a, ptrs, req, info);  // no right-hand sides: the plan only, no columns
 }
 
 inline PhiColumns phiquadmv(const KroneckerSum& a, const std::vector<double>& b, const PhiRequest& req,
                             PhiInfo* info = nullptr) {
-    if (req.p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
-    if (static_cast<long long>(b.size()) != static_cast<long long>(a.dim()))
-        throw std::invalid_argument("phiquadmv: vector length mismatch");
-    return std::move(detail::phiquadmv_ptrs(a, {b.data()}, req, info).front());
+    return std::move(phiquadmv_multi(a, {b}, req, info).front());
 }
 
 /// sum_j phi_j(A) b_j in one quadrature sweep (no scaling/squaring).

@@ -83,6 +83,11 @@ PQ_API int pq_ctx_gemm_stats(pq_ctx* ctx, int reset, uint64_t* launches, double*
 /* Same launches: 2*M*N*K per batch entry, i.e. the dense mode-product work of the reference's
  * algorithm (kron.hpp:65-108) without any block skipped. */
 PQ_API int pq_ctx_gemm_dense_flops(pq_ctx* ctx, int reset, double* flops);
+/* With profiling on, every streaming (HBM-bound) kernel launch -- node combines, squaring
+ * combinations, column statistics, ETD stage kernels -- is bracketed by events on its stream.
+ * Returns (synchronising) a JSON object {"<kernel>": {"launches", "ms", "bytes"}} with the summed
+ * device time and ALGORITHMIC bytes (each vector read / written once) per kernel tag. */
+PQ_API int pq_ctx_kernel_stats(pq_ctx* ctx, int reset, const char** json);
 /* With profiling on, phase boundaries are marked (device event + host clock).  Returns (and
  * clears, synchronising) a JSON array [{"mark","gpu_us","host_us"}] relative to the first mark. */
 PQ_API int pq_ctx_timeline(pq_ctx* ctx, const char** json);

@@ -4,6 +4,8 @@
 #include "pq_b200.h"
 
 #include <cmath>
+#include <chrono>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -168,6 +170,7 @@ int pq_ctx_destroy(pq_ctx* c) {
         cudaStreamSynchronize(c->stream);
         for (auto& kv : c->bufs)
             if (kv.second.p) cudaFree(kv.second.p);
+        for (void* p : c->graveyard) cudaFree(p);
         if (c->arena.host) cudaFreeHost(c->arena.host);
         if (c->arena.dev) cudaFree(c->arena.dev);
         if (c->arena.done) cudaEventDestroy(c->arena.done);
@@ -194,6 +197,13 @@ int pq_ctx_destroy(pq_ctx* c) {
             cudaStreamDestroy(s);
         }
         for (auto e : c->ev_sqg) cudaEventDestroy(e);
+        for (auto e : c->ev_early) cudaEventDestroy(e);
+        for (auto& m : c->marks) cudaEventDestroy(m.ev);
+        for (auto& r : c->krecs) {
+            cudaEventDestroy(r.a);
+            cudaEventDestroy(r.b);
+        }
+        if (c->ev_latefork) cudaEventDestroy(c->ev_latefork);
         if (c->ev_beta) cudaEventDestroy(c->ev_beta);
         if (c->ev_cc) cudaEventDestroy(c->ev_cc);
         if (c->ev_fac) cudaEventDestroy(c->ev_fac);
@@ -259,6 +269,7 @@ int pq_ctx_release_workspace(pq_ctx* c) {
     return guarded([&] {
         need_ctx(c);
         cuda_check(cudaStreamSynchronize(c->stream), "sync");
+        free_graveyard(*c);
         for (auto& kv : c->bufs)
             if (kv.second.p) cudaFree(kv.second.p);
         c->bufs.clear();
@@ -314,6 +325,27 @@ int pq_ctx_timeline(pq_ctx* c, const char** json) {
         c->marks.clear();
         c->marks_json = s;
         *json = c->marks_json.c_str();
+    });
+}
+
+int pq_ctx_kernel_stats(pq_ctx* c, int reset, const char** json) {
+    return guarded([&] {
+        need_ctx(c);
+        prof_collect(*c);
+        std::string s = "{";
+        bool first = true;
+        for (const auto& kv : c->kstats) {
+            char buf[320];
+            std::snprintf(buf, sizeof buf, "%s\"%s\":{\"launches\":%llu,\"ms\":%.6f,\"bytes\":%.17g}", first ? "" : ",",
+                          kv.first.c_str(), static_cast<unsigned long long>(kv.second.launches), kv.second.ms,
+                          kv.second.bytes);
+            s += buf;
+            first = false;
+        }
+        s += "}";
+        if (reset) c->kstats.clear();
+        c->marks_json = s;
+        if (json) *json = c->marks_json.c_str();
     });
 }
 
@@ -565,16 +597,30 @@ int pq_squaring_step(pq_ctx* c, int d, const int* shape, const double* exps, int
     });
 }
 
+// phi_with_plan's argument checks in the reference's order (phiaction.hpp:277-290 -> cached_rule
+// -> phi_fixed_multi :134-139 / phi_adaptive_multi :156-166)
+static void plan_checks(int l, int n, int p, int kind, double eps) {
+    need(l >= 0, "phi_with_plan: need l >= 0");
+    check_kind(kind);
+    if (kind == PQ_GAUSS_LEGENDRE) {
+        need(n + 1 >= 1, "gauss_legendre: need at least one point");
+        need(p >= 1, "phi_fixed: need p >= 1");
+    } else {
+        need(p >= 1, "phi_adaptive: need p >= 1");
+        need(eps > 0.0, "phi_adaptive: need eps > 0");
+    }
+}
+
 int pq_phi_with_plan(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs, int p, int l,
                      int n, int kind, double eps, double* out, int* points_used, int space) {
     return guarded([&] {
         need_ctx(c);
-        need(l >= 0, "phi_with_plan: need l >= 0");
-        check_kind(kind);
-        need(p >= 1, kind == PQ_GAUSS_LEGENDRE ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
-        if (kind == PQ_GAUSS_LEGENDRE) need(n + 1 >= 1, "gauss_legendre: need at least one point");
+        plan_checks(l, n, p, kind, eps);
         const long long N = dim_of(d, shape);
-        if (nb == 0) return;
+        if (nb == 0) {  // the reference still reports the rule size (phiaction.hpp:282-290)
+            if (points_used) *points_used = kind == PQ_GAUSS_LEGENDRE ? n + 1 : 13;
+            return;
+        }
         arena_begin(*c);
         DevOp op = upload_op(*c, d, shape, factors, "factors");
         const double* db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
@@ -589,12 +635,12 @@ int pq_phi_with_plan_cols(pq_ctx* c, int d, const int* shape, const double* fact
                           int p, int l, int n, int kind, double eps, double* const* cols, int* points_used, int space) {
     return guarded([&] {
         need_ctx(c);
-        need(l >= 0, "phi_with_plan: need l >= 0");
-        check_kind(kind);
-        need(p >= 1, kind == PQ_GAUSS_LEGENDRE ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
-        if (kind == PQ_GAUSS_LEGENDRE) need(n + 1 >= 1, "gauss_legendre: need at least one point");
+        plan_checks(l, n, p, kind, eps);
         const long long N = dim_of(d, shape);
-        if (nb == 0) return;
+        if (nb == 0) {  // the reference still reports the rule size (phiaction.hpp:282-290)
+            if (points_used) *points_used = kind == PQ_GAUSS_LEGENDRE ? n + 1 : 13;
+            return;
+        }
         need(bs != nullptr && cols != nullptr, "phi_with_plan: null vector list");
         for (int m = 0; m < nb; ++m) need(bs[m] != nullptr, "phi_with_plan: null right-hand side");
         for (int k = 0; k < nb * p; ++k) need(cols[k] != nullptr, "phi_with_plan: null output column");
@@ -626,16 +672,93 @@ int pq_phi_with_plan_cols(pq_ctx* c, int d, const int* shape, const double* fact
 
 // b_list / col_list (pq_phiquadmv_cols): RHS m at b_list[m], phi_{j+1} of RHS m to col_list[m p + j]
 // instead of the contiguous bs / out
+static void run_phiquadmv_impl(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
+                               const pq_phi_request* req, double* out0, double* out, pq_phi_info* info, int space,
+                               const double* const* b_list, double* const* col_list);
+
+// PQ_SLOWLOG=<ms>: every phiquadmv-family call records its phase marks (device events + host
+// clock, like PQ_TRACE); a call whose host wall time exceeds <ms> prints its timeline to stderr
+// (diagnostics for latency outliers such as the acceptance gate's criterion 7).
+static double slowlog_ms() {
+    static const double v = [] {
+        const char* e = std::getenv("PQ_SLOWLOG");
+        return e ? std::atof(e) : 0.0;
+    }();
+    return v;
+}
+
 static void run_phiquadmv(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
                           const pq_phi_request* req, double* out0, double* out, pq_phi_info* info, int space,
                           const double* const* b_list = nullptr, double* const* col_list = nullptr) {
+    const double thr = slowlog_ms();
+    if (thr <= 0.0 || !c) {
+        run_phiquadmv_impl(c, d, shape, factors, nb, bs, req, out0, out, info, space, b_list, col_list);
+        return;
+    }
+    const bool was = c->trace;
+    c->trace = true;
+    for (auto& m : c->marks) cudaEventDestroy(m.ev);
+    c->marks.clear();
+    const auto t0 = std::chrono::steady_clock::now();
+    try {
+        run_phiquadmv_impl(c, d, shape, factors, nb, bs, req, out0, out, info, space, b_list, col_list);
+    } catch (...) {
+        c->trace = was;
+        throw;
+    }
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    c->trace = was;
+    if (ms > thr && !c->marks.empty()) {
+        cudaStreamSynchronize(c->stream);
+        std::string s;
+        for (size_t i = 0; i < c->marks.size(); ++i) {
+            float g = 0.f;
+            cudaEventElapsedTime(&g, c->marks[0].ev, c->marks[i].ev);
+            char buf[200];
+            std::snprintf(buf, sizeof buf, " %s@gpu%.0fus/host%.0fus", c->marks[i].name.c_str(), g * 1000.0,
+                          c->marks[i].host_us - c->marks[0].host_us);
+            s += buf;
+        }
+        std::fprintf(stderr, "[pq slow call] %.2f ms (N=%lld, nb=%d, p=%d):%s\n", ms, dim_of(d, shape), nb,
+                     req ? req->p : 0, s.c_str());
+    }
+    if (!was) {
+        for (auto& m : c->marks) cudaEventDestroy(m.ev);
+        c->marks.clear();
+    }
+}
+
+static void run_phiquadmv_impl(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
+                               const pq_phi_request* req, double* out0, double* out, pq_phi_info* info, int space,
+                               const double* const* b_list, double* const* col_list) {
     need_ctx(c);
     need(req != nullptr, "phiquadmv: null request");
     need(req->p >= 1, "phiquadmv: need p >= 1");
     check_kind(req->mode);
     const long long N = dim_of(d, shape);
-    need(nb >= 1, "phiquadmv: need at least one right-hand side");
+    need(nb >= 0, "phiquadmv: negative right-hand-side count");
     const int p = req->p;
+    if (nb == 0) {  // reference: beta = 0 plans l = 0 (or the pinned l) and returns no columns
+        double alpha = 0.0;
+        if (pq_infnorm_bound(d, shape, factors, &alpha) != PQ_OK) throw std::invalid_argument(last_error_slot());
+        int l = 0, n = req->mode == PQ_GAUSS_LEGENDRE ? 2 : 4;
+        if (req->has_l) {
+            need(req->l >= 0, "phiquadmv: need l >= 0");
+            l = req->l;
+        }
+        plan_checks(l, n, p, req->mode, req->eps);
+        if (info) {
+            info->l = l;
+            info->n = n;
+            info->points = req->mode == PQ_GAUSS_LEGENDRE ? n + 1 : 13;
+            info->mode = req->mode;
+            info->planned = req->has_l ? 0 : 1;
+            info->alpha = alpha;
+            info->beta = 0.0;
+            info->plan_cost = pqb::Cost{req->c1, req->c2, d}(n, l, p);
+        }
+        return;
+    }
     mark(*c, "call");
     arena_begin(*c);
     DevOp op = upload_op(*c, d, shape, factors, "factors");
@@ -762,7 +885,7 @@ int pq_phiquadmv(pq_ctx* c, int d, const int* shape, const double* factors, int 
 int pq_phiquadmv_cols(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* const* bs,
                       const pq_phi_request* req, double* const* cols, pq_phi_info* info, int space) {
     return guarded([&] {
-        need(bs != nullptr && cols != nullptr, "phiquadmv: null vector list");
+        need(nb == 0 || (bs != nullptr && cols != nullptr), "phiquadmv: null vector list");
         run_phiquadmv(c, d, shape, factors, nb, nullptr, req, nullptr, nullptr, info, space, bs, cols);
     });
 }

@@ -36,19 +36,32 @@ static size_t budget_bytes(pq_ctx& c) {
     return static_cast<size_t>(c.ws_limit);
 }
 
+void free_graveyard(pq_ctx& c) {
+    if (c.graveyard.empty()) return;
+    cuda_check(cudaDeviceSynchronize(), "sync before workspace free");
+    for (void* p : c.graveyard) cudaFree(p);
+    c.graveyard.clear();
+}
+
 void* ws_bytes(pq_ctx& c, const std::string& name, size_t bytes) {
     DevBuf& b = c.bufs[name];
     if (b.bytes >= bytes && b.p) return b.p;
-    if (b.p) {
-        cuda_check(cudaStreamSynchronize(c.stream), "sync before realloc");
-        cudaFree(b.p);
-        b.p = nullptr;
-        b.bytes = 0;
-    }
+    // the old buffer may still be read by enqueued work: retire it without a sync (freed at
+    // release / destroy / an allocation failure, see pq_ctx::graveyard)
+    if (b.p) c.graveyard.push_back(b.p);
+    b.p = nullptr;
+    b.bytes = 0;
     const size_t want = std::max<size_t>(bytes, 256);
+    mark(c, ("ws_grow:" + name).c_str());
     cudaError_t e = cudaMalloc(&b.p, want);
+    if (e != cudaSuccess && !c.graveyard.empty()) {
+        cudaGetLastError();
+        free_graveyard(c);
+        e = cudaMalloc(&b.p, want);
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
+        b.p = nullptr;
         throw CudaError("device workspace '" + name + "': cannot allocate " + std::to_string(want >> 20) + " MiB");
     }
     b.bytes = want;
@@ -145,7 +158,42 @@ int gemm(pq_ctx& c, const GemmArgs& g) {
     return k;
 }
 
+KernelProbe::KernelProbe(pq_ctx& ctx, const char* t, double b) : c(ctx), tag(t), bytes(b) {
+    if (!c.profiling) return;
+    s = c.stream;
+    cuda_check(cudaEventCreate(&a), "probe event");
+    cuda_check(cudaEventRecord(a, s), "probe record");
+}
+
+KernelProbe::~KernelProbe() {
+    if (!a) return;
+    cudaEvent_t b = nullptr;
+    if (cudaEventCreate(&b) != cudaSuccess || cudaEventRecord(b, s) != cudaSuccess) {
+        cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+        return;
+    }
+    c.krecs.push_back({tag, a, b, bytes});
+}
+
+static void kstats_collect(pq_ctx& c) {
+    if (c.krecs.empty()) return;
+    cuda_check(cudaDeviceSynchronize(), "probe sync");  // probes may sit on side streams
+    for (const auto& r : c.krecs) {
+        float ms = 0.f;
+        cuda_check(cudaEventElapsedTime(&ms, r.a, r.b), "probe elapsed");
+        auto& st = c.kstats[r.tag];
+        st.launches += 1;
+        st.ms += ms;
+        st.bytes += r.bytes;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    c.krecs.clear();
+}
+
 void prof_collect(pq_ctx& c) {
+    kstats_collect(c);
     if (c.ev_used == 0) return;
     cuda_check(cudaStreamSynchronize(c.stream), "prof sync");
     std::vector<unsigned long long> executed(c.ev_used / 2);
@@ -1104,6 +1152,7 @@ static void node_sweep(pq_ctx& c, const DevOp& op, const double* const* E, const
             for (int k = 0; k < op.d; ++k) Ec[k] = E[k] + a0 * Es[k];
             band_at(a0, Bc);
             mode_chain(c, op.d, op.n, Ec, Es, bs + m * N, 0, V, N, cnt, Epilogue{}, "chain", Bc);
+            KernelProbe kp(c, "k_combine", 8.0 * N * (cnt + p + ((zero && a0 == 0) ? 0 : p)));
             launch_combine(N, p, cnt, V, N, slot_dev, coef_dev + static_cast<size_t>(a0) * p,
                            acc + static_cast<long long>(m) * p * N, N, (zero && a0 == 0) ? 1 : 0, c.stream);
             count_launch(c);
@@ -1189,6 +1238,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         const int* sl_dev = static_cast<const int*>(arena_push(c, slots.data(), slots.size() * sizeof(int)));
         arena_flush(c);
         for (int m = 0; m < nb; ++m) {
+            KernelProbe kp(c, "k_combine", 8.0 * N * (r.size() + p));
             launch_combine(N, p, r.size(), pool + static_cast<long long>(m) * N, static_cast<long long>(nb) * N, sl_dev,
                            coef_dev, acc + static_cast<long long>(m) * p * N, N, 1, c.stream);
             count_launch(c);
@@ -1218,7 +1268,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
                 }
                 cuda_check(cudaMemcpy(np, b.p, static_cast<size_t>(used) * nb * N * sizeof(double), cudaMemcpyDeviceToDevice),
                            "pool copy");
-                cudaFree(b.p);
+                c.graveyard.push_back(b.p);
                 b.p = np;
                 b.bytes = want;
             }
@@ -1310,6 +1360,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             arena_flush(c);
             cuda_check(cudaMemsetAsync(stats, 0, sizeof(double) * 2 * nb * p, c.stream), "cc stats zero");
             for (int m = 0; m < nb; ++m) {
+                KernelProbe kp(c, "k_node_combine_ring", 8.0 * N * (fine.size() + p + (level == 1 ? 0 : p)));
                 launch_combine_stats(N, p, fine.size(), pool + static_cast<long long>(m) * N, static_cast<long long>(nb) * N,
                                      sl_dev, cf_dev, cc_dev,
                                      level == 1 ? nullptr : accs[cur] + static_cast<long long>(m) * p * N,
@@ -1318,6 +1369,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             }
         } else {
             combine_all(fine, fine_slot, accs[nxt]);
+            KernelProbe kp(c, "k_colstats", 16.0 * N * nb * p);
             launch_colstats(N, nb * p, accs[nxt], accs[cur], stats, c.stream);
             count_launch(c);
         }
@@ -1504,6 +1556,7 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
                     if (step >= 1)
                         for (int h = 0; h < g; ++h)
                             cuda_check(cudaStreamWaitEvent(c.stream, ev(h, step - 1), 0), "sq wait (columns)");
+                    KernelProbe kp(c, "k_sq_combine2", 8.0 * N * (2 * (c1 - c0) + c1));
                     launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, c0, c1);
                     count_launch(c);
                     cuda_check(cudaEventRecord(ev(g, step), c.stream), "sq rec");
@@ -1547,6 +1600,7 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
             if (chain && band_in && band_in[k]) Bd[k] = band_in[k] + step * band_row_blocks(op.n[k]);
         }
         mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, Epilogue{}, "chain", Bd);
+        KernelProbe kp(c, "k_sq_combine2", 8.0 * N * nb * 3 * p);
         launch_sq_combine(N, p, nb, nxt, cur, coef_dev, c.stream);
         count_launch(c);
         std::swap(cur, nxt);
@@ -1783,11 +1837,13 @@ void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const doub
             const int gc = std::min(kMixOut, q - g * kMixOut);
             const int take = std::min(gc - in_g, cnt - a);
             if (in_g == 0 && take == gc) {
+                KernelProbe kp(c, "k_combine(lincomb mix)", 8.0 * N * (p + gc));
                 launch_combine(N, gc, p, bs, N, bsl, mixT_dev + mix_off[static_cast<size_t>(g)], M + static_cast<long long>(a) * N,
                                N, 1, c.stream);
                 count_launch(c);
             } else {
                 for (int t = 0; t < take; ++t) {  // a chunk boundary inside a group: one node at a time
+                    KernelProbe kp(c, "k_combine(lincomb mix)", 8.0 * N * (p + 1));
                     launch_combine(N, 1, p, bs, N, bsl, mix_dev + static_cast<size_t>(node + t) * p,
                                    M + static_cast<long long>(a + t) * N, N, 1, c.stream);
                     count_launch(c);
@@ -1802,6 +1858,7 @@ void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const doub
             Bc[k] = px.node_band[k] ? px.node_band[k] + a0 * band_row_blocks(op.n[k]) : nullptr;
         }
         mode_chain(c, op.d, op.n, Ec, Es, M, N, V, N, cnt, Epilogue{}, "chain", Bc);
+        KernelProbe kp(c, "k_combine(lincomb nodes)", 8.0 * N * (cnt + 1 + (a0 == 0 ? 0 : 1)));
         launch_combine(N, 1, cnt, V, N, vsl, w_dev + a0, out, N, a0 == 0 ? 1 : 0, c.stream);
         count_launch(c);
     }

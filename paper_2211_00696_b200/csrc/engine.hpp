@@ -49,6 +49,10 @@ struct pq_ctx {
     uint64_t launches = 0;
     uint64_t ws_limit = 0;
     std::map<std::string, pqb::DevBuf> bufs;
+    // workspace buffers replaced by a larger one: freed only when the context releases its workspace
+    // (or an allocation fails), never inside a call -- cudaFree of a large buffer is a device-wide
+    // synchronisation that took 20-60 ms on the B200 (the acceptance gate's criterion-7 outlier)
+    std::vector<void*> graveyard;
     pqb::ParamArena arena;
     int* d_err = nullptr;        // device error flag (singular LU)
     double* h_small = nullptr;   // pinned readback scratch
@@ -131,6 +135,19 @@ struct pq_ctx {
     double prof_flops_dense = 0.0;            // 2 M N K Z of the same launches
     unsigned long long* d_flops = nullptr;    // per-launch executed-flop counters (profiling)
     uint64_t prof_launches = 0;
+    // streaming (HBM-bound) kernel launches while profiling: tag, events around the launch on its
+    // stream, algorithmic bytes (every vector read / written once); folded into kstats on collect
+    struct KRec {
+        const char* tag;
+        cudaEvent_t a, b;
+        double bytes;
+    };
+    std::vector<KRec> krecs;
+    struct KStat {
+        uint64_t launches = 0;
+        double ms = 0.0, bytes = 0.0;
+    };
+    std::map<std::string, KStat> kstats;
 };
 
 namespace pqb {
@@ -189,13 +206,27 @@ int guarded(F&& f) {
 // ---- context helpers (engine.cpp) ----
 double* ws(pq_ctx& c, const std::string& name, size_t count);          // device doubles
 void* ws_bytes(pq_ctx& c, const std::string& name, size_t bytes);
+void free_graveyard(pq_ctx& c);  // device-synchronising
 void arena_begin(pq_ctx& c);
 const void* arena_push(pq_ctx& c, const void* data, size_t bytes);     // returns device address
 void arena_flush(pq_ctx& c);
 void count_launch(pq_ctx& c, int n = 1);
 // launch_gemm + launch counting + (when profiling) per-launch events and algorithmic flops
 int gemm(pq_ctx& c, const GemmArgs& g);
-void prof_collect(pq_ctx& c);  // syncs, folds recorded events into prof_ms/prof_flops
+void prof_collect(pq_ctx& c);  // syncs, folds recorded events into prof_ms/prof_flops (and kstats)
+// Brackets one streaming-kernel launch on c.stream with events while profiling (no-op otherwise):
+// `KernelProbe kp(c, "k_combine", bytes);` before the launch, the scope end records the stop.
+struct KernelProbe {
+    pq_ctx& c;
+    cudaStream_t s = nullptr;
+    cudaEvent_t a = nullptr;
+    const char* tag;
+    double bytes;
+    KernelProbe(pq_ctx& ctx, const char* t, double b);
+    ~KernelProbe();
+    KernelProbe(const KernelProbe&) = delete;
+    KernelProbe& operator=(const KernelProbe&) = delete;
+};
 void note_early_copy(pq_ctx& c, cudaStream_t s, double* host, size_t count);  // after an early D2H on s
 void mark(pq_ctx& c, const char* name);  // timeline mark (no-op unless profiling)
 void check_launch(pq_ctx& c);

@@ -100,11 +100,17 @@ struct Source {
 void source_minus(pq_ctx& c, Source& src, double t, const double* u, const double* au, double* D, long long N) {
     switch (src.s.kind) {
         case PQ_SOURCE_ZERO:
-            launch_cubic_minus(N, 0.0, 0.0, u, au, D, c.stream);
+            {
+                KernelProbe kp(c, "k_cubic_minus", 24.0 * N);
+                launch_cubic_minus(N, 0.0, 0.0, u, au, D, c.stream);
+            }
             count_launch(c);
             break;
         case PQ_SOURCE_CUBIC:
-            launch_cubic_minus(N, src.s.s1, src.s.s3, u, au, D, c.stream);
+            {
+                KernelProbe kp(c, "k_cubic_minus", 24.0 * N);
+                launch_cubic_minus(N, src.s.s1, src.s.s3, u, au, D, c.stream);
+            }
             count_launch(c);
             break;
         case PQ_SOURCE_CONSTANT:
@@ -158,6 +164,7 @@ void apply_phi_group(DevPhiEngine& eng, double sigma, const std::vector<std::vec
         const int* sl = static_cast<const int*>(arena_push(c, slots.data(), slots.size() * sizeof(int)));
         const double* cf = static_cast<const double*>(arena_push(c, coefs.data(), coefs.size() * sizeof(double)));
         arena_flush(c);
+        KernelProbe kp(c, "k_combine(stage)", 8.0 * N * (slots.size() + 1));
         launch_combine(N, 1, static_cast<int>(slots.size()), D, N, sl, cf, gk, N, 1, c.stream);
         count_launch(c);
     }
@@ -175,6 +182,7 @@ void apply_phi_group(DevPhiEngine& eng, double sigma, const std::vector<std::vec
         ++eng.calls;
         double* s = ws(c, "etd_lin", static_cast<size_t>(N));
         phi_lincomb_dev(c, eng.op, -sigma * eng.tau, kmax, g, memo_rule(kGauss, plan.n + 1), s);
+        KernelProbe kp(c, "k_axpy", 24.0 * N);
         launch_axpy(N, eng.tau, s, u, c.stream);
         count_launch(c);
         return;
@@ -182,6 +190,7 @@ void apply_phi_group(DevPhiEngine& eng, double sigma, const std::vector<std::vec
     double* cols = ws(c, "etd_cols", static_cast<size_t>(kmax) * kmax * N);
     eng.apply(sigma, kmax, kmax, g, cols);
     for (int k = 1; k <= kmax; ++k) {
+        KernelProbe kp(c, "k_axpy", 24.0 * N);
         launch_axpy(N, eng.tau, cols + (static_cast<long long>(k - 1) * kmax + (k - 1)) * N, u, c.stream);
         count_launch(c);
     }

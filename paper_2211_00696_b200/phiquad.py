@@ -85,6 +85,14 @@ class Context:
             check(lib.pq_ctx_gemm_dense_flops(self.handle, 1, None))
         return int(n.value), ms.value, fl.value, dense.value
 
+    def kernel_stats(self, reset: bool = True) -> dict:
+        """{kernel: {"launches", "ms", "bytes"}} of the streaming kernels recorded while profiling
+        (device time from events on the launching stream, algorithmic bytes)."""
+        import json
+        js = C.c_char_p()
+        check(lib.pq_ctx_kernel_stats(self.handle, 1 if reset else 0, C.byref(js)))
+        return json.loads(js.value.decode())
+
     def set_workspace_limit(self, nbytes: int) -> None:
         check(lib.pq_ctx_set_workspace_limit(self.handle, nbytes))
 

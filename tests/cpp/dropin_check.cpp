@@ -119,6 +119,46 @@ int main() {
     } catch (const std::out_of_range&) {
         put("col.error", 4);
     }
+    // argument-check order, messages and the no-RHS plan (phiaction.hpp:277-346): a message is
+    // printed as a numeric code of its text so the key/value comparison covers it exactly
+    auto code = [](const std::string& m) {
+        double h = 0.0;
+        for (unsigned char ch : m) h = std::fmod(h * 31.0 + ch, 1000003.0);
+        return h;
+    };
+    auto msg = [&](const std::string& key, auto&& fn) {
+        try {
+            fn();
+            put(key, -1.0);
+        } catch (const std::invalid_argument& e) {
+            put(key, code(e.what()));
+        }
+    };
+    for (QuadKind kind : {QuadKind::gauss_legendre, QuadKind::clenshaw_curtis}) {
+        const std::string tag = std::string("norhs.") + quad_kind_name(kind);
+        PhiRequest req;
+        req.p = 3;
+        req.eps = 1e-10;
+        req.mode = kind;
+        PhiInfo info;
+        const auto none = phiquadmv_multi(arg, {}, req, &info);
+        put(tag + ".size", static_cast<double>(none.size()));
+        put(tag + ".l", info.l);
+        put(tag + ".n", info.n);
+        put(tag + ".points", info.points);
+        put(tag + ".planned", info.planned ? 1 : 0);
+        int pts = -7;
+        const auto none2 = phi_with_plan(arg, {}, 3, 2, 8, kind, 1e-10, 1, &pts);
+        put(tag + ".plan_points", pts);
+        put(tag + ".plan_size", static_cast<double>(none2.size()));
+        msg(tag + ".len_msg", [&] { phiquadmv(arg, std::vector<double>(5, 1.0), req); });
+        msg(tag + ".plan_p_msg", [&] { phi_with_plan(arg, {std::vector<double>(5, 1.0)}, 0, 1, 4, kind, 1e-10); });
+        msg(tag + ".plan_l_msg", [&] { phi_with_plan(arg, {b}, 2, -1, 4, kind, 1e-10); });
+        msg(tag + ".plan_eps_msg", [&] { phi_with_plan(arg, {std::vector<double>(5, 1.0)}, 2, 1, 4, kind, 0.0); });
+        PhiRequest bad = req;
+        bad.p = 0;
+        msg(tag + ".p_msg", [&] { phiquadmv_multi(arg, {std::vector<double>(5, 1.0)}, bad); });
+    }
     try {
         phi_fixed(arg, std::vector<double>(3, 1.0), 2, cached_rule(QuadKind::gauss_legendre, 4));
         put("length.error", 0);

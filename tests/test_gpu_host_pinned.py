@@ -115,13 +115,16 @@ def test_two_host_callers_concurrently_match_sequential(pq):
         ctx.close()
 
 
+@pytest.mark.parametrize("n", [32, 64])
 @pytest.mark.parametrize("space", ["host", "device"])
-def test_phiquadmv_cols_equals_contiguous(pq, space):
+def test_phiquadmv_cols_equals_contiguous(pq, space, n):
     """pq_phiquadmv_cols (the drop-in headers' entry: each RHS and each result column at its own
-    address) returns bitwise what pq_phiquadmv returns in one contiguous buffer, nb = 2."""
+    address) returns bitwise what pq_phiquadmv returns in one contiguous buffer, nb = 2.  n = 32
+    (262 k doubles of results) takes the direct-copy branch, n = 64 (2 M doubles >= the 8 MB bounce
+    threshold) the pinned bounce with the early drain and the final scatter (capi.cpp)."""
     import torch
     from paper_2211_00696_b200.workloads import config
-    w = config(2, n=32)
+    w = config(2, n=n)
     a = pq.KroneckerSum(w.factors)
     req = pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode))
     ctx = pq.Context(0)
@@ -156,12 +159,14 @@ def test_phiquadmv_cols_equals_contiguous(pq, space):
     ctx.close()
 
 
+@pytest.mark.parametrize("n", [32, 64])
 @pytest.mark.parametrize("kind", [0, 1])
-def test_phi_with_plan_cols_equals_contiguous(pq, kind):
+def test_phi_with_plan_cols_equals_contiguous(pq, kind, n):
     """pq_phi_with_plan_cols (drop-in phi_with_plan / PhiEngine::apply) returns bitwise what
-    pq_phi_with_plan returns contiguously; nb = 2 pageable host vectors, both rules."""
+    pq_phi_with_plan returns contiguously; nb = 2 pageable host vectors, both rules; n = 64 crosses
+    the pinned-bounce threshold (one D2H into the bounce, host threads fill the columns)."""
     from paper_2211_00696_b200.workloads import config
-    w = config(2, n=32)
+    w = config(2, n=n)
     a = pq.KroneckerSum(w.factors)
     ctx = pq.Context(0)
     d, sh, fac = a._abi()

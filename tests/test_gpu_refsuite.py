@@ -24,11 +24,11 @@ HOST_ONLY = ["test_bounds", "test_quadrature", "test_roots"]  # planner / rules 
 DEVICE = ["test_dense", "test_kron", "test_oracle", "test_phiaction", "test_integrators", "test_problems", "test_cli"]
 
 
-def _run(name, timeout=900):
+def _run(name, timeout=900, env=None):
     exe = BIN / name
     if not exe.exists():
         pytest.skip(f"{exe} not built (needs /root/reference at build time: make -C tests/cpp refsuite)")
-    env = dict(os.environ, PHIQUAD_CLI=str(ROOT / "paper_2211_00696_b200" / "phiquad_cli"))
+    env = dict(os.environ, PHIQUAD_CLI=str(ROOT / "paper_2211_00696_b200" / "phiquad_cli"), **(env or {}))
     r = subprocess.run([str(exe)], capture_output=True, text=True, timeout=timeout, env=env)
     return r
 
@@ -50,18 +50,18 @@ def test_reference_unit_suite_on_b200(name):
 
 @pytest.mark.gpu
 def test_reference_acceptance_gate_on_b200():
-    # Criterion 7 times ONE phiquadmv call at r = 4 (~2-5 ms) against the dense oracle and needs
-    # >= 10x; on the shared boxes that single call occasionally stalls ~45 ms (seen with this round's
-    # first build as well, 1 run in 3: profiles/r01_summary.md).  A run that fails only that timing
-    # criterion is repeated, up to three runs; every other criterion must pass every time.
-    for _ in range(3):
-        r = _run("acceptance")
-        failed = [ln for ln in r.stdout.splitlines() if ln.startswith("criterion ") and ": FAIL" in ln]
-        if r.returncode == 0 or not all(ln.startswith("criterion 7:") for ln in failed) or not failed:
-            break
+    # Criterion 7 times ONE phiquadmv call at r = 4 (~3.5 ms) against the dense oracle and needs
+    # >= 10x.  Round 1 saw that call take 20-60 ms in most runs: the PQ_SLOWLOG timeline put the
+    # time in the workspace regrowth (cudaFree of the previous, larger chain buffers is a
+    # device-wide sync).  Replaced buffers are now retired without a free inside the call
+    # (engine.cpp ws_bytes / pq_ctx::graveyard), so the gate runs ONCE, no retry; a slow call prints
+    # its phase timeline to stderr (PQ_SLOWLOG) for the failure message.
+    r = _run("acceptance", env={"PQ_SLOWLOG": "10"})
+    c7 = [ln for ln in r.stdout.splitlines() if ln.startswith("criterion 7:")]
+    print(c7, r.stderr[-2000:])
     assert r.returncode == 0, r.stdout[-4000:] + r.stderr[-2000:]
     verdicts = [ln for ln in r.stdout.splitlines() if ln.startswith("criterion ") and ": " in ln and "note" not in ln]
-    assert len(verdicts) == 7 and all(": PASS" in ln for ln in verdicts), r.stdout
+    assert len(verdicts) == 7 and all(": PASS" in ln for ln in verdicts), r.stdout + r.stderr
     assert "acceptance: all 7 criteria passed" in r.stdout
 
 
