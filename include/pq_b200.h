@@ -202,6 +202,50 @@ PQ_API int pq_mode_product(pq_ctx* ctx, int d, const int* shape, int mode, const
                            const double* x, double* y);
 PQ_API int pq_squaring_combine(pq_ctx* ctx, long long n, int p, int nb, double* t, const double* y);
 
+/* multi-GPU (one process per GPU; paper_2211_00696_b200/csrc/dist.cpp) ------------ */
+/* The reference's node loop (phiaction.hpp:85 parallel_for, util.hpp:24-39) and its serial
+ * squaring (phiaction.hpp:255-272, 293-301), partitioned over the ranks of a communicator:
+ * quadrature nodes dealt round-robin (i % world == rank; each adaptive-CC level's fresh nodes
+ * likewise), ONE all-to-all moving each node vector's x-slab to its owner (rank r owns the
+ * x-indices [floor(n0 r/G), floor(n0 (r+1)/G)), a contiguous range of every vector, see
+ * pq_dist_slab), the weighted node sums formed per slab in ascending node order (the node phase is
+ * bitwise independent of the rank count), the adaptive-CC error as one exact all-reduce(max) of
+ * 2 nb p scalars per level, and the modified squaring + phi_0 on slabs (modes 1..d-1 in the slab,
+ * slab <-> pencil all-to-alls around mode 0).  Every rank passes the SAME inputs (factors, b, request). */
+enum { PQ_COMM_NCCL = 0, PQ_COMM_HOST = 1 };
+typedef struct pq_comm pq_comm;
+/* Host transport: collectives on pinned HOST buffers, e.g. torch.distributed over gloo, so several
+ * processes can share one GPU in tests (no kernel ever waits on another process).  alltoallv sends
+ * send_counts[h] doubles (consecutive, in rank order) to rank h and receives recv_counts[h] doubles
+ * from rank h into recv (consecutive, in rank order); allreduce_max is an in-place elementwise max
+ * over ranks.  Return 0 on success. */
+typedef struct {
+    void* user;
+    int (*alltoallv)(void* user, const double* send, const int64_t* send_counts, double* recv,
+                     const int64_t* recv_counts);
+    int (*allreduce_max)(void* user, double* buf, int64_t n);
+} pq_host_transport;
+/* NCCL (loaded at run time: the libnccl.so.2 already mapped in the process, else the system one,
+ * or $PQ_NCCL_LIB): rank 0 makes the 128-byte id, every rank passes it (broadcast by any means). */
+PQ_API int pq_nccl_unique_id(char* out128);
+PQ_API int pq_comm_create_nccl(pq_ctx* ctx, int world, int rank, const char* id128, pq_comm** out);
+PQ_API int pq_comm_create_host(int world, int rank, const pq_host_transport* transport, pq_comm** out);
+PQ_API int pq_comm_destroy(pq_comm* comm);
+/* Bytes this rank sent to other ranks and exchanges issued since the last reset. */
+PQ_API int pq_comm_stats(pq_comm* comm, int reset, double* bytes_sent, uint64_t* exchanges);
+/* [begin, end) of rank's x-slab inside a vector of the given shape. */
+PQ_API int pq_dist_slab(int d, const int* shape, int world, int rank, int64_t* begin, int64_t* end);
+/* phiquadmv_multi (+ phi_0 when out0 != NULL) across the communicator.  gather != 0: out [nb][p][N]
+ * and out0 [nb][N] hold full vectors on every rank; gather == 0: this rank's slabs, out
+ * [nb][p][end-begin], out0 [nb][end-begin].  The plan is computed identically on every rank. */
+PQ_API int pq_phiquadmv_dist(pq_ctx* ctx, pq_comm* comm, int d, const int* shape, const double* factors, int nb,
+                             const double* bs, const pq_phi_request* req, double* out0, double* out,
+                             pq_phi_info* info, int space, int gather);
+/* phi_with_plan (phiaction.hpp:277) across the communicator, layouts as pq_phiquadmv_dist. */
+PQ_API int pq_phi_with_plan_dist(pq_ctx* ctx, pq_comm* comm, int d, const int* shape, const double* factors,
+                                 int nb, const double* bs, int p, int l, int n, int kind, double eps, double* out,
+                                 int* points_used, int space, int gather);
+
 /* exponential integrators (integrators.hpp) ----------------------------------------------- */
 /* Increment-form tableau (ExpRKTableau, integrators.hpp:32-38) flattened into terms: a term
  * with row >= 1 is a_{row,col} += coef * phi_k, row == -1 is b_col += coef * phi_k. */

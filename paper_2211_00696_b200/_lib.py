@@ -45,6 +45,14 @@ class SourceC(C.Structure):
                 ("user", vp)]
 
 
+ALLTOALLV_CB = C.CFUNCTYPE(C.c_int, vp, dp, C.POINTER(C.c_int64), dp, C.POINTER(C.c_int64))
+ALLREDUCE_CB = C.CFUNCTYPE(C.c_int, vp, dp, C.c_int64)
+
+
+class HostTransportC(C.Structure):
+    _fields_ = [("user", vp), ("alltoallv", ALLTOALLV_CB), ("allreduce_max", ALLREDUCE_CB)]
+
+
 # name -> (restype, argtypes)
 SIGNATURES = {
     "pq_version": (C.c_char_p, []),
@@ -100,6 +108,16 @@ SIGNATURES = {
     "pq_phi_nodes_partial": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, vp, C.c_int, C.c_int, C.c_int, dp, dp,
                                        C.c_int, C.c_int, C.c_int, vp]),
     "pq_squaring_chain": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, C.c_int, C.c_int, vp]),
+    "pq_nccl_unique_id": (C.c_int, [C.c_char_p]),
+    "pq_comm_create_nccl": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]),
+    "pq_comm_create_host": (C.c_int, [C.c_int, C.c_int, C.POINTER(HostTransportC), C.POINTER(vp)]),
+    "pq_comm_destroy": (C.c_int, [vp]),
+    "pq_comm_stats": (C.c_int, [vp, C.c_int, dp, C.POINTER(C.c_uint64)]),
+    "pq_dist_slab": (C.c_int, [C.c_int, ip, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "pq_phiquadmv_dist": (C.c_int, [vp, vp, C.c_int, ip, dp, C.c_int, vp, C.POINTER(PhiRequestC), vp, vp,
+                                    C.POINTER(PhiInfoC), C.c_int, C.c_int]),
+    "pq_phi_with_plan_dist": (C.c_int, [vp, vp, C.c_int, ip, dp, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int,
+                                        C.c_double, vp, ip, C.c_int, C.c_int]),
     "pq_builtin_tableau": (C.c_int, [C.c_int, C.c_double, C.POINTER(TableauC)]),
     "pq_integrate": (C.c_int, [vp, C.c_int, ip, dp, C.POINTER(SourceC), vp, C.c_double, C.c_double, C.c_int,
                                C.POINTER(TableauC), C.POINTER(PhiRequestC), vp, ip, C.c_int]),

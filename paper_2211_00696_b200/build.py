@@ -24,7 +24,7 @@ CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU_SOURCES = ["gemm_nk.cu", "gemm_kk.cu", "kernels.cu"]
-CPP_SOURCES = ["estimator.cpp", "engine.cpp", "etd.cpp", "capi.cpp"]
+CPP_SOURCES = ["estimator.cpp", "engine.cpp", "etd.cpp", "capi.cpp", "dist.cpp"]
 
 
 def _headers() -> list[Path]:

@@ -159,6 +159,7 @@ int pq_ctx_create(int device, pq_ctx** out) {
         cuda_check(cudaMalloc(&c->d_int, 64 * sizeof(int)), "cudaMalloc(int)");
         cuda_check(cudaMalloc(&c->d_small, 1024 * sizeof(double)), "cudaMalloc(small)");
         cuda_check(cudaMallocHost(&c->h_small, 1024 * sizeof(double)), "cudaMallocHost(small)");
+        cuda_check(cudaMallocHost(&c->h_beta, 1024 * sizeof(double)), "cudaMallocHost(beta)");
         *out = c;
     });
 }
@@ -171,6 +172,7 @@ int pq_ctx_destroy(pq_ctx* c) {
         for (auto& kv : c->bufs)
             if (kv.second.p) cudaFree(kv.second.p);
         for (void* p : c->graveyard) cudaFree(p);
+        trim_pool(*c);
         if (c->arena.host) cudaFreeHost(c->arena.host);
         if (c->arena.dev) cudaFree(c->arena.dev);
         if (c->arena.done) cudaEventDestroy(c->arena.done);
@@ -178,7 +180,9 @@ int pq_ctx_destroy(pq_ctx* c) {
         cudaFree(c->d_int);
         cudaFree(c->d_small);
         if (c->d_flops) cudaFree(c->d_flops);
+        worker_stop(*c);
         cudaFreeHost(c->h_small);
+        cudaFreeHost(c->h_beta);
         for (auto e : c->ev_pool) cudaEventDestroy(e);
         if (c->side) {
             cudaStreamSynchronize(c->side);
@@ -274,6 +278,7 @@ int pq_ctx_release_workspace(pq_ctx* c) {
             if (kv.second.p) cudaFree(kv.second.p);
         c->bufs.clear();
         c->fac_cache.clear();
+        trim_pool(*c);
     });
 }
 

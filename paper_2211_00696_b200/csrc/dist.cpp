@@ -1,0 +1,800 @@
+// Multi-GPU phi actions, one process per GPU.  Replaces the reference's node
+// loop parallel_for (phiaction.hpp:85, util.hpp:24-39) and its serial squaring
+// (phiaction.hpp:255-272, 293-301) with a partition over the ranks of one node:
+//
+//  1. quadrature nodes: rank r evaluates the node vectors v_i = (E_i0 (x) E_i1 (x) E_i2) b of the
+//     nodes it owns (i % G == r; the adaptive CC ladder deals each level's fresh nodes the same
+//     way) -- exponentials and DMMA mode products for its nodes only;
+//  2. node transpose: ONE all-to-all moves every node vector's x-slab to the slab's owner (rank h
+//     owns x-indices i0 in [s_h, s_h+1), a contiguous range of every vector).  Each rank then holds
+//     all q node vectors of its slab and forms the weighted sums y_j = sum_i w_i theta_i^(j-1)/(j-1)! v_i
+//     in ascending node order exactly as the single-GPU combine (phiaction.hpp:96-111) -- no
+//     floating-point reduction across ranks, so the node phase is bitwise independent of G.
+//     Bytes per rank: (q/G) nb N (G-1)/G doubles, versus p nb N (G-1)/G for a reduce-scatter of
+//     the partial sums -- fewer whenever q/G < p (configs 3 and 5 at G >= 4), and the CC ladder
+//     needs no per-level reduction of fine AND coarse sums (its error statistics are max-norms:
+//     one all-reduce(max) of 2 nb p scalars per level, exact);
+//  3. distributed squaring on slabs: per step modes 1..d-1 act inside the slab, the slab is
+//     packed into per-destination blocks and flipped to pencils (rank r: all i0, trailing indices
+//     [c_r, c_r+1)) by an all-to-all, mode 0 acts on the pencil, a second all-to-all flips back,
+//     the blocks are unpacked, and the doubling combination is elementwise (k_sq_combine2).
+//     phi_0 = exp_action(b) is one more distributed Kronecker apply;
+//  4. optionally, the slabs are all-gathered into full vectors on every rank.
+//
+// Transport: NCCL (loaded with dlopen -- the copy torch already mapped when present, else the
+// system libnccl.so.2) with grouped ncclSend/ncclRecv and ncclAllReduce on the context stream;
+// or a host transport (caller-supplied alltoallv / allreduce-max callbacks on pinned host
+// buffers -- e.g. torch.distributed over gloo), which lets several processes share ONE GPU in the
+// tests: collectives go through the host, so no kernel ever waits on another process.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <limits>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "engine.hpp"
+#include "pq_b200.h"
+
+using namespace pqb;
+
+struct pq_comm {
+    int world = 1, rank = 0;
+    int kind = PQ_COMM_HOST;
+    ncclComm_t nccl = nullptr;
+    pq_host_transport host{};
+    double* hs = nullptr;  // pinned staging (host transport)
+    size_t hs_cap = 0;
+    double* hr = nullptr;
+    size_t hr_cap = 0;
+    double bytes_sent = 0.0;  // doubles * 8 sent to other ranks
+    uint64_t exchanges = 0;
+};
+
+namespace {
+
+void need(bool ok, const char* what) {
+    if (!ok) throw std::invalid_argument(what);
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen) --------
+
+struct NcclApi {
+    ncclResult_t (*getUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*commInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*groupStart)() = nullptr;
+    ncclResult_t (*groupEnd)() = nullptr;
+    ncclResult_t (*allReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                              cudaStream_t) = nullptr;
+    const char* (*errorString)(ncclResult_t) = nullptr;
+    std::string why;
+};
+
+const NcclApi& nccl_api() {
+    static const NcclApi api = [] {
+        NcclApi a;
+        const char* env = std::getenv("PQ_NCCL_LIB");
+        void* h = env ? nullptr : dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);  // torch's copy, if mapped
+        if (!h) h = dlopen(env ? env : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) {
+            a.why = std::string("cannot load NCCL: ") + dlerror();
+            return a;
+        }
+        auto sym = [&](auto& f, const char* name) {
+            f = reinterpret_cast<std::remove_reference_t<decltype(f)>>(dlsym(h, name));
+            if (!f && a.why.empty()) a.why = std::string("NCCL symbol missing: ") + name;
+        };
+        sym(a.getUniqueId, "ncclGetUniqueId");
+        sym(a.commInitRank, "ncclCommInitRank");
+        sym(a.commDestroy, "ncclCommDestroy");
+        sym(a.send, "ncclSend");
+        sym(a.recv, "ncclRecv");
+        sym(a.groupStart, "ncclGroupStart");
+        sym(a.groupEnd, "ncclGroupEnd");
+        sym(a.allReduce, "ncclAllReduce");
+        sym(a.errorString, "ncclGetErrorString");
+        return a;
+    }();
+    if (!api.why.empty()) throw CudaError(api.why);
+    return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+    if (r != ncclSuccess) throw CudaError(std::string("NCCL ") + what + ": " + nccl_api().errorString(r));
+}
+
+// ------------------------------------------------------------------ transport ------------
+
+struct Piece {
+    int peer;
+    double* ptr;
+    long long count;
+};
+
+double* grow_pinned(double*& buf, size_t& cap, size_t count) {
+    if (cap < count) {
+        if (buf) cudaFreeHost(buf);
+        buf = nullptr;
+        cap = 0;
+        cuda_check(cudaMallocHost(reinterpret_cast<void**>(&buf), std::max<size_t>(count, 1) * sizeof(double)),
+                   "cudaMallocHost(transport)");
+        cap = std::max<size_t>(count, 1);
+    }
+    return buf;
+}
+
+// Point-to-point exchange on the context stream.  Pieces to / from the same peer are matched in
+// the order given (sender and receiver enumerate them in the same order).  Self pieces are local
+// device copies (the i-th self send lands in the i-th self receive).
+void exchange(pq_ctx& c, pq_comm& m, const std::vector<Piece>& sends, const std::vector<Piece>& recvs) {
+    ++m.exchanges;
+    std::vector<const Piece*> self_s, self_r;
+    for (const auto& s : sends)
+        if (s.peer == m.rank && s.count > 0) self_s.push_back(&s);
+    for (const auto& r : recvs)
+        if (r.peer == m.rank && r.count > 0) self_r.push_back(&r);
+    need(self_s.size() == self_r.size(), "exchange: unmatched local pieces");
+    for (size_t i = 0; i < self_s.size(); ++i) {
+        need(self_s[i]->count == self_r[i]->count, "exchange: local piece size mismatch");
+        cuda_check(cudaMemcpyAsync(self_r[i]->ptr, self_s[i]->ptr, sizeof(double) * self_s[i]->count,
+                                   cudaMemcpyDeviceToDevice, c.stream),
+                   "exchange (local)");
+    }
+    for (const auto& s : sends)
+        if (s.peer != m.rank) m.bytes_sent += 8.0 * static_cast<double>(s.count);
+    if (m.world == 1) return;
+    if (m.kind == PQ_COMM_NCCL) {
+        const NcclApi& api = nccl_api();
+        nccl_check(api.groupStart(), "group start");
+        for (const auto& s : sends)
+            if (s.peer != m.rank && s.count > 0)
+                nccl_check(api.send(s.ptr, static_cast<size_t>(s.count), ncclFloat64, s.peer, m.nccl, c.stream), "send");
+        for (const auto& r : recvs)
+            if (r.peer != m.rank && r.count > 0)
+                nccl_check(api.recv(r.ptr, static_cast<size_t>(r.count), ncclFloat64, r.peer, m.nccl, c.stream), "recv");
+        nccl_check(api.groupEnd(), "group end");
+        return;
+    }
+    // host transport: stage per-peer concatenations through pinned memory, one alltoallv callback
+    std::vector<int64_t> sc(static_cast<size_t>(m.world), 0), rc(static_cast<size_t>(m.world), 0);
+    for (const auto& s : sends)
+        if (s.peer != m.rank) sc[static_cast<size_t>(s.peer)] += s.count;
+    for (const auto& r : recvs)
+        if (r.peer != m.rank) rc[static_cast<size_t>(r.peer)] += r.count;
+    const size_t st = std::accumulate(sc.begin(), sc.end(), size_t(0));
+    const size_t rt = std::accumulate(rc.begin(), rc.end(), size_t(0));
+    double* hs = grow_pinned(m.hs, m.hs_cap, st);
+    double* hr = grow_pinned(m.hr, m.hr_cap, rt);
+    std::vector<size_t> off(static_cast<size_t>(m.world), 0);
+    for (int h = 1; h < m.world; ++h) off[static_cast<size_t>(h)] = off[static_cast<size_t>(h) - 1] + sc[static_cast<size_t>(h) - 1];
+    for (const auto& s : sends) {
+        if (s.peer == m.rank || s.count == 0) continue;
+        size_t& o = off[static_cast<size_t>(s.peer)];
+        cuda_check(cudaMemcpyAsync(hs + o, s.ptr, sizeof(double) * s.count, cudaMemcpyDeviceToHost, c.stream), "D2H (send)");
+        o += static_cast<size_t>(s.count);
+    }
+    cuda_check(cudaStreamSynchronize(c.stream), "exchange sync");
+    need(m.host.alltoallv != nullptr, "host transport: no alltoallv");
+    if (m.host.alltoallv(m.host.user, hs, sc.data(), hr, rc.data()) != 0)
+        throw CudaError("host transport: alltoallv callback failed");
+    std::fill(off.begin(), off.end(), 0);
+    for (int h = 1; h < m.world; ++h) off[static_cast<size_t>(h)] = off[static_cast<size_t>(h) - 1] + rc[static_cast<size_t>(h) - 1];
+    for (const auto& r : recvs) {
+        if (r.peer == m.rank || r.count == 0) continue;
+        size_t& o = off[static_cast<size_t>(r.peer)];
+        cuda_check(cudaMemcpyAsync(r.ptr, hr + o, sizeof(double) * r.count, cudaMemcpyHostToDevice, c.stream), "H2D (recv)");
+        o += static_cast<size_t>(r.count);
+    }
+}
+
+// In-place all-reduce (max) of n device doubles.
+void allreduce_max(pq_ctx& c, pq_comm& m, double* dev, int n) {
+    if (m.world == 1 || n == 0) return;
+    if (m.kind == PQ_COMM_NCCL) {
+        nccl_check(nccl_api().allReduce(dev, dev, static_cast<size_t>(n), ncclFloat64, ncclMax, m.nccl, c.stream),
+                   "allreduce");
+        return;
+    }
+    double* hs = grow_pinned(m.hs, m.hs_cap, static_cast<size_t>(n));
+    cuda_check(cudaMemcpyAsync(hs, dev, sizeof(double) * n, cudaMemcpyDeviceToHost, c.stream), "D2H (allreduce)");
+    cuda_check(cudaStreamSynchronize(c.stream), "allreduce sync");
+    need(m.host.allreduce_max != nullptr, "host transport: no allreduce_max");
+    if (m.host.allreduce_max(m.host.user, hs, n) != 0) throw CudaError("host transport: allreduce_max callback failed");
+    cuda_check(cudaMemcpyAsync(dev, hs, sizeof(double) * n, cudaMemcpyHostToDevice, c.stream), "H2D (allreduce)");
+}
+
+// ------------------------------------------------------------------ geometry -------------
+
+struct Geom {
+    int G = 1, r = 0, d = 1;
+    int n[3] = {1, 1, 1};
+    long long N = 1, rest = 1;
+    std::vector<int> s;  // x-slab bounds, G + 1
+    SlabCuts cuts;       // pencil bounds over the trailing index
+    int sg(int h) const { return s[static_cast<size_t>(h) + 1] - s[static_cast<size_t>(h)]; }
+    long long S(int h) const { return static_cast<long long>(sg(h)) * rest; }
+    long long lo(int h) const { return static_cast<long long>(s[static_cast<size_t>(h)]) * rest; }
+    long long C(int h) const { return cuts.cb[h + 1] - cuts.cb[h]; }
+};
+
+Geom make_geom(int d, const int* shape, int world, int rank) {
+    need(world >= 1 && world <= 16, "distributed phi: 1 to 16 ranks");
+    need(rank >= 0 && rank < world, "distributed phi: bad rank");
+    Geom g;
+    g.G = world;
+    g.r = rank;
+    g.d = d;
+    for (int k = 0; k < d; ++k) {
+        g.n[k] = shape[k];
+        g.N *= shape[k];
+    }
+    g.rest = g.N / shape[0];
+    need(shape[0] >= world, "distributed phi: the first factor needs at least one x-slab per rank");
+    g.s.resize(static_cast<size_t>(world) + 1);
+    for (int h = 0; h <= world; ++h) g.s[static_cast<size_t>(h)] = static_cast<int>(static_cast<long long>(shape[0]) * h / world);
+    g.cuts.G = world;
+    for (int h = 0; h <= world; ++h) g.cuts.cb[h] = g.rest * h / world;
+    return g;
+}
+
+// ------------------------------------------------------------------ distributed pieces ---
+
+// y[col] = (E_0 (x) ... (x) E_{d-1}) x[col] for ncols columns in slab layout (x[col] at
+// x + col*x_stride, S_r doubles; y[col] at y + col*S_r).  Modes 1..d-1 inside the slab, slab ->
+// pencil all-to-all, mode 0 on the pencil, pencil -> slab all-to-all.
+void dist_kron(pq_ctx& c, pq_comm& m, const Geom& g, const double* const* E, const int2* const* B, const double* x,
+               long long x_stride, int ncols, double* y) {
+    const int r = g.r, sg = g.sg(r);
+    const long long S = g.S(r), Cr = g.C(r);
+    const size_t tot = static_cast<size_t>(ncols) * std::max<long long>(S, 1);
+    const size_t ptot = static_cast<size_t>(ncols) * g.n[0] * std::max<long long>(Cr, 1);
+    double* U = ws(c, "dk_U", std::max(tot, ptot));
+    double* Bk = ws(c, "dk_B", tot);
+    double* P = ws(c, "dk_P", ptot);
+    // 1. modes 1..d-1 on the slab (each column a (sg, n1[, n2]) tensor)
+    if (g.d == 1) {
+        for (int col = 0; col < ncols; ++col)
+            cuda_check(cudaMemcpyAsync(U + col * S, x + col * x_stride, sizeof(double) * S, cudaMemcpyDeviceToDevice,
+                                       c.stream),
+                       "slab copy");
+    } else if (sg > 0) {
+        const int sh[3] = {sg, g.n[1], g.d > 2 ? g.n[2] : 1};
+        if (g.d == 2) {
+            mode_product_dev(c, 2, sh, 1, E[1], B ? B[1] : nullptr, x, x_stride, U, S, ncols);
+        } else {
+            double* T = ws(c, "dk_T", tot);
+            mode_product_dev(c, 3, sh, 1, E[1], B ? B[1] : nullptr, x, x_stride, T, S, ncols);
+            mode_product_dev(c, 3, sh, 2, E[2], B ? B[2] : nullptr, T, S, U, S, ncols);
+        }
+    }
+    // 2. pack into per-destination blocks, 3. flip to pencils
+    SlabCuts cuts = g.cuts;
+    cuts.ncols = ncols;
+    {
+        KernelProbe kp(c, "k_slab_blocks(pack)", 16.0 * static_cast<double>(tot));
+        launch_slab_blocks(true, sg, g.rest, cuts, U, Bk, c.stream);
+        count_launch(c);
+    }
+    std::vector<Piece> sends, recvs;
+    for (int h = 0; h < g.G; ++h)
+        for (int col = 0; col < ncols; ++col) {
+            sends.push_back({h, Bk + ncols * sg * cuts.cb[h] + col * sg * g.C(h), sg * g.C(h)});
+            recvs.push_back({h, P + (col * g.n[0] + g.s[static_cast<size_t>(h)]) * Cr, g.sg(h) * Cr});
+        }
+    exchange(c, m, sends, recvs);
+    // 4. mode 0 on the pencil (n0 x C_r per column)
+    if (Cr > 0) {
+        const int sh[2] = {g.n[0], static_cast<int>(Cr)};
+        mode_product_dev(c, 2, sh, 0, E[0], B ? B[0] : nullptr, P, g.n[0] * Cr, U, g.n[0] * Cr, ncols);
+    }
+    // 5. flip back into blocks, 6. unpack into the slab
+    sends.clear();
+    recvs.clear();
+    for (int h = 0; h < g.G; ++h)
+        for (int col = 0; col < ncols; ++col) {
+            sends.push_back({h, U + (col * g.n[0] + g.s[static_cast<size_t>(h)]) * Cr, g.sg(h) * Cr});
+            recvs.push_back({h, Bk + ncols * sg * cuts.cb[h] + col * sg * g.C(h), sg * g.C(h)});
+        }
+    exchange(c, m, sends, recvs);
+    KernelProbe kp(c, "k_slab_blocks(unpack)", 16.0 * static_cast<double>(tot));
+    launch_slab_blocks(false, sg, g.rest, cuts, Bk, y, c.stream);
+    count_launch(c);
+}
+
+// node vectors of the owned nodes (full length, pool [a][m][N]) -> every node's slab on its
+// owner (slab pool [slot][m][S_r]); `owner_of(slot)` and the local index of owned slots
+void node_transpose(pq_ctx& c, pq_comm& m, const Geom& g, int nb, const std::vector<int>& slots, const double* pool,
+                    double* slab_pool) {
+    std::vector<Piece> sends, recvs;
+    int a = 0;
+    for (int slot : slots) {
+        const int owner = slot % g.G;
+        if (owner == g.r) {
+            for (int mm = 0; mm < nb; ++mm)
+                for (int h = 0; h < g.G; ++h)
+                    sends.push_back({h, const_cast<double*>(pool) + (static_cast<long long>(a) * nb + mm) * g.N + g.lo(h),
+                                     g.S(h)});
+            ++a;
+        }
+        for (int mm = 0; mm < nb; ++mm)
+            recvs.push_back({owner, slab_pool + (static_cast<long long>(slot) * nb + mm) * g.S(g.r), g.S(g.r)});
+    }
+    exchange(c, m, sends, recvs);
+}
+
+std::vector<int> owned(const std::vector<int>& slots, const Geom& g) {
+    std::vector<int> o;
+    for (int s : slots)
+        if (s % g.G == g.r) o.push_back(s);
+    return o;
+}
+
+double* slab_pool_grow(pq_ctx& c, int slots, int nb, long long S, int used) {
+    DevBuf& b = c.bufs["dslabpool"];
+    const size_t want = static_cast<size_t>(std::max(slots, 1)) * nb * std::max<long long>(S, 1) * sizeof(double);
+    if (b.bytes < want) {
+        double* np = static_cast<double*>(dev_alloc(c, want, "dslabpool"));
+        if (b.p && used > 0)
+            cuda_check(cudaMemcpyAsync(np, b.p, static_cast<size_t>(used) * nb * S * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       c.stream),
+                       "pool copy");
+        if (b.p) c.graveyard.push_back(b.p);
+        b.p = np;
+        b.bytes = want;
+    }
+    return static_cast<double*>(b.p);
+}
+
+// Gauss node phase: acc [nb][p][S_r] = the slab of phi_j(2^-l A) b (phiaction.hpp:134-145)
+void gauss_nodes(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, const double* bs, int p,
+                 const NodesWeights& rule, const PhiExps& px, const std::vector<int>& own, double* acc) {
+    const int q = rule.size();
+    const long long S = g.S(g.r);
+    long long Es[3];
+    for (int k = 0; k < op.d; ++k) Es[k] = static_cast<long long>(op.n[k]) * op.n[k];
+    double* pool = ws(c, "dpool", std::max<size_t>(own.size(), 1) * nb * op.N);
+    node_sweep(c, op, px.node, Es, static_cast<int>(own.size()), nb, bs, p, nullptr, nullptr, 0, pool, 0, px.node_band);
+    std::vector<int> all(static_cast<size_t>(q));
+    std::iota(all.begin(), all.end(), 0);
+    double* slab = slab_pool_grow(c, q, nb, S, 0);
+    node_transpose(c, m, g, nb, all, pool, slab);
+    std::vector<double> coef;
+    node_coefs(rule, all, p, coef);
+    const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
+    const int* sl_dev = static_cast<const int*>(arena_push(c, all.data(), all.size() * sizeof(int)));
+    arena_flush(c);
+    if (S == 0) return;
+    for (int mm = 0; mm < nb; ++mm) {
+        KernelProbe kp(c, "k_combine", 8.0 * S * (q + p));
+        launch_combine(S, p, q, slab + mm * S, static_cast<long long>(nb) * S, sl_dev, coef_dev, acc + mm * p * S, S, 1,
+                       c.stream);
+        count_launch(c);
+    }
+}
+
+// Adaptive CC ladder (phiaction.hpp:156-245) on slabs.  Pool slots as in the single-GPU ladder:
+// 0..12 = the 13-point rule, then each level's fresh (odd) nodes; slot s is evaluated by rank
+// s % G.  px25 holds the exponentials of the owned slots among the first 25 (own25 order).
+void cc_nodes(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int l, int nb, const double* bs, int p,
+              double eps, const PhiExps& px25, const std::vector<int>& own25, double* out, int* points_used) {
+    if (!(eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
+    const long long S = g.S(g.r);
+    const size_t col = static_cast<size_t>(nb) * p * S;
+    long long nn[3], Es[3];
+    for (int k = 0; k < op.d; ++k) Es[k] = nn[k] = static_cast<long long>(op.n[k]) * op.n[k];
+    const NodesWeights& r25 = memo_rule(kClenshaw, 25);
+    // sweeps the owned slots among `slots` (exponentials E[k] + idx*nn[k], idx = position among the
+    // owned ones) and moves every slot's slab to this rank's slab pool
+    double* slab = slab_pool_grow(c, 25, nb, S, 0);
+    int used = 0;
+    auto sweep = [&](const std::vector<int>& slots, const double* const* E, const int2* const* B) {
+        const std::vector<int> mine = owned(slots, g);
+        double* pool = ws(c, "dpool", std::max<size_t>(mine.size(), 1) * nb * op.N);
+        if (!mine.empty()) node_sweep(c, op, E, Es, static_cast<int>(mine.size()), nb, bs, p, nullptr, nullptr, 0, pool, 0, B);
+        slab = slab_pool_grow(c, used + static_cast<int>(slots.size()), nb, S, used);
+        node_transpose(c, m, g, nb, slots, pool, slab);
+        used += static_cast<int>(slots.size());
+    };
+    // exponentials of owned slots in a contiguous subrange [first, first+count) of own25
+    auto sub = [&](int first, const double** E, const int2** B) {
+        for (int k = 0; k < op.d; ++k) {
+            E[k] = px25.node[k] ? px25.node[k] + first * nn[k] : nullptr;
+            B[k] = px25.node_band[k] ? px25.node_band[k] + first * band_row_blocks(op.n[k]) : nullptr;
+        }
+    };
+    {
+        std::vector<int> s13(13);
+        std::iota(s13.begin(), s13.end(), 0);
+        const double* E[3];
+        const int2* B[3];
+        sub(0, E, B);
+        sweep(s13, E, B);
+    }
+    int half = 3;
+    const NodesWeights* rule = &memo_rule(kClenshaw, 2 * half + 1);
+    std::vector<int> slot_of(static_cast<size_t>(rule->size()));
+    for (int i = 0; i < rule->size(); ++i) slot_of[static_cast<size_t>(i)] = 2 * i;
+    double* accs[2] = {out, ws(c, "dccacc", std::max<size_t>(col, 1))};
+    int cur = 0;
+    const bool fused = p <= 8;
+    double* stats = ws(c, "dccstats", 2 * static_cast<size_t>(nb) * p);
+    std::vector<double> hstats(2 * static_cast<size_t>(nb) * p);
+    int level = 0;
+    (void)r25;
+    while (true) {
+        const int half_next = 2 * half;
+        if (half_next > (1 << 14)) throw ConvergenceFailure("phi_adaptive: no convergence within the node budget");
+        const NodesWeights& fine = memo_rule(kClenshaw, 2 * half_next + 1);
+        const int fresh = fine.size() / 2;
+        ++level;
+        int base = 2 * 0 + 1;  // level 1: fresh 13-rule nodes are slots 1, 3, ..., 11
+        if (level >= 2) {
+            base = used;
+            std::vector<int> fs(static_cast<size_t>(fresh));
+            std::iota(fs.begin(), fs.end(), used);
+            const std::vector<int> mine = owned(fs, g);
+            const double* E[3];
+            const int2* B[3];
+            PhiExps pxl;
+            if (level == 2) {  // 25-rule odd nodes: own25 entries after the owned slots < 13
+                const int first = static_cast<int>(std::count_if(own25.begin(), own25.end(), [](int s) { return s < 13; }));
+                sub(first, E, B);
+            } else {
+                std::vector<double> th;
+                for (int s : mine) th.push_back(fine.x[static_cast<size_t>(2 * (s - used) + 1)]);
+                pxl = phi_exponentials(c, op, 1.0, l, th, false, false, "dccE" + std::to_string(level));
+                for (int k = 0; k < op.d; ++k) {
+                    E[k] = pxl.node[k];
+                    B[k] = pxl.node_band[k];
+                }
+            }
+            sweep(fs, E, B);
+        }
+        std::vector<int> fine_slot(static_cast<size_t>(fine.size()));
+        for (int i = 0; i < rule->size(); ++i) fine_slot[static_cast<size_t>(2 * i)] = slot_of[static_cast<size_t>(i)];
+        for (int k = 0; k < fresh; ++k)
+            fine_slot[static_cast<size_t>(2 * k + 1)] = level == 1 ? 2 * k + 1 : base + k;
+        const int nxt = 1 - cur;
+        std::vector<int> idx(static_cast<size_t>(fine.size()));
+        std::iota(idx.begin(), idx.end(), 0);
+        std::vector<double> cf;
+        node_coefs(fine, idx, p, cf);
+        const double* cf_dev = static_cast<const double*>(arena_push(c, cf.data(), cf.size() * sizeof(double)));
+        const int* sl_dev = static_cast<const int*>(arena_push(c, fine_slot.data(), fine_slot.size() * sizeof(int)));
+        const double* cc_dev = nullptr;
+        if (fused && level == 1) {  // coarse rule node k = fine node 2k
+            std::vector<int> cidx(static_cast<size_t>(rule->size()));
+            std::iota(cidx.begin(), cidx.end(), 0);
+            std::vector<double> c7, cc(cf.size(), 0.0);
+            node_coefs(*rule, cidx, p, c7);
+            for (int k = 0; k < rule->size(); ++k)
+                for (int j = 0; j < p; ++j) cc[static_cast<size_t>(2 * k) * p + j] = c7[static_cast<size_t>(k) * p + j];
+            cc_dev = static_cast<const double*>(arena_push(c, cc.data(), cc.size() * sizeof(double)));
+        }
+        arena_flush(c);
+        cuda_check(cudaMemsetAsync(stats, 0, sizeof(double) * 2 * nb * p, c.stream), "cc stats zero");
+        if (S > 0) {
+            if (fused) {
+                for (int mm = 0; mm < nb; ++mm) {
+                    KernelProbe kp(c, "k_node_combine_ring", 8.0 * S * (fine.size() + p + (level == 1 ? 0 : p)));
+                    launch_combine_stats(S, p, fine.size(), slab + mm * S, static_cast<long long>(nb) * S, sl_dev, cf_dev,
+                                         cc_dev, level == 1 ? nullptr : accs[cur] + mm * p * S, accs[nxt] + mm * p * S, S,
+                                         stats + 2 * mm * p, c.stream);
+                    count_launch(c);
+                }
+            } else {
+                if (level == 1) {  // the 7-point sums this level is compared against
+                    std::vector<int> cidx(static_cast<size_t>(rule->size()));
+                    std::iota(cidx.begin(), cidx.end(), 0);
+                    std::vector<double> c7;
+                    node_coefs(*rule, cidx, p, c7);
+                    const double* c7_dev = static_cast<const double*>(arena_push(c, c7.data(), c7.size() * sizeof(double)));
+                    const int* s7_dev = static_cast<const int*>(arena_push(c, slot_of.data(), slot_of.size() * sizeof(int)));
+                    arena_flush(c);
+                    for (int mm = 0; mm < nb; ++mm) {
+                        launch_combine(S, p, rule->size(), slab + mm * S, static_cast<long long>(nb) * S, s7_dev, c7_dev,
+                                       accs[cur] + mm * p * S, S, 1, c.stream);
+                        count_launch(c);
+                    }
+                }
+                for (int mm = 0; mm < nb; ++mm) {
+                    launch_combine(S, p, fine.size(), slab + mm * S, static_cast<long long>(nb) * S, sl_dev, cf_dev,
+                                   accs[nxt] + mm * p * S, S, 1, c.stream);
+                    count_launch(c);
+                }
+                launch_colstats(S, nb * p, accs[nxt], accs[cur], stats, c.stream);
+                count_launch(c);
+            }
+        }
+        // the statistics are max-norms: one exact all-reduce(max) gives every rank the global
+        // ||y - y_prev||_inf and ||y||_inf per column (phiaction.hpp:225-239)
+        allreduce_max(c, m, stats, 2 * nb * p);
+        cuda_check(cudaMemcpyAsync(hstats.data(), stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
+                   "cc stats readback");
+        cuda_check(cudaStreamSynchronize(c.stream), "cc stats wait");
+        half = half_next;
+        rule = &fine;
+        slot_of = std::move(fine_slot);
+        cur = nxt;
+        double err = 0.0;
+        for (int k = 0; k < nb * p; ++k) {
+            const double diff = hstats[2 * static_cast<size_t>(k)], norm = hstats[2 * static_cast<size_t>(k) + 1];
+            if (diff == 0.0) continue;
+            err = std::max(err, norm == 0.0 ? std::numeric_limits<double>::infinity() : diff / norm);
+        }
+        if (err <= eps) break;
+    }
+    if (accs[cur] != out && col > 0)
+        cuda_check(cudaMemcpyAsync(out, accs[cur], col * sizeof(double), cudaMemcpyDeviceToDevice, c.stream), "cc copy");
+    if (points_used) *points_used = rule->size();
+}
+
+// The whole distributed call: out [nb][p][S_r] (phi_1..phi_p slabs), phi0 [nb][S_r] (nullable).
+void phi_dist(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, const double* bs, int p, int l, int n,
+              int kind, double eps, double* out, double* phi0, int* points_used) {
+    if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
+    const long long S = g.S(g.r);
+    const NodesWeights& rule = kind == kGauss ? memo_rule(kGauss, n + 1) : memo_rule(kClenshaw, 25);
+    // owned node slots and their thetas: Gauss slot i = node i; CC slots 0..12 = 25-rule nodes 2s,
+    // slots 13..24 = 25-rule nodes 2(s - 13) + 1
+    std::vector<int> all(static_cast<size_t>(rule.size()));
+    std::iota(all.begin(), all.end(), 0);
+    const std::vector<int> own = owned(all, g);
+    std::vector<double> th;
+    for (int s : own) th.push_back(kind == kGauss ? rule.x[static_cast<size_t>(s)]
+                                                  : rule.x[static_cast<size_t>(s < 13 ? 2 * s : 2 * (s - 13) + 1)]);
+    const PhiExps px = phi_exponentials(c, op, 1.0, l, th, l > 0, phi0 != nullptr, "dnodeE", true, false);
+    mark(c, "exps");
+    const size_t col = static_cast<size_t>(nb) * p * std::max<long long>(S, 1);
+    double* y = out;
+    double* t = l > 0 ? ws(c, "dsqT", col) : nullptr;
+    double* first = (l % 2 == 1) ? t : out;
+    if (kind == kGauss) {
+        gauss_nodes(c, m, g, op, nb, bs, p, rule, px, own, first);
+        if (points_used) *points_used = rule.size();
+    } else {
+        cc_nodes(c, m, g, op, l, nb, bs, p, eps, px, own, first, points_used);
+    }
+    mark(c, "nodes");
+    // phi_0: one distributed Kronecker apply of expm(A) to the slabs of b (b is replicated)
+    if (phi0) {
+        dist_kron(c, m, g, px.phi0, px.phi0_band, bs + g.lo(g.r), op.N, nb, phi0);
+    }
+    // l modified-squaring steps on the slabs (phiaction.hpp:255-272): T = (E (x) E (x) E) y,
+    // T_i <- 2^-i (T_i + sum_{j<=i} y_j/(i-j)!); E_j = expm(2^(j-l) A) from the chain
+    if (l > 0) {
+        std::vector<double> inv(static_cast<size_t>(p), 1.0);
+        for (int k = 1; k < p; ++k) inv[static_cast<size_t>(k)] = inv[static_cast<size_t>(k) - 1] / k;
+        std::vector<double> coef(static_cast<size_t>(p) * p, 0.0);
+        for (int i = 0; i < p; ++i)
+            for (int j = 0; j <= i; ++j)
+                coef[static_cast<size_t>(i) * p + j] = std::ldexp(1.0, -(i + 1)) * inv[static_cast<size_t>(i - j)];
+        const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
+        arena_flush(c);
+        double* cur = first;
+        double* nxt = first == out ? t : out;
+        for (int step = 0; step < l; ++step) {
+            const double* E[3];
+            const int2* B[3];
+            for (int k = 0; k < op.d; ++k) {
+                const long long nk = static_cast<long long>(op.n[k]) * op.n[k];
+                E[k] = px.sq[k] + step * nk;
+                B[k] = px.sq_band[k] ? px.sq_band[k] + step * band_row_blocks(op.n[k]) : nullptr;
+            }
+            dist_kron(c, m, g, E, B, cur, S, nb * p, nxt);
+            if (S > 0) {
+                KernelProbe kp(c, "k_sq_combine2", 8.0 * S * nb * 3 * p);
+                launch_sq_combine(S, p, nb, nxt, cur, coef_dev, c.stream);
+                count_launch(c);
+            }
+            std::swap(cur, nxt);
+        }
+        y = cur;
+        (void)y;
+    }
+    mark(c, "squaring");
+}
+
+// slabs [ncols][S_r] -> full vectors [ncols][N] on every rank
+void gather_slabs(pq_ctx& c, pq_comm& m, const Geom& g, const double* slab, int ncols, double* full) {
+    std::vector<Piece> sends, recvs;
+    for (int col = 0; col < ncols; ++col)
+        for (int h = 0; h < g.G; ++h) {
+            sends.push_back({h, const_cast<double*>(slab) + col * g.S(g.r), g.S(g.r)});
+            recvs.push_back({h, full + col * g.N + g.lo(h), g.S(h)});
+        }
+    exchange(c, m, sends, recvs);
+}
+
+void need_comm(pq_comm* m) {
+    if (!m) throw std::invalid_argument("pq: null communicator");
+}
+
+long long dim_of(int d, const int* shape) {
+    need(d >= 1 && d <= 3 && shape, "KroneckerSum: need one to three factors");
+    long long n = 1;
+    for (int k = 0; k < d; ++k) {
+        need(shape[k] > 0, "KroneckerSum: factors must be square and nonempty");
+        n *= shape[k];
+    }
+    return n;
+}
+
+// common body of the two distributed entry points
+void run_dist(pq_ctx* c, pq_comm* m, int d, const int* shape, const double* factors, int nb, const double* bs,
+              const pq_phi_request* req, bool plan, int p, int l, int n, int kind, double eps, double* out0, double* out,
+              pq_phi_info* info, int* points_used, int space, int gather) {
+    if (!c) throw std::invalid_argument("pq: null context");
+    need_comm(m);
+    cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+    const long long N = dim_of(d, shape);
+    need(nb >= 1, "phiquadmv: need at least one right-hand side");
+    const Geom g = make_geom(d, shape, m->world, m->rank);
+    arena_begin(*c);
+    DevOp op = upload_op(*c, d, shape, factors, "factors");
+    const double* db = bs;
+    if (space == PQ_HOST) {
+        double* t = ws(*c, "hin_b", static_cast<size_t>(nb) * N);
+        cuda_check(cudaMemcpyAsync(t, bs, sizeof(double) * nb * N, cudaMemcpyHostToDevice, c->stream), "H2D");
+        db = t;
+    }
+    PlanInfo pi;
+    if (plan) {
+        pi = plan_phi(*c, op, nb, db, req->p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2);
+        p = req->p;
+        l = pi.l;
+        n = pi.n;
+        kind = req->mode;
+        eps = req->eps;
+    }
+    if (p < 1) throw std::invalid_argument(kind == kGauss ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
+    const long long S = g.S(g.r);
+    double* os = ws(*c, "dout", static_cast<size_t>(nb) * p * std::max<long long>(S, 1));
+    double* o0 = out0 ? ws(*c, "dout0", static_cast<size_t>(nb) * std::max<long long>(S, 1)) : nullptr;
+    int points = 0;
+    phi_dist(*c, *m, g, op, nb, db, p, l, n, kind, eps, os, o0, &points);
+    // results: slabs (gather == 0) or full vectors on every rank
+    auto deliver = [&](const double* slab, int ncols, double* dst) {
+        if (!dst) return;
+        if (gather) {
+            double* full = space == PQ_DEVICE ? dst : ws(*c, "dgather", static_cast<size_t>(ncols) * N);
+            gather_slabs(*c, *m, g, slab, ncols, full);
+            if (space == PQ_HOST)
+                cuda_check(cudaMemcpyAsync(dst, full, sizeof(double) * ncols * N, cudaMemcpyDeviceToHost, c->stream), "D2H");
+        } else {
+            cuda_check(cudaMemcpyAsync(dst, slab, sizeof(double) * ncols * S,
+                                       space == PQ_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream),
+                       "slab out");
+        }
+    };
+    deliver(os, nb * p, out);
+    deliver(o0, nb, out0);
+    if (space == PQ_HOST) cuda_check(cudaStreamSynchronize(c->stream), "sync");
+    if (info) {
+        info->l = l;
+        info->n = n;
+        info->points = points;
+        info->mode = kind;
+        info->planned = pi.planned;
+        info->alpha = pi.alpha;
+        info->beta = pi.beta;
+        info->plan_cost = pi.cost;
+    }
+    if (points_used) *points_used = points;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pq_nccl_unique_id(char* out128) {
+    return guarded([&] {
+        need(out128 != nullptr, "pq_nccl_unique_id: null output");
+        ncclUniqueId id;
+        nccl_check(nccl_api().getUniqueId(&id), "get unique id");
+        static_assert(sizeof(id.internal) == 128, "ncclUniqueId is 128 bytes");
+        std::memcpy(out128, id.internal, 128);
+    });
+}
+
+int pq_comm_create_nccl(pq_ctx* ctx, int world, int rank, const char* id128, pq_comm** out) {
+    return guarded([&] {
+        need(ctx && out && id128, "pq_comm_create_nccl: null argument");
+        need(world >= 1 && world <= 16 && rank >= 0 && rank < world, "pq_comm_create_nccl: bad world/rank");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        auto* m = new pq_comm();
+        m->world = world;
+        m->rank = rank;
+        m->kind = PQ_COMM_NCCL;
+        if (world > 1) {
+            ncclUniqueId id;
+            std::memcpy(id.internal, id128, 128);
+            const ncclResult_t r = nccl_api().commInitRank(&m->nccl, world, id, rank);
+            if (r != ncclSuccess) {
+                delete m;
+                nccl_check(r, "comm init");
+            }
+        }
+        *out = m;
+    });
+}
+
+int pq_comm_create_host(int world, int rank, const pq_host_transport* t, pq_comm** out) {
+    return guarded([&] {
+        need(out != nullptr, "pq_comm_create_host: null output");
+        need(world >= 1 && world <= 16 && rank >= 0 && rank < world, "pq_comm_create_host: bad world/rank");
+        need(world == 1 || (t && t->alltoallv && t->allreduce_max), "pq_comm_create_host: transport callbacks missing");
+        auto* m = new pq_comm();
+        m->world = world;
+        m->rank = rank;
+        m->kind = PQ_COMM_HOST;
+        if (t) m->host = *t;
+        *out = m;
+    });
+}
+
+int pq_comm_destroy(pq_comm* m) {
+    return guarded([&] {
+        if (!m) return;
+        if (m->nccl) nccl_api().commDestroy(m->nccl);
+        if (m->hs) cudaFreeHost(m->hs);
+        if (m->hr) cudaFreeHost(m->hr);
+        delete m;
+    });
+}
+
+int pq_comm_stats(pq_comm* m, int reset, double* bytes_sent, uint64_t* exchanges) {
+    return guarded([&] {
+        need_comm(m);
+        if (bytes_sent) *bytes_sent = m->bytes_sent;
+        if (exchanges) *exchanges = m->exchanges;
+        if (reset) {
+            m->bytes_sent = 0.0;
+            m->exchanges = 0;
+        }
+    });
+}
+
+int pq_dist_slab(int d, const int* shape, int world, int rank, int64_t* begin, int64_t* end) {
+    return guarded([&] {
+        dim_of(d, shape);
+        const Geom g = make_geom(d, shape, world, rank);
+        if (begin) *begin = g.lo(rank);
+        if (end) *end = g.lo(rank) + g.S(rank);
+    });
+}
+
+int pq_phiquadmv_dist(pq_ctx* ctx, pq_comm* comm, int d, const int* shape, const double* factors, int nb,
+                      const double* bs, const pq_phi_request* req, double* out0, double* out, pq_phi_info* info,
+                      int space, int gather) {
+    return guarded([&] {
+        need(req != nullptr, "phiquadmv: null request");
+        need(req->p >= 1, "phiquadmv: need p >= 1");
+        need(req->mode == PQ_GAUSS_LEGENDRE || req->mode == PQ_CLENSHAW_CURTIS, "QuadKind: unknown rule");
+        run_dist(ctx, comm, d, shape, factors, nb, bs, req, true, 0, 0, 0, 0, 0.0, out0, out, info, nullptr, space,
+                 gather);
+    });
+}
+
+int pq_phi_with_plan_dist(pq_ctx* ctx, pq_comm* comm, int d, const int* shape, const double* factors, int nb,
+                          const double* bs, int p, int l, int n, int kind, double eps, double* out, int* points_used,
+                          int space, int gather) {
+    return guarded([&] {
+        need(l >= 0, "phi_with_plan: need l >= 0");
+        need(kind == PQ_GAUSS_LEGENDRE || kind == PQ_CLENSHAW_CURTIS, "QuadKind: unknown rule");
+        if (kind == PQ_GAUSS_LEGENDRE) need(n + 1 >= 1, "gauss_legendre: need at least one point");
+        need(p >= 1, kind == PQ_GAUSS_LEGENDRE ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
+        run_dist(ctx, comm, d, shape, factors, nb, bs, nullptr, false, p, l, n, kind, eps, nullptr, out, nullptr,
+                 points_used, space, gather);
+    });
+}
+
+}  // extern "C"

@@ -15,6 +15,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <numeric>
 
 namespace pqb {
@@ -36,6 +38,31 @@ static size_t budget_bytes(pq_ctx& c) {
     return static_cast<size_t>(c.ws_limit);
 }
 
+// Workspace memory comes from a per-device stream-ordered pool that keeps what it holds
+// (release threshold = max): after the first calls at a size no allocation reaches the driver,
+// and retired buffers return to the pool with cudaFreeAsync at the next call's start.  Plain
+// cudaMalloc / cudaFree inside a call cost 10-100 ms on the B200 in the acceptance gate's
+// criterion 7 (PQ_SLOWLOG timelines, profiles/r02_summary.md).
+static cudaMemPool_t device_pool(int dev) {
+    static std::mutex mu;
+    static std::map<int, cudaMemPool_t> pools;
+    std::lock_guard<std::mutex> hold(mu);
+    auto it = pools.find(dev);
+    if (it != pools.end()) return it->second;
+    cudaMemPoolProps props{};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = dev;
+    cudaMemPool_t p = nullptr;
+    cuda_check(cudaMemPoolCreate(&p, &props), "cudaMemPoolCreate");
+    uint64_t keep = ~uint64_t(0);
+    cuda_check(cudaMemPoolSetAttribute(p, cudaMemPoolAttrReleaseThreshold, &keep), "pool threshold");
+    pools[dev] = p;
+    return p;
+}
+
+void trim_pool(pq_ctx& c) { cudaMemPoolTrimTo(device_pool(c.device), 0); }
+
 void free_graveyard(pq_ctx& c) {
     if (c.graveyard.empty()) return;
     cuda_check(cudaDeviceSynchronize(), "sync before workspace free");
@@ -43,27 +70,40 @@ void free_graveyard(pq_ctx& c) {
     c.graveyard.clear();
 }
 
+// retired buffers back to the pool, stream-ordered after everything this context enqueued so far
+// (every call joins its helper streams into c.stream before returning)
+void recycle_graveyard(pq_ctx& c) {
+    for (void* p : c.graveyard) cuda_check(cudaFreeAsync(p, c.stream), "cudaFreeAsync(workspace)");
+    c.graveyard.clear();
+}
+
+void* dev_alloc(pq_ctx& c, size_t bytes, const char* what) {
+    void* p = nullptr;
+    cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, device_pool(c.device), c.stream);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        free_graveyard(c);
+        trim_pool(c);
+        e = cudaMallocFromPoolAsync(&p, bytes, device_pool(c.device), c.stream);
+    }
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        throw CudaError(std::string("device workspace '") + what + "': cannot allocate " + std::to_string(bytes >> 20) +
+                        " MiB");
+    }
+    return p;
+}
+
 void* ws_bytes(pq_ctx& c, const std::string& name, size_t bytes) {
     DevBuf& b = c.bufs[name];
     if (b.bytes >= bytes && b.p) return b.p;
-    // the old buffer may still be read by enqueued work: retire it without a sync (freed at
-    // release / destroy / an allocation failure, see pq_ctx::graveyard)
+    // the old buffer may still be read by enqueued work: retire it (pq_ctx::graveyard)
     if (b.p) c.graveyard.push_back(b.p);
     b.p = nullptr;
     b.bytes = 0;
     const size_t want = std::max<size_t>(bytes, 256);
     mark(c, ("ws_grow:" + name).c_str());
-    cudaError_t e = cudaMalloc(&b.p, want);
-    if (e != cudaSuccess && !c.graveyard.empty()) {
-        cudaGetLastError();
-        free_graveyard(c);
-        e = cudaMalloc(&b.p, want);
-    }
-    if (e != cudaSuccess) {
-        cudaGetLastError();
-        b.p = nullptr;
-        throw CudaError("device workspace '" + name + "': cannot allocate " + std::to_string(want >> 20) + " MiB");
-    }
+    b.p = dev_alloc(c, want, name.c_str());
     b.bytes = want;
     return b.p;
 }
@@ -74,6 +114,7 @@ double* ws(pq_ctx& c, const std::string& name, size_t count) {
 
 void arena_begin(pq_ctx& c) {
     c.deferred.clear();  // never carry side-stream work from an earlier (failed) call
+    recycle_graveyard(c);
     ParamArena& a = c.arena;
     if (!a.host) {
         a.cap = size_t(8) << 20;
@@ -787,21 +828,10 @@ void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_
 // Bitwise-identical factors are exponentiated once (e.g. the isotropic Laplacians of configs
 // 1, 3, 4, 5): dims sharing a factor share the pointers.  With late_async the squaring chain and
 // phi_0 matrices are finished on the side stream (late = true: wait on c.ev_late before use).
-struct PhiExps {
-    const double* node[3] = {nullptr, nullptr, nullptr};
-    const double* sq[3] = {nullptr, nullptr, nullptr};
-    const double* phi0[3] = {nullptr, nullptr, nullptr};
-    int sq_len = 1;
-    bool late = false;
-    // negligible-block tables parallel to node/sq/phi0 (band_row_blocks(n_k) entries per matrix)
-    const int2* node_band[3] = {nullptr, nullptr, nullptr};
-    const int2* sq_band[3] = {nullptr, nullptr, nullptr};
-    const int2* phi0_band[3] = {nullptr, nullptr, nullptr};
-};
 
-static PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, const std::vector<double>& thetas,
-                                bool want_sq, bool want_phi0, const std::string& tag, bool sq_chain = false,
-                                bool late_async = false) {
+
+PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, const std::vector<double>& thetas,
+                         bool want_sq, bool want_phi0, const std::string& tag, bool sq_chain, bool late_async) {
     PhiExps px;
     const int q = static_cast<int>(thetas.size());
     const int L = want_sq ? (sq_chain ? std::max(l, 1) : 1) : 0;
@@ -958,6 +988,21 @@ GemmArgs mode_gemm_public(int d, const int* n, int mode, const double* E, const 
     return mode_gemm(d, n, mode, E, 0, x, N, y, N, nb, N);
 }
 
+void mode_product_dev(pq_ctx& c, int d, const int* n, int k, const double* E, const int2* band, const double* x,
+                      long long x_stride, double* y, long long y_stride, int Z1) {
+    long long N = 1;
+    for (int i = 0; i < d; ++i) N *= n[i];
+    GemmArgs g = mode_gemm(d, n, k, E, 0, x, x_stride, y, y_stride, Z1, N);
+    if (band) {  // one exponential shared by the batch (E_stride 0), as mode_chain sets it up
+        g.band = band;
+        g.band_rows = n[k];
+        g.band_stride = 0;
+        g.band_mode = g.b_kmajor ? 3 : 2;
+    }
+    gemm(c, g);
+    check_launch(c);
+}
+
 void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride, const double* x,
                 long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep, const char* tmp_tag,
                 const int2* const* band) {
@@ -1053,7 +1098,7 @@ void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, 
     check_launch(c);
 }
 
-static void apply_phi0(pq_ctx& c, const DevOp& op, const PhiExps& px, int nb, const double* b, double* y) {
+void apply_phi0(pq_ctx& c, const DevOp& op, const PhiExps& px, int nb, const double* b, double* y) {
     long long Es[3] = {0, 0, 0};
     mode_chain(c, op.d, op.n, px.phi0, Es, b, op.N, y, op.N, nb, Epilogue{}, "phi0", px.phi0_band);
 }
@@ -1079,7 +1124,7 @@ double max_inf_norm_dev(pq_ctx& c, const double* v, long long N, int ncols) {
 // ------------------------------------------------------------------ the node sweep -------
 
 // phiaction.hpp:102-107: coefficient w_i theta_i^{j-1}/(j-1)! by the same running product.
-static void node_coefs(const NodesWeights& r, const std::vector<int>& idx, int p, std::vector<double>& out) {
+void node_coefs(const NodesWeights& r, const std::vector<int>& idx, int p, std::vector<double>& out) {
     out.assign(idx.size() * static_cast<size_t>(p), 0.0);
     for (size_t a = 0; a < idx.size(); ++a) {
         const double th = r.x[static_cast<size_t>(idx[a])];
@@ -1099,7 +1144,7 @@ static int node_chunk(pq_ctx& c, long long N, int q, int per_node_vectors) {
     return std::min(q, qc);
 }
 
-static std::vector<double> thetas_of(const NodesWeights& r, const std::vector<int>& idx) {
+std::vector<double> thetas_of(const NodesWeights& r, const std::vector<int>& idx) {
     std::vector<double> t;
     for (int i : idx) t.push_back(r.x[static_cast<size_t>(i)]);
     return t;
@@ -1108,9 +1153,9 @@ static std::vector<double> thetas_of(const NodesWeights& r, const std::vector<in
 // For the selected nodes (exponentials E[k] + a*Es[k], a < q), v_a = (E_a0 (x) E_a1 (x) E_a2) b_m;
 // either combined into acc [nb][p][N] with coefficients coef [q][p] (zeroing first if `zero`),
 // or stored into pool + (slot0 + a)*nb*N + m*N.
-static void node_sweep(pq_ctx& c, const DevOp& op, const double* const* E, const long long* Es, int q, int nb,
-                       const double* bs, int p, const std::vector<double>* coef, double* acc, int zero, double* pool,
-                       int slot0, const int2* const* band = nullptr) {
+void node_sweep(pq_ctx& c, const DevOp& op, const double* const* E, const long long* Es, int q, int nb,
+                const double* bs, int p, const std::vector<double>* coef, double* acc, int zero, double* pool,
+                int slot0, const int2* const* band) {
     // band tables follow their exponentials: matrix a of E[k] (stride Es[k]) <-> band[k] + a (Es[k]/n^2) RB
     auto band_at = [&](int a0, const int2** out) {
         for (int k = 0; k < op.d; ++k) {
@@ -1260,13 +1305,9 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             DevBuf& b = c.bufs["ccpool"];
             const size_t want = static_cast<size_t>(used + fr) * nb * N * sizeof(double);
             if (b.bytes < want) {
-                double* np = nullptr;
-                cuda_check(cudaStreamSynchronize(c.stream), "pool grow sync");
-                if (cudaMalloc(&np, want) != cudaSuccess) {
-                    cudaGetLastError();
-                    throw CudaError("adaptive CC node pool: out of device memory");
-                }
-                cuda_check(cudaMemcpy(np, b.p, static_cast<size_t>(used) * nb * N * sizeof(double), cudaMemcpyDeviceToDevice),
+                double* np = static_cast<double*>(dev_alloc(c, want, "ccpool"));
+                cuda_check(cudaMemcpyAsync(np, b.p, static_cast<size_t>(used) * nb * N * sizeof(double),
+                                           cudaMemcpyDeviceToDevice, c.stream),
                            "pool copy");
                 c.graveyard.push_back(b.p);
                 b.p = np;
@@ -1720,35 +1761,34 @@ void phi_with_plan_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const d
 }
 
 // phiaction.hpp:307-346 (+ phi_0 when phi0_out).
-void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l, int l,
-                   double c1, double c2, double* out, PlanInfo* info, double* phi0_out, double* phi0_host,
-                   double* out_host, bool* out_copied) {
-    if (p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
-    double alpha = 0.0;
-    for (int k = 0; k < op.d; ++k) alpha += op.inf_norm[k];
-    // beta = max ||b||_inf: reduce on the device, read back through pinned memory on an event;
-    // phi_0 (independent of the plan) is enqueued first so the GPU works while the host plans.
+// beta = max ||b||_inf: reduced on the device and read back into pinned c.h_beta on ev_beta
+// (nb <= 512); larger batches reduce synchronously and return beta directly (>= 0 then).
+static double beta_enqueue(pq_ctx& c, const DevOp& op, int nb, const double* bs) {
+    if (nb > 512) return max_inf_norm_dev(c, bs, op.N, nb);
+    if (nb <= 0) return 0.0;
+    double* stats = ws(c, "colstats", 2 * static_cast<size_t>(nb));
+    launch_colstats(op.N, nb, bs, nullptr, stats, c.stream);
+    count_launch(c);
+    if (!c.ev_beta) cuda_check(cudaEventCreateWithFlags(&c.ev_beta, cudaEventDisableTiming), "beta event");
+    cuda_check(cudaMemcpyAsync(c.h_beta, stats, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, c.stream),
+               "beta readback");
+    cuda_check(cudaEventRecord(c.ev_beta, c.stream), "beta record");
+    return -1.0;
+}
+
+// waits for the readback (any thread) and reduces the per-column maxima
+static double beta_collect(pq_ctx& c, int nb) {
+    cuda_check(cudaEventSynchronize(c.ev_beta), "beta wait");
     double beta = 0.0;
-    if (nb > 512) {  // beyond the pinned scratch: plain synchronous reduction
-        beta = max_inf_norm_dev(c, bs, op.N, nb);
-    } else if (nb > 0) {
-        double* stats = ws(c, "colstats", 2 * static_cast<size_t>(nb));
-        launch_colstats(op.N, nb, bs, nullptr, stats, c.stream);
-        count_launch(c);
-        if (!c.ev_beta) cuda_check(cudaEventCreateWithFlags(&c.ev_beta, cudaEventDisableTiming), "beta event");
-        cuda_check(cudaMemcpyAsync(c.h_small, stats, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, c.stream),
-                   "beta readback");
-        cuda_check(cudaEventRecord(c.ev_beta, c.stream), "beta record");
-    }
-    // the exponentials' shared Taylor powers do not depend on the plan: enqueue them before the
-    // host waits for beta, so the GPU computes them while the host plans
-    taylor_prefetch(c, op, 1.0);
-    if (nb > 0 && nb <= 512) {
-        cuda_check(cudaEventSynchronize(c.ev_beta), "beta wait");
-        for (int m = 0; m < nb; ++m) beta = std::max(beta, c.h_small[2 * m + 1]);
-    }
-    mark(c, "beta_ready");
-    Cost cost{c1, c2, op.d};
+    for (int m = 0; m < nb; ++m) beta = std::max(beta, c.h_beta[2 * m + 1]);
+    return beta;
+}
+
+// phiaction.hpp:312-340 on the host: setup_quadrature (or quadnodes at a pinned l)
+static PlanInfo plan_host(int d, double alpha, double beta, int p, double eps, int mode, bool has_l, int l, double c1,
+                          double c2) {
+    Cost cost{c1, c2, d};
+    PlanInfo info;
     int n = 0;
     bool planned = false;
     double plan_cost = 0.0;
@@ -1771,19 +1811,163 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
         plan_cost = cost(n, l, p);
         planned = true;
     }
+    info.l = l;
+    info.n = n;
+    info.mode = mode;
+    info.planned = planned ? 1 : 0;
+    info.alpha = alpha;
+    info.beta = beta;
+    info.cost = plan_cost;
+    return info;
+}
+
+static double alpha_of(const DevOp& op) {
+    double alpha = 0.0;
+    for (int k = 0; k < op.d; ++k) alpha += op.inf_norm[k];
+    return alpha;
+}
+
+PlanInfo plan_phi(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l, int l,
+                  double c1, double c2) {
+    if (p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
+    double beta = beta_enqueue(c, op, nb, bs);
+    // the exponentials' shared Taylor powers do not depend on the plan: enqueue them before the
+    // host waits for beta, so the GPU computes them while the host plans
+    taylor_prefetch(c, op, 1.0);
+    if (beta < 0.0) beta = beta_collect(c, nb);
+    mark(c, "beta_ready");
+    const PlanInfo info = plan_host(op.d, alpha_of(op), beta, p, eps, mode, has_l, l, c1, c2);
     mark(c, "planned");
-    int points = 0;
-    phi_call_dev(c, op, 1.0, nb, bs, p, l, n, mode, eps, out, &points, phi0_out, phi0_host, out_host, out_copied);
-    if (info) {
-        info->l = l;
-        info->n = n;
-        info->points = points;
-        info->mode = mode;
-        info->planned = planned ? 1 : 0;
-        info->alpha = alpha;
-        info->beta = beta;
-        info->cost = plan_cost;
+    return info;
+}
+
+// ---- planner worker thread ----
+void worker_submit(pq_ctx& c, std::function<void()> job) {
+    if (!c.worker) {
+        c.worker = std::make_unique<pq_ctx::Worker>();
+        pq_ctx::Worker* w = c.worker.get();
+        w->th = std::thread([w] {
+            std::unique_lock<std::mutex> lk(w->mu);
+            while (true) {
+                w->cv.wait(lk, [w] { return w->has_job || w->stop; });
+                if (w->stop) return;
+                std::function<void()> f = std::move(w->job);
+                w->has_job = false;
+                lk.unlock();
+                std::exception_ptr err;
+                try {
+                    f();
+                } catch (...) {
+                    err = std::current_exception();
+                }
+                lk.lock();
+                w->err = err;
+                w->busy = false;
+                w->cv.notify_all();
+            }
+        });
     }
+    pq_ctx::Worker* w = c.worker.get();
+    std::lock_guard<std::mutex> lk(w->mu);
+    w->job = std::move(job);
+    w->has_job = true;
+    w->busy = true;
+    w->err = nullptr;
+    w->cv.notify_all();
+}
+
+void worker_wait(pq_ctx& c) {
+    if (!c.worker) return;
+    pq_ctx::Worker* w = c.worker.get();
+    std::unique_lock<std::mutex> lk(w->mu);
+    w->cv.wait(lk, [w] { return !w->busy; });
+    if (w->err) {
+        std::exception_ptr e = w->err;
+        w->err = nullptr;
+        std::rethrow_exception(e);
+    }
+}
+
+void worker_stop(pq_ctx& c) {
+    if (!c.worker) return;
+    {
+        std::lock_guard<std::mutex> lk(c.worker->mu);
+        c.worker->stop = true;
+        c.worker->cv.notify_all();
+    }
+    if (c.worker->th.joinable()) c.worker->th.join();
+    c.worker.reset();
+}
+
+static bool plan_spec_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PQ_PLAN_SPEC");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l, int l,
+                   double c1, double c2, double* out, PlanInfo* info, double* phi0_out, double* phi0_host,
+                   double* out_host, bool* out_copied) {
+    if (p < 1) throw std::invalid_argument("phiquadmv: need p >= 1");
+    // the last plan for this operator (bit-identical factors share the cached host copy) and request
+    pq_ctx::PlanMemo* memo = nullptr;
+    for (auto& m : c.plan_memo)
+        if (m.host == op.host && m.p == p && m.mode == mode && m.has_l == (has_l ? 1 : 0) && m.l_in == (has_l ? l : 0) &&
+            m.eps == eps && m.c1 == c1 && m.c2 == c2)
+            memo = &m;
+    const bool spec = memo && plan_spec_enabled() && nb > 0 && nb <= 512 && !c.profiling;
+    PlanInfo pi;
+    int points = 0;
+    if (!spec) {
+        pi = plan_phi(c, op, nb, bs, p, eps, mode, has_l, l, c1, c2);
+        phi_call_dev(c, op, 1.0, nb, bs, p, pi.l, pi.n, mode, eps, out, &points, phi0_out, phi0_host, out_host,
+                     out_copied);
+    } else {
+        // speculation: the pipeline with the remembered plan is enqueued while the worker thread
+        // waits for beta and plans; the GPU never idles for the host planner
+        const int sl = memo->l, sn = memo->n;
+        beta_enqueue(c, op, nb, bs);
+        const double alpha = alpha_of(op);
+        const int d = op.d;
+        worker_submit(c, [&c, &pi, nb, d, alpha, p, eps, mode, has_l, l, c1, c2] {
+            pi = plan_host(d, alpha, beta_collect(c, nb), p, eps, mode, has_l, l, c1, c2);
+        });
+        try {
+            phi_call_dev(c, op, 1.0, nb, bs, p, sl, sn, mode, eps, out, &points, phi0_out, phi0_host, out_host,
+                         out_copied);
+        } catch (...) {
+            try {
+                worker_wait(c);
+            } catch (...) {
+            }
+            throw;
+        }
+        worker_wait(c);
+        mark(c, "planned");
+        // for the adaptive CC rule n only sets the ladder speculation depth, not the result
+        if (pi.l != sl || (mode == kGauss && pi.n != sn)) {
+            ++c.plan_spec_misses;
+            c.early.clear();  // the speculative run's early host copies are superseded
+            if (out_copied) *out_copied = false;
+            phi_call_dev(c, op, 1.0, nb, bs, p, pi.l, pi.n, mode, eps, out, &points, phi0_out, phi0_host, out_host,
+                         out_copied);
+        } else {
+            ++c.plan_spec_hits;
+        }
+    }
+    if (!memo) {
+        c.plan_memo.push_back({});
+        memo = &c.plan_memo.back();
+        if (c.plan_memo.size() > 16) {
+            c.plan_memo.erase(c.plan_memo.begin());
+            memo = &c.plan_memo.back();
+        }
+    }
+    *memo = pq_ctx::PlanMemo{op.host, p, mode, has_l ? 1 : 0, has_l ? l : 0, eps, c1, c2, pi.l, pi.n};
+    pi.points = points;
+    if (info) *info = pi;
 }
 
 // phiaction.hpp:355-389: one sweep of the combined integrand sum_j theta^{j-1}/(j-1)! b_j.

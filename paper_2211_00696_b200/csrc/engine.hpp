@@ -6,12 +6,16 @@
 
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdint>
+#include <exception>
 #include <functional>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "estimator.hpp"
@@ -56,6 +60,7 @@ struct pq_ctx {
     pqb::ParamArena arena;
     int* d_err = nullptr;        // device error flag (singular LU)
     double* h_small = nullptr;   // pinned readback scratch
+    double* h_beta = nullptr;    // pinned readback of the planner's beta (read by the planner thread)
     double* d_small = nullptr;   // device scratch for reductions
     int* d_int = nullptr;        // device int scratch (expm squaring counts)
     bool profiling = false;
@@ -90,6 +95,27 @@ struct pq_ctx {
     uint64_t fac_band_serial = 0;
     const int2* fac_band[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev_beta = nullptr;  // beta readback (phiquadmv) completes
+    // Plan speculation (engine.cpp phiquadmv_dev): the last plan per operator/request; a call on
+    // the same operator enqueues its pipeline with that plan while a host worker thread reads beta
+    // back and runs the planner; a different plan re-runs the pipeline (results depend only on
+    // (l, n), so a confirmed speculation returns exactly the non-speculative result)
+    struct PlanMemo {
+        std::shared_ptr<const std::vector<double>> host;
+        int p = 0, mode = 0, has_l = 0, l_in = 0;
+        double eps = 0.0, c1 = 0.0, c2 = 0.0;
+        int l = 0, n = 0;
+    };
+    std::vector<PlanMemo> plan_memo;
+    uint64_t plan_spec_hits = 0, plan_spec_misses = 0;
+    struct Worker {
+        std::thread th;
+        std::mutex mu;
+        std::condition_variable cv;
+        std::function<void()> job;
+        bool has_job = false, busy = false, stop = false;
+        std::exception_ptr err;
+    };
+    std::unique_ptr<Worker> worker;
     cudaEvent_t ev_cc = nullptr;    // adaptive CC error readback completes
     // factor uploads: pinned staging (no implicit stream sync) + per-slot cache of the last
     // operator (reused when the caller passes bit-identical factors again)
@@ -178,6 +204,21 @@ struct Epilogue {
     int accumulate = 0;
 };
 
+// The exponentials one phi call needs (engine.cpp phi_exponentials): per dimension k, the node
+// matrices expm((1 - theta_a) 2^-l s A_k) (a < q, stride n_k^2), the squaring chain expm(2^(j-l) s A_k)
+// (j < sq_len) and expm(s A_k) for phi_0, with their negligible-block tables.
+struct PhiExps {
+    const double* node[3] = {nullptr, nullptr, nullptr};
+    const double* sq[3] = {nullptr, nullptr, nullptr};
+    const double* phi0[3] = {nullptr, nullptr, nullptr};
+    int sq_len = 1;
+    bool late = false;
+    // negligible-block tables parallel to node/sq/phi0 (band_row_blocks(n_k) entries per matrix)
+    const int2* node_band[3] = {nullptr, nullptr, nullptr};
+    const int2* sq_band[3] = {nullptr, nullptr, nullptr};
+    const int2* phi0_band[3] = {nullptr, nullptr, nullptr};
+};
+
 // ---- C-ABI error plumbing (capi.cpp owns the thread-local message) ----
 std::string& last_error_slot();
 template <class F>
@@ -206,7 +247,10 @@ int guarded(F&& f) {
 // ---- context helpers (engine.cpp) ----
 double* ws(pq_ctx& c, const std::string& name, size_t count);          // device doubles
 void* ws_bytes(pq_ctx& c, const std::string& name, size_t bytes);
-void free_graveyard(pq_ctx& c);  // device-synchronising
+void free_graveyard(pq_ctx& c);     // device-synchronising
+void recycle_graveyard(pq_ctx& c);  // cudaFreeAsync on c.stream
+void trim_pool(pq_ctx& c);          // returns the pool's unused memory to the driver
+void* dev_alloc(pq_ctx& c, size_t bytes, const char* what);  // stream-ordered pool allocation on c.stream
 void arena_begin(pq_ctx& c);
 const void* arena_push(pq_ctx& c, const void* data, size_t bytes);     // returns device address
 void arena_flush(pq_ctx& c);
@@ -264,6 +308,15 @@ struct PlanInfo {
     int l = 0, n = 0, points = 0, mode = 0, planned = 0;
     double alpha = 0, beta = 0, cost = 0;
 };
+// phiquadmv's planner (phiaction.hpp:307-340): alpha from the factor norms, beta = max ||b||_inf
+// read back from the device (one sync), then setup_quadrature / quadnodes.  points is left 0.
+PlanInfo plan_phi(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, double eps, int mode, bool has_l, int l,
+                  double c1, double c2);
+// The planner on a host worker thread of the context (one job at a time): submit, then wait
+// (rethrows the job's exception).  worker_stop joins the thread (pq_ctx_destroy).
+void worker_submit(pq_ctx& c, std::function<void()> job);
+void worker_wait(pq_ctx& c);
+void worker_stop(pq_ctx& c);
 // Enqueues the Taylor powers of op's factors at `scale` (they do not depend on the plan), so they
 // run while the host waits for beta and plans; phi_exponentials of the same call reuses them.
 void taylor_prefetch(pq_ctx& c, const DevOp& op, double scale);
@@ -276,6 +329,22 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
                    double* phi0_host = nullptr, double* out_host = nullptr, bool* out_copied = nullptr);
 void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p,
                            const NodesWeights& rule, const std::vector<int>& nodes, int zero, double* acc);
+PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, const std::vector<double>& thetas,
+                         bool want_sq, bool want_phi0, const std::string& tag, bool sq_chain = false,
+                         bool late_async = false);
+void apply_phi0(pq_ctx& c, const DevOp& op, const PhiExps& px, int nb, const double* b, double* y);
+// phiaction.hpp:102-107 coefficients w_i theta_i^(j-1)/(j-1)! of the nodes idx, [a][p]
+void node_coefs(const NodesWeights& r, const std::vector<int>& idx, int p, std::vector<double>& out);
+std::vector<double> thetas_of(const NodesWeights& r, const std::vector<int>& idx);
+// q node vectors v_a = (E_a0 (x) E_a1 (x) E_a2) b_m (E[k] + a*Es[k]): combined into acc [nb][p][N]
+// with coef [q][p], or (pool != null) stored at pool + ((slot0 + a)*nb + m)*N
+void node_sweep(pq_ctx& c, const DevOp& op, const double* const* E, const long long* Es, int q, int nb,
+                const double* bs, int p, const std::vector<double>* coef, double* acc, int zero, double* pool,
+                int slot0, const int2* const* band = nullptr);
+// one mode-k product of Z1 tensors of shape n[0..d) (x[z] at x + z*x_stride, y[z] likewise) with
+// ONE matrix E (band: its negligible-block table or null): y[z] = (I (x) .. E .. (x) I) x[z]
+void mode_product_dev(pq_ctx& c, int d, const int* n, int k, const double* E, const int2* band, const double* x,
+                      long long x_stride, double* y, long long y_stride, int Z1);
 void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const double* bs, const NodesWeights& rule,
                      double* out);
 

@@ -1111,4 +1111,54 @@ void launch_sub(long long N, const double* x, const double* au, double* y, cudaS
     k_sub<<<grid_for(N, 256), 256, 0, s>>>(N, x, au, y);
 }
 
+// ---- slab <-> exchange blocks (distributed squaring, dist.cpp) ----
+// slab: [col][row][t], t < rest.  blocks: block h at ncols*rows*cb[h], laid out [col][row][t - cb[h]]
+// for cb[h] <= t < cb[h+1].  One thread per element pair (W = 2) or element (W = 1); the block of
+// an index is found by a scan of the <= 17 bounds held in registers (uniform across a warp except at
+// block edges).  PACK: slab -> blocks; else blocks -> slab.
+template <int W, bool PACK>
+__global__ void k_slab_blocks(long long total, int rows, long long rest, SlabCuts cuts, const double* __restrict__ src,
+                              double* __restrict__ dst) {
+    const long long per_col = static_cast<long long>(rows) * rest;
+    for (long long e = (blockIdx.x * (long long)blockDim.x + threadIdx.x) * W; e < total;
+         e += (long long)gridDim.x * blockDim.x * W) {
+        const long long col = e / per_col, rem = e - col * per_col;
+        const long long r = rem / rest, t = rem - r * rest;
+        int h = 0;
+        while (h + 1 < cuts.G && t >= cuts.cb[h + 1]) ++h;
+        const long long ch = cuts.cb[h + 1] - cuts.cb[h];
+        const long long b = cuts.ncols * rows * cuts.cb[h] + (col * rows + r) * ch + (t - cuts.cb[h]);
+        if (W == 2) {
+            if (PACK)
+                *reinterpret_cast<double2*>(dst + b) = *reinterpret_cast<const double2*>(src + e);
+            else
+                *reinterpret_cast<double2*>(dst + e) = *reinterpret_cast<const double2*>(src + b);
+        } else {
+            if (PACK)
+                dst[b] = src[e];
+            else
+                dst[e] = src[b];
+        }
+    }
+}
+
+void launch_slab_blocks(bool pack, int rows, long long rest, const SlabCuts& cuts, const double* src, double* dst,
+                        cudaStream_t s) {
+    const long long total = static_cast<long long>(cuts.ncols) * rows * rest;
+    if (total == 0) return;
+    bool even = rest % 2 == 0 && (reinterpret_cast<uintptr_t>(src) & 15u) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15u) == 0;
+    for (int h = 0; h <= cuts.G; ++h) even = even && cuts.cb[h] % 2 == 0;
+    if (even) {
+        if (pack)
+            k_slab_blocks<2, true><<<grid_for(total / 2, 256), 256, 0, s>>>(total, rows, rest, cuts, src, dst);
+        else
+            k_slab_blocks<2, false><<<grid_for(total / 2, 256), 256, 0, s>>>(total, rows, rest, cuts, src, dst);
+    } else {
+        if (pack)
+            k_slab_blocks<1, true><<<grid_for(total, 256), 256, 0, s>>>(total, rows, rest, cuts, src, dst);
+        else
+            k_slab_blocks<1, false><<<grid_for(total, 256), 256, 0, s>>>(total, rows, rest, cuts, src, dst);
+    }
+}
+
 }  // namespace pqb

@@ -111,4 +111,16 @@ void launch_axpy(long long N, double c, const double* x, double* y, cudaStream_t
 // y = x - au  (generic source already evaluated)
 void launch_sub(long long N, const double* x, const double* au, double* y, cudaStream_t s);
 
+// ---- distributed squaring layout flips (dist.cpp) ----
+// Trailing-index cuts of a slab: rank h's pencil owns t in [cb[h], cb[h+1]), cb[0] = 0, cb[G] = rest.
+struct SlabCuts {
+    int G = 1;
+    long long ncols = 1;
+    long long cb[17] = {0};
+};
+// pack: slab [col][row][t] (t < rest) -> blocks, block h at ncols*rows*cb[h] laid out
+// [col][row][t - cb[h]] (contiguous per (h, col)); !pack: blocks -> slab.
+void launch_slab_blocks(bool pack, int rows, long long rest, const SlabCuts& cuts, const double* src, double* dst,
+                        cudaStream_t s);
+
 }  // namespace pqb
