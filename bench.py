@@ -405,7 +405,20 @@ def run_ours_phi(args, world, rank, local) -> None:
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     req = pq.PhiRequest(p=w.p, eps=w.eps, mode=pq.QuadKind(w.mode))
-    seeds = step_seeds(args, rank, nb)
+    nodes = args.shard == "nodes"
+    comm = None
+    if nodes:
+        # one phi call spans all ranks: quadrature nodes dealt round-robin, node vectors moved
+        # into x-slabs, distributed squaring (csrc/dist.cpp); every rank passes the same b
+        from paper_2211_00696_b200 import sharded as S
+        if world == 1:
+            comm = S.Communicator.single()
+        elif _backend() == "gloo":
+            comm = S.Communicator.host()  # plumbing check: ranks share one GPU, collectives via the host
+        else:
+            comm = S.Communicator.nccl(ctx)
+        sb, se = S.slab_range(a.shape(), world, rank)
+    seeds = step_seeds(args, 0 if nodes else rank, nb)
     per_step = nb * N * 8
     free = torch.cuda.mem_get_info()[0]
     npool = _pool(seeds, per_step, min(8 << 30, free // 6))
@@ -413,27 +426,33 @@ def run_ours_phi(args, world, rank, local) -> None:
     b_dev = [torch.from_numpy(hosts[i]).cuda() for i in range(npool)]
     npin = _pool(seeds, per_step, 4 << 30)
     b_pin = [torch.from_numpy(hosts[i]).pin_memory() for i in range(npin)]
-    out0_pin = torch.empty((nb, N), dtype=torch.float64).pin_memory()
-    out_pin = torch.empty((nb, w.p, N), dtype=torch.float64).pin_memory()
+    NO = (se - sb) if nodes else N  # result length per column on this rank (slab or full vector)
+    out0_pin = torch.empty((nb, NO), dtype=torch.float64).pin_memory()
+    out_pin = torch.empty((nb, w.p, NO), dtype=torch.float64).pin_memory()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")  # 256 MiB > 126 MB L2
 
     d, sh, fac = a._abi()
     rc = req._c()
-    out0 = torch.empty((nb, N), dtype=torch.float64, device="cuda")
-    out = torch.empty((nb, w.p, N), dtype=torch.float64, device="cuda")
+    out0 = torch.empty((nb, NO), dtype=torch.float64, device="cuda")
+    out = torch.empty((nb, w.p, NO), dtype=torch.float64, device="cuda")
     info = pq._lib.PhiInfoC()
     plans = set()
 
+    def call(cx, b, o0, o, inf, space):
+        if nodes:
+            pq._lib.check(pq._lib.lib.pq_phiquadmv_dist(cx.handle, comm.handle, d, sh, fac, nb, C.c_void_p(b),
+                                                        C.byref(rc), C.c_void_p(o0), C.c_void_p(o), C.byref(inf),
+                                                        space, 0))
+        else:
+            pq._lib.check(pq._lib.lib.pq_phi_0p(cx.handle, d, sh, fac, nb, C.c_void_p(b), C.byref(rc), C.c_void_p(o0),
+                                                C.c_void_p(o), C.byref(inf), space))
+
     def step_device(i):
-        pq._lib.check(pq._lib.lib.pq_phi_0p(ctx.handle, d, sh, fac, nb, C.c_void_p(b_dev[i % npool].data_ptr()),
-                                            C.byref(rc), C.c_void_p(out0.data_ptr()), C.c_void_p(out.data_ptr()),
-                                            C.byref(info), pq._lib.PQ_DEVICE))
+        call(ctx, b_dev[i % npool].data_ptr(), out0.data_ptr(), out.data_ptr(), info, pq._lib.PQ_DEVICE)
         plans.add((info.l, info.n, info.points))
 
     def host_call(cx, i, bufs, inf):
-        pq._lib.check(pq._lib.lib.pq_phi_0p(cx.handle, d, sh, fac, nb, C.c_void_p(b_pin[i % npin].data_ptr()),
-                                            C.byref(rc), C.c_void_p(bufs[0].data_ptr()),
-                                            C.c_void_p(bufs[1].data_ptr()), C.byref(inf), pq._lib.PQ_HOST))
+        call(cx, b_pin[i % npin].data_ptr(), bufs[0].data_ptr(), bufs[1].data_ptr(), inf, pq._lib.PQ_HOST)
 
     def timed(fn, first, k):
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
@@ -459,7 +478,7 @@ def run_ours_phi(args, world, rank, local) -> None:
         ms_dev, launches = timed(step_device, args.warmup, args.steps)
     clocks = nvml.summary() or clk.summary()
     ms_dev_max = max_over_ranks(ms_dev, world)
-    units = world * nb * args.steps
+    units = (1 if nodes else world) * nb * args.steps  # node sharding: the ranks share each action
     value = units / (ms_dev_max / 1e3)
 
     # roofline pass: the same K steps (same b's) with every DMMA GEMM and streaming kernel bracketed
@@ -487,6 +506,8 @@ def run_ours_phi(args, world, rank, local) -> None:
     # callers; the region spans from one start event to the last caller's end event.  Inputs are
     # larger than L2 (b arrives by H2D, the workspaces are GB), so no flush between the calls.
     ncall = max(1, min(args.e2e_callers, 1 + int(0.8 * torch.cuda.mem_get_info()[0] // ctx_bytes)))
+    if nodes:
+        ncall = 1  # one communicator: distributed calls must not interleave their collectives
     pr = torch.cuda.Stream.priority_range() if hasattr(torch.cuda.Stream, "priority_range") else (0, -1)
     lo_prio, hi_prio = max(pr), min(pr)
     prios = [hi_prio + (lo_prio - hi_prio) * k // max(1, ncall - 1) for k in range(ncall)]
@@ -495,8 +516,8 @@ def run_ours_phi(args, world, rank, local) -> None:
         st = torch.cuda.Stream(priority=prios[k])
         cx = ctx if k == 0 else pq.Context(local)
         cx.set_stream(st.cuda_stream)
-        bufs = (out0_pin, out_pin) if k == 0 else (torch.empty((nb, N), dtype=torch.float64).pin_memory(),
-                                                   torch.empty((nb, w.p, N), dtype=torch.float64).pin_memory())
+        bufs = (out0_pin, out_pin) if k == 0 else (torch.empty((nb, NO), dtype=torch.float64).pin_memory(),
+                                                   torch.empty((nb, w.p, NO), dtype=torch.float64).pin_memory())
         callers.append((cx, st, bufs))
     for k, (cx, st, bufs) in enumerate(callers):  # warm the other contexts (workspaces, caches)
         host_call(cx, k, bufs, pq._lib.PhiInfoC())
@@ -534,21 +555,25 @@ def run_ours_phi(args, world, rank, local) -> None:
         barrier(world)
         return max(start.elapsed_time(e) for e, m in zip(ends, mine) if m)
 
+    if nodes:
+        comm.stats(reset=True)
     ms_e2e2_max = max_over_ranks(e2e_callers(args.steps), world)
+    comm_bytes = comm.stats(reset=True)[0] / args.steps if nodes else None
     e2e_value = units / (ms_e2e2_max / 1e3)
 
     line = {
         "metric": METRIC, "value": value, "unit": "actions/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_dev_max / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (fresh seeded N(0,1) RHS per step and rank, BASELINE operator built in fp64)",
+        "higher_is_better": True, "scaling": "strong" if nodes else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": ("synthetic (fresh seeded N(0,1) RHS per step" + ("" if nodes else " and rank")
+                 + ", BASELINE operator built in fp64)"),
         "config": bench_config(w, args, world),
         "plans": sorted(list(p) for p in plans),
         "gpu_launches": launches,
         "clocks": clocks,
         "roofline": roof, "cpu_baseline": None,
         "e2e": {"value": e2e_value, "unit": "actions/s", "h2d_bytes_per_step": int(nb * N * 8),
-                "d2h_bytes_per_step": int(nb * (w.p + 1) * N * 8), "callers": ncall,
+                "d2h_bytes_per_step": int(nb * (w.p + 1) * NO * 8), "callers": ncall,
                 "single_caller_value": e2e_single,
                 "distinct_rhs": {"device": npool, "pinned_host": npin},
                 "note": ("pq_phi_0p with pinned host b in and all p+1 vectors back every step; concurrent "
@@ -556,6 +581,11 @@ def run_ours_phi(args, world, rank, local) -> None:
                          "another's compute; single_caller_value = one synchronous caller; the operator's "
                          "factors are uploaded once (bit-identical factors are not re-copied) and not counted")},
     }
+    if nodes:
+        line["distributed"] = {"transport": "host (gloo)" if (world > 1 and _backend() == "gloo") else "nccl",
+                               "slab": [sb, se], "bytes_sent_per_step_rank0": comm_bytes,
+                               "outputs": "x-slabs per rank (gather=0)"}
+        comm.close()
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_line(w, args)
     if rank == 0:
@@ -668,12 +698,17 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=2, choices=[1, 2, 3, 4, 5])
-    ap.add_argument("--shard", default="rhs", choices=["rhs"])
+    ap.add_argument("--shard", default=None, choices=["rhs", "nodes"],
+                    help="N > 1: rhs = independent right-hand sides per rank (weak scaling; default for the CC "
+                         "configs 2 and 4), nodes = one action across all ranks (csrc/dist.cpp, strong scaling; "
+                         "default for the Gauss configs 1, 3, 5)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-callers", type=int, default=4, help="concurrent host callers in the e2e leg")
     ap.add_argument("--etd-steps", type=int, default=100, help="config 4: ETDRK4 steps per bench step")
     ap.add_argument("--ref-etd-steps", type=int, default=2, help="config 4: reference ETDRK4 steps per sample")
     args = ap.parse_args()
+    if args.shard is None:
+        args.shard = "nodes" if (args.config in (1, 3, 5) and int(os.environ.get("WORLD_SIZE", "1")) > 1) else "rhs"
     if args.impl == "reference":
         world, rank = int(os.environ.get("WORLD_SIZE", "1")), int(os.environ.get("RANK", "0"))
         run_reference(args, world, rank)

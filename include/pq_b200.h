@@ -88,6 +88,9 @@ PQ_API int pq_ctx_gemm_dense_flops(pq_ctx* ctx, int reset, double* flops);
  * Returns (synchronising) a JSON object {"<kernel>": {"launches", "ms", "bytes"}} with the summed
  * device time and ALGORITHMIC bytes (each vector read / written once) per kernel tag. */
 PQ_API int pq_ctx_kernel_stats(pq_ctx* ctx, int reset, const char** json);
+/* The profiled DMMA GEMM launches grouped by call site and shape: JSON {"<site> M.. N.. K.. Z..":
+ * {"launches", "ms", "flops" (executed), "dense"}} (synchronising). */
+PQ_API int pq_ctx_gemm_breakdown(pq_ctx* ctx, int reset, const char** json);
 /* With profiling on, phase boundaries are marked (device event + host clock).  Returns (and
  * clears, synchronising) a JSON array [{"mark","gpu_us","host_us"}] relative to the first mark. */
 PQ_API int pq_ctx_timeline(pq_ctx* ctx, const char** json);

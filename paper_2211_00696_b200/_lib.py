@@ -73,6 +73,7 @@ SIGNATURES = {
     "pq_squaring_combine": (C.c_int, [vp, C.c_longlong, C.c_int, C.c_int, vp, vp]),
     "pq_ctx_timeline": (C.c_int, [vp, C.POINTER(C.c_char_p)]),
     "pq_ctx_kernel_stats": (C.c_int, [vp, C.c_int, C.POINTER(C.c_char_p)]),
+    "pq_ctx_gemm_breakdown": (C.c_int, [vp, C.c_int, C.POINTER(C.c_char_p)]),
     "pq_gauss_legendre": (C.c_int, [C.c_int, dp, dp]),
     "pq_clenshaw_curtis": (C.c_int, [C.c_int, dp, dp]),
     "pq_cached_rule": (C.c_int, [C.c_int, C.c_int, C.POINTER(dp), C.POINTER(dp)]),

@@ -333,6 +333,27 @@ int pq_ctx_timeline(pq_ctx* c, const char** json) {
     });
 }
 
+int pq_ctx_gemm_breakdown(pq_ctx* c, int reset, const char** json) {
+    return guarded([&] {
+        need_ctx(c);
+        prof_collect(*c);
+        std::string s = "{";
+        bool first = true;
+        for (const auto& kv : c->gstats) {
+            char buf[400];
+            std::snprintf(buf, sizeof buf, "%s\"%s\":{\"launches\":%llu,\"ms\":%.6f,\"flops\":%.17g,\"dense\":%.17g}",
+                          first ? "" : ",", kv.first.c_str(), static_cast<unsigned long long>(kv.second.launches),
+                          kv.second.ms, kv.second.flops, kv.second.dense);
+            s += buf;
+            first = false;
+        }
+        s += "}";
+        if (reset) c->gstats.clear();
+        c->marks_json = s;
+        if (json) *json = c->marks_json.c_str();
+    });
+}
+
 int pq_ctx_kernel_stats(pq_ctx* c, int reset, const char** json) {
     return guarded([&] {
         need_ctx(c);

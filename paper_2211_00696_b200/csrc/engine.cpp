@@ -195,6 +195,10 @@ int gemm(pq_ctx& c, const GemmArgs& g) {
     cuda_check(cudaEventRecord(b, c.stream), "event record");
     count_launch(c, k);
     c.ev_flops.push_back(2.0 * g.M * static_cast<double>(g.N) * g.K * g.Z);
+    char key[160];
+    std::snprintf(key, sizeof key, "%s M%d N%d K%d Z%d %s%s", g.tag ? g.tag : "?", g.M, g.N, g.K, g.Z,
+                  g.b_kmajor ? "kk" : "nk", g.band ? " band" : "");
+    c.ev_keys.push_back(key);
     c.prof_launches += static_cast<uint64_t>(k);
     return k;
 }
@@ -247,9 +251,15 @@ void prof_collect(pq_ctx& c) {
         c.prof_ms += ms;
         c.prof_flops += static_cast<double>(executed[i / 2]);
         c.prof_flops_dense += c.ev_flops[i / 2];
+        auto& gs = c.gstats[c.ev_keys[i / 2]];
+        gs.launches += 1;
+        gs.ms += ms;
+        gs.flops += static_cast<double>(executed[i / 2]);
+        gs.dense += c.ev_flops[i / 2];
     }
     c.ev_used = 0;
     c.ev_flops.clear();
+    c.ev_keys.clear();
 }
 
 void note_early_copy(pq_ctx& c, cudaStream_t s, double* host, size_t count) {
@@ -526,9 +536,9 @@ static void expm_core(pq_ctx& c, int n, const double* base, double op_scale, con
         cuda_check(cudaStreamSynchronize(st), "expm s sync");
         s_max = h;
     }
-    gemm(c, square_batch(n, count, X, X, A2));
-    gemm(c, square_batch(n, count, A2, A2, A4));
-    gemm(c, square_batch(n, count, A2, A4, A6));
+    { GemmArgs t = square_batch(n, count, X, X, A2); t.tag = "pade"; gemm(c, t); }
+    { GemmArgs t = square_batch(n, count, A2, A2, A4); t.tag = "pade"; gemm(c, t); }
+    { GemmArgs t = square_batch(n, count, A2, A4, A6); t.tag = "pade"; gemm(c, t); }
     launch_pade_mid(n, count, A2, A4, A6, TZ, TZ + blk, st);
     count_launch(c);
     {
@@ -538,11 +548,12 @@ static void expm_core(pq_ctx& c, int n, const double* base, double op_scale, con
         g.sA2 = static_cast<long long>(nn);
         g.sB1 = g.sC1 = static_cast<long long>(blk);
         g.sB2 = g.sC2 = static_cast<long long>(nn);
+        g.tag = "pade";
         gemm(c, g);
     }
     launch_pade_fin(n, count, WZ, WZ + blk, A2, A4, A6, W2, V, st);
     count_launch(c);
-    gemm(c, square_batch(n, count, X, W2, U));
+    { GemmArgs t = square_batch(n, count, X, W2, U); t.tag = "pade"; gemm(c, t); }
     double* P = TZ;
     double* Q = (s_max % 2 == 0) ? out : WZ;
     double* other = (s_max % 2 == 0) ? WZ : out;
@@ -586,6 +597,7 @@ static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>&
                                   other + static_cast<size_t>(z0) * nn);
         g.sq_count = s_dev + z0;
         g.sq_round = r;
+        g.tag = "expm_squaring";
         gemm(c, g);
         std::swap(cur, other);
     }
@@ -667,6 +679,7 @@ static const double* taylor_powers(pq_ctx& c, int n, const double* base, double 
         g.sB2 = lnn;
         g.sC1 = fs;
         g.sC2 = lnn;
+        g.tag = "taylor_powers";
         gemm(c, g);
     }
     pc.P = P;
@@ -999,6 +1012,7 @@ void mode_product_dev(pq_ctx& c, int d, const int* n, int k, const double* E, co
         g.band_stride = 0;
         g.band_mode = g.b_kmajor ? 3 : 2;
     }
+    g.tag = "mode_product";
     gemm(c, g);
     check_launch(c);
 }
@@ -1018,6 +1032,7 @@ void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const lo
         double* dst = last ? y : tmp[k % 2];
         const long long dstride = last ? y_stride : N;
         GemmArgs g = mode_gemm(d, n, k, E[k], E_stride[k], src, sstride, dst, dstride, Z1, N);
+        const std::string tagk = std::string(tmp_tag) + ":mode" + std::to_string(k);
         const long long nn = static_cast<long long>(n[k]) * n[k];
         if (band && band[k] && E_stride[k] % nn == 0) {
             // which operand holds the exponentials, and how the tile finds its matrix (gemm.cuh)
@@ -1038,6 +1053,7 @@ void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const lo
             g.accumulate = ep.accumulate;
             if (ep.cld > 0) g.ext_group = ep.cld;
         }
+        g.tag = tagk.c_str();
         gemm(c, g);
         src = dst;
         sstride = dstride;
@@ -1093,6 +1109,7 @@ void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, 
             g.band_stride = 0;
             g.band_mode = g.b_kmajor ? 3 : 2;
         }
+        g.tag = "kron_matvec";
         gemm(c, g);
     }
     check_launch(c);
@@ -1651,7 +1668,11 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
                 const int cnt = static_cast<int>(G.dims.size());
                 double* src = G.buf + static_cast<size_t>(parity) * cnt * nn;
                 double* dst = G.buf + static_cast<size_t>(1 - parity) * cnt * nn;
-                gemm(c, square_batch(G.n, cnt, src, src, dst));
+                {
+                    GemmArgs sb = square_batch(G.n, cnt, src, src, dst);
+                    sb.tag = "sq_E^2";
+                    gemm(c, sb);
+                }
             }
             parity = 1 - parity;
         }

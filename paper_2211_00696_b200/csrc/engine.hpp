@@ -157,6 +157,12 @@ struct pq_ctx {
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_used = 0;
     std::vector<double> ev_flops;
+    std::vector<std::string> ev_keys;  // launch signature per recorded GEMM (breakdown)
+    struct GStat {
+        uint64_t launches = 0;
+        double ms = 0.0, flops = 0.0, dense = 0.0;
+    };
+    std::map<std::string, GStat> gstats;
     double prof_ms = 0.0, prof_flops = 0.0;  // prof_flops: executed (negligible blocks skipped)
     double prof_flops_dense = 0.0;            // 2 M N K Z of the same launches
     unsigned long long* d_flops = nullptr;    // per-launch executed-flop counters (profiling)

@@ -45,6 +45,7 @@ struct GemmArgs {
     int band_mode = 0, band_rows = 0;
     // profiling: every CTA adds the flops it actually executed (2 rows cols k) here
     unsigned long long* flop_counter = nullptr;
+    const char* tag = nullptr;  // call site, for the profiling breakdown only
 };
 int launch_gemm(const GemmArgs& g, cudaStream_t s);  // returns number of kernel launches
 

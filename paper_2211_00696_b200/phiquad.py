@@ -93,6 +93,13 @@ class Context:
         check(lib.pq_ctx_kernel_stats(self.handle, 1 if reset else 0, C.byref(js)))
         return json.loads(js.value.decode())
 
+    def gemm_breakdown(self, reset: bool = True) -> dict:
+        """{"<call site> M N K Z layout": {"launches", "ms", "flops", "dense"}} of the profiled GEMMs."""
+        import json
+        js = C.c_char_p()
+        check(lib.pq_ctx_gemm_breakdown(self.handle, 1 if reset else 0, C.byref(js)))
+        return json.loads(js.value.decode())
+
     def set_workspace_limit(self, nbytes: int) -> None:
         check(lib.pq_ctx_set_workspace_limit(self.handle, nbytes))
 

@@ -35,20 +35,27 @@ def test_bench_line_contract():
     assert d["gpu_launches"] > 0
 
 
-def test_bench_two_ranks_plumbing():
+@pytest.mark.parametrize("shard", ["rhs", "nodes"])
+def test_bench_two_ranks_plumbing(shard):
     """The N > 1 launch the driver uses (torch.distributed.run, one process per rank), with gloo
-    carrying the barrier / max-over-ranks so both ranks can share the one GPU of this box: the RHS
-    shards have no data-path collective, so this checks the rank plumbing and the aggregate line."""
+    carrying the barrier / max-over-ranks so both ranks can share the one GPU of this box.  rhs: the
+    RHS shards have no data-path collective (weak scaling); nodes: one action across both ranks
+    through the distributed engine path with the host transport (strong scaling)."""
     import os
     env = dict(os.environ, PQ_BENCH_BACKEND="gloo")
+    port = 29517 if shard == "rhs" else 29519
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", "29517", str(ROOT / "bench.py"),
-                        "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "1", "--e2e-callers", "1"],
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
+                        "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "1", "--e2e-callers", "1",
+                        "--shard", shard],
                        capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
     assert len(lines) == 1, r.stdout[-2000:]
     d = json.loads(lines[0])
-    assert d["n_gpus"] == 2 and d["scaling"] == "weak" and d["value"] > 0
-    assert "x2" in d["config"]["parallelism"]
+    assert d["n_gpus"] == 2 and d["value"] > 0
+    assert d["scaling"] == ("weak" if shard == "rhs" else "strong")
+    assert f"{shard}-sharded x2" in d["config"]["parallelism"]
     assert d["e2e"]["value"] > 0
+    if shard == "nodes":
+        assert d["distributed"]["bytes_sent_per_step_rank0"] > 0
