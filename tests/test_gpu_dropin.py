@@ -48,3 +48,23 @@ def test_dropin_matches_reference_build():
         else:
             den = max(np.linalg.norm(w), 1e-300)
             assert np.linalg.norm(g - w) / den <= 1e-11, (k, np.linalg.norm(g - w) / den)
+
+
+def test_dist_header_builds():
+    r = subprocess.run(["make", "-s", "-C", str(ROOT / "tests" / "cpp"), "_bin/dist_b200"], capture_output=True,
+                       text=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+def test_dropin_distributed_extension_world1():
+    """include/phiquad/distributed.hpp from C++: b200::phiquadmv_multi over a one-rank communicator
+    (node phase, slab combine, slab squaring and the layout flips all run) equals the single-GPU
+    phiquadmv_multi: identical plans, columns within 1e-11."""
+    test_dist_header_builds()
+    out = subprocess.run([str(ROOT / "tests" / "cpp" / "_bin" / "dist_b200")], capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0, out.stderr
+    got = parse(out.stdout)
+    assert got["plans_equal"][0] == 1
+    assert got["max_rel"][0] <= 1e-11
