@@ -91,6 +91,11 @@ PQ_API int pq_ctx_kernel_stats(pq_ctx* ctx, int reset, const char** json);
 /* The profiled DMMA GEMM launches grouped by call site and shape: JSON {"<site> M.. N.. K.. Z..":
  * {"launches", "ms", "flops" (executed), "dense"}} (synchronising). */
 PQ_API int pq_ctx_gemm_breakdown(pq_ctx* ctx, int reset, const char** json);
+/* Debug (environment PQ_WS_GUARD=1 at first use): every workspace buffer is allocated with 4 KB
+ * canary regions before and after it.  Synchronises and counts the buffers whose canaries were
+ * overwritten (*damaged; their names in pq_last_error()) -- an out-of-bounds-write check that needs
+ * no compute-sanitizer. */
+PQ_API int pq_ctx_check_guards(pq_ctx* ctx, int* damaged);
 /* With profiling on, phase boundaries are marked (device event + host clock).  Returns (and
  * clears, synchronising) a JSON array [{"mark","gpu_us","host_us"}] relative to the first mark. */
 PQ_API int pq_ctx_timeline(pq_ctx* ctx, const char** json);

@@ -74,6 +74,7 @@ SIGNATURES = {
     "pq_ctx_timeline": (C.c_int, [vp, C.POINTER(C.c_char_p)]),
     "pq_ctx_kernel_stats": (C.c_int, [vp, C.c_int, C.POINTER(C.c_char_p)]),
     "pq_ctx_gemm_breakdown": (C.c_int, [vp, C.c_int, C.POINTER(C.c_char_p)]),
+    "pq_ctx_check_guards": (C.c_int, [vp, ip]),
     "pq_gauss_legendre": (C.c_int, [C.c_int, dp, dp]),
     "pq_clenshaw_curtis": (C.c_int, [C.c_int, dp, dp]),
     "pq_cached_rule": (C.c_int, [C.c_int, C.c_int, C.POINTER(dp), C.POINTER(dp)]),

@@ -169,8 +169,7 @@ int pq_ctx_destroy(pq_ctx* c) {
         if (!c) return;
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
-        for (auto& kv : c->bufs)
-            if (kv.second.p) cudaFree(kv.second.p);
+        for (auto& kv : c->bufs) ws_free_now(*c, kv.second.p);
         for (void* p : c->graveyard) cudaFree(p);
         trim_pool(*c);
         if (c->arena.host) cudaFreeHost(c->arena.host);
@@ -274,8 +273,7 @@ int pq_ctx_release_workspace(pq_ctx* c) {
         need_ctx(c);
         cuda_check(cudaStreamSynchronize(c->stream), "sync");
         free_graveyard(*c);
-        for (auto& kv : c->bufs)
-            if (kv.second.p) cudaFree(kv.second.p);
+        for (auto& kv : c->bufs) ws_free_now(*c, kv.second.p);
         c->bufs.clear();
         c->fac_cache.clear();
         trim_pool(*c);
@@ -351,6 +349,16 @@ int pq_ctx_gemm_breakdown(pq_ctx* c, int reset, const char** json) {
         if (reset) c->gstats.clear();
         c->marks_json = s;
         if (json) *json = c->marks_json.c_str();
+    });
+}
+
+int pq_ctx_check_guards(pq_ctx* c, int* damaged) {
+    return guarded([&] {
+        need_ctx(c);
+        std::string names;
+        const int bad = check_guards(*c, &names);
+        if (damaged) *damaged = bad;
+        last_error_slot() = bad ? "damaged workspace guards: " + names : std::string();
     });
 }
 

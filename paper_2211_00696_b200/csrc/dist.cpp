@@ -341,12 +341,12 @@ double* slab_pool_grow(pq_ctx& c, int slots, int nb, long long S, int used) {
     DevBuf& b = c.bufs["dslabpool"];
     const size_t want = static_cast<size_t>(std::max(slots, 1)) * nb * std::max<long long>(S, 1) * sizeof(double);
     if (b.bytes < want) {
-        double* np = static_cast<double*>(dev_alloc(c, want, "dslabpool"));
+        double* np = static_cast<double*>(ws_alloc(c, want, "dslabpool"));
         if (b.p && used > 0)
             cuda_check(cudaMemcpyAsync(np, b.p, static_cast<size_t>(used) * nb * S * sizeof(double), cudaMemcpyDeviceToDevice,
                                        c.stream),
                        "pool copy");
-        if (b.p) c.graveyard.push_back(b.p);
+        ws_retire(c, b.p);
         b.p = np;
         b.bytes = want;
     }

@@ -63,6 +63,65 @@ static cudaMemPool_t device_pool(int dev) {
 
 void trim_pool(pq_ctx& c) { cudaMemPoolTrimTo(device_pool(c.device), 0); }
 
+static bool ws_guard_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PQ_WS_GUARD");
+        return v && v[0] == '1';
+    }();
+    return on;
+}
+constexpr size_t kGuardBytes = 4096;
+constexpr unsigned char kCanary = 0xA7;
+
+void* ws_alloc(pq_ctx& c, size_t bytes, const std::string& name) {
+    if (!ws_guard_enabled()) return dev_alloc(c, bytes, name.c_str());
+    const size_t body = (bytes + 255) & ~size_t(255);
+    char* base = static_cast<char*>(dev_alloc(c, body + 2 * kGuardBytes, name.c_str()));
+    cuda_check(cudaMemsetAsync(base, kCanary, kGuardBytes, c.stream), "guard fill");
+    cuda_check(cudaMemsetAsync(base + kGuardBytes + bytes, kCanary, body - bytes + kGuardBytes, c.stream), "guard fill");
+    void* p = base + kGuardBytes;
+    c.guards[p] = {base, bytes, name};
+    return p;
+}
+
+static void* base_of(pq_ctx& c, void* p) {
+    auto it = c.guards.find(p);
+    if (it == c.guards.end()) return p;
+    void* b = it->second.base;
+    c.guards.erase(it);
+    return b;
+}
+
+void ws_retire(pq_ctx& c, void* p) {
+    if (p) c.graveyard.push_back(base_of(c, p));
+}
+
+void ws_free_now(pq_ctx& c, void* p) {
+    if (p) cudaFree(base_of(c, p));
+}
+
+int check_guards(pq_ctx& c, std::string* what) {
+    cuda_check(cudaDeviceSynchronize(), "guard check sync");
+    int bad = 0;
+    std::vector<unsigned char> h(kGuardBytes + 256);
+    for (const auto& kv : c.guards) {
+        const char* base = static_cast<const char*>(kv.second.base);
+        const size_t bytes = kv.second.bytes, body = (bytes + 255) & ~size_t(255);
+        bool ok = true;
+        cuda_check(cudaMemcpy(h.data(), base, kGuardBytes, cudaMemcpyDeviceToHost), "guard read");
+        for (size_t i = 0; i < kGuardBytes; ++i) ok = ok && h[i] == kCanary;
+        const size_t tail = body - bytes + kGuardBytes;
+        std::vector<unsigned char> t(tail);
+        cuda_check(cudaMemcpy(t.data(), base + kGuardBytes + bytes, tail, cudaMemcpyDeviceToHost), "guard read");
+        for (size_t i = 0; i < tail; ++i) ok = ok && t[i] == kCanary;
+        if (!ok) {
+            ++bad;
+            if (what) *what += kv.second.name + " ";
+        }
+    }
+    return bad;
+}
+
 void free_graveyard(pq_ctx& c) {
     if (c.graveyard.empty()) return;
     cuda_check(cudaDeviceSynchronize(), "sync before workspace free");
@@ -98,12 +157,12 @@ void* ws_bytes(pq_ctx& c, const std::string& name, size_t bytes) {
     DevBuf& b = c.bufs[name];
     if (b.bytes >= bytes && b.p) return b.p;
     // the old buffer may still be read by enqueued work: retire it (pq_ctx::graveyard)
-    if (b.p) c.graveyard.push_back(b.p);
+    ws_retire(c, b.p);
     b.p = nullptr;
     b.bytes = 0;
     const size_t want = std::max<size_t>(bytes, 256);
     mark(c, ("ws_grow:" + name).c_str());
-    b.p = dev_alloc(c, want, name.c_str());
+    b.p = ws_alloc(c, want, name);
     b.bytes = want;
     return b.p;
 }
@@ -1322,11 +1381,11 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             DevBuf& b = c.bufs["ccpool"];
             const size_t want = static_cast<size_t>(used + fr) * nb * N * sizeof(double);
             if (b.bytes < want) {
-                double* np = static_cast<double*>(dev_alloc(c, want, "ccpool"));
+                double* np = static_cast<double*>(ws_alloc(c, want, "ccpool"));
                 cuda_check(cudaMemcpyAsync(np, b.p, static_cast<size_t>(used) * nb * N * sizeof(double),
                                            cudaMemcpyDeviceToDevice, c.stream),
                            "pool copy");
-                c.graveyard.push_back(b.p);
+                ws_retire(c, b.p);
                 b.p = np;
                 b.bytes = want;
             }

@@ -57,6 +57,14 @@ struct pq_ctx {
     // (or an allocation fails), never inside a call -- cudaFree of a large buffer is a device-wide
     // synchronisation that took 20-60 ms on the B200 (the acceptance gate's criterion-7 outlier)
     std::vector<void*> graveyard;
+    // PQ_WS_GUARD=1 (debug, the memcheck substitute on pools where compute-sanitizer is closed):
+    // every workspace buffer carries 4 KB canary regions before and after it; user pointer -> base
+    struct Guarded {
+        void* base;
+        size_t bytes;
+        std::string name;
+    };
+    std::map<void*, Guarded> guards;
     pqb::ParamArena arena;
     int* d_err = nullptr;        // device error flag (singular LU)
     double* h_small = nullptr;   // pinned readback scratch
@@ -257,6 +265,12 @@ void free_graveyard(pq_ctx& c);     // device-synchronising
 void recycle_graveyard(pq_ctx& c);  // cudaFreeAsync on c.stream
 void trim_pool(pq_ctx& c);          // returns the pool's unused memory to the driver
 void* dev_alloc(pq_ctx& c, size_t bytes, const char* what);  // stream-ordered pool allocation on c.stream
+// a workspace-sized allocation (canary-guarded under PQ_WS_GUARD=1) and its release
+void* ws_alloc(pq_ctx& c, size_t bytes, const std::string& name);
+void ws_retire(pq_ctx& c, void* p);     // into the graveyard (stream-ordered free at the next call)
+void ws_free_now(pq_ctx& c, void* p);   // synchronous free (release / destroy)
+// canary check of every guarded buffer (syncs); returns the number of damaged buffers, names in *what
+int check_guards(pq_ctx& c, std::string* what);
 void arena_begin(pq_ctx& c);
 const void* arena_push(pq_ctx& c, const void* data, size_t bytes);     // returns device address
 void arena_flush(pq_ctx& c);

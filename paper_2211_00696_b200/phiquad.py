@@ -93,6 +93,12 @@ class Context:
         check(lib.pq_ctx_kernel_stats(self.handle, 1 if reset else 0, C.byref(js)))
         return json.loads(js.value.decode())
 
+    def check_guards(self) -> tuple:
+        """(damaged buffer count, names) of the canary-guarded workspace (PQ_WS_GUARD=1)."""
+        n = C.c_int()
+        check(lib.pq_ctx_check_guards(self.handle, C.byref(n)))
+        return n.value, (lib.pq_last_error() or b"").decode() if n.value else ""
+
     def gemm_breakdown(self, reset: bool = True) -> dict:
         """{"<call site> M N K Z layout": {"launches", "ms", "flops", "dense"}} of the profiled GEMMs."""
         import json
