@@ -496,6 +496,7 @@ int pq_infnorm_bound(int d, const int* shape, const double* factors, double* out
 
 int pq_expm(pq_ctx* c, int n, int batch, const double* a, const double* scale, double* out, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_expm");
         need_ctx(c);
         need(n >= 0 && batch >= 0, "expm: bad extent");
         if (n == 0 || batch == 0) return;
@@ -530,6 +531,7 @@ int pq_expm(pq_ctx* c, int n, int batch, const double* a, const double* scale, d
 
 int pq_mode_apply(pq_ctx* c, int d, const int* shape, const double* mats, const double* x, double* y, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_mode_apply");
         need_ctx(c);
         const long long N = dim_of(d, shape);
         arena_begin(*c);
@@ -546,6 +548,7 @@ int pq_mode_apply(pq_ctx* c, int d, const int* shape, const double* mats, const 
 
 int pq_kron_matvec(pq_ctx* c, int d, const int* shape, const double* factors, const double* x, double* y, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_kron_matvec");
         need_ctx(c);
         const long long N = dim_of(d, shape);
         arena_begin(*c);
@@ -560,6 +563,7 @@ int pq_kron_matvec(pq_ctx* c, int d, const int* shape, const double* factors, co
 
 int pq_exp_action(pq_ctx* c, int d, const int* shape, const double* factors, const double* b, double* y, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_exp_action");
         need_ctx(c);
         const long long N = dim_of(d, shape);
         arena_begin(*c);
@@ -577,6 +581,7 @@ int pq_exp_action(pq_ctx* c, int d, const int* shape, const double* factors, con
 int pq_phi_fixed(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs, int p, int m,
                  const double* nodes, const double* weights, double* out, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_phi_fixed");
         need_ctx(c);
         need(p >= 1, "phi_fixed: need p >= 1");
         need(nb >= 0, "phi_fixed: need nb >= 0");
@@ -596,6 +601,7 @@ int pq_phi_fixed(pq_ctx* c, int d, const int* shape, const double* factors, int 
 int pq_phi_adaptive(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs, int p,
                     double eps, double* out, int* points_used, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_phi_adaptive");
         need_ctx(c);
         need(p >= 1, "phi_adaptive: need p >= 1");
         need(eps > 0.0, "phi_adaptive: need eps > 0");
@@ -613,6 +619,7 @@ int pq_phi_adaptive(pq_ctx* c, int d, const int* shape, const double* factors, i
 
 int pq_squaring_step(pq_ctx* c, int d, const int* shape, const double* exps, int p, double* y, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_squaring_step");
         need_ctx(c);
         need(p >= 1, "squaring_step: need p >= 1");
         const long long N = dim_of(d, shape);
@@ -648,6 +655,7 @@ static void plan_checks(int l, int n, int p, int kind, double eps) {
 int pq_phi_with_plan(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs, int p, int l,
                      int n, int kind, double eps, double* out, int* points_used, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_phi_with_plan");
         need_ctx(c);
         plan_checks(l, n, p, kind, eps);
         const long long N = dim_of(d, shape);
@@ -668,6 +676,7 @@ int pq_phi_with_plan(pq_ctx* c, int d, const int* shape, const double* factors, 
 int pq_phi_with_plan_cols(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* const* bs,
                           int p, int l, int n, int kind, double eps, double* const* cols, int* points_used, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_phi_with_plan_cols");
         need_ctx(c);
         plan_checks(l, n, p, kind, eps);
         const long long N = dim_of(d, shape);
@@ -914,11 +923,13 @@ static void run_phiquadmv_impl(pq_ctx* c, int d, const int* shape, const double*
 int pq_phiquadmv(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
                  const pq_phi_request* req, double* out, pq_phi_info* info, int space) {
     return guarded([&] { run_phiquadmv(c, d, shape, factors, nb, bs, req, nullptr, out, info, space); });
+        NvtxRange nvtx("pq_phiquadmv");
 }
 
 int pq_phiquadmv_cols(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* const* bs,
                       const pq_phi_request* req, double* const* cols, pq_phi_info* info, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_phiquadmv_cols");
         need(nb == 0 || (bs != nullptr && cols != nullptr), "phiquadmv: null vector list");
         run_phiquadmv(c, d, shape, factors, nb, nullptr, req, nullptr, nullptr, info, space, bs, cols);
     });
@@ -927,6 +938,7 @@ int pq_phiquadmv_cols(pq_ctx* c, int d, const int* shape, const double* factors,
 int pq_phi_0p(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* bs,
               const pq_phi_request* req, double* out0, double* out, pq_phi_info* info, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_phi_0p");
         need(out0 != nullptr, "phi_0p: null phi_0 output");
         run_phiquadmv(c, d, shape, factors, nb, bs, req, out0, out, info, space);
     });
@@ -935,6 +947,7 @@ int pq_phi_0p(pq_ctx* c, int d, const int* shape, const double* factors, int nb,
 int pq_phi_lincomb(pq_ctx* c, int d, const int* shape, const double* factors, int p, const double* bs, int m,
                    const double* nodes, const double* weights, double* out, int space) {
     return guarded([&] {
+        NvtxRange nvtx("pq_phi_lincomb");
         need_ctx(c);
         need(p >= 1, "phi_lincomb: need at least one vector");
         const long long N = dim_of(d, shape);

@@ -135,6 +135,7 @@ double* grow_pinned(double*& buf, size_t& cap, size_t count) {
 // the order given (sender and receiver enumerate them in the same order).  Self pieces are local
 // device copies (the i-th self send lands in the i-th self receive).
 void exchange(pq_ctx& c, pq_comm& m, const std::vector<Piece>& sends, const std::vector<Piece>& recvs) {
+    NvtxRange nvtx("pq_exchange");
     ++m.exchanges;
     std::vector<const Piece*> self_s, self_r;
     for (const auto& s : sends)
@@ -776,6 +777,7 @@ int pq_phiquadmv_dist(pq_ctx* ctx, pq_comm* comm, int d, const int* shape, const
                       const double* bs, const pq_phi_request* req, double* out0, double* out, pq_phi_info* info,
                       int space, int gather) {
     return guarded([&] {
+        NvtxRange nvtx("pq_phiquadmv_dist");
         need(req != nullptr, "phiquadmv: null request");
         need(req->p >= 1, "phiquadmv: need p >= 1");
         need(req->mode == PQ_GAUSS_LEGENDRE || req->mode == PQ_CLENSHAW_CURTIS, "QuadKind: unknown rule");
@@ -788,6 +790,7 @@ int pq_phi_with_plan_dist(pq_ctx* ctx, pq_comm* comm, int d, const int* shape, c
                           const double* bs, int p, int l, int n, int kind, double eps, double* out, int* points_used,
                           int space, int gather) {
     return guarded([&] {
+        NvtxRange nvtx("pq_phi_with_plan_dist");
         need(l >= 0, "phi_with_plan: need l >= 0");
         need(kind == PQ_GAUSS_LEGENDRE || kind == PQ_CLENSHAW_CURTIS, "QuadKind: unknown rule");
         if (kind == PQ_GAUSS_LEGENDRE) need(n + 1 >= 1, "gauss_legendre: need at least one point");

@@ -333,6 +333,7 @@ void note_early_copy(pq_ctx& c, cudaStream_t s, double* host, size_t count) {
 }
 
 void mark(pq_ctx& c, const char* name) {
+    nvtxMarkA(name);
     if (!c.profiling && !c.trace) return;
     static const auto t0 = std::chrono::steady_clock::now();
     cudaEvent_t e;

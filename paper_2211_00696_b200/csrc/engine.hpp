@@ -18,6 +18,8 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "estimator.hpp"
 #include "kernels.hpp"
 
@@ -292,7 +294,14 @@ struct KernelProbe {
     KernelProbe& operator=(const KernelProbe&) = delete;
 };
 void note_early_copy(pq_ctx& c, cudaStream_t s, double* host, size_t count);  // after an early D2H on s
-void mark(pq_ctx& c, const char* name);  // timeline mark (no-op unless profiling)
+void mark(pq_ctx& c, const char* name);  // NVTX marker; timeline mark (device event + host clock) when profiling / tracing
+// NVTX range over one C-ABI call (visible under nsys / ncu --nvtx; a few ns when no tool is attached)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 void check_launch(pq_ctx& c);
 void ensure_side(pq_ctx& c);  // creates the side stream and its fork/join events on first use
 void run_deferred(pq_ctx& c);

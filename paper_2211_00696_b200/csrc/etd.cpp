@@ -326,6 +326,7 @@ static int run_etd(pq_ctx* c, int d, const int* shape, const double* factors, co
                    double t0, double tau, int m, const pq_tableau* tab, const pq_phi_request* base, double* u_out,
                    int* phi_calls, int space) {
     return guarded([&] {
+        NvtxRange nvtx(m == 1 ? "pq_erk_step" : "pq_integrate");
         if (!c) throw std::invalid_argument("pq: null context");
         cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
         if (!f) throw std::invalid_argument("erk_step: null source");

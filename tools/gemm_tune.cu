@@ -5,9 +5,11 @@
 #include <cstdio>
 #include <algorithm>
 #include <vector>
+#include <cmath>
 
 #include "gemm.cuh"
 #include "gemm_ws_experiment.cuh"
+#include "gemm_tma_experiment.cuh"
 
 using namespace pqb;
 
@@ -73,6 +75,43 @@ float run_ws(const Case& c, int reps, cudaEvent_t e0, cudaEvent_t e1) {
     return ms / reps;
 }
 
+// TMA variant of the exponential-as-A band tile; checks its output against the cp.async tile first
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB>
+float run_tma(const Case& c, int reps, cudaEvent_t e0, cudaEvent_t e1, double* Yref, long long count) {
+    GemmArgs g = c.g;
+    if (g.b_kmajor || (g.band_mode != 1 && g.band_mode != 2)) return -1;
+    char why[128] = "";
+    launch_cfg<32, 128, 16, 32, 32, 2, false, 2, 4>(g, 0);  // reference result
+    cudaMemcpy(Yref, g.C, count * sizeof(double), cudaMemcpyDeviceToDevice);
+    cudaMemset(g.C, 0, count * sizeof(double));
+    if (launch_tma<BM, BN, BK, WM, WN, ST, MINB>(g, 0, why) < 0) {
+        printf("  TMA maps rejected: %s\n", why);
+        return -1;
+    }
+    cudaDeviceSynchronize();
+    std::vector<double> a(count), b(count);
+    cudaMemcpy(a.data(), Yref, count * sizeof(double), cudaMemcpyDeviceToHost);
+    cudaMemcpy(b.data(), g.C, count * sizeof(double), cudaMemcpyDeviceToHost);
+    double diff = 0, mx = 0;
+    for (long long i = 0; i < count; ++i) {
+        diff = std::max(diff, std::abs(a[i] - b[i]));
+        mx = std::max(mx, std::abs(a[i]));
+    }
+    printf("  TMA check: max|diff| %.3g (max|y| %.3g)%s\n", diff, mx, diff == 0 ? " bitwise equal" : "");
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) launch_tma<BM, BN, BK, WM, WN, ST, MINB>(g, 0);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    cudaError_t err = cudaGetLastError();
+    if (err != cudaSuccess) {
+        printf("  launch error %s\n", cudaGetErrorString(err));
+        return -1;
+    }
+    return ms / reps;
+}
+
 __global__ void fill_rand(double* p, long long n, unsigned seed) {
     for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
         unsigned long long x = (i + 1) * 6364136223846793005ull + seed * 1442695040888963407ull;
@@ -101,6 +140,8 @@ int main(int argc, char** argv) {
         printf("random operands\n");
     }
     cudaMemset(EXT, 0, sizeof(double) * N * Z);
+    double* YREF;
+    CK(cudaMalloc(&YREF, sizeof(double) * N * Z));
     double *coef, *alpha;
     int* nterms;
     CK(cudaMalloc(&coef, 64 * 64 * 8));
@@ -190,11 +231,30 @@ int main(int argc, char** argv) {
     }
         T(32, 128, 16, 32, 32, 2, 4)
         T(32, 128, 16, 32, 32, 2, 5)
+        T(32, 128, 8, 32, 32, 2, 6)
+        T(32, 128, 8, 32, 32, 2, 7)
+        T(32, 128, 8, 32, 32, 3, 6)
         T(32, 128, 16, 32, 32, 3, 3)
         T(32, 128, 16, 32, 32, 3, 4)
         T(32, 256, 16, 32, 32, 2, 2)
         T(32, 256, 16, 32, 64, 2, 2)
         T(32, 128, 16, 32, 64, 2, 4)
+#define TT(BM, BN, BK, WM, WN, ST, MINB)                                                               \
+    {                                                                                                  \
+        float ms = run_tma<BM, BN, BK, WM, WN, ST, MINB>(c, 5, e0, e1, YREF, N * Z);                   \
+        if (ms > 0)                                                                                    \
+            printf("  TMA %3dx%3dx%2d w%2dx%2d st%d minb%d : %8.1f us  %6.2f TF/s\n", BM, BN, BK, WM, WN, ST, MINB, \
+                   ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
+    }
+        TT(32, 128, 16, 32, 32, 2, 4)
+        TT(32, 128, 16, 32, 32, 3, 3)
+        TT(32, 128, 16, 32, 32, 3, 4)
+        TT(32, 128, 16, 32, 32, 4, 3)
+        TT(32, 128, 16, 32, 32, 2, 5)
+        TT(32, 128, 8, 32, 32, 3, 7)
+        TT(32, 128, 8, 32, 32, 4, 5)
+        TT(32, 128, 8, 32, 32, 2, 8)
+        TT(32, 128, 8, 32, 32, 3, 6)
         TW(32, 128, 16, 32, 32, 2, 3)
         TW(32, 128, 16, 32, 32, 3, 3)
         TW(32, 128, 16, 32, 32, 2, 4)
