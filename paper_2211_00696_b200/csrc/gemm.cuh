@@ -12,6 +12,10 @@
 
 #include "kernels.hpp"
 
+#ifndef PQ_GEMM_AFFINE
+#define PQ_GEMM_AFFINE 1
+#endif
+
 namespace pqb {
 
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
@@ -81,45 +85,86 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
     constexpr int KV = BK / VEC;
     constexpr int A_CH = BM * KV, A_IT = (A_CH + NT - 1) / NT;
     constexpr int B_CH = BKM ? BN * KV : BK * (BN / VEC), B_IT = (B_CH + NT - 1) / NT;
-    const double* a_src[A_IT];
-    unsigned a_dst[A_IT];
-    int a_k[A_IT];
-    bool a_ok[A_IT];
     const unsigned sA_base = static_cast<unsigned>(__cvta_generic_to_shared(sA));
     const unsigned sB_base = static_cast<unsigned>(__cvta_generic_to_shared(sB));
+    // Affine descriptors: when every thread's chunks sit at a fixed row stride (NT a multiple of
+    // the chunks per row), a thread keeps ONE source pointer per operand and walks it by that
+    // stride -- ~14 registers instead of ~45 for per-chunk pointer / destination / bound arrays.
+#if PQ_GEMM_AFFINE
+    constexpr bool AFF = (A_CH % NT == 0) && (B_CH % NT == 0) && (NT % KV == 0) && (BKM || NT % (BN / VEC) == 0);
+#else
+    constexpr bool AFF = false;
+#endif
+    constexpr int NVB = BN / VEC;
+    constexpr int RA = NT / KV;                  // A rows between a thread's chunks
+    constexpr int RB = BKM ? NT / KV : NT / NVB;  // B rows (n for k-major, k otherwise) between chunks
+    const double* a_p = nullptr;
+    const double* b_p = nullptr;
+    long long a_rowstep = 0, b_rowstep = 0;
+    unsigned a_mask = 0, b_mask = 0, a_dst0 = 0, b_dst0 = 0;
+    int a_kc = 0, b_r0 = 0;
+    const double* a_src[AFF ? 1 : A_IT];
+    unsigned a_dst[AFF ? 1 : A_IT];
+    int a_k[AFF ? 1 : A_IT];
+    bool a_ok[AFF ? 1 : A_IT];
+    const double* b_src[AFF ? 1 : B_IT];
+    unsigned b_dst[AFF ? 1 : B_IT];
+    int b_k[AFF ? 1 : B_IT];
+    bool b_ok[AFF ? 1 : B_IT];
+    const long long b_kstep = BKM ? 1 : g.ldb;  // global stride of one k row of B
+    if constexpr (AFF) {
+        const int ra0 = tid / KV;
+        a_kc = (tid % KV) * VEC;
+        a_p = A + (long long)min(m0 + ra0, g.M - 1) * g.lda + a_kc;
+        a_rowstep = (long long)RA * g.lda;
+        a_dst0 = sA_base + 8u * (ra0 * T::SA + a_kc);
 #pragma unroll
-    for (int it = 0; it < A_IT; ++it) {
-        const int c = tid + it * NT;
-        const int r = c / KV, kc = (c % KV) * VEC;
-        a_ok[it] = c < A_CH && m0 + r < g.M;
-        a_src[it] = A + (long long)(a_ok[it] ? m0 + r : 0) * g.lda + kc;
-        a_dst[it] = sA_base + 8u * (r * T::SA + kc);
-        a_k[it] = kc;
-    }
-    const double* b_src[B_IT];
-    unsigned b_dst[B_IT];
-    int b_k[B_IT];
-    bool b_ok[B_IT];
-    long long b_kstep;  // global stride of one k row of B
-#pragma unroll
-    for (int it = 0; it < B_IT; ++it) {
-        const int c = tid + it * NT;
+        for (int it = 0; it < A_IT; ++it)
+            if (m0 + ra0 + it * RA < g.M) a_mask |= 1u << it;
         if constexpr (BKM) {
-            const int r = c / KV, kc = (c % KV) * VEC;  // r = n, kc = k
-            b_ok[it] = c < B_CH && n0 + r < g.N;
-            b_src[it] = B + (long long)(b_ok[it] ? n0 + r : 0) * g.ldb + kc;
-            b_dst[it] = sB_base + 8u * (r * T::SB + kc);
-            b_k[it] = kc;
+            const int rb0 = tid / KV, kc = (tid % KV) * VEC;  // rows = n, kc = k
+            b_r0 = kc;
+            b_p = B + (long long)min(n0 + rb0, g.N - 1) * g.ldb + kc;
+            b_dst0 = sB_base + 8u * (rb0 * T::SB + kc);
+#pragma unroll
+            for (int it = 0; it < B_IT; ++it)
+                if (n0 + rb0 + it * RB < g.N) b_mask |= 1u << it;
         } else {
-            constexpr int NV = BN / VEC;
-            const int r = c / NV, nc = (c % NV) * VEC;  // r = k, nc = n
-            b_ok[it] = c < B_CH && n0 + nc < g.N;
-            b_src[it] = B + (long long)r * g.ldb + (b_ok[it] ? n0 + nc : 0);
-            b_dst[it] = sB_base + 8u * (r * T::SB + nc);
-            b_k[it] = r;
+            const int rb0 = tid / NVB, nc = (tid % NVB) * VEC;  // rows = k, nc = n
+            b_r0 = rb0;
+            b_p = B + (long long)rb0 * g.ldb + (n0 + nc < g.N ? n0 + nc : 0);
+            b_dst0 = sB_base + 8u * (rb0 * T::SB + nc);
+            b_mask = n0 + nc < g.N ? ~0u : 0u;
+        }
+        b_rowstep = (long long)RB * g.ldb;
+    } else {
+#pragma unroll
+        for (int it = 0; it < A_IT; ++it) {
+            const int c = tid + it * NT;
+            const int r = c / KV, kc = (c % KV) * VEC;
+            a_ok[it] = c < A_CH && m0 + r < g.M;
+            a_src[it] = A + (long long)(a_ok[it] ? m0 + r : 0) * g.lda + kc;
+            a_dst[it] = sA_base + 8u * (r * T::SA + kc);
+            a_k[it] = kc;
+        }
+#pragma unroll
+        for (int it = 0; it < B_IT; ++it) {
+            const int c = tid + it * NT;
+            if constexpr (BKM) {
+                const int r = c / KV, kc = (c % KV) * VEC;  // r = n, kc = k
+                b_ok[it] = c < B_CH && n0 + r < g.N;
+                b_src[it] = B + (long long)(b_ok[it] ? n0 + r : 0) * g.ldb + kc;
+                b_dst[it] = sB_base + 8u * (r * T::SB + kc);
+                b_k[it] = kc;
+            } else {
+                const int r = c / NVB, nc = (c % NVB) * VEC;  // r = k, nc = n
+                b_ok[it] = c < B_CH && n0 + nc < g.N;
+                b_src[it] = B + (long long)r * g.ldb + (b_ok[it] ? n0 + nc : 0);
+                b_dst[it] = sB_base + 8u * (r * T::SB + nc);
+                b_k[it] = r;
+            }
         }
     }
-    b_kstep = BKM ? 1 : g.ldb;
 
     // consecutive k slices are loaded in order: the source pointers advance by one slice per call
     // (no per-slice 64-bit multiply in the issue path)
@@ -127,19 +172,39 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
     int k_next = 0;
     auto load_next = [&](int stage) {
         const int k0 = k_next;
+        if constexpr (AFF) {
+            const double* p = a_p;
+            const bool kok = k0 + a_kc < g.K;
 #pragma unroll
-        for (int it = 0; it < A_IT; ++it) {
-            if (A_CH % NT != 0 && tid + it * NT >= A_CH) continue;
-            const bool ok = a_ok[it] && k0 + a_k[it] < g.K;
-            cp_async<VEC>(a_dst[it] + 8u * stage * T::ASZ, ok ? a_src[it] : A, ok);
-            a_src[it] += BK;
-        }
+            for (int it = 0; it < A_IT; ++it) {
+                const bool ok = kok && ((a_mask >> it) & 1u);
+                cp_async<VEC>(a_dst0 + 8u * (it * RA * T::SA + stage * T::ASZ), ok ? p : A, ok);
+                p += a_rowstep;
+            }
+            a_p += BK;
+            p = b_p;
 #pragma unroll
-        for (int it = 0; it < B_IT; ++it) {
-            if (B_CH % NT != 0 && tid + it * NT >= B_CH) continue;
-            const bool ok = b_ok[it] && k0 + b_k[it] < g.K;
-            cp_async<VEC>(b_dst[it] + 8u * stage * T::BSZ, ok ? b_src[it] : B, ok);
-            b_src[it] += b_step;
+            for (int it = 0; it < B_IT; ++it) {
+                const bool ok = ((b_mask >> (BKM ? it : 0)) & 1u) && (BKM ? k0 + b_r0 < g.K : k0 + b_r0 + it * RB < g.K);
+                cp_async<VEC>(b_dst0 + 8u * (it * RB * T::SB + stage * T::BSZ), ok ? p : B, ok);
+                p += b_rowstep;
+            }
+            b_p += b_step;
+        } else {
+#pragma unroll
+            for (int it = 0; it < A_IT; ++it) {
+                if (A_CH % NT != 0 && tid + it * NT >= A_CH) continue;
+                const bool ok = a_ok[it] && k0 + a_k[it] < g.K;
+                cp_async<VEC>(a_dst[it] + 8u * stage * T::ASZ, ok ? a_src[it] : A, ok);
+                a_src[it] += BK;
+            }
+#pragma unroll
+            for (int it = 0; it < B_IT; ++it) {
+                if (B_CH % NT != 0 && tid + it * NT >= B_CH) continue;
+                const bool ok = b_ok[it] && k0 + b_k[it] < g.K;
+                cp_async<VEC>(b_dst[it] + 8u * stage * T::BSZ, ok ? b_src[it] : B, ok);
+                b_src[it] += b_step;
+            }
         }
         k_next += BK;
     };
@@ -203,10 +268,15 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
         atomicAdd(g.flop_counter, static_cast<unsigned long long>(2 * rows * cols * kexec));
     }
     k_next = kt_lo * BK;
+    if constexpr (AFF) {
+        a_p += k_next;
+        b_p += static_cast<long long>(k_next) * b_kstep;
+    } else {
 #pragma unroll
-    for (int it = 0; it < A_IT; ++it) a_src[it] += k_next;
+        for (int it = 0; it < A_IT; ++it) a_src[it] += k_next;
 #pragma unroll
-    for (int it = 0; it < B_IT; ++it) b_src[it] += static_cast<long long>(k_next) * b_kstep;
+        for (int it = 0; it < B_IT; ++it) b_src[it] += static_cast<long long>(k_next) * b_kstep;
+    }
 #pragma unroll
     for (int s = 0; s < ST - 1; ++s) {
         if (s < NKT) load_next(s);

@@ -39,6 +39,7 @@ def main():
     ap.add_argument("--case", required=True)
     ap.add_argument("--out", required=True)
     ap.add_argument("--device-inputs", action="store_true")
+    ap.add_argument("--transport", default="host", choices=["host", "nccl"])
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -50,7 +51,7 @@ def main():
     w, bs, plan = case_inputs(args.case)
     a = pq.KroneckerSum(w.factors)
     ctx = pq.Context(0)
-    comm = S.Communicator.host()
+    comm = S.Communicator.nccl(ctx) if args.transport == "nccl" else S.Communicator.host()
     inp = torch.from_numpy(bs).cuda() if args.device_inputs else bs
     res = {}
     if plan == "plan":

@@ -102,11 +102,11 @@ def test_host_transport_gloo_world2():
 
 # ------------------------------------------------------------------ GPU: the real product ----
 
-def _launch(case, world, tmp_path, device_inputs=False):
+def _launch(case, world, tmp_path, device_inputs=False, transport="host"):
     out = str(tmp_path / case)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), str(ROOT / "tests" / "dist_worker.py"),
-           "--case", case, "--out", out] + (["--device-inputs"] if device_inputs else [])
+           "--case", case, "--out", out, "--transport", transport] + (["--device-inputs"] if device_inputs else [])
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=str(ROOT))
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-5000:]
     return [dict(np.load(f"{out}.r{k}.npz")) for k in range(world)]
@@ -157,6 +157,20 @@ def test_distributed_device_inputs_world2(ref, tmp_path):
     for res in ranks:
         assert list(res["plan"]) == plan
         assert max(rel2(res["cols"][m, j], want[m, j]) for m in range(want.shape[0]) for j in range(w.p)) <= 1e-11
+
+
+@pytest.mark.gpu
+def test_distributed_nccl_transport_world1(ref, tmp_path):
+    """The NCCL transport end to end on the one GPU this environment has: libnccl.so.2 loaded by
+    dlopen, the unique id broadcast through torch.distributed, ncclCommInitRank, the distributed
+    call (its exchanges are local copies at world 1) and ncclCommDestroy; results against the
+    reference."""
+    ranks = _launch("cfg3_gauss", 1, tmp_path, device_inputs=True, transport="nccl")
+    w, want, want0, plan = _reference(ref, "cfg3_gauss")
+    res = ranks[0]
+    assert list(res["plan"]) == plan
+    assert max(rel2(res["cols"][m, j], want[m, j]) for m in range(want.shape[0]) for j in range(w.p)) <= 1e-11
+    assert max(rel2(res["phi0"][m], want0[m]) for m in range(want.shape[0])) <= 1e-11
 
 
 @pytest.mark.gpu
