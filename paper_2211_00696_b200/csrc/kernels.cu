@@ -36,6 +36,11 @@ static const bool g_band_tile32 = [] {
     const char* e = std::getenv("PQ_BAND_TILE");
     return !(e && std::string(e) == "64");
 }();
+// PQ_SMALL_GRID_TILE=0 keeps the 32x128 band tile on small grids (shape 8 off)
+static const bool g_small_grid_tile = [] {
+    const char* e = std::getenv("PQ_SMALL_GRID_TILE");
+    return !(e && e[0] == '0');
+}();
 static const bool g_persistent_enabled = [] {
     const char* e = std::getenv("PQ_PERSISTENT");
     return e && e[0] == '1';
@@ -59,6 +64,10 @@ int launch_gemm(const GemmArgs& g, cudaStream_t s) {
     // negligible-block skip (g.band): 32-extent tiles along the exponential's rows, so each CTA
     // streams exactly the k-slices its 32-row block needs (PQ_BAND_TILE=64 keeps 64x64 tiles)
     if (shape == 3 && vec2 && g.band && g_band_tile32) shape = g.band_mode == 3 ? 7 : 6;
+    // (64-row tiles must not straddle two stacked exponentials: band_rows a multiple of 64)
+    if (shape == 6 && !g.b_kmajor && ctas(32, 128) <= 1024 && g_small_grid_tile &&
+        (g.band_mode == 2 || (g.band_mode == 1 && g.band_rows % 64 == 0)))
+        shape = 8;
     return g.b_kmajor ? launch_gemm_kk(g, vec2, shape, s) : launch_gemm_nk(g, vec2, shape, s);
 }
 
