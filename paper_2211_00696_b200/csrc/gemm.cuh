@@ -617,9 +617,8 @@ int launch_gemm_family(const GemmArgs& g, bool vec2, int shape, cudaStream_t s) 
             return launch_cfg<32, 128, 16, 32, 32, 2, BKM, 2, 4>(g, s);
         case 7:  // negligible-block skip, exponential = B (k-major): 32-column tiles (BK 16: +3-6%)
             return launch_cfg<64, 32, 16, 32, 16, 2, BKM, 2, 6>(g, s);
-        case 8:  // exponential = A on small grids (<= 1024 32x128 tiles, e.g. the squaring's column
-                 // halves): 64x32 tiles at 7 CTAs/SM fill the last wave (2048 CTAs in 1.98 waves
-                 // instead of 1024 in 1.73): -7% on those launches (profiles/r02_gemm_affine_descriptors_ab.txt)
+        case 8:  // exponential = A on small grids (PQ_SMALL_GRID_TILE=1 only, kernels.cu): 64x32 tiles at
+                 // 7 CTAs/SM fill the last wave (2048 CTAs in 1.98 waves instead of 1024 in 1.73)
             return launch_cfg<64, 32, 16, 32, 16, 2, BKM, 2, 7>(g, s);
         case 3:
             // 16-byte path: BK = 8, 4 stages and <= 128 registers give 4 CTAs (16 warps) per SM,

@@ -36,10 +36,12 @@ static const bool g_band_tile32 = [] {
     const char* e = std::getenv("PQ_BAND_TILE");
     return !(e && std::string(e) == "64");
 }();
-// PQ_SMALL_GRID_TILE=0 keeps the 32x128 band tile on small grids (shape 8 off)
+// PQ_SMALL_GRID_TILE=1: 64x32 tiles at 7 CTAs/SM for exponential-as-A launches with <= 1024 32x128
+// tiles.  -7% per launch in isolation (tools/gemm_tune.cu), but slower in the pipeline, where the
+// squaring's two column halves already overlap on two streams (451 vs 470 actions/s): off.
 static const bool g_small_grid_tile = [] {
     const char* e = std::getenv("PQ_SMALL_GRID_TILE");
-    return !(e && e[0] == '0');
+    return e && e[0] == '1';
 }();
 static const bool g_persistent_enabled = [] {
     const char* e = std::getenv("PQ_PERSISTENT");
