@@ -7,6 +7,12 @@
 
 #include <algorithm>
 #include <cmath>
+#include <condition_variable>
+#include <deque>
+#include <exception>
+#include <functional>
+#include <thread>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <map>
@@ -261,19 +267,16 @@ Quartic stationary_quartic(const BoundArgs& q) {
 // are memoised by the exact coefficient bits (a pure function: results are bit-identical).
 static std::vector<double> stationary_roots(const Quartic& c) {
     using Key = std::array<unsigned long long, 3>;  // exact bit patterns of a3, a2, a1
-    static std::mutex mu;
-    static std::map<Key, std::vector<double>> memo;
+    // per thread (the planner's level evaluations run on several threads at once; a shared map
+    // behind one mutex serialised them)
+    thread_local std::map<Key, std::vector<double>> memo;
     Key key;
     std::memcpy(key.data(), c.data(), sizeof(key));
     if (c[3] == 1.0 && std::isfinite(c[0]) && std::isfinite(c[1]) && std::isfinite(c[2])) {
-        {
-            std::lock_guard<std::mutex> hold(mu);
-            auto it = memo.find(key);
-            if (it != memo.end()) return it->second;
-        }
+        auto it = memo.find(key);
+        if (it != memo.end()) return it->second;
         auto r = real_zeros_above_one(c);
-        std::lock_guard<std::mutex> hold(mu);
-        if (memo.size() > (1u << 18)) memo.clear();
+        if (memo.size() > (1u << 16)) memo.clear();
         memo.emplace(key, r);
         return r;
     }
@@ -341,14 +344,111 @@ int node_count(double eps, int p, double alpha, double beta, int kind) {
     return out;
 }
 
-// bounds.hpp:185-207 (Alg. 5): scan l downward, stop at the first strict cost increase.
+// A small process-wide pool for the planner's independent quadnodes evaluations (one per
+// scaling level l).  Pure functions of their arguments, so running them concurrently changes no
+// result; the caller keeps the reference's sequential scan order for the decisions.
+namespace {
+class PlannerPool {
+public:
+    static PlannerPool& get() {
+        static PlannerPool pool;
+        return pool;
+    }
+    void run(std::vector<std::function<void()>>& jobs) {
+        if (jobs.empty()) return;
+        struct Latch {
+            std::mutex mu;
+            std::condition_variable cv;
+            size_t left;
+        } latch;
+        latch.left = jobs.size();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            for (auto& j : jobs)
+                q_.push_back([&latch, &j] {
+                    j();
+                    std::lock_guard<std::mutex> l2(latch.mu);
+                    if (--latch.left == 0) latch.cv.notify_all();
+                });
+        }
+        cv_.notify_all();
+        std::unique_lock<std::mutex> lk(latch.mu);
+        latch.cv.wait(lk, [&latch] { return latch.left == 0; });
+    }
+    int threads() const { return static_cast<int>(th_.size()); }
+
+private:
+    PlannerPool() {
+        const unsigned hw = std::thread::hardware_concurrency();
+        const int n = static_cast<int>(std::min(6u, hw > 1 ? hw - 1 : 1u));
+        for (int i = 0; i < n; ++i)
+            th_.emplace_back([this] {
+                while (true) {
+                    std::function<void()> f;
+                    {
+                        std::unique_lock<std::mutex> lk(mu_);
+                        cv_.wait(lk, [this] { return stop_ || !q_.empty(); });
+                        if (stop_ && q_.empty()) return;
+                        f = std::move(q_.front());
+                        q_.pop_front();
+                    }
+                    f();
+                }
+            });
+    }
+    ~PlannerPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    std::deque<std::function<void()>> q_;
+    std::vector<std::thread> th_;
+    bool stop_ = false;
+};
+}  // namespace
+
+// bounds.hpp:185-207 (Alg. 5): scan l downward, stop at the first strict cost increase.  The
+// node counts of the first levels of the scan are evaluated concurrently (each ~0.1 ms of root
+// finding; the scan typically stops 3-5 levels below the top); the scan itself, and which
+// evaluation's exception surfaces, follow the reference's sequential order exactly.
 Plan plan_quadrature(double eps, int p, double alpha, double beta, int kind, const Cost& cost) {
     require(alpha > 0.0, "setup_quadrature: need alpha > 0");
     const int top = alpha > 1.0 ? static_cast<int>(std::ceil(std::log2(alpha) - 1e-12)) : 0;
+    static const int kAhead = [] {
+        const char* v = std::getenv("PQ_PLAN_THREADS");
+        return v ? std::max(1, std::atoi(v)) : 6;
+    }();
+    const int ahead = std::min(top + 1, kAhead);
+    std::vector<int> pre(static_cast<size_t>(ahead), 0);
+    std::vector<std::exception_ptr> err(static_cast<size_t>(ahead));
+    if (ahead > 1) {
+        std::vector<std::function<void()>> jobs;
+        for (int i = 0; i < ahead; ++i)
+            jobs.push_back([&, i] {
+                try {
+                    pre[static_cast<size_t>(i)] = node_count(eps, p, std::ldexp(alpha, -(top - i)), beta, kind);
+                } catch (...) {
+                    err[static_cast<size_t>(i)] = std::current_exception();
+                }
+            });
+        PlannerPool::get().run(jobs);
+    }
     Plan best;
     bool seen = false;
     for (int l = top; l >= 0; --l) {
-        const int n = node_count(eps, p, std::ldexp(alpha, -l), beta, kind);
+        const int i = top - l;
+        int n;
+        if (ahead > 1 && i < ahead) {
+            if (err[static_cast<size_t>(i)]) std::rethrow_exception(err[static_cast<size_t>(i)]);
+            n = pre[static_cast<size_t>(i)];
+        } else {
+            n = node_count(eps, p, std::ldexp(alpha, -l), beta, kind);
+        }
         const double c = cost(n, l, p);
         if (!seen || c < best.cost) {
             best = Plan{l, n, c};
