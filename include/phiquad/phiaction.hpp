@@ -106,12 +106,21 @@ inline std::vector<PhiColumns> phi_fixed_multi(const KroneckerSum& a, const std:
     (void)threads;
     if (p < 1) throw std::invalid_argument("phi_fixed: need p >= 1");
     const int dim = a.dim();
-    const auto flat = detail::gather(bs, dim, "phi_fixed");
+    std::vector<const double*> ptrs;
+    for (const auto& b : bs) {
+        if (static_cast<int>(b.size()) != dim) throw std::invalid_argument("phi_fixed: vector length mismatch");
+        ptrs.push_back(b.data());
+    }
     const auto f = detail::flatten(a);
-    std::vector<double> out(bs.size() * static_cast<size_t>(p) * dim);
-    b200::check(pq_phi_fixed(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
-                             flat.data(), p, rule.points(), rule.nodes.data(), rule.weights.data(), out.data(), PQ_HOST));
-    return detail::scatter(out, static_cast<int>(bs.size()), p, dim);
+    const int nb = static_cast<int>(bs.size());
+    // read each b in place and write straight into the returned PhiColumns (pq_phi_fixed_cols)
+    std::vector<PhiColumns> out = detail::alloc_columns(nb, p, dim);
+    std::vector<double*> cols;
+    for (auto& pc : out)
+        for (auto& c : pc.cols) cols.push_back(c.data());
+    b200::check(pq_phi_fixed_cols(b200::context(), a.order(), f.shape.data(), f.data.data(), nb, ptrs.data(), p,
+                                  rule.points(), rule.nodes.data(), rule.weights.data(), cols.data(), PQ_HOST));
+    return out;
 }
 
 inline PhiColumns phi_fixed(const KroneckerSum& a, const std::vector<double>& b, int p, const QuadratureRule& rule,
@@ -125,14 +134,22 @@ inline std::vector<PhiColumns> phi_adaptive_multi(const KroneckerSum& a, const s
     if (p < 1) throw std::invalid_argument("phi_adaptive: need p >= 1");
     if (!(eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
     const int dim = a.dim();
-    const auto flat = detail::gather(bs, dim, "phi_adaptive");
+    std::vector<const double*> ptrs;
+    for (const auto& b : bs) {
+        if (static_cast<int>(b.size()) != dim) throw std::invalid_argument("phi_adaptive: vector length mismatch");
+        ptrs.push_back(b.data());
+    }
     const auto f = detail::flatten(a);
-    std::vector<double> out(bs.size() * static_cast<size_t>(p) * dim);
+    const int nb = static_cast<int>(bs.size());
+    std::vector<PhiColumns> out = detail::alloc_columns(nb, p, dim);
+    std::vector<double*> cols;
+    for (auto& pc : out)
+        for (auto& c : pc.cols) cols.push_back(c.data());
     int pts = 0;
-    b200::check(pq_phi_adaptive(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
-                                flat.data(), p, eps, out.data(), &pts, PQ_HOST));
+    b200::check(pq_phi_adaptive_cols(b200::context(), a.order(), f.shape.data(), f.data.data(), nb, ptrs.data(), p, eps,
+                                     cols.data(), &pts, PQ_HOST));
     if (points_used) *points_used = pts;
-    return detail::scatter(out, static_cast<int>(bs.size()), p, dim);
+    return out;
 }
 
 inline PhiColumns phi_adaptive(const KroneckerSum& a, const std::vector<double>& b, int p, double eps, int threads = 1,
@@ -144,13 +161,20 @@ inline PhiColumns phi_adaptive(const KroneckerSum& a, const std::vector<double>&
 inline void squaring_step(PhiColumns& y, const std::vector<DenseMatrix>& exps, const std::vector<int>& shape) {
     const int p = y.p();
     if (p == 0) return;
+    // the reference's mode_apply checks, in its order (kron.hpp:92-102)
+    if (exps.size() != shape.size()) throw std::invalid_argument("mode_apply: rank mismatch");
+    const long long dim = detail::shape_product(shape);
+    std::vector<double*> cols;
+    for (auto& c : y.cols) {
+        if (static_cast<long long>(c.size()) != dim) throw std::invalid_argument("mode_apply: vector length mismatch");
+        cols.push_back(c.data());
+    }
+    for (size_t k = 0; k < exps.size(); ++k)
+        if (exps[k].rows() != shape[k]) throw std::invalid_argument("mode_apply: factor extent mismatch");
     const auto f = detail::flatten(exps);
-    if (f.shape != shape) throw std::invalid_argument("mode_apply: factor extent mismatch");
-    const int dim = static_cast<int>(detail::shape_product(shape));
-    auto flat = detail::gather(y.cols, dim, "mode_apply");
-    b200::check(pq_squaring_step(b200::context(), static_cast<int>(shape.size()), shape.data(), f.data.data(), p,
-                                 flat.data(), PQ_HOST));
-    y.cols = detail::scatter(flat, 1, p, dim).front().cols;
+    // the columns are rewritten in place (pq_squaring_step_cols): no flattening copy
+    b200::check(pq_squaring_step_cols(b200::context(), static_cast<int>(shape.size()), shape.data(), f.data.data(), p,
+                                      cols.data(), PQ_HOST));
 }
 
 inline std::vector<PhiColumns> phi_with_plan(const KroneckerSum& a, const std::vector<std::vector<double>>& bs, int p,

@@ -159,9 +159,20 @@ PQ_API int pq_phi_fixed(pq_ctx* ctx, int d, const int* shape, const double* fact
 /* phiaction.hpp:156 phi_adaptive_multi (CC ladder 7 -> 13 -> 25 ...). Synchronises once per level. */
 PQ_API int pq_phi_adaptive(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb,
                     const double* bs, int p, double eps, double* out, int* points_used, int space);
+/* The same with the caller's vectors as they are (the drop-in headers' phi_fixed(_multi) /
+ * phi_adaptive(_multi)): RHS m at bs[m], phi_{j+1} of RHS m to cols[m*p + j] (N doubles each). */
+PQ_API int pq_phi_fixed_cols(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb,
+                             const double* const* bs, int p, int m, const double* nodes, const double* weights,
+                             double* const* cols, int space);
+PQ_API int pq_phi_adaptive_cols(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb,
+                                const double* const* bs, int p, double eps, double* const* cols, int* points_used,
+                                int space);
 /* phiaction.hpp:255 squaring_step: y [p][N] rewritten in place to phi_j(2A). exps host-side. */
 PQ_API int pq_squaring_step(pq_ctx* ctx, int d, const int* shape, const double* exps, int p, double* y,
                      int space);
+/* squaring_step on the caller's column vectors in place (cols[j], N doubles each). */
+PQ_API int pq_squaring_step_cols(pq_ctx* ctx, int d, const int* shape, const double* exps, int p,
+                                 double* const* cols, int space);
 /* phiaction.hpp:277 phi_with_plan. */
 PQ_API int pq_phi_with_plan(pq_ctx* ctx, int d, const int* shape, const double* factors, int nb,
                      const double* bs, int p, int l, int n, int kind, double eps, double* out,

@@ -96,6 +96,11 @@ SIGNATURES = {
     "pq_phi_fixed": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, vp, C.c_int, C.c_int, dp, dp, vp, C.c_int]),
     "pq_phi_adaptive": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, vp, C.c_int, C.c_double, vp, ip, C.c_int]),
     "pq_squaring_step": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, vp, C.c_int]),
+    "pq_phi_fixed_cols": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, C.POINTER(vp), C.c_int, C.c_int, dp, dp,
+                                    C.POINTER(vp), C.c_int]),
+    "pq_phi_adaptive_cols": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, C.POINTER(vp), C.c_int, C.c_double,
+                                       C.POINTER(vp), ip, C.c_int]),
+    "pq_squaring_step_cols": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, C.POINTER(vp), C.c_int]),
     "pq_phi_with_plan": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, vp, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_double, vp, ip, C.c_int]),
     "pq_phiquadmv": (C.c_int, [vp, C.c_int, ip, dp, C.c_int, vp, C.POINTER(PhiRequestC), vp,

@@ -113,6 +113,39 @@ void finish(pq_ctx& c, int space) {
     }
 }
 
+// Caller vectors at their own addresses (the drop-in headers' std::vectors): gathered into one
+// contiguous device buffer, and results scattered back -- pageable results of 8 MB and more
+// through the context's pinned bounce, moved by several host threads.
+const double* gather_cols(pq_ctx& c, const double* const* v, int count, long long N, int space, const char* slot) {
+    need(v != nullptr, "null vector list");
+    for (int k = 0; k < count; ++k) need(v[k] != nullptr, "null vector");
+    if (space == PQ_DEVICE && count == 1) return v[0];
+    double* g = ws(c, slot, static_cast<size_t>(count) * N);
+    for (int k = 0; k < count; ++k)
+        cuda_check(cudaMemcpyAsync(g + static_cast<size_t>(k) * N, v[k], N * sizeof(double),
+                                   space == PQ_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c.stream),
+                   "gather vectors");
+    return g;
+}
+
+void scatter_cols(pq_ctx& c, const double* dout, double* const* cols, int count, long long N, int space) {
+    need(cols != nullptr, "null output list");
+    for (int k = 0; k < count; ++k) need(cols[k] != nullptr, "null output vector");
+    const size_t total = static_cast<size_t>(count) * N;
+    if (space == PQ_HOST && total >= kBounceMin) {
+        double* bnc = pinned_bounce(c, "cols", total);
+        cuda_check(cudaMemcpyAsync(bnc, dout, total * sizeof(double), cudaMemcpyDeviceToHost, c.stream), "D2H");
+        finish(c, space);
+        host_scatter(cols, bnc, count, static_cast<size_t>(N));
+        return;
+    }
+    for (int k = 0; k < count; ++k)
+        cuda_check(cudaMemcpyAsync(cols[k], dout + static_cast<size_t>(k) * N, N * sizeof(double),
+                                   space == PQ_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c.stream),
+                   "scatter columns");
+    finish(c, space);
+}
+
 NodesWeights rule_from(int m, const double* nodes, const double* weights) {
     need(m >= 1 && nodes && weights, "phi_fixed: rule needs at least one point");
     NodesWeights r;
@@ -605,8 +638,12 @@ int pq_phi_adaptive(pq_ctx* c, int d, const int* shape, const double* factors, i
         need_ctx(c);
         need(p >= 1, "phi_adaptive: need p >= 1");
         need(eps > 0.0, "phi_adaptive: need eps > 0");
-        need(nb >= 1, "phi_adaptive: need at least one right-hand side");
+        need(nb >= 0, "phi_adaptive: need nb >= 0");
         const long long N = dim_of(d, shape);
+        if (nb == 0) {  // the reference still climbs to the 13-point rule (phiaction.hpp:175-240)
+            if (points_used) *points_used = 13;
+            return;
+        }
         arena_begin(*c);
         DevOp op = upload_op(*c, d, shape, factors, "factors");
         const double* db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");
@@ -614,6 +651,70 @@ int pq_phi_adaptive(pq_ctx* c, int d, const int* shape, const double* factors, i
         phi_adaptive_dev(*c, op, 1.0, nb, db, p, eps, dout, points_used);
         finish_out(*c, out, dout, static_cast<size_t>(nb) * p * N, space);
         finish(*c, space);
+    });
+}
+
+int pq_phi_fixed_cols(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* const* bs,
+                      int p, int m, const double* nodes, const double* weights, double* const* cols, int space) {
+    return guarded([&] {
+        NvtxRange nvtx("pq_phi_fixed_cols");
+        need_ctx(c);
+        need(p >= 1, "phi_fixed: need p >= 1");
+        need(nb >= 0, "phi_fixed: need nb >= 0");
+        const long long N = dim_of(d, shape);
+        const NodesWeights rule = rule_from(m, nodes, weights);
+        if (nb == 0) return;
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        const double* db = gather_cols(*c, bs, nb, N, space, "hin_b");
+        double* dout = ws(*c, "hout", static_cast<size_t>(nb) * p * N);
+        phi_fixed_dev(*c, op, 1.0, nb, db, p, rule, dout);
+        scatter_cols(*c, dout, cols, nb * p, N, space);
+    });
+}
+
+int pq_phi_adaptive_cols(pq_ctx* c, int d, const int* shape, const double* factors, int nb, const double* const* bs,
+                         int p, double eps, double* const* cols, int* points_used, int space) {
+    return guarded([&] {
+        NvtxRange nvtx("pq_phi_adaptive_cols");
+        need_ctx(c);
+        need(p >= 1, "phi_adaptive: need p >= 1");
+        need(eps > 0.0, "phi_adaptive: need eps > 0");
+        need(nb >= 0, "phi_adaptive: need nb >= 0");
+        const long long N = dim_of(d, shape);
+        if (nb == 0) {
+            if (points_used) *points_used = 13;
+            return;
+        }
+        arena_begin(*c);
+        DevOp op = upload_op(*c, d, shape, factors, "factors");
+        const double* db = gather_cols(*c, bs, nb, N, space, "hin_b");
+        double* dout = ws(*c, "hout", static_cast<size_t>(nb) * p * N);
+        phi_adaptive_dev(*c, op, 1.0, nb, db, p, eps, dout, points_used);
+        scatter_cols(*c, dout, cols, nb * p, N, space);
+    });
+}
+
+int pq_squaring_step_cols(pq_ctx* c, int d, const int* shape, const double* exps, int p, double* const* cols,
+                          int space) {
+    return guarded([&] {
+        NvtxRange nvtx("pq_squaring_step_cols");
+        need_ctx(c);
+        need(p >= 1, "squaring_step: need p >= 1");
+        const long long N = dim_of(d, shape);
+        arena_begin(*c);
+        DevOp ex = upload_op(*c, d, shape, exps, "exps");
+        need(cols != nullptr, "null vector list");
+        double* dy = ws(*c, "hio_y", static_cast<size_t>(p) * N);
+        for (int k = 0; k < p; ++k) {
+            need(cols[k] != nullptr, "null vector");
+            cuda_check(cudaMemcpyAsync(dy + static_cast<size_t>(k) * N, cols[k], N * sizeof(double),
+                                       space == PQ_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
+                                       c->stream),
+                       "gather columns");
+        }
+        squaring_steps_dev(*c, ex, 1.0, 1, p, 1, dy, ex.F[0]);
+        scatter_cols(*c, dy, cols, p, N, space);
     });
 }
 
