@@ -262,6 +262,65 @@ int gemm(pq_ctx& c, const GemmArgs& g) {
     return k;
 }
 
+constexpr int kMaxChainLevels = 12;  // kernels.hpp launch_gemm_chain (gemm.cuh kMaxChain)
+
+static bool chain_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PQ_GEMM_CHAIN");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+// Dependent levels of small batched products in one cooperative launch (launch_gemm_chain);
+// per-level launches when the chain does not qualify or PQ_GEMM_CHAIN=0.
+int gemm_chain(pq_ctx& c, std::vector<GemmArgs> levels, const char* tag) {
+    if (levels.empty()) return 0;
+    for (auto& g : levels) g.tag = tag;
+    if (!chain_enabled() || levels.size() == 1) {
+        int k = 0;
+        for (const auto& g : levels) k += gemm(c, g);
+        return k;
+    }
+    unsigned* bar = static_cast<unsigned*>(ws_bytes(c, "chain_bar", 256));
+    cudaEvent_t a = nullptr, b = nullptr;
+    size_t slot = 0;
+    if (c.profiling) {
+        if (c.ev_used + 2 > 4096) prof_collect(c);
+        if (!c.d_flops) cuda_check(cudaMalloc(&c.d_flops, sizeof(unsigned long long) * 2048), "flop counters");
+        slot = c.ev_used / 2;
+        if (slot == 0)
+            cuda_check(cudaMemsetAsync(c.d_flops, 0, sizeof(unsigned long long) * 2048, c.stream), "flop counters zero");
+        for (auto& g : levels) g.flop_counter = c.d_flops + slot;
+        a = prof_event(c);
+        b = prof_event(c);
+        cuda_check(cudaEventRecord(a, c.stream), "event record");
+    }
+    const int k = launch_gemm_chain(levels.data(), static_cast<int>(levels.size()), bar, c.stream);
+    if (k == 0) {  // not eligible: one launch per level (undo the profiling slot)
+        if (c.profiling) c.ev_used -= 2;
+        int n = 0;
+        for (auto& g : levels) {
+            g.flop_counter = nullptr;
+            n += gemm(c, g);
+        }
+        return n;
+    }
+    count_launch(c, k);
+    if (c.profiling) {
+        cuda_check(cudaEventRecord(b, c.stream), "event record");
+        double dense = 0.0;
+        for (const auto& g : levels) dense += 2.0 * g.M * static_cast<double>(g.N) * g.K * g.Z;
+        c.ev_flops.push_back(dense);
+        char key[160];
+        std::snprintf(key, sizeof key, "%s chain of %zu levels M%d N%d K%d", tag, levels.size(), levels[0].M,
+                      levels[0].N, levels[0].K);
+        c.ev_keys.push_back(key);
+        c.prof_launches += static_cast<uint64_t>(k);
+    }
+    return k;
+}
+
 KernelProbe::KernelProbe(pq_ctx& ctx, const char* t, double b) : c(ctx), tag(t), bytes(b) {
     if (!c.profiling) return;
     s = c.stream;
@@ -638,6 +697,28 @@ static void expm_core(pq_ctx& c, int n, const double* base, double op_scale, con
 static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>& hint, const int* s_dev, int s_max,
                             double* cur, double* other, double* out) {
     const size_t nn = static_cast<size_t>(n) * n;
+    if (chain_enabled() && s_max > 1 && s_max <= kMaxChainLevels) {
+        // all rounds in one chained launch over every entry: an entry whose squarings are done
+        // (sq_round >= its count) is carried through unchanged, so after s_max rounds every entry
+        // sits in the buffer round s_max - 1 wrote
+        std::vector<GemmArgs> levels;
+        double* a = cur;
+        double* b = other;
+        for (int r = 0; r < s_max; ++r) {
+            GemmArgs g = square_batch(n, count, a, a, b);
+            g.sq_count = s_dev;
+            g.sq_round = r;
+            levels.push_back(g);
+            std::swap(a, b);
+        }
+        gemm_chain(c, levels, "expm_squaring");
+        if (a != out)
+            cuda_check(cudaMemcpyAsync(out, a, static_cast<size_t>(count) * nn * sizeof(double), cudaMemcpyDeviceToDevice,
+                                       c.stream),
+                       "expm copy");
+        check_launch(c);
+        return;
+    }
     cudaStream_t st = c.stream;
     int z_done = 0;
     auto flush = [&](int z_from, int z_to) {
@@ -729,7 +810,10 @@ static const double* taylor_powers(pq_ctx& c, int n, const double* base, double 
     launch_taylor_base(n, nf, kTaylorM, base, foff_dev, op_scale, pow2_dev, P, c.stream);
     count_launch(c);
     const long long lnn = static_cast<long long>(nn), fs = static_cast<long long>(kTaylorM) * lnn;
-    for (int h = 1; h < kTaylorM; h *= 2) {  // P^(h+j) = P^h P^j, j = 1..min(h, m-h), all factors in one launch
+    // P^(h+j) = P^h P^j, j = 1..min(h, m-h), all factors per level; the log2(m) dependent levels
+    // run as one chained cooperative launch (gemm_chain)
+    std::vector<GemmArgs> levels;
+    for (int h = 1; h < kTaylorM; h *= 2) {
         const int J = std::min(h, kTaylorM - h);
         GemmArgs g = square_batch(n, nf * J, P + (h - 1) * lnn, P, P + h * lnn);
         g.zdiv = J;
@@ -739,9 +823,9 @@ static const double* taylor_powers(pq_ctx& c, int n, const double* base, double 
         g.sB2 = lnn;
         g.sC1 = fs;
         g.sC2 = lnn;
-        g.tag = "taylor_powers";
-        gemm(c, g);
+        levels.push_back(g);
     }
+    gemm_chain(c, levels, "taylor_powers");
     pc.P = P;
     pc.base = base;
     pc.foff = tf.foff;

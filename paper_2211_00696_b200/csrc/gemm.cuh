@@ -7,6 +7,7 @@
 // 64-bit address arithmetic) and the epilogue is compact (the extra-addend loop is not
 // unrolled) so the whole kernel stays inside the instruction cache.
 #pragma once
+#include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -51,32 +52,36 @@ struct TileCfg {
     static constexpr int MI = WM / 8, NI = WN / 8;
 };
 
-template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC, int MINB = 1>
-__global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB) k_gemm(const GemmArgs g) {
+// One output tile (bx, by, bz) of a GemmArgs launch; the body of k_gemm and of the chained
+// persistent kernel k_gemm_chain.  pdl: the programmatic-dependent-launch wait / trigger (plain
+// stream launches only).
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC>
+__device__ __forceinline__ void gemm_tile(const GemmArgs& g, int bx, int by, int bz, double* smem, bool pdl) {
     using T = TileCfg<BM, BN, BK, WM, WN, ST, BKM>;
     constexpr int NT = T::NT;
-    extern __shared__ __align__(16) double smem[];
     double* sA = smem;
     double* sB = smem + ST * T::ASZ;
 
-    const int z = blockIdx.z + g.z_off;
+    const int z = bz + g.z_off;
     const int z1 = z / g.zdiv, z2 = z - z1 * g.zdiv;
     const double* __restrict__ A = g.A + z1 * g.sA1 + z2 * g.sA2;
     const double* __restrict__ B = g.B + z1 * g.sB1 + z2 * g.sB2;
     double* C = g.C + z1 * g.sC1 + z2 * g.sC2;
-    const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+    const int m0 = bx * BM, n0 = by * BN;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / T::NWN, wn = warp % T::NWN;
     const int gid = lane >> 2, tig = lane & 3;
 
     // programmatic dependent launch: everything above is index math; global data written by the
     // preceding kernel (operands, band tables, squaring counts) is read only after this wait
-    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (pdl) asm volatile("griddepcontrol.wait;" ::: "memory");
     if (g.sq_count && g.sq_round >= g.sq_count[z]) {
         // expm squaring already finished for this matrix: carry it through unchanged.
         for (int e = tid; e < BM * BN; e += NT) {
             const int m = m0 + e / BN, n = n0 + e % BN;
-            if (m < g.M && n < g.N) C[(long long)m * g.ldc + n] = A[(long long)m * g.lda + n];
+            // __ldcg: in a chained launch A may have been written by other CTAs since this SM last
+            // read it (L1 is not coherent across SMs; the operand tiles use cp.async.cg, L2 only)
+            if (m < g.M && n < g.N) C[(long long)m * g.ldc + n] = __ldcg(&A[(long long)m * g.lda + n]);
         }
         return;
     }
@@ -314,7 +319,7 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
     cp_wait<0>();
     // this CTA no longer needs the SM for DMMA work: let the next kernel in the stream launch its
     // CTAs (they stop at griddepcontrol.wait until this grid has completed)
-    asm volatile("griddepcontrol.launch_dependents;");
+    if (pdl) asm volatile("griddepcontrol.launch_dependents;");
 
     // ---- epilogue (registers -> global) ----
     const double alpha = g.alpha_z ? g.alpha_z[z1] : g.alpha;
@@ -385,6 +390,57 @@ __global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB
                 if (n + 1 < g.N) row[n + 1] = acc[i][j][1];
             }
         }
+    }
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC, int MINB = 1>
+__global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB) k_gemm(const GemmArgs g) {
+    extern __shared__ __align__(16) double smem[];
+    gemm_tile<BM, BN, BK, WM, WN, ST, BKM, VEC>(g, blockIdx.x, blockIdx.y, blockIdx.z, smem, true);
+}
+
+// A chain of dependent batched GEMM levels in ONE cooperative launch (the Taylor powers
+// P^(h+j) = P^h P^j of the shared-power exponentials and the expm squaring rounds): every CTA
+// walks the tiles of a level (grid-stride), then the grid synchronises before the next level
+// reads its results.  Replaces 5-7 short dependent launches per chain, each a fraction of a wave.
+constexpr int kMaxChain = 12;
+struct GemmChain {
+    int levels = 0;
+    GemmArgs g[kMaxChain];
+};
+
+__device__ __forceinline__ void chain_grid_sync(unsigned* bar, unsigned nblocks, unsigned& gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned target = (gen + 1) * nblocks;
+        atomicAdd(bar, 1u);
+        while (true) {
+            unsigned v;
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+            if (v >= target) break;
+            __nanosleep(32);
+        }
+    }
+    ++gen;
+    __syncthreads();
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM, int VEC, int MINB>
+__global__ void __launch_bounds__(TileCfg<BM, BN, BK, WM, WN, ST, BKM>::NT, MINB)
+    k_gemm_chain(const __grid_constant__ GemmChain ch, unsigned* bar) {
+    extern __shared__ __align__(16) double smem[];
+    unsigned gen = 0;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    for (int lv = 0; lv < ch.levels; ++lv) {
+        const GemmArgs& g = ch.g[lv];
+        const int gx = (g.M + BM - 1) / BM, gy = (g.N + BN - 1) / BN;
+        const int tiles = gx * gy * g.Z;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+            gemm_tile<BM, BN, BK, WM, WN, ST, BKM, VEC>(g, t % gx, (t / gx) % gy, t / (gx * gy), smem, false);
+            __syncthreads();  // the next tile's prologue overwrites the stages this one read
+        }
+        if (lv + 1 < ch.levels) chain_grid_sync(bar, gridDim.x, gen);
     }
 }
 
@@ -584,6 +640,44 @@ static int launch_cfg(const GemmArgs& g, cudaStream_t s) {
         ++launches;
     }
     return launches;
+}
+
+template <int BM, int BN, int BK, int WM, int WN, int ST, int MINB>
+static int launch_chain_cfg(const GemmChain& ch, unsigned* bar, cudaStream_t s) {
+    using T = TileCfg<BM, BN, BK, WM, WN, ST, false>;
+    auto kern = k_gemm_chain<BM, BN, BK, WM, WN, ST, false, 2, MINB>;
+    static int per_sm = -1, sms = 0;
+    if (per_sm < 0) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, T::SMEM);
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, T::NT, T::SMEM) != cudaSuccess) per_sm = 0;
+    }
+    if (per_sm <= 0 || sms <= 0) return 0;
+    long long tiles = 0;
+    for (int lv = 0; lv < ch.levels; ++lv) {
+        const GemmArgs& g = ch.g[lv];
+        tiles = std::max(tiles, (long long)((g.M + BM - 1) / BM) * ((g.N + BN - 1) / BN) * g.Z);
+    }
+    const int grid = (int)std::min<long long>((long long)per_sm * sms, tiles);
+    if (grid <= 0) return 0;
+    cudaMemsetAsync(bar, 0, sizeof(unsigned), s);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(T::NT);
+    cfg.dynamicSmemBytes = T::SMEM;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA resident: the level barrier cannot deadlock
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, kern, ch, bar) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return 1;
 }
 
 // Tile shapes: 0 = 128x128 (8 warps of 64x32), 1 = 128x64, 2 = 64x128, 3 = 64x64, 4 = 32x32.

@@ -48,6 +48,10 @@ struct GemmArgs {
     const char* tag = nullptr;  // call site, for the profiling breakdown only
 };
 int launch_gemm(const GemmArgs& g, cudaStream_t s);  // returns number of kernel launches
+// `count` dependent batched GEMM levels (plain products, row-major B, 16-byte aligned) in ONE
+// cooperative launch with a grid barrier between levels; bar = one device unsigned (zeroed by
+// the launcher).  Returns 1, or 0 when the chain does not qualify (the caller launches per level).
+int launch_gemm_chain(const GemmArgs* levels, int count, unsigned* bar, cudaStream_t s);
 
 // ---- batched Pade-13 expm building blocks (dense.hpp:194-228) ----
 // X[z] = (scale[z] * (op_scale * base)) * 2^-s_z  (each product rounded, as the reference's

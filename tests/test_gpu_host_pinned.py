@@ -187,3 +187,48 @@ def test_phi_with_plan_cols_equals_contiguous(pq, kind, n):
     assert np.array_equal(np.stack(cols).reshape(nb, p, N), want)
     assert pts2.value == pts.value
     ctx.close()
+
+
+@pytest.mark.parametrize("n", [16, 64])
+def test_fixed_adaptive_squaring_cols_equal_contiguous(pq, n):
+    """pq_phi_fixed_cols / pq_phi_adaptive_cols / pq_squaring_step_cols (the drop-in headers'
+    phi_fixed_multi, phi_adaptive_multi and squaring_step on the caller's vectors) return bitwise
+    what the contiguous entry points return; n = 64 crosses the pinned-bounce threshold."""
+    from paper_2211_00696_b200.workloads import config
+    w = config(2, n=n)
+    a = pq.KroneckerSum(w.factors)
+    ctx = pq.Context(0)
+    d, sh, fac = a._abi()
+    nb, N, p = 2, w.N, w.p
+    bs = np.stack([w.rhs(40), w.rhs(41)])
+    b_sep = [np.ascontiguousarray(bs[m]) for m in range(nb)]
+    barr = (C.c_void_p * nb)(*[x.ctypes.data for x in b_sep])
+    H = pq._lib.PQ_HOST
+    rule = pq.cached_rule(pq.QuadKind.gauss_legendre, 9)
+    x, wt = np.ascontiguousarray(rule.nodes), np.ascontiguousarray(rule.weights)
+    want = np.empty((nb, p, N))
+    pq._lib.check(pq._lib.lib.pq_phi_fixed(ctx.handle, d, sh, fac, nb, C.c_void_p(bs.ctypes.data), p, 9,
+                                           x.ctypes.data_as(pq._lib.dp), wt.ctypes.data_as(pq._lib.dp),
+                                           C.c_void_p(want.ctypes.data), H))
+    cols = [np.full(N, np.nan) for _ in range(nb * p)]
+    carr = (C.c_void_p * (nb * p))(*[c.ctypes.data for c in cols])
+    pq._lib.check(pq._lib.lib.pq_phi_fixed_cols(ctx.handle, d, sh, fac, nb, barr, p, 9, x.ctypes.data_as(pq._lib.dp),
+                                                wt.ctypes.data_as(pq._lib.dp), carr, H))
+    assert np.array_equal(np.stack(cols).reshape(nb, p, N), want)
+    want = np.empty((nb, p, N))
+    pts, pts2 = C.c_int(), C.c_int()
+    pq._lib.check(pq._lib.lib.pq_phi_adaptive(ctx.handle, d, sh, fac, nb, C.c_void_p(bs.ctypes.data), p, 1e-10,
+                                              C.c_void_p(want.ctypes.data), C.byref(pts), H))
+    cols = [np.full(N, np.nan) for _ in range(nb * p)]
+    carr = (C.c_void_p * (nb * p))(*[c.ctypes.data for c in cols])
+    pq._lib.check(pq._lib.lib.pq_phi_adaptive_cols(ctx.handle, d, sh, fac, nb, barr, p, 1e-10, carr, C.byref(pts2), H))
+    assert np.array_equal(np.stack(cols).reshape(nb, p, N), want) and pts.value == pts2.value
+    exps = np.concatenate([pq.expm(np.ascontiguousarray(f), scale=[0.25], ctx=ctx)[0].reshape(-1) for f in w.factors])
+    y = np.ascontiguousarray(want[0])
+    y2 = [np.ascontiguousarray(want[0, j]) for j in range(p)]
+    pq._lib.check(pq._lib.lib.pq_squaring_step(ctx.handle, d, sh, exps.ctypes.data_as(pq._lib.dp), p,
+                                               C.c_void_p(y.ctypes.data), H))
+    yarr = (C.c_void_p * p)(*[c.ctypes.data for c in y2])
+    pq._lib.check(pq._lib.lib.pq_squaring_step_cols(ctx.handle, d, sh, exps.ctypes.data_as(pq._lib.dp), p, yarr, H))
+    assert np.array_equal(np.stack(y2), y)
+    ctx.close()

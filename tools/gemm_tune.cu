@@ -230,6 +230,10 @@ int main(int argc, char** argv) {
                    ms * 1e3, c.flops / (ms * 1e-3) / 1e12);                                            \
     }
         T(32, 128, 16, 32, 32, 2, 4)
+        T(32, 96, 16, 32, 32, 2, 5)
+        T(32, 96, 16, 32, 32, 2, 6)
+        T(32, 160, 16, 32, 32, 2, 3)
+        T(32, 160, 16, 32, 32, 2, 4)
         T(32, 128, 16, 32, 32, 2, 5)
         T(32, 128, 8, 32, 32, 2, 6)
         T(32, 128, 8, 32, 32, 2, 7)
