@@ -264,10 +264,15 @@ int gemm(pq_ctx& c, const GemmArgs& g) {
 
 constexpr int kMaxChainLevels = 12;  // kernels.hpp launch_gemm_chain (gemm.cuh kMaxChain)
 
+// PQ_GEMM_CHAIN=1: chained cooperative launches for the Taylor powers and the expm squaring
+// rounds.  Measured (profiles/r02_summary.md): the Taylor chain is as slow as its 5 launches
+// (55 vs 56 us: each level is bound by one tile's dependent K loop, not by launch gaps), the
+// squaring chain saves 20 us, but the cooperative grid occupies every SM and blocks the side
+// stream's overlap: 462 vs 471 actions/s at config 2.  Off by default.
 static bool chain_enabled() {
     static const bool on = [] {
         const char* v = std::getenv("PQ_GEMM_CHAIN");
-        return !(v && v[0] == '0');
+        return v && v[0] == '1';
     }();
     return on;
 }
