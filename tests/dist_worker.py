@@ -31,6 +31,15 @@ def case_inputs(case):
     if case == "cc_pinned_l0":    # CC at l = 0 (no squaring), 3 RHS
         w = config(2, n=20)
         return w, np.stack([w.rhs(k) for k in range(3)]), (0, 0)
+    if case == "d1_gauss":        # one factor: slabs of a single dimension, one rank owns the pencil
+        w = config(1, n=48)
+        w.d, w.factors = 1, [w.factors[0]]
+        w.n = 48
+        rng = np.random.default_rng(3)
+        return w, rng.standard_normal((1, 48)), (3, 6)
+    if case == "cc_2rhs_planned":  # adaptive CC with 2 RHS and l > 0 (squaring on 2 x p columns)
+        w = config(2, n=20)
+        return w, np.stack([w.rhs(k) for k in range(2)]), "plan"
     raise ValueError(case)
 
 

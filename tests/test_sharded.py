@@ -127,7 +127,8 @@ def _reference(ref, case):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("case,world", [("cfg3_gauss", 2), ("cfg2_cc", 2), ("cfg5_pinned", 3), ("cfg1_2d", 2),
-                                        ("cc_pinned_l0", 3), ("cfg2_cc", 3)])
+                                        ("cc_pinned_l0", 3), ("cfg2_cc", 3), ("d1_gauss", 2),
+                                        ("cc_2rhs_planned", 2)])
 def test_distributed_vs_reference(ref, tmp_path, case, world):
     """world processes on the one GPU; every rank's gathered phi_0..phi_p equals the reference's
     (1e-11 relative 2-norm per column, identical plan), and the slabs tile the gathered result."""
