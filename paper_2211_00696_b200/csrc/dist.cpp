@@ -355,9 +355,52 @@ double* slab_pool_grow(pq_ctx& c, int slots, int nb, long long S, int used) {
 }
 
 // Gauss node phase: acc [nb][p][S_r] = the slab of phi_j(2^-l A) b (phiaction.hpp:134-145)
+// The reduce-scatter alternative: every rank forms the weighted partial sums of its
+// own nodes over the FULL vector (node_sweep's fused combine), sends slab h of them to rank h, and
+// each rank adds the G partial slabs in ascending rank order.  Moves p nb (N - S_r) doubles per rank
+// against (q/G) nb (N - S_r) for the node transpose: used when ceil(q/G) > p.
+bool gauss_use_reduce_scatter(int q, int G, int p) { return G > 1 && (q + G - 1) / G > p; }
+
+void gauss_nodes_rs(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, const double* bs, int p,
+                    const NodesWeights& rule, const PhiExps& px, const std::vector<int>& own, double* acc) {
+    const long long S = g.S(g.r), N = op.N;
+    long long Es[3];
+    for (int k = 0; k < op.d; ++k) Es[k] = static_cast<long long>(op.n[k]) * op.n[k];
+    double* part = ws(c, "dpart", static_cast<size_t>(nb) * p * N);  // [m][j][N]
+    std::vector<double> coef;
+    node_coefs(rule, own, p, coef);
+    node_sweep(c, op, px.node, Es, static_cast<int>(own.size()), nb, bs, p, &coef, part, 1, nullptr, 0, px.node_band);
+    const int cols = nb * p;
+    double* recv = ws(c, "dpartslabs", static_cast<size_t>(g.G) * cols * std::max<long long>(S, 1));  // [h][col][S]
+    std::vector<Piece> sends, recvs;
+    for (int h = 0; h < g.G; ++h)
+        for (int col = 0; col < cols; ++col) {
+            sends.push_back({h, part + col * N + g.lo(h), g.S(h)});
+            recvs.push_back({h, recv + (static_cast<long long>(h) * cols + col) * S, S});
+        }
+    exchange(c, m, sends, recvs);
+    // acc[col] = sum over ranks h ascending of their partial slab (coefficient 1, fixed order)
+    std::vector<double> ones(static_cast<size_t>(g.G), 1.0);
+    std::vector<int> slots(static_cast<size_t>(g.G));
+    std::iota(slots.begin(), slots.end(), 0);
+    const double* one_dev = static_cast<const double*>(arena_push(c, ones.data(), ones.size() * sizeof(double)));
+    const int* sl_dev = static_cast<const int*>(arena_push(c, slots.data(), slots.size() * sizeof(int)));
+    arena_flush(c);
+    for (int col = 0; col < cols; ++col) {
+        KernelProbe kp(c, "k_combine(rank sum)", 8.0 * S * (g.G + 1));
+        launch_combine(S, 1, g.G, recv + static_cast<long long>(col) * S, static_cast<long long>(cols) * S, sl_dev,
+                       one_dev, acc + static_cast<long long>(col) * S, S, 1, c.stream);
+        count_launch(c);
+    }
+}
+
 void gauss_nodes(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, const double* bs, int p,
                  const NodesWeights& rule, const PhiExps& px, const std::vector<int>& own, double* acc) {
     const int q = rule.size();
+    if (gauss_use_reduce_scatter(q, g.G, p)) {
+        gauss_nodes_rs(c, m, g, op, nb, bs, p, rule, px, own, acc);
+        return;
+    }
     const long long S = g.S(g.r);
     long long Es[3];
     for (int k = 0; k < op.d; ++k) Es[k] = static_cast<long long>(op.n[k]) * op.n[k];

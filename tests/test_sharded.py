@@ -177,8 +177,8 @@ def test_distributed_nccl_transport_world1(ref, tmp_path):
 @pytest.mark.gpu
 def test_distributed_bytes_per_call(tmp_path):
     """Bytes a rank sends in a slab-output call (gather=False), against the DESIGN.md count for
-    Gauss: node transpose (own nodes) * nb * (N - S_r) + (l + 1 phi_0) exchanges of the slab <->
-    pencil flips."""
+    Gauss: node transpose (own nodes) or reduce-scatter (p partial sums, when ceil(q/G) > p) times
+    nb (N - S_r), plus the slab <-> pencil flips of the l squaring steps and phi_0."""
     ranks = _launch("cfg3_gauss", 2, tmp_path)
     sys.path.insert(0, str(ROOT / "tests"))
     from dist_worker import case_inputs
@@ -190,7 +190,8 @@ def test_distributed_bytes_per_call(tmp_path):
         b, e = (int(x) for x in res["slab"])
         S = e - b
         own = len(range(r, q, 2))
-        node = own * nb * (N - S)
+        # node transpose (own nodes' slabs) or, when ceil(q/G) > p, the reduce-scatter of p partial sums
+        node = (w.p if (q + 1) // 2 > w.p else own) * nb * (N - S)
         # a flip sends this rank's slab except its own pencil columns, twice per Kronecker apply
         c_lo, c_hi = rest * r // 2, rest * (r + 1) // 2
         flip = 2 * (S // rest) * (rest - (c_hi - c_lo))
