@@ -807,7 +807,13 @@ static const double* taylor_powers(pq_ctx& c, int n, const double* base, double 
     const size_t nn = static_cast<size_t>(n) * n;
     double* P = ws(c, "taylorP" + std::to_string(n), static_cast<size_t>(nf) * kTaylorM * nn);
     pq_ctx::PowCache& pc = c.pow_cache[n];
-    if (serial != 0 && pc.serial == serial && pc.P == P && pc.base == base && pc.foff == tf.foff && pc.scale == op_scale)
+    // The powers only depend on the scale's mantissa: fl(2^k m A) = 2^k fl(m A) exactly and the
+    // normalisation 2^-e_f absorbs 2^k, so B_f is bit-identical for every power-of-two multiple of
+    // the scale (the ETD stages' sigma = 1/2 and 1 share one set of powers within a call).
+    int e_new = 0, e_old = 0;
+    const double m_new = std::frexp(op_scale, &e_new), m_old = std::frexp(pc.scale, &e_old);
+    if (serial != 0 && pc.serial == serial && pc.P == P && pc.base == base && pc.foff == tf.foff && m_new == m_old &&
+        std::abs(e_new - e_old) <= 64)
         return P;
     const long long* foff_dev = static_cast<const long long*>(arena_push(c, tf.foff.data(), sizeof(long long) * nf));
     const double* pow2_dev = static_cast<const double*>(arena_push(c, tf.pow2.data(), sizeof(double) * nf));
