@@ -1239,7 +1239,44 @@ static void factor_bands(pq_ctx& c, const DevOp& op, const int2** out) {
 }
 
 // kron.hpp:111-119: y = sum_k mode_k(A_k) x (factor scaled by `scale` first when != 1).
+// every factor tridiagonal (|i - j| > 1 -> 0)?  From the operator's host copy, cached per upload.
+static bool factors_tridiagonal(pq_ctx& c, const DevOp& op) {
+    if (op.serial != 0 && c.tri_serial == op.serial) return c.tri;
+    bool tri = op.host != nullptr;
+    size_t off = 0;
+    for (int k = 0; k < op.d && tri; ++k) {
+        const int n = op.n[k];
+        const double* f = op.host->data() + off;
+        for (int i = 0; i < n && tri; ++i)
+            for (int j = 0; j < n; ++j)
+                if ((j < i - 1 || j > i + 1) && f[static_cast<size_t>(i) * n + j] != 0.0) {
+                    tri = false;
+                    break;
+                }
+        off += static_cast<size_t>(n) * n;
+    }
+    c.tri_serial = op.serial;
+    c.tri = tri;
+    return tri;
+}
+
+static bool stencil_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PQ_KMV_STENCIL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, double* y) {
+    if (stencil_enabled() && factors_tridiagonal(c, op)) {
+        // tridiagonal factors (the FD operators of every BASELINE config): one streaming pass,
+        // the reference's term order (bitwise its kron_matvec)
+        KernelProbe kp(c, "k_kron_tridiag", 16.0 * op.N);
+        launch_kron_tridiag(op.d, op.n, op.N, op.F, scale, x, y, c.stream);
+        count_launch(c);
+        return;
+    }
     const double* F[3] = {op.F[0], op.F[1], op.F[2]};
     if (scale != 1.0) {
         size_t total = 0;

@@ -103,6 +103,8 @@ struct pq_ctx {
     uint64_t op_serial = 0;  // incremented per operator upload (one per API call)
     // negligible-block tables of the operator's own factors (kron_matvec), per upload serial
     uint64_t fac_band_serial = 0;
+    uint64_t tri_serial = 0;  // operator upload whose factors were checked for tridiagonality
+    bool tri = false;
     const int2* fac_band[3] = {nullptr, nullptr, nullptr};
     cudaEvent_t ev_beta = nullptr;  // beta readback (phiquadmv) completes
     // Plan speculation (engine.cpp phiquadmv_dev): the last plan per operator/request; a call on

@@ -116,6 +116,11 @@ void launch_axpy(long long N, double c, const double* x, double* y, cudaStream_t
 // y = x - au  (generic source already evaluated)
 void launch_sub(long long N, const double* x, const double* au, double* y, cudaStream_t s);
 
+// kron_matvec with every factor tridiagonal (a 3-point stencil per mode, the reference's term order):
+// y = sum_k (I (x) .. fl(scale A_k) .. (x) I) x, F[k] row-major n[k] x n[k]
+void launch_kron_tridiag(int d, const int* n, long long N, const double* const* F, double scale, const double* x,
+                         double* y, cudaStream_t s);
+
 // ---- distributed squaring layout flips (dist.cpp) ----
 // Trailing-index cuts of a slab: rank h's pencil owns t in [cb[h], cb[h+1]), cb[0] = 0, cb[G] = rest.
 struct SlabCuts {

@@ -35,6 +35,25 @@ def test_kron_matvec(pq, ref, shape):
     assert relinf(got, ref.kron_matvec(fs, x)) < 1e-13
 
 
+@pytest.mark.parametrize("shape,scale", [((128, 128, 128), 1.0), ((31, 7, 12), -0.37), ((64, 48), 2.5), ((200,), 1.0)])
+def test_kron_matvec_tridiagonal_bitwise(pq, ref, shape, scale):
+    """Tridiagonal factors (every BASELINE operator) take the one-pass stencil kernel, which adds the
+    terms in the reference's order with separate multiply and add: bitwise the reference's
+    kron_matvec, scaled operators included (fl(s a_ij) as KroneckerSum::scaled)."""
+    rng = np.random.default_rng(len(shape) + int(10 * abs(scale)))
+    fs = []
+    for n in shape:
+        t = np.diag(rng.uniform(1.0, 3.0, n)) + np.diag(rng.uniform(-1.0, 0.0, n - 1), 1) + \
+            np.diag(rng.uniform(-1.0, 0.0, n - 1), -1)
+        t[rng.integers(0, n), :] *= 0.0  # a zero row: skipped terms
+        fs.append(t)
+    x = rng.standard_normal(int(np.prod(shape)))
+    a = pq.KroneckerSum(fs).scaled(scale) if scale != 1.0 else pq.KroneckerSum(fs)
+    want = ref.kron_matvec([scale * f for f in fs] if scale != 1.0 else fs, x)
+    got = pq.kron_matvec(a, x)
+    assert np.array_equal(np.asarray(got), want)
+
+
 @pytest.mark.parametrize("n,scale", [(1, 3.0), (2, 0.5), (5, 2.0), (17, 10.0), (64, 0.05), (128, 1.0), (129, 4.0)])
 def test_expm(pq, ref, n, scale):
     rng = np.random.default_rng(n)
