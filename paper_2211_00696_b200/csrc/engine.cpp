@@ -1272,9 +1272,12 @@ void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, 
     if (stencil_enabled() && factors_tridiagonal(c, op)) {
         // tridiagonal factors (the FD operators of every BASELINE config): one streaming pass,
         // the reference's term order (bitwise its kron_matvec)
+        int nmax = 1;
+        for (int k = 0; k < op.d; ++k) nmax = std::max(nmax, op.n[k]);
+        double* diag = ws(c, "kmv_diag", 9 * static_cast<size_t>(nmax));
         KernelProbe kp(c, "k_kron_tridiag", 16.0 * op.N);
-        launch_kron_tridiag(op.d, op.n, op.N, op.F, scale, x, y, c.stream);
-        count_launch(c);
+        launch_kron_tridiag(op.d, op.n, op.N, op.F, scale, x, y, diag, c.stream);
+        count_launch(c, 2);
         return;
     }
     const double* F[3] = {op.F[0], op.F[1], op.F[2]};

@@ -1178,43 +1178,70 @@ void launch_slab_blocks(bool pack, int rows, long long rest, const SlabCuts& cut
 // accumulate_mode_apply (kron.hpp:65-87) does: modes in order, within a mode the columns j
 // ascending, zero entries skipped, separate multiply and add; scaled factors are rounded once
 // (fl(scale a_ij), KroneckerSum::scaled).
-__global__ void k_kron_tridiag(int d, int n0, int n1, int n2, long long N, const double* __restrict__ F0,
-                               const double* __restrict__ F1, const double* __restrict__ F2, double scale, int scaled,
-                               const double* __restrict__ x, double* __restrict__ y) {
-    const int nk[3] = {n0, n1, n2};
-    const double* Fk[3] = {F0, F1, F2};
-    const long long st[3] = {(long long)n1 * n2, (long long)n2, 1};
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
-        const int i2 = (int)(t % n2);
-        const long long r = t / n2;
-        const int i1 = (int)(r % n1);
-        const int i0 = (int)(r / n1);
-        const int ik[3] = {i0, i1, i2};
-        double acc = 0.0;
+// diag[k][0..2][i] = fl(scale A_k[i][i-1]), fl(scale A_k[i][i]), fl(scale A_k[i][i+1]) (0 outside)
+__global__ void k_tridiag_diags(int d, int nmax, int n0, int n1, int n2, const double* __restrict__ F0,
+                                const double* __restrict__ F1, const double* __restrict__ F2, double scale, int scaled,
+                                double* __restrict__ diag) {
+    const int k = blockIdx.y;
+    if (k >= d) return;
+    const int n = k == 0 ? n0 : (k == 1 ? n1 : n2);
+    const double* F = k == 0 ? F0 : (k == 1 ? F1 : F2);
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
 #pragma unroll
-        for (int k = 0; k < 3; ++k) {
-            if (k >= d) break;
-            const int i = ik[k], n = nk[k];
-            const double* row = Fk[k] + (long long)i * n;
-#pragma unroll
-            for (int o = -1; o <= 1; ++o) {
-                const int j = i + o;
-                if (j < 0 || j >= n) continue;
-                double m = row[j];
-                if (scaled) m = __dmul_rn(scale, m);
-                if (m == 0.0) continue;
-                acc = __dadd_rn(acc, __dmul_rn(m, x[t + o * st[k]]));
-            }
+        for (int o = -1; o <= 1; ++o) {
+            const int j = i + o;
+            double m = (j >= 0 && j < n) ? F[(long long)i * n + j] : 0.0;
+            if (scaled) m = __dmul_rn(scale, m);
+            diag[((long long)k * 3 + (o + 1)) * nmax + i] = m;
         }
-        y[t] = acc;
-    }
 }
+
+// one CTA row per (i0, a 256-wide chunk of the (i1, i2) plane); consecutive threads walk i2, so
+// every x / diagonal load of a warp is coalesced
+__global__ void __launch_bounds__(256) k_kron_tridiag(int d, int nmax, int n1, int n2, const double* __restrict__ diag,
+                                                      const double* __restrict__ x, double* __restrict__ y, int n0) {
+    const int plane = n1 * n2;
+    const int pidx = blockIdx.x * blockDim.x + threadIdx.x;
+    if (pidx >= plane) return;
+    const int i0 = blockIdx.y;
+    const int i1 = pidx / n2, i2 = pidx - i1 * n2;
+    const long long t = (long long)i0 * plane + pidx;
+    const int ik[3] = {i0, i1, i2};
+    const int nk[3] = {n0, n1, n2};
+    const long long st[3] = {plane, n2, 1};
+    double acc = 0.0;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+        if (k >= d) break;
+        const int i = ik[k];
+#pragma unroll
+        for (int o = -1; o <= 1; ++o) {
+            const int j = i + o;
+            if (j < 0 || j >= nk[k]) continue;
+            const double m = __ldg(&diag[((long long)k * 3 + (o + 1)) * nmax + i]);
+            if (m == 0.0) continue;
+            acc = __dadd_rn(acc, __dmul_rn(m, x[t + o * st[k]]));
+        }
+    }
+    y[t] = acc;
+}
+
 void launch_kron_tridiag(int d, const int* n, long long N, const double* const* F, double scale, const double* x,
-                         double* y, cudaStream_t s) {
-    const int n0 = n[0], n1 = d > 1 ? n[1] : 1, n2 = d > 2 ? n[2] : 1;
-    // the index split assumes d = 3 layout; pad lower ranks with unit trailing dims
-    k_kron_tridiag<<<grid_for(N, 256), 256, 0, s>>>(d, n0, n1, n2, N, F[0], d > 1 ? F[1] : F[0], d > 2 ? F[2] : F[0],
-                                                    scale, scale != 1.0 ? 1 : 0, x, y);
+                         double* y, double* diag_scratch, cudaStream_t s) {
+    (void)N;
+    // ranks below 3 become leading unit dims: (n0, n1, n2) = (1, .., n[0..d)) keeps the plane layout
+    int sh[3] = {1, 1, 1};
+    for (int k = 0; k < d; ++k) sh[3 - d + k] = n[k];
+    const double* Fs[3] = {F[0], F[0], F[0]};
+    for (int k = 0; k < d; ++k) Fs[3 - d + k] = F[k];
+    const int nmax = std::max(sh[0], std::max(sh[1], sh[2]));
+    // unit leading dims carry a 1x1 "factor" that must contribute nothing: only modes 3-d.. are real
+    k_tridiag_diags<<<dim3((nmax + 127) / 128, 3), 128, 0, s>>>(3, nmax, sh[0], sh[1], sh[2], Fs[0], Fs[1], Fs[2], scale,
+                                                                scale != 1.0 ? 1 : 0, diag_scratch);
+    for (int k = 0; k < 3 - d; ++k)
+        cudaMemsetAsync(diag_scratch + (long long)k * 3 * nmax, 0, sizeof(double) * 3 * nmax, s);
+    const int plane = sh[1] * sh[2];
+    k_kron_tridiag<<<dim3((plane + 255) / 256, sh[0]), 256, 0, s>>>(3, nmax, sh[1], sh[2], diag_scratch, x, y, sh[0]);
 }
 
 }  // namespace pqb

@@ -118,8 +118,9 @@ void launch_sub(long long N, const double* x, const double* au, double* y, cudaS
 
 // kron_matvec with every factor tridiagonal (a 3-point stencil per mode, the reference's term order):
 // y = sum_k (I (x) .. fl(scale A_k) .. (x) I) x, F[k] row-major n[k] x n[k]
+// diag_scratch: 9 * max(n) doubles (the scaled diagonals, recomputed per call)
 void launch_kron_tridiag(int d, const int* n, long long N, const double* const* F, double scale, const double* x,
-                         double* y, cudaStream_t s);
+                         double* y, double* diag_scratch, cudaStream_t s);
 
 // ---- distributed squaring layout flips (dist.cpp) ----
 // Trailing-index cuts of a slab: rank h's pencil owns t in [cb[h], cb[h+1]), cb[0] = 0, cb[G] = rest.
