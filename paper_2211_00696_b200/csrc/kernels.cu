@@ -1093,25 +1093,73 @@ void launch_colstats(long long N, int ncols, const double* y, const double* yp, 
     k_colstats<<<dim3((unsigned)bx, (unsigned)ncols), 256, 0, s>>>(N, y, yp, out);
 }
 
+// ETD elementwise terms.  Each thread handles element pairs with 16-byte loads/stores when the
+// vectors are 16-byte aligned and N is even (the BASELINE sizes), else single elements; grids of
+// 148 x 8 CTAs with grid-stride loops (two memory transactions in flight per thread).
+template <class Op>
+__device__ __forceinline__ void elementwise2(long long N, Op op) {
+    const long long N2 = N / 2;
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N2; t += (long long)gridDim.x * blockDim.x)
+        op(2 * t, true);
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (N & 1)) op(N - 1, false);
+}
+static bool al16v(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+static unsigned grid_elem(long long N) {
+    long long b = (N / 2 + 255) / 256;
+    if (b > 148LL * 8) b = 148LL * 8;
+    return (unsigned)(b < 1 ? 1 : b);
+}
+
+__device__ __forceinline__ double cubic_minus1(double s1, double s3, double x, double a) {
+    const double f = __dadd_rn(__dmul_rn(s1, x), __dmul_rn(s3, __dmul_rn(__dmul_rn(x, x), x)));
+    return __dsub_rn(f, a);
+}
+
 __global__ void k_cubic_minus(long long N, double s1, double s3, const double* __restrict__ u,
                               const double* __restrict__ au, double* __restrict__ out) {
-    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x) {
-        const double x = u[t];
-        const double f = __dadd_rn(__dmul_rn(s1, x), __dmul_rn(s3, __dmul_rn(__dmul_rn(x, x), x)));
-        out[t] = __dsub_rn(f, au[t]);
-    }
+    elementwise2(N, [&](long long t, bool pair) {
+        if (pair) {
+            const double2 x = *reinterpret_cast<const double2*>(u + t);
+            const double2 a = *reinterpret_cast<const double2*>(au + t);
+            *reinterpret_cast<double2*>(out + t) = make_double2(cubic_minus1(s1, s3, x.x, a.x), cubic_minus1(s1, s3, x.y, a.y));
+        } else {
+            out[t] = cubic_minus1(s1, s3, u[t], au[t]);
+        }
+    });
+}
+__global__ void k_cubic_minus1(long long N, double s1, double s3, const double* __restrict__ u,
+                               const double* __restrict__ au, double* __restrict__ out) {
+    for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x)
+        out[t] = cubic_minus1(s1, s3, u[t], au[t]);
 }
 void launch_cubic_minus(long long N, double s1, double s3, const double* u, const double* au, double* out,
                         cudaStream_t s) {
-    k_cubic_minus<<<grid_for(N, 256), 256, 0, s>>>(N, s1, s3, u, au, out);
+    if (al16v(u) && al16v(au) && al16v(out))
+        k_cubic_minus<<<grid_elem(N), 256, 0, s>>>(N, s1, s3, u, au, out);
+    else
+        k_cubic_minus1<<<grid_for(N, 256), 256, 0, s>>>(N, s1, s3, u, au, out);
 }
 
 __global__ void k_axpy(long long N, double c, const double* __restrict__ x, double* __restrict__ y) {
+    elementwise2(N, [&](long long t, bool pair) {
+        if (pair) {
+            const double2 a = *reinterpret_cast<const double2*>(x + t);
+            const double2 b = *reinterpret_cast<const double2*>(y + t);
+            *reinterpret_cast<double2*>(y + t) = make_double2(__dadd_rn(b.x, __dmul_rn(c, a.x)), __dadd_rn(b.y, __dmul_rn(c, a.y)));
+        } else {
+            y[t] = __dadd_rn(y[t], __dmul_rn(c, x[t]));
+        }
+    });
+}
+__global__ void k_axpy1(long long N, double c, const double* __restrict__ x, double* __restrict__ y) {
     for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N; t += (long long)gridDim.x * blockDim.x)
         y[t] = __dadd_rn(y[t], __dmul_rn(c, x[t]));
 }
 void launch_axpy(long long N, double c, const double* x, double* y, cudaStream_t s) {
-    k_axpy<<<grid_for(N, 256), 256, 0, s>>>(N, c, x, y);
+    if (al16v(x) && al16v(y))
+        k_axpy<<<grid_elem(N), 256, 0, s>>>(N, c, x, y);
+    else
+        k_axpy1<<<grid_for(N, 256), 256, 0, s>>>(N, c, x, y);
 }
 
 __global__ void k_sub(long long N, const double* __restrict__ x, const double* __restrict__ au, double* __restrict__ y) {
