@@ -231,7 +231,7 @@ PQ_API int pq_squaring_combine(pq_ctx* ctx, long long n, int p, int nb, double* 
  * bitwise independent of the rank count), the adaptive-CC error as one exact all-reduce(max) of
  * 2 nb p scalars per level, and the modified squaring + phi_0 on slabs (modes 1..d-1 in the slab,
  * slab <-> pencil all-to-alls around mode 0).  Every rank passes the SAME inputs (factors, b, request). */
-enum { PQ_COMM_NCCL = 0, PQ_COMM_HOST = 1 };
+enum { PQ_COMM_NCCL = 0, PQ_COMM_HOST = 1, PQ_COMM_PEER = 2 };
 typedef struct pq_comm pq_comm;
 /* Host transport: collectives on pinned HOST buffers, e.g. torch.distributed over gloo, so several
  * processes can share one GPU in tests (no kernel ever waits on another process).  alltoallv sends
@@ -249,6 +249,14 @@ typedef struct {
 PQ_API int pq_nccl_unique_id(char* out128);
 PQ_API int pq_comm_create_nccl(pq_ctx* ctx, int world, int rank, const char* id128, pq_comm** out);
 PQ_API int pq_comm_create_host(int world, int rank, const pq_host_transport* transport, pq_comm** out);
+/* Peer transport: the squaring's slab <-> pencil flips are fused into the mode products -- their
+ * epilogues store each output row straight into the owning rank's buffer through CUDA IPC mappings
+ * (NVLink between the GPUs of a node; processes sharing one GPU in the tests), no pack / unpack
+ * kernels and no staging.  The host transport carries the IPC-handle exchange and the per-flip
+ * barrier (each rank drains its stream, then the allreduce acts as the barrier) and the remaining
+ * exchanges.  Applies to 3-D operators whose second extent the world size divides; other shapes
+ * fall back to the host transport's packed exchanges. */
+PQ_API int pq_comm_create_peer(pq_ctx* ctx, int world, int rank, const pq_host_transport* transport, pq_comm** out);
 PQ_API int pq_comm_destroy(pq_comm* comm);
 /* Bytes this rank sent to other ranks and exchanges issued since the last reset. */
 PQ_API int pq_comm_stats(pq_comm* comm, int reset, double* bytes_sent, uint64_t* exchanges);

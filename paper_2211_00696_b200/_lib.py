@@ -118,6 +118,7 @@ SIGNATURES = {
     "pq_nccl_unique_id": (C.c_int, [C.c_char_p]),
     "pq_comm_create_nccl": (C.c_int, [vp, C.c_int, C.c_int, C.c_char_p, C.POINTER(vp)]),
     "pq_comm_create_host": (C.c_int, [C.c_int, C.c_int, C.POINTER(HostTransportC), C.POINTER(vp)]),
+    "pq_comm_create_peer": (C.c_int, [vp, C.c_int, C.c_int, C.POINTER(HostTransportC), C.POINTER(vp)]),
     "pq_comm_destroy": (C.c_int, [vp]),
     "pq_comm_stats": (C.c_int, [vp, C.c_int, dp, C.POINTER(C.c_uint64)]),
     "pq_dist_slab": (C.c_int, [C.c_int, ip, C.c_int, C.c_int, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),

@@ -34,6 +34,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -54,6 +55,13 @@ struct pq_comm {
     size_t hr_cap = 0;
     double bytes_sent = 0.0;  // doubles * 8 sent to other ranks
     uint64_t exchanges = 0;
+    // peer transport: symmetric buffers (cudaMalloc + CUDA IPC), every rank's copy mapped here
+    struct PeerBuf {
+        double* local = nullptr;
+        size_t bytes = 0;
+        std::vector<double*> peer;  // [rank] -> mapped pointer (peer[rank] = local)
+    };
+    std::map<std::string, PeerBuf> pbufs;
 };
 
 namespace {
@@ -308,6 +316,124 @@ void dist_kron(pq_ctx& c, pq_comm& m, const Geom& g, const double* const* E, con
     KernelProbe kp(c, "k_slab_blocks(unpack)", 16.0 * static_cast<double>(tot));
     launch_slab_blocks(false, sg, g.rest, cuts, Bk, y, c.stream);
     count_launch(c);
+}
+
+// ------------------------------------------------------------------ peer transport -------
+// Symmetric buffers mapped into every rank (CUDA IPC: NVLink loads/stores between the GPUs of a
+// node; in the tests, processes sharing one GPU) and mode products whose epilogue stores each
+// output row straight into the rank that owns it (kernels.hpp RemoteMap): the slab <-> pencil
+// flips need no pack / unpack kernel and no staging -- the transfer is the GEMM's own store
+// stream.  Ranks synchronise at each flip with a stream drain and a host barrier (the host
+// transport's allreduce), so no kernel ever waits on another rank's kernel.
+
+void peer_barrier(pq_ctx& c, pq_comm& m) {
+    NvtxRange nvtx("pq_peer_barrier");
+    cuda_check(cudaStreamSynchronize(c.stream), "peer barrier sync");
+    if (m.world == 1) return;
+    double token = 0.0;
+    if (m.host.allreduce_max(m.host.user, &token, 1) != 0) throw CudaError("peer transport: barrier failed");
+}
+
+// collective: every rank calls it with the same name and byte count at the same point
+pq_comm::PeerBuf& peer_buffer(pq_ctx& c, pq_comm& m, const std::string& name, size_t bytes) {
+    pq_comm::PeerBuf& b = m.pbufs[name];
+    if (b.bytes >= bytes && b.local) return b;
+    peer_barrier(c, m);  // nobody writes into the old buffers any more
+    for (int h = 0; h < m.world; ++h)
+        if (h != m.rank && h < static_cast<int>(b.peer.size()) && b.peer[static_cast<size_t>(h)])
+            cudaIpcCloseMemHandle(b.peer[static_cast<size_t>(h)]);
+    if (b.local) cudaFree(b.local);
+    b = pq_comm::PeerBuf{};
+    cuda_check(cudaMalloc(&b.local, std::max<size_t>(bytes, 256)), "cudaMalloc(peer buffer)");
+    b.bytes = std::max<size_t>(bytes, 256);
+    b.peer.assign(static_cast<size_t>(m.world), nullptr);
+    b.peer[static_cast<size_t>(m.rank)] = b.local;
+    if (m.world > 1) {
+        static_assert(sizeof(cudaIpcMemHandle_t) == 64, "IPC handle size");
+        cudaIpcMemHandle_t mine;
+        cuda_check(cudaIpcGetMemHandle(&mine, b.local), "cudaIpcGetMemHandle");
+        // all-gather of the 64-byte handles through the host transport (8 doubles each)
+        std::vector<double> send(static_cast<size_t>(m.world - 1) * 8), recv(static_cast<size_t>(m.world - 1) * 8);
+        std::vector<int64_t> sc(static_cast<size_t>(m.world), 8), rc(static_cast<size_t>(m.world), 8);
+        sc[static_cast<size_t>(m.rank)] = rc[static_cast<size_t>(m.rank)] = 0;
+        for (int k = 0; k < m.world - 1; ++k) std::memcpy(send.data() + 8 * k, &mine, 64);
+        if (m.host.alltoallv(m.host.user, send.data(), sc.data(), recv.data(), rc.data()) != 0)
+            throw CudaError("peer transport: handle exchange failed");
+        int k = 0;
+        for (int h = 0; h < m.world; ++h) {
+            if (h == m.rank) continue;
+            cudaIpcMemHandle_t theirs;
+            std::memcpy(&theirs, recv.data() + 8 * k++, 64);
+            void* ptr = nullptr;
+            cuda_check(cudaIpcOpenMemHandle(&ptr, theirs, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+            b.peer[static_cast<size_t>(h)] = static_cast<double*>(ptr);
+        }
+    }
+    return b;
+}
+
+// the fused flips apply when every pencil owns whole n2-rows of the trailing plane (G | n1) and
+// all row offsets keep 16-byte alignment
+bool peer_fused_ok(const Geom& g) {
+    if (g.d != 3 || g.n[1] % g.G != 0 || g.n[2] % 2 != 0 || g.rest % 2 != 0) return false;
+    for (int h = 0; h <= g.G; ++h)
+        if (g.cuts.cb[h] % g.n[2] != 0) return false;
+    return true;
+}
+
+// dist_kron with the flips fused into the mode products: modes 1 (local) -> mode 2 storing into
+// every rank's pencil buffer -> barrier -> mode 0 on the pencil storing into every rank's slab of
+// `ydst` -> barrier.  The result is ydst.local [col][S_r].
+void dist_kron_peer(pq_ctx& c, pq_comm& m, const Geom& g, const double* const* E, const int2* const* B,
+                    const double* x, long long x_stride, int ncols, pq_comm::PeerBuf& ydst) {
+    const int r = g.r, sg = g.sg(r);
+    const long long S = g.S(r);
+    long long cmax = 0;
+    for (int h = 0; h < g.G; ++h) cmax = std::max(cmax, g.C(h));
+    pq_comm::PeerBuf& pen = peer_buffer(c, m, "ppencil", sizeof(double) * ncols * g.n[0] * std::max<long long>(cmax, 1));
+    RemoteMap rm1, rm2;
+    rm1.mode = 1;
+    rm2.mode = 2;
+    for (RemoteMap* rm : {&rm1, &rm2}) {
+        rm->G = g.G;
+        rm->me = r;
+        rm->n0 = g.n[0];
+        rm->n1 = g.n[1];
+        rm->n2 = g.n[2];
+        rm->rest = g.rest;
+        for (int h = 0; h <= g.G; ++h) {
+            rm->s[h] = g.s[static_cast<size_t>(h)];
+            rm->cb[h] = g.cuts.cb[h];
+        }
+    }
+    for (int h = 0; h < g.G; ++h) {
+        rm1.base[h] = pen.peer[static_cast<size_t>(h)];
+        rm2.base[h] = ydst.peer[static_cast<size_t>(h)];
+    }
+    const RemoteMap* rm1_dev = static_cast<const RemoteMap*>(arena_push(c, &rm1, sizeof rm1));
+    const RemoteMap* rm2_dev = static_cast<const RemoteMap*>(arena_push(c, &rm2, sizeof rm2));
+    arena_flush(c);
+    const size_t tot = static_cast<size_t>(ncols) * std::max<long long>(S, 1);
+    double* U = ws(c, "dk_U", tot);
+    const int sh[3] = {sg, g.n[1], g.n[2]};
+    mode_product_dev(c, 3, sh, 1, E[1], B ? B[1] : nullptr, x, x_stride, U, S, ncols);
+    // mode 2: each output row (r, i1) is an n2-row of the pencil of the rank owning i1*n2
+    mode_product_dev(c, 3, sh, 2, E[2], B ? B[2] : nullptr, U, S, U, S, ncols, rm1_dev);
+    for (int h = 0; h < g.G; ++h)
+        if (h != r) m.bytes_sent += 8.0 * ncols * sg * static_cast<double>(g.C(h));
+    ++m.exchanges;
+    peer_barrier(c, m);
+    const long long Cr = g.C(r);
+    if (Cr > 0) {
+        const int shp[2] = {g.n[0], static_cast<int>(Cr)};
+        // mode 0: output row i0 goes to the rank owning x-slab row i0, at its pencil columns
+        mode_product_dev(c, 2, shp, 0, E[0], B ? B[0] : nullptr, pen.local, g.n[0] * Cr, pen.local, g.n[0] * Cr, ncols,
+                         rm2_dev);
+        for (int h = 0; h < g.G; ++h)
+            if (h != r) m.bytes_sent += 8.0 * ncols * g.sg(h) * static_cast<double>(Cr);
+    }
+    ++m.exchanges;
+    peer_barrier(c, m);
 }
 
 // node vectors of the owned nodes (full length, pool [a][m][N]) -> every node's slab on its
@@ -598,9 +724,20 @@ void phi_dist(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, con
     const PhiExps px = phi_exponentials(c, op, 1.0, l, th, l > 0, phi0 != nullptr, "dnodeE", true, false);
     mark(c, "exps");
     const size_t col = static_cast<size_t>(nb) * p * std::max<long long>(S, 1);
-    double* y = out;
-    double* t = l > 0 ? ws(c, "dsqT", col) : nullptr;
-    double* first = (l % 2 == 1) ? t : out;
+    // the peer transport fuses the squaring's flips into the mode products: the ping-pong columns
+    // and phi_0 then live in symmetric (IPC-mapped) buffers, sized for the largest slab
+    const bool fused = m.kind == PQ_COMM_PEER && peer_fused_ok(g);
+    long long smax = 0;
+    for (int h = 0; h < g.G; ++h) smax = std::max(smax, g.S(h));
+    pq_comm::PeerBuf* pa = nullptr;
+    pq_comm::PeerBuf* pb = nullptr;
+    if (fused) {
+        pa = &peer_buffer(c, m, "psqA", sizeof(double) * nb * p * std::max<long long>(smax, 1));
+        pb = &peer_buffer(c, m, "psqB", sizeof(double) * nb * p * std::max<long long>(smax, 1));
+    }
+    double* t = l > 0 ? (fused ? pb->local : ws(c, "dsqT", col)) : nullptr;
+    double* base_out = fused ? pa->local : out;
+    double* first = (l % 2 == 1) ? t : base_out;
     if (kind == kGauss) {
         gauss_nodes(c, m, g, op, nb, bs, p, rule, px, own, first);
         if (points_used) *points_used = rule.size();
@@ -610,10 +747,18 @@ void phi_dist(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, con
     mark(c, "nodes");
     // phi_0: one distributed Kronecker apply of expm(A) to the slabs of b (b is replicated)
     if (phi0) {
-        dist_kron(c, m, g, px.phi0, px.phi0_band, bs + g.lo(g.r), op.N, nb, phi0);
+        if (fused) {
+            pq_comm::PeerBuf& p0 = peer_buffer(c, m, "pphi0", sizeof(double) * nb * std::max<long long>(smax, 1));
+            dist_kron_peer(c, m, g, px.phi0, px.phi0_band, bs + g.lo(g.r), op.N, nb, p0);
+            cuda_check(cudaMemcpyAsync(phi0, p0.local, sizeof(double) * nb * S, cudaMemcpyDeviceToDevice, c.stream),
+                       "phi_0 slab");
+        } else {
+            dist_kron(c, m, g, px.phi0, px.phi0_band, bs + g.lo(g.r), op.N, nb, phi0);
+        }
     }
     // l modified-squaring steps on the slabs (phiaction.hpp:255-272): T = (E (x) E (x) E) y,
     // T_i <- 2^-i (T_i + sum_{j<=i} y_j/(i-j)!); E_j = expm(2^(j-l) A) from the chain
+    double* res = first;
     if (l > 0) {
         std::vector<double> inv(static_cast<size_t>(p), 1.0);
         for (int k = 1; k < p; ++k) inv[static_cast<size_t>(k)] = inv[static_cast<size_t>(k) - 1] / k;
@@ -624,7 +769,7 @@ void phi_dist(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, con
         const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
         arena_flush(c);
         double* cur = first;
-        double* nxt = first == out ? t : out;
+        double* nxt = first == base_out ? t : base_out;
         for (int step = 0; step < l; ++step) {
             const double* E[3];
             const int2* B[3];
@@ -633,7 +778,10 @@ void phi_dist(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, con
                 E[k] = px.sq[k] + step * nk;
                 B[k] = px.sq_band[k] ? px.sq_band[k] + step * band_row_blocks(op.n[k]) : nullptr;
             }
-            dist_kron(c, m, g, E, B, cur, S, nb * p, nxt);
+            if (fused)
+                dist_kron_peer(c, m, g, E, B, cur, S, nb * p, nxt == pa->local ? *pa : *pb);
+            else
+                dist_kron(c, m, g, E, B, cur, S, nb * p, nxt);
             if (S > 0) {
                 KernelProbe kp(c, "k_sq_combine2", 8.0 * S * nb * 3 * p);
                 launch_sq_combine(S, p, nb, nxt, cur, coef_dev, c.stream);
@@ -641,9 +789,10 @@ void phi_dist(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, con
             }
             std::swap(cur, nxt);
         }
-        y = cur;
-        (void)y;
+        res = cur;
     }
+    if (res != out)
+        cuda_check(cudaMemcpyAsync(out, res, sizeof(double) * col, cudaMemcpyDeviceToDevice, c.stream), "slab result");
     mark(c, "squaring");
 }
 
@@ -785,9 +934,30 @@ int pq_comm_create_host(int world, int rank, const pq_host_transport* t, pq_comm
     });
 }
 
+int pq_comm_create_peer(pq_ctx* ctx, int world, int rank, const pq_host_transport* t, pq_comm** out) {
+    return guarded([&] {
+        need(ctx && out, "pq_comm_create_peer: null argument");
+        need(world >= 1 && world <= 16 && rank >= 0 && rank < world, "pq_comm_create_peer: bad world/rank");
+        need(world == 1 || (t && t->alltoallv && t->allreduce_max), "pq_comm_create_peer: transport callbacks missing");
+        cuda_check(cudaSetDevice(ctx->device), "cudaSetDevice");
+        auto* m = new pq_comm();
+        m->world = world;
+        m->rank = rank;
+        m->kind = PQ_COMM_PEER;
+        if (t) m->host = *t;
+        *out = m;
+    });
+}
+
 int pq_comm_destroy(pq_comm* m) {
     return guarded([&] {
         if (!m) return;
+        for (auto& kv : m->pbufs) {
+            for (int h = 0; h < m->world; ++h)
+                if (h != m->rank && h < static_cast<int>(kv.second.peer.size()) && kv.second.peer[static_cast<size_t>(h)])
+                    cudaIpcCloseMemHandle(kv.second.peer[static_cast<size_t>(h)]);
+            if (kv.second.local) cudaFree(kv.second.local);
+        }
         if (m->nccl) nccl_api().commDestroy(m->nccl);
         if (m->hs) cudaFreeHost(m->hs);
         if (m->hr) cudaFreeHost(m->hr);

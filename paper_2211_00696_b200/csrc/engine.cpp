@@ -1157,10 +1157,11 @@ GemmArgs mode_gemm_public(int d, const int* n, int mode, const double* E, const 
 }
 
 void mode_product_dev(pq_ctx& c, int d, const int* n, int k, const double* E, const int2* band, const double* x,
-                      long long x_stride, double* y, long long y_stride, int Z1) {
+                      long long x_stride, double* y, long long y_stride, int Z1, const RemoteMap* remote) {
     long long N = 1;
     for (int i = 0; i < d; ++i) N *= n[i];
     GemmArgs g = mode_gemm(d, n, k, E, 0, x, x_stride, y, y_stride, Z1, N);
+    g.remote = remote;
     if (band) {  // one exponential shared by the batch (E_stride 0), as mode_chain sets it up
         g.band = band;
         g.band_rows = n[k];

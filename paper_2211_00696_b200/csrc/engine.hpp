@@ -374,8 +374,9 @@ void node_sweep(pq_ctx& c, const DevOp& op, const double* const* E, const long l
                 int slot0, const int2* const* band = nullptr);
 // one mode-k product of Z1 tensors of shape n[0..d) (x[z] at x + z*x_stride, y[z] likewise) with
 // ONE matrix E (band: its negligible-block table or null): y[z] = (I (x) .. E .. (x) I) x[z]
+// remote (device table, nullable): the outputs go to other ranks' buffers (dist.cpp peer transport)
 void mode_product_dev(pq_ctx& c, int d, const int* n, int k, const double* E, const int2* band, const double* x,
-                      long long x_stride, double* y, long long y_stride, int Z1);
+                      long long x_stride, double* y, long long y_stride, int Z1, const RemoteMap* remote = nullptr);
 void phi_lincomb_dev(pq_ctx& c, const DevOp& op, double scale, int p, const double* bs, const NodesWeights& rule,
                      double* out);
 

@@ -39,6 +39,21 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// destination row of the remote-store epilogue (kernels.hpp RemoteMap)
+__device__ __forceinline__ double* remote_row(const RemoteMap& rm, int z1, int m) {
+    if (rm.mode == 1) {
+        const int r = m / rm.n1, i1 = m - r * rm.n1;
+        const long long t0 = (long long)i1 * rm.n2;
+        int h = 0;
+        while (h + 1 < rm.G && t0 >= rm.cb[h + 1]) ++h;
+        const long long ch = rm.cb[h + 1] - rm.cb[h];
+        return rm.base[h] + ((long long)z1 * rm.n0 + rm.s[rm.me] + r) * ch + (t0 - rm.cb[h]);
+    }
+    int h = 0;
+    while (h + 1 < rm.G && m >= rm.s[h + 1]) ++h;
+    return rm.base[h] + ((long long)z1 * (rm.s[h + 1] - rm.s[h]) + (m - rm.s[h])) * rm.rest + rm.cb[rm.me];
+}
+
 template <int BM, int BN, int BK, int WM, int WN, int ST, bool BKM>
 struct TileCfg {
     static constexpr int NWM = BM / WM, NWN = BN / WN, NT = NWM * NWN * 32;
@@ -379,7 +394,7 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int bx, int by, int
     for (int i = 0; i < T::MI; ++i) {
         const int m = mb + i * 8;
         if (m >= g.M) continue;
-        double* row = C + (long long)m * g.ldc;
+        double* row = g.remote ? remote_row(*g.remote, z1, m) : C + (long long)m * g.ldc;
 #pragma unroll
         for (int j = 0; j < T::NI; ++j) {
             const int n = nbase + j * 8;

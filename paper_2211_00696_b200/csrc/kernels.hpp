@@ -13,6 +13,20 @@ namespace pqb {
 // as N x K rows ("k contiguous").  z = z1*zdiv + z2 indexes a two-level batch with independent
 // strides, which maps every mode product of the engine (node-batched, column-batched, shared
 // inputs with stride 0) onto one launch.
+// Remote-store epilogue of the multi-GPU peer transport (dist.cpp): output rows go straight to
+// other ranks' buffers (CUDA IPC mappings; NVLink stores between GPUs) instead of C.
+//   mode 1, slab -> pencil (the last slab mode, rows m = r*n1 + i1 of column z1): rank h = owner of the
+//     trailing index i1*n2; destination base[h] + (z1*n0 + s[me] + r)*(cb[h+1]-cb[h]) + i1*n2 - cb[h];
+//   mode 2, pencil -> slab (mode 0 on the pencil, rows i0 of column z1): rank h = owner of i0;
+//     destination base[h] + (z1*(s[h+1]-s[h]) + i0 - s[h])*rest + cb[me].
+struct RemoteMap {
+    int mode = 0, G = 1, me = 0, n0 = 1, n1 = 1, n2 = 1;
+    long long rest = 1;
+    int s[17] = {0};
+    long long cb[17] = {0};
+    double* base[16] = {nullptr};
+};
+
 struct GemmArgs {
     const double* A = nullptr;
     const double* B = nullptr;
@@ -46,6 +60,7 @@ struct GemmArgs {
     // profiling: every CTA adds the flops it actually executed (2 rows cols k) here
     unsigned long long* flop_counter = nullptr;
     const char* tag = nullptr;  // call site, for the profiling breakdown only
+    const RemoteMap* remote = nullptr;  // device table: remote-store epilogue (plain stores only)
 };
 int launch_gemm(const GemmArgs& g, cudaStream_t s);  // returns number of kernel launches
 // `count` dependent batched GEMM levels (plain products, row-major B, 16-byte aligned) in ONE

@@ -71,6 +71,18 @@ class Communicator:
     def host(cls, group=None) -> "Communicator":
         """Collectives through torch.distributed on host buffers (gloo): all_to_all_single for the
         exchanges, all_reduce(MAX) for the adaptive-CC statistics."""
+        return cls._with_host_transport(group, None)
+
+    @classmethod
+    def peer(cls, ctx: Context, group=None) -> "Communicator":
+        """Peer transport: the squaring's slab <-> pencil flips fused into the mode products, whose
+        epilogues store straight into the owning rank's CUDA-IPC-mapped buffer (NVLink between GPUs;
+        processes sharing one GPU in the tests); torch.distributed (gloo) carries the handle
+        exchange and the per-flip barrier."""
+        return cls._with_host_transport(group, ctx)
+
+    @classmethod
+    def _with_host_transport(cls, group, peer_ctx) -> "Communicator":
         import torch
         import torch.distributed as dist
         world, rank = dist.get_world_size(group), dist.get_rank(group)
@@ -100,7 +112,10 @@ class Communicator:
         cb_a2a, cb_max = L.ALLTOALLV_CB(a2a), L.ALLREDUCE_CB(amax)
         t = L.HostTransportC(None, cb_a2a, cb_max)
         h = C.c_void_p()
-        L.check(L.lib.pq_comm_create_host(world, rank, C.byref(t), C.byref(h)))
+        if peer_ctx is None:
+            L.check(L.lib.pq_comm_create_host(world, rank, C.byref(t), C.byref(h)))
+        else:
+            L.check(L.lib.pq_comm_create_peer(peer_ctx.handle, world, rank, C.byref(t), C.byref(h)))
         return cls(h, world, rank, keep=(cb_a2a, cb_max, t))
 
     @classmethod

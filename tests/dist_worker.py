@@ -48,7 +48,7 @@ def main():
     ap.add_argument("--case", required=True)
     ap.add_argument("--out", required=True)
     ap.add_argument("--device-inputs", action="store_true")
-    ap.add_argument("--transport", default="host", choices=["host", "nccl"])
+    ap.add_argument("--transport", default="host", choices=["host", "nccl", "peer"])
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -60,7 +60,8 @@ def main():
     w, bs, plan = case_inputs(args.case)
     a = pq.KroneckerSum(w.factors)
     ctx = pq.Context(0)
-    comm = S.Communicator.nccl(ctx) if args.transport == "nccl" else S.Communicator.host()
+    comm = (S.Communicator.nccl(ctx) if args.transport == "nccl" else
+            S.Communicator.peer(ctx) if args.transport == "peer" else S.Communicator.host())
     inp = torch.from_numpy(bs).cuda() if args.device_inputs else bs
     res = {}
     if plan == "plan":

@@ -161,6 +161,27 @@ def test_distributed_device_inputs_world2(ref, tmp_path):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("case,world", [("cfg3_gauss", 2), ("cfg2_cc", 3), ("cfg5_pinned", 2), ("cfg5_pinned", 3)])
+def test_distributed_peer_transport(ref, tmp_path, case, world):
+    """The peer transport: the squaring's and phi_0's slab <-> pencil flips fused into the mode
+    products (remote-store epilogues into CUDA-IPC-mapped buffers of the other processes on this
+    GPU; host barriers between the flips, so no kernel waits on another process).  cfg5_pinned at
+    world 3 (n1 = 40 not divisible by 3) exercises the fallback to packed exchanges."""
+    ranks = _launch(case, world, tmp_path, transport="peer")
+    w, want, want0, plan = _reference(ref, case)
+    nb, p, N = want.shape
+    for k, res in enumerate(ranks):
+        assert list(res["plan"]) == plan, (k, res["plan"], plan)
+        assert max(rel2(res["cols"][m, j], want[m, j]) for m in range(nb) for j in range(p)) <= 1e-11
+        if want0 is not None:
+            assert max(rel2(res["phi0"][m], want0[m]) for m in range(nb)) <= 1e-11
+        b, e = res["slab"]
+        assert np.array_equal(res["cols_slab"], res["cols"][:, :, b:e])
+    for res in ranks[1:]:
+        assert np.array_equal(res["cols"], ranks[0]["cols"])
+
+
+@pytest.mark.gpu
 def test_distributed_nccl_transport_world1(ref, tmp_path):
     """The NCCL transport end to end on the one GPU this environment has: libnccl.so.2 loaded by
     dlopen, the unique id broadcast through torch.distributed, ncclCommInitRank, the distributed
