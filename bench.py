@@ -413,7 +413,9 @@ def run_ours_phi(args, world, rank, local) -> None:
         from paper_2211_00696_b200 import sharded as S
         if world == 1:
             comm = S.Communicator.single()
-        elif _backend() == "gloo":
+        elif args.transport == "peer":
+            comm = S.Communicator.peer(ctx)  # flips fused into the mode products (CUDA IPC / NVLink stores)
+        elif _backend() == "gloo" or args.transport == "host":
             comm = S.Communicator.host()  # plumbing check: ranks share one GPU, collectives via the host
         else:
             comm = S.Communicator.nccl(ctx)
@@ -582,7 +584,8 @@ def run_ours_phi(args, world, rank, local) -> None:
                          "factors are uploaded once (bit-identical factors are not re-copied) and not counted")},
     }
     if nodes:
-        line["distributed"] = {"transport": "host (gloo)" if (world > 1 and _backend() == "gloo") else "nccl",
+        line["distributed"] = {"transport": ("peer (fused IPC stores)" if args.transport == "peer" else
+                                              "host (gloo)" if (world > 1 and _backend() == "gloo") else "nccl"),
                                "slab": [sb, se], "bytes_sent_per_step_rank0": comm_bytes,
                                "outputs": "x-slabs per rank (gather=0)"}
         comm.close()
@@ -702,6 +705,9 @@ def main() -> None:
                     help="N > 1: rhs = independent right-hand sides per rank (weak scaling; default for the CC "
                          "configs 2 and 4), nodes = one action across all ranks (csrc/dist.cpp, strong scaling; "
                          "default for the Gauss configs 1, 3, 5)")
+    ap.add_argument("--transport", default="nccl", choices=["nccl", "peer", "host"],
+                    help="--shard nodes: NCCL packed exchanges, peer (flips fused into the mode products "
+                         "through CUDA IPC), or the host transport")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-callers", type=int, default=4, help="concurrent host callers in the e2e leg")
     ap.add_argument("--etd-steps", type=int, default=100, help="config 4: ETDRK4 steps per bench step")

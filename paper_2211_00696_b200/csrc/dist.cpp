@@ -335,16 +335,23 @@ void peer_barrier(pq_ctx& c, pq_comm& m) {
 }
 
 // collective: every rank calls it with the same name and byte count at the same point
-pq_comm::PeerBuf& peer_buffer(pq_ctx& c, pq_comm& m, const std::string& name, size_t bytes) {
+// (keep: leading bytes of the old buffer carried into a grown one)
+pq_comm::PeerBuf& peer_buffer(pq_ctx& c, pq_comm& m, const std::string& name, size_t bytes, size_t keep = 0) {
     pq_comm::PeerBuf& b = m.pbufs[name];
     if (b.bytes >= bytes && b.local) return b;
     peer_barrier(c, m);  // nobody writes into the old buffers any more
     for (int h = 0; h < m.world; ++h)
         if (h != m.rank && h < static_cast<int>(b.peer.size()) && b.peer[static_cast<size_t>(h)])
             cudaIpcCloseMemHandle(b.peer[static_cast<size_t>(h)]);
-    if (b.local) cudaFree(b.local);
+    double* old = b.local;
+    const size_t old_bytes = b.bytes;
     b = pq_comm::PeerBuf{};
     cuda_check(cudaMalloc(&b.local, std::max<size_t>(bytes, 256)), "cudaMalloc(peer buffer)");
+    if (old) {
+        if (keep > 0)
+            cuda_check(cudaMemcpy(b.local, old, std::min(keep, old_bytes), cudaMemcpyDeviceToDevice), "peer buffer copy");
+        cudaFree(old);
+    }
     b.bytes = std::max<size_t>(bytes, 256);
     b.peer.assign(static_cast<size_t>(m.world), nullptr);
     b.peer[static_cast<size_t>(m.rank)] = b.local;
@@ -440,6 +447,26 @@ void dist_kron_peer(pq_ctx& c, pq_comm& m, const Geom& g, const double* const* E
 // owner (slab pool [slot][m][S_r]); `owner_of(slot)` and the local index of owned slots
 void node_transpose(pq_ctx& c, pq_comm& m, const Geom& g, int nb, const std::vector<int>& slots, const double* pool,
                     double* slab_pool) {
+    if (m.kind == PQ_COMM_PEER) {
+        // straight into every rank's IPC-mapped slab pool (peer copies over NVLink), one barrier
+        pq_comm::PeerBuf& sp = m.pbufs["pslabpool"];
+        int a = 0;
+        for (int slot : slots) {
+            if (slot % g.G != g.r) continue;
+            for (int mm = 0; mm < nb; ++mm)
+                for (int h = 0; h < g.G; ++h) {
+                    double* dst = sp.peer[static_cast<size_t>(h)] + (static_cast<long long>(slot) * nb + mm) * g.S(h);
+                    const double* src = pool + (static_cast<long long>(a) * nb + mm) * g.N + g.lo(h);
+                    cuda_check(cudaMemcpyAsync(dst, src, sizeof(double) * g.S(h), cudaMemcpyDeviceToDevice, c.stream),
+                               "node transpose (peer)");
+                    if (h != g.r) m.bytes_sent += 8.0 * g.S(h);
+                }
+            ++a;
+        }
+        ++m.exchanges;
+        peer_barrier(c, m);
+        return;
+    }
     std::vector<Piece> sends, recvs;
     int a = 0;
     for (int slot : slots) {
@@ -464,7 +491,13 @@ std::vector<int> owned(const std::vector<int>& slots, const Geom& g) {
     return o;
 }
 
-double* slab_pool_grow(pq_ctx& c, int slots, int nb, long long S, int used) {
+double* slab_pool_grow(pq_ctx& c, pq_comm& m, const Geom& g, int slots, int nb, long long S, int used) {
+    if (m.kind == PQ_COMM_PEER) {  // symmetric, sized for the largest slab
+        long long smax = 0;
+        for (int h = 0; h < g.G; ++h) smax = std::max(smax, g.S(h));
+        const size_t want = static_cast<size_t>(std::max(slots, 1)) * nb * std::max<long long>(smax, 1) * sizeof(double);
+        return peer_buffer(c, m, "pslabpool", want, static_cast<size_t>(used) * nb * S * sizeof(double)).local;
+    }
     DevBuf& b = c.bufs["dslabpool"];
     const size_t want = static_cast<size_t>(std::max(slots, 1)) * nb * std::max<long long>(S, 1) * sizeof(double);
     if (b.bytes < want) {
@@ -523,7 +556,8 @@ void gauss_nodes_rs(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int n
 void gauss_nodes(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, const double* bs, int p,
                  const NodesWeights& rule, const PhiExps& px, const std::vector<int>& own, double* acc) {
     const int q = rule.size();
-    if (gauss_use_reduce_scatter(q, g.G, p)) {
+    // (the peer transport moves node slabs with direct peer copies: no staging to save)
+    if (m.kind != PQ_COMM_PEER && gauss_use_reduce_scatter(q, g.G, p)) {
         gauss_nodes_rs(c, m, g, op, nb, bs, p, rule, px, own, acc);
         return;
     }
@@ -534,7 +568,7 @@ void gauss_nodes(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int nb, 
     node_sweep(c, op, px.node, Es, static_cast<int>(own.size()), nb, bs, p, nullptr, nullptr, 0, pool, 0, px.node_band);
     std::vector<int> all(static_cast<size_t>(q));
     std::iota(all.begin(), all.end(), 0);
-    double* slab = slab_pool_grow(c, q, nb, S, 0);
+    double* slab = slab_pool_grow(c, m, g, q, nb, S, 0);
     node_transpose(c, m, g, nb, all, pool, slab);
     std::vector<double> coef;
     node_coefs(rule, all, p, coef);
@@ -563,13 +597,13 @@ void cc_nodes(pq_ctx& c, pq_comm& m, const Geom& g, const DevOp& op, int l, int 
     const NodesWeights& r25 = memo_rule(kClenshaw, 25);
     // sweeps the owned slots among `slots` (exponentials E[k] + idx*nn[k], idx = position among the
     // owned ones) and moves every slot's slab to this rank's slab pool
-    double* slab = slab_pool_grow(c, 25, nb, S, 0);
+    double* slab = slab_pool_grow(c, m, g, 25, nb, S, 0);
     int used = 0;
     auto sweep = [&](const std::vector<int>& slots, const double* const* E, const int2* const* B) {
         const std::vector<int> mine = owned(slots, g);
         double* pool = ws(c, "dpool", std::max<size_t>(mine.size(), 1) * nb * op.N);
         if (!mine.empty()) node_sweep(c, op, E, Es, static_cast<int>(mine.size()), nb, bs, p, nullptr, nullptr, 0, pool, 0, B);
-        slab = slab_pool_grow(c, used + static_cast<int>(slots.size()), nb, S, used);
+        slab = slab_pool_grow(c, m, g, used + static_cast<int>(slots.size()), nb, S, used);
         node_transpose(c, m, g, nb, slots, pool, slab);
         used += static_cast<int>(slots.size());
     };

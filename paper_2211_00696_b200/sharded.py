@@ -85,6 +85,8 @@ class Communicator:
     def _with_host_transport(cls, group, peer_ctx) -> "Communicator":
         import torch
         import torch.distributed as dist
+        if group is None and dist.get_backend() != "gloo":
+            group = dist.new_group(backend="gloo")  # the host transport moves CPU tensors
         world, rank = dist.get_world_size(group), dist.get_rank(group)
 
         def view(ptr, n):

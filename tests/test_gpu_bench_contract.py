@@ -35,7 +35,7 @@ def test_bench_line_contract():
     assert d["gpu_launches"] > 0
 
 
-@pytest.mark.parametrize("shard", ["rhs", "nodes"])
+@pytest.mark.parametrize("shard", ["rhs", "nodes", "nodes-peer"])
 def test_bench_two_ranks_plumbing(shard):
     """The N > 1 launch the driver uses (torch.distributed.run, one process per rank), with gloo
     carrying the barrier / max-over-ranks so both ranks can share the one GPU of this box.  rhs: the
@@ -43,11 +43,12 @@ def test_bench_two_ranks_plumbing(shard):
     through the distributed engine path with the host transport (strong scaling)."""
     import os
     env = dict(os.environ, PQ_BENCH_BACKEND="gloo")
-    port = 29517 if shard == "rhs" else 29519
+    port = {"rhs": 29517, "nodes": 29519, "nodes-peer": 29521}[shard]
+    extra = ["--transport", "peer", "--config", "2"] if shard == "nodes-peer" else ["--config", "1"]
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"),
-                        "--gpus", "2", "--steps", "2", "--warmup", "3", "--config", "1", "--e2e-callers", "1",
-                        "--shard", shard],
+                        "--gpus", "2", "--steps", "2", "--warmup", "3", "--e2e-callers", "1",
+                        "--shard", shard.split("-")[0]] + extra,
                        capture_output=True, text=True, timeout=900, cwd=str(ROOT), env=env)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.splitlines() if ln.strip().startswith("{")]
@@ -55,7 +56,7 @@ def test_bench_two_ranks_plumbing(shard):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0
     assert d["scaling"] == ("weak" if shard == "rhs" else "strong")
-    assert f"{shard}-sharded x2" in d["config"]["parallelism"]
+    assert f"{shard.split('-')[0]}-sharded x2" in d["config"]["parallelism"]
     assert d["e2e"]["value"] > 0
-    if shard == "nodes":
+    if shard != "rhs":
         assert d["distributed"]["bytes_sent_per_step_rank0"] > 0
