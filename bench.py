@@ -44,9 +44,10 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-# Measured on this pool's B200s by tools/fp64_peak.cu (profiles/fp64_peak_r01.jsonl): mma.sync
-# m8n8k4 f64 (SASS DMMA.8x8x4) register-only loop; MEASURED_PEAKS.json has no FP64 entry.
-DMMA_PEAK_TFLOPS = 36.95
+# Measured on this pool's B200s by tools/fp64_peak.cu (profiles/fp64_peak_r02.jsonl, best of 3 runs
+# x 9 launch shapes; r01: 36.95): mma.sync m8n8k4 f64 (SASS DMMA.8x8x4) register-only loop at
+# 1965 MHz = 148 SMs x 4 SMSPs x 32 flop/clk; MEASURED_PEAKS.json has no FP64 entry.
+DMMA_PEAK_TFLOPS = 37.15
 FP64_COPY_GBS = 6288.3
 METRIC = "phi_0..p(tau A)v actions/sec at N=n^d DOF"
 
@@ -345,7 +346,7 @@ def roofline_line(ctx, steps: int, ms_step_dev: float, w, kstats=None) -> dict:
           "dense_equiv_note": "2*M*N*K of the same launches (the reference's dense mode products) / the same time",
           "launches_per_step": g_launches / steps, "gemm_ms_per_step": g_ms / steps,
           "gemm_share_of_step": (g_ms / steps) / ms_step_dev if ms_step_dev > 0 else None,
-          "peak_source": "measured DMMA loop, profiles/fp64_peak_r01.jsonl (MEASURED_PEAKS.json has no FP64 entry)"}
+          "peak_source": "measured DMMA loop, profiles/fp64_peak_r02.jsonl (MEASURED_PEAKS.json has no FP64 entry)"}
     if kstats:
         hbm = load_peaks().get("hbm_gbs") or FP64_COPY_GBS
         rows = {}

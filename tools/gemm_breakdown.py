@@ -13,7 +13,7 @@ import torch  # noqa: E402
 import paper_2211_00696_b200 as pq  # noqa: E402
 from paper_2211_00696_b200.workloads import config  # noqa: E402
 
-PEAK = 36.95
+PEAK = 37.15
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 w = config(cfg)
