@@ -105,9 +105,9 @@ void finish(pq_ctx& c, int space) {
     int err = 0;
     // singular LU flag (dense.hpp:167) -- checked whenever the host already waits
     if (space == PQ_HOST) {
-        cuda_check(cudaMemcpy(&err, c.d_err, sizeof(int), cudaMemcpyDeviceToHost), "err readback");
+        err = *static_cast<volatile int*>(c.h_err);  // mapped: visible once the stream has drained
         if (err) {
-            cudaMemset(c.d_err, 0, sizeof(int));
+            *c.h_err = 0;
             throw std::runtime_error("lu_solve: singular matrix");
         }
     }
@@ -187,12 +187,18 @@ int pq_ctx_create(int device, pq_ctx** out) {
         c->own_stream = true;
         const char* tr = std::getenv("PQ_TRACE");
         c->trace = tr && tr[0] == '1';
-        cuda_check(cudaMalloc(&c->d_err, sizeof(int)), "cudaMalloc(err)");
-        cuda_check(cudaMemset(c->d_err, 0, sizeof(int)), "memset(err)");
+        // small flags and readbacks in mapped pinned memory: kernels store into them directly, so
+        // they never wait on the copy engines behind MB-sized transfers
+        const unsigned mapped = cudaHostAllocMapped | cudaHostAllocPortable;
+        cuda_check(cudaHostAlloc(&c->h_err, sizeof(int), mapped), "cudaHostAlloc(err)");
+        *c->h_err = 0;
+        cuda_check(cudaHostGetDevicePointer(&c->d_err, c->h_err, 0), "err device view");
         cuda_check(cudaMalloc(&c->d_int, 64 * sizeof(int)), "cudaMalloc(int)");
         cuda_check(cudaMalloc(&c->d_small, 1024 * sizeof(double)), "cudaMalloc(small)");
-        cuda_check(cudaMallocHost(&c->h_small, 1024 * sizeof(double)), "cudaMallocHost(small)");
-        cuda_check(cudaMallocHost(&c->h_beta, 1024 * sizeof(double)), "cudaMallocHost(beta)");
+        cuda_check(cudaHostAlloc(&c->h_small, 1024 * sizeof(double), mapped), "cudaHostAlloc(small)");
+        cuda_check(cudaHostGetDevicePointer(&c->h_small_d, c->h_small, 0), "small device view");
+        cuda_check(cudaHostAlloc(&c->h_beta, 1024 * sizeof(double), mapped), "cudaHostAlloc(beta)");
+        cuda_check(cudaHostGetDevicePointer(&c->h_beta_d, c->h_beta, 0), "beta device view");
         *out = c;
     });
 }
@@ -202,13 +208,14 @@ int pq_ctx_destroy(pq_ctx* c) {
         if (!c) return;
         cudaSetDevice(c->device);
         cudaStreamSynchronize(c->stream);
+        gate_forget(*c);
         for (auto& kv : c->bufs) ws_free_now(*c, kv.second.p);
         for (void* p : c->graveyard) cudaFree(p);
         trim_pool(*c);
         if (c->arena.host) cudaFreeHost(c->arena.host);
         if (c->arena.dev) cudaFree(c->arena.dev);
         if (c->arena.done) cudaEventDestroy(c->arena.done);
-        cudaFree(c->d_err);
+        cudaFreeHost(c->h_err);
         cudaFree(c->d_int);
         cudaFree(c->d_small);
         if (c->d_flops) cudaFree(c->d_flops);
@@ -952,8 +959,23 @@ static void run_phiquadmv_impl(pq_ctx* c, int d, const int* shape, const double*
     }
     bool cols_copied = false;
     c->early.clear();
+    // several host callers: this call's compute waits for the previous caller's compute, not for its
+    // result copies (engine.hpp gate_acquire)
+    struct GateHold {
+        pq_ctx* c = nullptr;
+        void done() {
+            if (c) gate_enqueued(*c);
+            c = nullptr;
+        }
+        ~GateHold() { done(); }
+    } gate;
+    if (space == PQ_HOST && gate_wanted(static_cast<size_t>(nb) * (p + (out0 ? 1 : 0)) * N * sizeof(double))) {
+        gate_acquire(*c);
+        gate.c = c;
+    }
     phiquadmv_dev(*c, op, nb, db, p, req->eps, req->mode, req->has_l != 0, req->l, req->c1, req->c2, dout, &pi, d0, h0,
                   hc, &cols_copied);
+    gate.done();
     // bounced results that are already on their way: move each to the caller's memory as soon as
     // its copy lands, while the device finishes the rest of the call
     bool done0 = false;

@@ -177,7 +177,9 @@ void arena_begin(pq_ctx& c) {
     ParamArena& a = c.arena;
     if (!a.host) {
         a.cap = size_t(8) << 20;
-        cuda_check(cudaMallocHost(reinterpret_cast<void**>(&a.host), a.cap), "cudaMallocHost(arena)");
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&a.host), a.cap, cudaHostAllocMapped | cudaHostAllocPortable),
+                   "cudaHostAlloc(arena)");
+        cuda_check(cudaHostGetDevicePointer(reinterpret_cast<void**>(&a.host_d), a.host, 0), "arena device view");
         cuda_check(cudaMalloc(reinterpret_cast<void**>(&a.dev), a.cap), "cudaMalloc(arena)");
         cuda_check(cudaEventCreateWithFlags(&a.done, cudaEventDisableTiming), "event(arena)");
         cuda_check(cudaEventRecord(a.done, c.stream), "record(arena)");
@@ -211,12 +213,33 @@ const void* arena_push(pq_ctx& c, const void* data, size_t bytes) {
 void arena_flush(pq_ctx& c) {
     ParamArena& a = c.arena;
     if (a.used > a.flushed) {
-        cuda_check(cudaMemcpyAsync(a.dev + a.flushed, a.host + a.flushed, a.used - a.flushed, cudaMemcpyHostToDevice,
-                                   c.stream),
-                   "arena upload");
+        // up to 256 KB: SM loads from the mapped staging buffer (the H2D engine may be busy with
+        // another call's right-hand sides for 0.3 ms); the 16-byte rounding only rewrites bytes
+        // with their current staged values or bytes not handed out yet (cap is 16-byte aligned)
+        const size_t lo = a.flushed & ~size_t(15), hi = (a.used + 15) & ~size_t(15);
+        if (hi - lo <= (256u << 10) && hi <= a.cap) {
+            launch_copy_vec4(a.host_d + lo, a.dev + lo, (hi - lo) / 16, c.stream);
+            count_launch(c);
+        } else {
+            cuda_check(cudaMemcpyAsync(a.dev + a.flushed, a.host + a.flushed, a.used - a.flushed, cudaMemcpyHostToDevice,
+                                       c.stream),
+                       "arena upload");
+        }
         a.flushed = a.used;
         cuda_check(cudaEventRecord(a.done, c.stream), "record(arena)");
     }
+}
+
+// device-to-device copy of `count` doubles: on the SMs when small and 16-byte aligned (matrix-sized
+// copies would otherwise queue on a copy engine behind MB-sized transfers), else cudaMemcpyAsync
+void dev_copy(pq_ctx& c, double* dst, const double* src, size_t count, cudaStream_t s) {
+    const bool aligned = ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0;
+    if (aligned && count % 2 == 0 && count * sizeof(double) <= (4u << 20)) {
+        launch_copy_vec4(src, dst, count / 2, s);
+        count_launch(c);
+        return;
+    }
+    cuda_check(cudaMemcpyAsync(dst, src, count * sizeof(double), cudaMemcpyDeviceToDevice, s), "device copy");
 }
 
 // Every launch site counts its kernels here, so launch-configuration errors surface at the launch
@@ -383,6 +406,74 @@ void prof_collect(pq_ctx& c) {
     c.ev_used = 0;
     c.ev_flops.clear();
     c.ev_keys.clear();
+}
+
+namespace {
+// per device: the compute-done events of the call that last held the gate
+struct ComputeGate {
+    std::mutex mu;
+    const pq_ctx* owner = nullptr;
+    std::vector<cudaEvent_t> done;
+};
+ComputeGate& device_gate(int dev) {
+    static ComputeGate gates[64];
+    return gates[static_cast<unsigned>(dev) % 64];
+}
+}  // namespace
+
+bool gate_wanted(size_t result_bytes) {
+    static const bool on = [] {
+        // measured on config 2 with 4 callers: 386-388 actions/s gated, 407-421 ungated (the
+        // serialised compute loses the overlap of one call's low-occupancy phases with another's)
+        const char* e = std::getenv("PQ_COMPUTE_GATE");
+        return e && std::atoi(e) != 0;
+    }();
+    return on && result_bytes >= (8u << 20);
+}
+
+void gate_acquire(pq_ctx& c) {
+    ComputeGate& g = device_gate(c.device);
+    g.mu.lock();  // held until gate_enqueued: the next caller chains behind this call's events
+    for (cudaEvent_t e : g.done) cuda_check(cudaStreamWaitEvent(c.stream, e, 0), "gate wait");
+    c.gate_held = true;
+    c.gate_covered = false;
+    c.gate_used = 0;
+}
+
+void gate_point(pq_ctx& c, cudaStream_t s) {
+    if (!c.gate_held) return;
+    if (c.gate_ev.size() <= c.gate_used) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "gate event");
+        c.gate_ev.push_back(e);
+    }
+    cuda_check(cudaEventRecord(c.gate_ev[c.gate_used++], s), "gate record");
+}
+
+void gate_enqueued(pq_ctx& c) {
+    if (!c.gate_held) return;
+    ComputeGate& g = device_gate(c.device);
+    try {
+        if (!c.gate_covered) gate_point(c, c.stream);
+        g.done.assign(c.gate_ev.begin(), c.gate_ev.begin() + static_cast<long>(c.gate_used));
+        g.owner = &c;
+    } catch (...) {
+        g.done.clear();
+        g.owner = nullptr;
+    }
+    c.gate_held = false;
+    g.mu.unlock();
+}
+
+void gate_forget(pq_ctx& c) {
+    ComputeGate& g = device_gate(c.device);
+    std::lock_guard<std::mutex> lk(g.mu);
+    if (g.owner == &c) {
+        g.done.clear();
+        g.owner = nullptr;
+    }
+    for (cudaEvent_t e : c.gate_ev) cudaEventDestroy(e);
+    c.gate_ev.clear();
 }
 
 void note_early_copy(pq_ctx& c, cudaStream_t s, double* host, size_t count) {
@@ -717,10 +808,7 @@ static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>&
             std::swap(a, b);
         }
         gemm_chain(c, levels, "expm_squaring");
-        if (a != out)
-            cuda_check(cudaMemcpyAsync(out, a, static_cast<size_t>(count) * nn * sizeof(double), cudaMemcpyDeviceToDevice,
-                                       c.stream),
-                       "expm copy");
+        if (a != out) dev_copy(c, out, a, static_cast<size_t>(count) * nn, c.stream);
         check_launch(c);
         return;
     }
@@ -728,10 +816,8 @@ static void squaring_rounds(pq_ctx& c, int n, int count, const std::vector<int>&
     int z_done = 0;
     auto flush = [&](int z_from, int z_to) {
         if (z_to > z_from && cur != out)
-            cuda_check(cudaMemcpyAsync(out + static_cast<size_t>(z_from) * nn, cur + static_cast<size_t>(z_from) * nn,
-                                       static_cast<size_t>(z_to - z_from) * nn * sizeof(double), cudaMemcpyDeviceToDevice,
-                                       st),
-                       "expm copy");
+            dev_copy(c, out + static_cast<size_t>(z_from) * nn, cur + static_cast<size_t>(z_from) * nn,
+                     static_cast<size_t>(z_to - z_from) * nn, st);
     };
     for (int r = 0; r < s_max; ++r) {
         int z0 = z_done;
@@ -1630,9 +1716,14 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         half = half_next;
         rule = &fine;
         slot_of = std::move(fine_slot);
-        double* hs = pinned_stats ? c.h_small : hstats.data();
-        cuda_check(cudaMemcpyAsync(hs, stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost, c.stream),
-                   "cc stats readback");
+        if (pinned_stats) {  // mapped: stored by a kernel, no copy engine
+            launch_store_words(stats, c.h_small_d, hstats.size(), c.stream);
+            count_launch(c);
+        } else {
+            cuda_check(cudaMemcpyAsync(hstats.data(), stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost,
+                                       c.stream),
+                       "cc stats readback");
+        }
         cuda_check(cudaEventRecord(c.ev_cc, c.stream), "cc record");
         if (offload) {
             c.stream = main_stream;
@@ -1646,6 +1737,7 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         cuda_check(cudaEventSynchronize(c.ev_cc), "cc stats wait");
         mark(c, "cc_level_synced");
         cur = nxt;
+        const volatile double* hs = pinned_stats ? c.h_small : hstats.data();
         double err = 0.0;
         for (int k = 0; k < nb * p; ++k) {
             const double diff = hs[2 * k], norm = hs[2 * k + 1];
@@ -1714,10 +1806,7 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
         Group& G = groups[g];
         const size_t nn = static_cast<size_t>(G.n) * G.n;
         G.buf = ws(c, "sqE" + std::to_string(g), 2 * G.dims.size() * nn);
-        for (size_t i = 0; i < G.dims.size(); ++i)
-            cuda_check(cudaMemcpyAsync(G.buf + i * nn, E_in[G.dims[i]], nn * sizeof(double), cudaMemcpyDeviceToDevice,
-                                       c.stream),
-                       "sq exps");
+        for (size_t i = 0; i < G.dims.size(); ++i) dev_copy(c, G.buf + i * nn, E_in[G.dims[i]], nn, c.stream);
     }
     int parity = 0;
     auto cur_E = [&](int k) {
@@ -1828,6 +1917,7 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
             c.stream = st;
             mark(c, "sq_group_done");
             if (host_out) {  // this group's columns are final on its stream now
+                gate_point(c, st);
                 cuda_check(cudaMemcpyAsync(host_out + static_cast<size_t>(c0) * N, res + static_cast<size_t>(c0) * N,
                                            sizeof(double) * (c1 - c0) * N, cudaMemcpyDeviceToHost, st),
                            "phi columns D2H");
@@ -1841,6 +1931,7 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
             }
         }
         if (host_out && copied) *copied = true;
+        if (host_out) c.gate_covered = true;  // (only copies follow on the context stream)
         check_launch(c);
         return b[static_cast<size_t>(l % R)];
     }
@@ -1941,6 +2032,7 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
         try {
             apply_phi0(c, op, px, nb, bs, phi0_out);
             if (phi0_host) {  // pinned destination: the D2H overlaps the squaring
+                gate_point(c, c.side);
                 cuda_check(cudaMemcpyAsync(phi0_host, phi0_out, sizeof(double) * nb * op.N, cudaMemcpyDeviceToHost, c.side),
                            "phi_0 D2H");
                 note_early_copy(c, c.side, phi0_host, static_cast<size_t>(nb) * op.N);
@@ -1987,8 +2079,8 @@ static double beta_enqueue(pq_ctx& c, const DevOp& op, int nb, const double* bs)
     launch_colstats(op.N, nb, bs, nullptr, stats, c.stream);
     count_launch(c);
     if (!c.ev_beta) cuda_check(cudaEventCreateWithFlags(&c.ev_beta, cudaEventDisableTiming), "beta event");
-    cuda_check(cudaMemcpyAsync(c.h_beta, stats, sizeof(double) * 2 * nb, cudaMemcpyDeviceToHost, c.stream),
-               "beta readback");
+    launch_store_words(stats, c.h_beta_d, 2 * static_cast<size_t>(nb), c.stream);  // (mapped: no copy engine)
+    count_launch(c);
     cuda_check(cudaEventRecord(c.ev_beta, c.stream), "beta record");
     return -1.0;
 }

@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <exception>
@@ -39,6 +40,7 @@ struct DevBuf {
 // Pinned staging arena for small per-call parameter tables (rule coefficients, epilogue tables).
 struct ParamArena {
     char* host = nullptr;
+    char* host_d = nullptr;  // device view of the mapped pinned staging buffer
     char* dev = nullptr;
     size_t cap = 0, used = 0, flushed = 0;
     cudaEvent_t done = nullptr;
@@ -68,9 +70,12 @@ struct pq_ctx {
     };
     std::map<void*, Guarded> guards;
     pqb::ParamArena arena;
-    int* d_err = nullptr;        // device error flag (singular LU)
-    double* h_small = nullptr;   // pinned readback scratch
-    double* h_beta = nullptr;    // pinned readback of the planner's beta (read by the planner thread)
+    int* d_err = nullptr;        // error flag (singular LU): mapped pinned host memory, device view
+    int* h_err = nullptr;        //   ... and its host view
+    double* h_small = nullptr;   // mapped pinned readback scratch (host view)
+    double* h_small_d = nullptr; //   ... device view (launch_store_words target)
+    double* h_beta = nullptr;    // mapped pinned readback of the planner's beta (read by the planner thread)
+    double* h_beta_d = nullptr;  //   ... device view
     double* d_small = nullptr;   // device scratch for reductions
     int* d_int = nullptr;        // device int scratch (expm squaring counts)
     bool profiling = false;
@@ -143,6 +148,11 @@ struct pq_ctx {
     };
     std::vector<EarlyCopy> early;
     std::vector<cudaEvent_t> ev_early;
+    // compute gate (gate_acquire .. gate_enqueued): this call's compute-done events
+    std::vector<cudaEvent_t> gate_ev;
+    size_t gate_used = 0;
+    bool gate_held = false;
+    bool gate_covered = false;  // the points cover every stream's compute (else one on c.stream)
     // pinned bounce buffers for pageable host results (capi.cpp run_phiquadmv): name -> (ptr, bytes)
     std::map<std::string, std::pair<double*, size_t>> pin_bounce;
     cudaEvent_t ev_fac = nullptr;
@@ -296,6 +306,19 @@ struct KernelProbe {
     KernelProbe& operator=(const KernelProbe&) = delete;
 };
 void note_early_copy(pq_ctx& c, cudaStream_t s, double* host, size_t count);  // after an early D2H on s
+// Compute gate: several host-buffer callers on one device compute one after the other, each call's
+// kernels queued behind the previous call's compute (device-side event waits, no host blocking on
+// the GPU) but not behind its result copies, which drain under the next call's kernels.
+// gate_acquire takes the device's gate (host mutex, held while this call enqueues) and makes
+// c.stream wait for the last holder's compute-done events; gate_point(c, s) records one on stream s
+// (s has only this call's result copies left); gate_enqueued publishes them (plus one on c.stream
+// unless c.gate_covered) and passes the gate on; gate_forget drops a context being destroyed.
+void dev_copy(pq_ctx& c, double* dst, const double* src, size_t count, cudaStream_t s);  // small D2D on the SMs
+void gate_acquire(pq_ctx& c);
+void gate_point(pq_ctx& c, cudaStream_t s);
+void gate_enqueued(pq_ctx& c);
+void gate_forget(pq_ctx& c);
+bool gate_wanted(size_t result_bytes);  // PQ_COMPUTE_GATE=1 (default off) and a result of >= 8 MB
 void mark(pq_ctx& c, const char* name);  // NVTX marker; timeline mark (device event + host clock) when profiling / tracing
 // NVTX range over one C-ABI call (visible under nsys / ncu --nvtx; a few ns when no tool is attached)
 struct NvtxRange {

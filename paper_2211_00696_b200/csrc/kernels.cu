@@ -1084,6 +1084,34 @@ bool launch_combine_stats(long long N, int p, int q, const double* V, long long 
     return node_combine(N, p, q, V, vstride, slots, cf, cc, prev, acc, acc_stride, 1, stats, cc ? 1 : 2, s);
 }
 
+// Small result readbacks (beta, the adaptive-CC statistics) stored by a kernel straight into
+// mapped pinned host memory: the stores travel as posted PCIe writes, so the readback does not queue
+// on the D2H copy engine behind other calls' (or this call's early) result copies of many MB.
+__global__ void k_store_words(const unsigned long long* __restrict__ src, unsigned long long* __restrict__ dst, int n) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = src[i];
+}
+
+void launch_store_words(const void* src, void* dst_mapped, size_t words, cudaStream_t s) {
+    if (words == 0) return;
+    k_store_words<<<1, 256, 0, s>>>(static_cast<const unsigned long long*>(src),
+                                    static_cast<unsigned long long*>(dst_mapped), static_cast<int>(words));
+}
+
+// Small copies on the SMs instead of the copy engines (whose queues hold other calls' MB-sized
+// H2D / D2H transfers): parameter-table uploads read from mapped pinned host memory, matrix-sized
+// device copies.  16-byte words, one word per thread.
+__global__ void k_copy_vec4(const uint4* __restrict__ src, uint4* __restrict__ dst, long long n) {
+    const long long i = blockIdx.x * static_cast<long long>(blockDim.x) + threadIdx.x;
+    if (i < n) dst[i] = src[i];
+}
+
+void launch_copy_vec4(const void* src, void* dst, size_t vec4s, cudaStream_t s) {
+    if (vec4s == 0) return;
+    const unsigned blocks = static_cast<unsigned>((vec4s + 255) / 256);
+    k_copy_vec4<<<blocks, 256, 0, s>>>(static_cast<const uint4*>(src), static_cast<uint4*>(dst),
+                                        static_cast<long long>(vec4s));
+}
+
 void launch_colstats(long long N, int ncols, const double* y, const double* yp, double* out, cudaStream_t s) {
     cudaMemsetAsync(out, 0, sizeof(double) * 2 * ncols, s);
     long long bx = (N + 255) / 256;

@@ -123,6 +123,10 @@ bool launch_combine_stats(long long N, int p, int q, const double* V, long long 
                           double* stats, cudaStream_t s);
 // per column c < ncols: out[2c] = max|y_c - yp_c| (yp may be null -> max|y_c|), out[2c+1] = max|y_c|.
 void launch_colstats(long long N, int ncols, const double* y, const double* yp, double* out, cudaStream_t s);
+// copy `words` 8-byte words from device memory into mapped pinned host memory with one small kernel
+void launch_store_words(const void* src, void* dst_mapped, size_t words, cudaStream_t s);
+// copy vec4s 16-byte words (both pointers 16-byte aligned; either side may be mapped host memory)
+void launch_copy_vec4(const void* src, void* dst, size_t vec4s, cudaStream_t s);
 // out = s1*u + s3*u^3 - au   (Allen-Cahn source minus A u)
 void launch_cubic_minus(long long N, double s1, double s3, const double* u, const double* au, double* out,
                         cudaStream_t s);

@@ -106,3 +106,28 @@ for g, at in gaps:
 print("D2H bytes/s while active: ", end="")
 tot_bytes = sum(e.get("args", {}).get("bytes", 0) for e in ev if e.get("cat") == "gpu_memcpy" and "DtoH" in e["name"])
 print(f"{tot_bytes / (db / 1e6) / 1e9:.1f} GB/s over {tot_bytes / 1e6:.0f} MB")
+
+if "--streams" in sys.argv:  # per stream: kernel busy windows and copies, in ms from the start
+    by = {}
+    for e in ev:
+        if e.get("cat") in ("kernel", "gpu_memcpy"):
+            by.setdefault(e["args"].get("stream"), []).append(e)
+    rows = []
+    for sid, es in by.items():
+        es.sort(key=lambda e: e["ts"])
+        seg = None
+        for e in es:
+            kind = "K" if e["cat"] == "kernel" else ("D2H" if "DtoH" in e["name"] else "H2D" if "HtoD" in e["name"] else "D2D")
+            if kind != "K" and e["args"].get("bytes", 1 << 30) < (1 << 20):
+                kind += "(%s %dB)" % ("pageable" if "Pageable" in e["name"] else "pinned", e["args"]["bytes"])
+            s, f = (e["ts"] - t0) / 1e3, (e["ts"] + e["dur"] - t0) / 1e3
+            if seg and seg[0] == kind and s - seg[2] < 0.05:
+                seg[2] = f
+            else:
+                if seg:
+                    rows.append((seg[1], sid, *seg))
+                seg = [kind, s, f]
+        rows.append((seg[1], sid, *seg))
+    for _, sid, kind, s, f in sorted(rows):
+        if kind != "K" or f - s > 0.05:
+            print(f"  stream {sid:>4} {kind:>24} {s:8.3f} .. {f:8.3f}")
