@@ -562,7 +562,11 @@ def run_ours_phi(args, world, rank, local) -> None:
         comm.stats(reset=True)
     ms_e2e2_max = max_over_ranks(e2e_callers(args.steps), world)
     comm_bytes = comm.stats(reset=True)[0] / args.steps if nodes else None
-    e2e_value = units / (ms_e2e2_max / 1e3)
+    e2e_multi = units / (ms_e2e2_max / 1e3)
+    # a deployment runs as many host callers as pays: small problems (config 1, ~0.2 ms per call)
+    # are host-latency bound and lose to thread contention with 4 callers; report the better of
+    # the two measured configurations and say which
+    e2e_value, e2e_callers = (e2e_multi, ncall) if e2e_multi >= e2e_single else (e2e_single, 1)
 
     line = {
         "metric": METRIC, "value": value, "unit": "actions/s",
@@ -576,12 +580,13 @@ def run_ours_phi(args, world, rank, local) -> None:
         "clocks": clocks,
         "roofline": roof, "cpu_baseline": None,
         "e2e": {"value": e2e_value, "unit": "actions/s", "h2d_bytes_per_step": int(nb * N * 8),
-                "d2h_bytes_per_step": int(nb * (w.p + 1) * NO * 8), "callers": ncall,
-                "single_caller_value": e2e_single,
+                "d2h_bytes_per_step": int(nb * (w.p + 1) * NO * 8), "callers": e2e_callers,
+                "single_caller_value": e2e_single, "multi_caller_value": e2e_multi, "multi_callers": ncall,
                 "distinct_rhs": {"device": npool, "pinned_host": npin},
                 "note": ("pq_phi_0p with pinned host b in and all p+1 vectors back every step; concurrent "
                          "host threads with their own contexts/streams overlap one call's PCIe transfers with "
-                         "another's compute; single_caller_value = one synchronous caller; the operator's "
+                         "another's compute; value = the better of single_caller_value (one synchronous caller) "
+                         "and multi_caller_value (multi_callers threads), `callers` says which; the operator's "
                          "factors are uploaded once (bit-identical factors are not re-copied) and not counted")},
     }
     if nodes:
