@@ -79,6 +79,30 @@ int main(int argc, char** argv) {
         }
         t_free += ms_since(t);
     }
+    // the header's current path (phiquadmv_ptrs): threaded column allocation, in-place columns call, free
+    double u_alloc = 0, u_call = 0, u_free = 0;
+    for (int k = 0; k < steps; ++k) {
+        auto T = [] { return std::chrono::steady_clock::now(); };
+        auto ms_since = [](auto t) { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t).count(); };
+        auto t = T();
+        const auto f = detail::flatten(s);
+        const pq_phi_request r = detail::abi_request(req);
+        pq_phi_info pi{};
+        {
+            std::vector<PhiColumns> out = detail::alloc_columns(1, req.p, s.dim());
+            u_alloc += ms_since(t); t = T();
+            std::vector<double*> cols;
+            for (auto& c : out[0].cols) cols.push_back(c.data());
+            const double* bp = b.data();
+            b200::check(pq_phiquadmv_cols(b200::context(), s.order(), f.shape.data(), f.data.data(), 1, &bp, &r,
+                                          cols.data(), &pi, PQ_HOST));
+            u_call += ms_since(t); t = T();
+            sink += out[0].cols[1][5];
+        }
+        u_free += ms_since(t);
+    }
+    std::printf("{\"path\": \"phiquadmv_ptrs\", \"alloc_columns\": %.2f, \"pq_phiquadmv_cols\": %.2f, \"free\": %.2f}\n",
+                u_alloc / steps, u_call / steps, u_free / steps);
     std::printf("{\"wrap\": %.2f, \"gather\": %.2f, \"alloc_out\": %.2f, \"pq_call\": %.2f, \"scatter\": %.2f, \"free\": %.2f}\n",
                 t_wrap / steps, t_gather / steps, t_alloc / steps, t_call / steps, t_scatter / steps, t_free / steps);
     std::printf("{\"api\": \"drop-in headers, pageable std::vector\", \"ms_per_action\": %.3f, \"actions_per_s\": %.1f, "
