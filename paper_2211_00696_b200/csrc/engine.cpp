@@ -1261,7 +1261,7 @@ void mode_product_dev(pq_ctx& c, int d, const int* n, int k, const double* E, co
 
 void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride, const double* x,
                 long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep, const char* tmp_tag,
-                const int2* const* band) {
+                const int2* const* band, const std::function<void()>& before_last) {
     long long N = 1;
     for (int k = 0; k < d; ++k) N *= n[k];
     double* tmp[2] = {nullptr, nullptr};
@@ -1296,6 +1296,7 @@ void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const lo
             if (ep.cld > 0) g.ext_group = ep.cld;
         }
         g.tag = tagk.c_str();
+        if (last && before_last) before_last();
         gemm(c, g);
         src = dst;
         sstride = dstride;
@@ -1828,8 +1829,43 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
         for (int j = 0; j <= i; ++j)
             coef[static_cast<size_t>(i) * p + j] = std::ldexp(1.0, -(i + 1)) * inv[static_cast<size_t>(i - j)];
     const double* coef_dev = static_cast<const double*>(arena_push(c, coef.data(), coef.size() * sizeof(double)));
-    arena_flush(c);
     const int Z1 = nb * p;
+    // The combination fused into the last mode product's epilogue (PQ_SQ_FUSE=1; default off):
+    // column z1 (i = z1 mod p) = 2^-(i+1) acc + sum_{j <= i} coef[i][j] b_j, with the same
+    // roundings in the same order as k_sq_combine2 (bitwise identical results, checked with
+    // tools/bitwise_env_ab.py).  Measured at config 2: 461.7 vs 461-471 actions/s -- the k-major
+    // last-mode tiles (6 CTAs/SM, 80 registers) read the i + 1 addend columns term by term in
+    // their epilogue (645 us per call vs 340 us + 237 us for the separate streaming combination,
+    // which loads each b_j once for all columns i >= j).
+    static const bool fuse = [] {
+        const char* e = std::getenv("PQ_SQ_FUSE");
+        return e && std::atoi(e) != 0;
+    }();
+    Epilogue fused{};
+    if (fuse) {
+        std::vector<double> alpha(static_cast<size_t>(Z1)), rows(static_cast<size_t>(Z1) * p, 0.0);
+        std::vector<int> nterms(static_cast<size_t>(Z1));
+        for (int z = 0; z < Z1; ++z) {
+            const int i = z % p;
+            alpha[static_cast<size_t>(z)] = std::ldexp(1.0, -(i + 1));
+            nterms[static_cast<size_t>(z)] = i + 1;
+            for (int j = 0; j <= i; ++j) rows[static_cast<size_t>(z) * p + j] = coef[static_cast<size_t>(i) * p + j];
+        }
+        fused.alpha_z = static_cast<const double*>(arena_push(c, alpha.data(), alpha.size() * sizeof(double)));
+        fused.coef = static_cast<const double*>(arena_push(c, rows.data(), rows.size() * sizeof(double)));
+        fused.nterms = static_cast<const int*>(arena_push(c, nterms.data(), nterms.size() * sizeof(int)));
+        fused.cld = p;  // = ext_group: batch z1 reads addends (z1 / p) p + t, its own right-hand side's
+        fused.ext_s = N;
+    }
+    auto fused_at = [&](const double* cur, int c0) {
+        Epilogue e = fused;
+        e.ext = cur;
+        e.alpha_z += c0;
+        e.coef += static_cast<size_t>(c0) * p;
+        e.nterms += c0;
+        return e;
+    };
+    arena_flush(c);
     long long Es[3] = {0, 0, 0};
     if (chain && squaring_split_ok(c, nb, p, N)) {
         // Column groups on their own streams, R rotating buffers b_s (step s reads b_s, writes
@@ -1894,14 +1930,25 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
                     if (step + 1 >= R)
                         for (int h = g + 1; h < G; ++h)
                             cuda_check(cudaStreamWaitEvent(c.stream, ev(h, step + 1 - R), 0), "sq wait (reuse)");
-                    mode_chain(c, op.d, op.n, E, Es, cur + static_cast<size_t>(c0) * N, N, nxt + static_cast<size_t>(c0) * N,
-                               N, c1 - c0, Epilogue{}, tags[g], Bd);
-                    if (step >= 1)
-                        for (int h = 0; h < g; ++h)
-                            cuda_check(cudaStreamWaitEvent(c.stream, ev(h, step - 1), 0), "sq wait (columns)");
-                    KernelProbe kp(c, "k_sq_combine2", 8.0 * N * (2 * (c1 - c0) + c1));
-                    launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, c0, c1);
-                    count_launch(c);
+                    // the combination reads columns j < c0 of this step's input: the lower groups'
+                    // results of the previous step
+                    auto lower_done = [&] {
+                        if (step >= 1)
+                            for (int h = 0; h < g; ++h)
+                                cuda_check(cudaStreamWaitEvent(c.stream, ev(h, step - 1), 0), "sq wait (columns)");
+                    };
+                    if (fuse) {
+                        mode_chain(c, op.d, op.n, E, Es, cur + static_cast<size_t>(c0) * N, N,
+                                   nxt + static_cast<size_t>(c0) * N, N, c1 - c0, fused_at(cur, c0), tags[g], Bd,
+                                   lower_done);
+                    } else {
+                        mode_chain(c, op.d, op.n, E, Es, cur + static_cast<size_t>(c0) * N, N,
+                                   nxt + static_cast<size_t>(c0) * N, N, c1 - c0, Epilogue{}, tags[g], Bd);
+                        lower_done();
+                        KernelProbe kp(c, "k_sq_combine2", 8.0 * N * (2 * (c1 - c0) + c1));
+                        launch_sq_combine(N, p, 1, nxt, cur, coef_dev, c.stream, c0, c1);
+                        count_launch(c);
+                    }
                     cuda_check(cudaEventRecord(ev(g, step), c.stream), "sq rec");
                 }
             }
@@ -1944,10 +1991,14 @@ static double* squaring_pingpong(pq_ctx& c, const DevOp& op, int l, int nb, int 
             E[k] = chain ? E_in[k] + static_cast<size_t>(step) * op.n[k] * op.n[k] : cur_E(k);
             if (chain && band_in && band_in[k]) Bd[k] = band_in[k] + step * band_row_blocks(op.n[k]);
         }
-        mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, Epilogue{}, "chain", Bd);
-        KernelProbe kp(c, "k_sq_combine2", 8.0 * N * nb * 3 * p);
-        launch_sq_combine(N, p, nb, nxt, cur, coef_dev, c.stream);
-        count_launch(c);
+        if (fuse) {
+            mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, fused_at(cur, 0), "chain", Bd);
+        } else {
+            mode_chain(c, op.d, op.n, E, Es, cur, N, nxt, N, Z1, Epilogue{}, "chain", Bd);
+            KernelProbe kp(c, "k_sq_combine2", 8.0 * N * nb * 3 * p);
+            launch_sq_combine(N, p, nb, nxt, cur, coef_dev, c.stream);
+            count_launch(c);
+        }
         std::swap(cur, nxt);
         if (step < l - 1 && !chain) {
             for (const Group& G : groups) {

@@ -339,9 +339,12 @@ void expm_batch(pq_ctx& c, int n, int count, const double* base, long long base_
 // y[z1] = (E_0[z1] (x) ... (x) E_{d-1}[z1]) x[z1] for z1 < Z1, epilogue fused into the last mode.
 // band (nullable, per dim): negligible-block tables of E[k]'s matrices (launch_band_ranges),
 // matrix a of E[k] at band[k] + a (E_stride[k]/n_k^2) ceil(n_k/64).
+// before_last (optional) runs on the host right before the last mode's GEMM is enqueued (e.g. a
+// stream wait that only the epilogue's extra addends need).
 void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const long long* E_stride,
                 const double* x, long long x_stride, double* y, long long y_stride, int Z1, const Epilogue& ep,
-                const char* tmp_tag = "chain", const int2* const* band = nullptr);
+                const char* tmp_tag = "chain", const int2* const* band = nullptr,
+                const std::function<void()>& before_last = {});
 void kron_matvec_dev(pq_ctx& c, const DevOp& op, double scale, const double* x, double* y);
 // one mode product of nb columns (no band table): the GEMM the mode chain issues for `mode`
 GemmArgs mode_gemm_public(int d, const int* n, int mode, const double* E, const double* x, double* y, int nb,
