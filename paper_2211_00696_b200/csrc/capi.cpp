@@ -92,6 +92,27 @@ static bool host_pinned(const void* p) {
     return yes;
 }
 
+// dst + k*count <- src[k] for each k (the inverse of host_scatter), same thread split
+static void host_gather(double* dst, const double* const* src, int parts, size_t count) {
+    const size_t piece = size_t(1) << 19;
+    const size_t per = (count + piece - 1) / piece, total = per * static_cast<size_t>(parts);
+    auto work = [&](size_t t0, size_t step) {
+        for (size_t t = t0; t < total; t += step) {
+            const size_t k = t / per, o = (t % per) * piece, len = std::min(piece, count - o);
+            std::memcpy(dst + k * count + o, src[k] + o, len * sizeof(double));
+        }
+    };
+    const size_t threads = std::min<size_t>(8, total);
+    if (threads <= 1) {
+        work(0, 1);
+        return;
+    }
+    std::vector<std::thread> team;
+    for (size_t w = 1; w < threads; ++w) team.emplace_back(work, w, threads);
+    work(0, threads);
+    for (auto& t : team) t.join();
+}
+
 // Device view of a caller vector: device pointers pass through; host data is staged.  Pageable
 // inputs of 8 MB and more are first copied into a pinned bounce by several host threads: the
 // driver's own staging of a pageable H2D runs at a fraction of the pinned PCIe rate.
@@ -146,6 +167,17 @@ const double* gather_cols(pq_ctx& c, const double* const* v, int count, long lon
     for (int k = 0; k < count; ++k) need(v[k] != nullptr, "null vector");
     if (space == PQ_DEVICE && count == 1) return v[0];
     double* g = ws(c, slot, static_cast<size_t>(count) * N);
+    const size_t total = static_cast<size_t>(count) * N;
+    if (space == PQ_HOST && total >= kBounceMin) {
+        bool all_pinned = true;
+        for (int k = 0; k < count && all_pinned; ++k) all_pinned = host_pinned(v[k]);
+        if (!all_pinned) {  // pageable: several host threads fill a pinned bounce, then one H2D
+            double* bnc = pinned_bounce(c, std::string("in:") + slot, total);
+            host_gather(bnc, v, count, static_cast<size_t>(N));
+            cuda_check(cudaMemcpyAsync(g, bnc, total * sizeof(double), cudaMemcpyHostToDevice, c.stream), "gather H2D");
+            return g;
+        }
+    }
     for (int k = 0; k < count; ++k)
         cuda_check(cudaMemcpyAsync(g + static_cast<size_t>(k) * N, v[k], N * sizeof(double),
                                    space == PQ_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice, c.stream),
@@ -946,13 +978,7 @@ static void run_phiquadmv_impl(pq_ctx* c, int d, const int* shape, const double*
         } else if (space == PQ_HOST && nb == 1) {
             db = stage_in(*c, b_list[0], static_cast<size_t>(N), space, "hin_b");
         } else {
-            double* g = ws(*c, "hin_b", static_cast<size_t>(nb) * N);
-            for (int m = 0; m < nb; ++m)
-                cuda_check(cudaMemcpyAsync(g + static_cast<size_t>(m) * N, b_list[m], N * sizeof(double),
-                                           space == PQ_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice,
-                                           c->stream),
-                           "gather b");
-            db = g;
+            db = gather_cols(*c, b_list, nb, N, space, "hin_b");
         }
     } else {
         db = stage_in(*c, bs, static_cast<size_t>(nb) * N, space, "hin_b");

@@ -115,13 +115,15 @@ def test_two_host_callers_concurrently_match_sequential(pq):
         ctx.close()
 
 
-@pytest.mark.parametrize("n", [32, 64])
+@pytest.mark.parametrize("n", [32, 64, 104])
 @pytest.mark.parametrize("space", ["host", "device"])
 def test_phiquadmv_cols_equals_contiguous(pq, space, n):
     """pq_phiquadmv_cols (the drop-in headers' entry: each RHS and each result column at its own
     address) returns bitwise what pq_phiquadmv returns in one contiguous buffer, nb = 2.  n = 32
     (262 k doubles of results) takes the direct-copy branch, n = 64 (2 M doubles >= the 8 MB bounce
-    threshold) the pinned bounce with the early drain and the final scatter (capi.cpp)."""
+    threshold) the pinned bounce with the early drain and the final scatter (capi.cpp); n = 104
+    (2 x 1.1 M doubles of right-hand sides) also the gathered input bounce (gather_cols), and the
+    contiguous call the pageable input bounce (stage_in)."""
     import torch
     from paper_2211_00696_b200.workloads import config
     w = config(2, n=n)
