@@ -243,6 +243,11 @@ int main(int argc, char** argv) {
         T(32, 256, 16, 32, 32, 2, 2)
         T(32, 256, 16, 32, 64, 2, 2)
         T(32, 128, 16, 32, 64, 2, 4)
+        T(32, 128, 16, 32, 16, 2, 3)
+        T(32, 128, 16, 32, 16, 2, 2)
+        T(32, 128, 16, 32, 16, 3, 2)
+        T(32, 128, 8, 32, 16, 3, 3)
+        T(32, 128, 16, 16, 32, 2, 3)
 #define TT(BM, BN, BK, WM, WN, ST, MINB)                                                               \
     {                                                                                                  \
         float ms = run_tma<BM, BN, BK, WM, WN, ST, MINB>(c, 5, e0, e1, YREF, N * Z);                   \
@@ -268,6 +273,9 @@ int main(int argc, char** argv) {
         T(64, 32, 16, 32, 16, 2, 8)
         T(64, 32, 16, 32, 16, 3, 5)
         T(64, 32, 16, 32, 16, 3, 6)
+        T(64, 32, 16, 16, 16, 2, 4)
+        T(64, 32, 16, 16, 16, 2, 3)
+        T(64, 32, 16, 32, 8, 2, 4)
         TW(64, 32, 16, 32, 16, 2, 4)
         TW(64, 32, 16, 32, 16, 3, 4)
         TW(64, 32, 16, 32, 16, 4, 4)
