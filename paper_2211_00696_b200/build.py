@@ -23,7 +23,7 @@ CLI = PKG / "phiquad_cli"  # the reference CLI's wire format on this engine (cli
 CUDA = Path(os.environ.get("CUDA_HOME", "/usr/local/cuda"))
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU_SOURCES = ["gemm_nk.cu", "gemm_kk.cu", "kernels.cu"]
+CU_SOURCES = ["gemm_nk.cu", "gemm_kk.cu", "slab12.cu", "kernels.cu"]
 CPP_SOURCES = ["estimator.cpp", "engine.cpp", "etd.cpp", "capi.cpp", "dist.cpp"]
 
 

@@ -285,6 +285,46 @@ int gemm(pq_ctx& c, const GemmArgs& g) {
     return k;
 }
 
+// Fused mode-1+2 launch (slab12.cu), profiled like gemm(): one event pair, executed-flop counter,
+// dense-equivalent flops of the two mode products it replaces.
+int slab12(pq_ctx& c, const Slab12Args& g, const char* tag) {
+    if (!c.profiling) {
+        const int k = launch_slab12(g, c.stream);
+        count_launch(c, k);
+        return k;
+    }
+    if (c.ev_used + 2 > 4096) prof_collect(c);
+    if (!c.d_flops) cuda_check(cudaMalloc(&c.d_flops, sizeof(unsigned long long) * 2048), "flop counters");
+    const size_t slot = c.ev_used / 2;
+    if (slot == 0)
+        cuda_check(cudaMemsetAsync(c.d_flops, 0, sizeof(unsigned long long) * 2048, c.stream), "flop counters zero");
+    Slab12Args gp = g;
+    gp.flop_counter = c.d_flops + slot;
+    cudaEvent_t a = prof_event(c), b = prof_event(c);
+    cuda_check(cudaEventRecord(a, c.stream), "event record");
+    const int k = launch_slab12(gp, c.stream);
+    cuda_check(cudaEventRecord(b, c.stream), "event record");
+    count_launch(c, k);
+    const double slabs = static_cast<double>(g.n0) * g.Z1;
+    c.ev_flops.push_back(2.0 * 2.0 * 128.0 * 128.0 * 128.0 * slabs);
+    char key[160];
+    std::snprintf(key, sizeof key, "%s M128 N128 K128 Z%lld slab12%s", tag ? tag : "?",
+                  static_cast<long long>(g.n0) * g.Z1, g.band1 || g.band2 ? " band" : "");
+    c.ev_keys.push_back(key);
+    c.prof_launches += static_cast<uint64_t>(k);
+    return k;
+}
+
+// PQ_SLAB12=0 runs modes 1 and 2 of 3-D applies as two band-tile launches (A/B switch; the fused
+// kernel is bitwise the same)
+static bool slab12_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PQ_SLAB12");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 constexpr int kMaxChainLevels = 12;  // kernels.hpp launch_gemm_chain (gemm.cuh kMaxChain)
 
 // PQ_GEMM_CHAIN=1: chained cooperative launches for the Taylor powers and the expm squaring
@@ -1264,12 +1304,46 @@ void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const lo
                 const int2* const* band, const std::function<void()>& before_last) {
     long long N = 1;
     for (int k = 0; k < d; ++k) N *= n[k];
+    // modes 1 and 2 of a 3-D apply in one kernel (slab12.cu) when the last mode's epilogue is a
+    // plain store and the operands are 16-byte aligned
+    const bool fuse12 = d == 3 && slab12_enabled() && slab12_supported(n[1], n[2]) && !ep.alpha_z && !ep.ext &&
+                        !ep.coef && !ep.nterms && !ep.accumulate && E_stride[1] % 2 == 0 && E_stride[2] % 2 == 0 &&
+                        y_stride % 2 == 0 && (reinterpret_cast<uintptr_t>(y) & 15) == 0 &&
+                        (reinterpret_cast<uintptr_t>(E[1]) & 15) == 0 && (reinterpret_cast<uintptr_t>(E[2]) & 15) == 0;
     double* tmp[2] = {nullptr, nullptr};
     if (d > 1) tmp[0] = ws(c, std::string(tmp_tag) + "A", static_cast<size_t>(Z1) * N);
-    if (d > 2) tmp[1] = ws(c, std::string(tmp_tag) + "B", static_cast<size_t>(Z1) * N);
+    if (d > 2 && !fuse12) tmp[1] = ws(c, std::string(tmp_tag) + "B", static_cast<size_t>(Z1) * N);
     const double* src = x;
     long long sstride = x_stride;
     for (int k = 0; k < d; ++k) {
+        if (fuse12 && k == 1) {
+            Slab12Args sg;
+            for (int m = 1; m <= 2; ++m) {
+                const long long nn = static_cast<long long>(n[m]) * n[m];
+                const int2* bt = band && band[m] && E_stride[m] % nn == 0 ? band[m] : nullptr;
+                const long long bs = bt ? (E_stride[m] / nn) * band_row_blocks(n[m]) : 0;
+                if (m == 1) {
+                    sg.E1 = E[1];
+                    sg.sE1 = E_stride[1];
+                    sg.band1 = bt;
+                    sg.sband1 = bs;
+                } else {
+                    sg.E2 = E[2];
+                    sg.sE2 = E_stride[2];
+                    sg.band2 = bt;
+                    sg.sband2 = bs;
+                }
+            }
+            sg.X = src;
+            sg.sX = sstride;
+            sg.Y = y;
+            sg.sY = y_stride;
+            sg.n0 = n[0];
+            sg.Z1 = Z1;
+            if (before_last) before_last();
+            slab12(c, sg, (std::string(tmp_tag) + ":mode12").c_str());
+            break;
+        }
         const bool last = k == d - 1;
         double* dst = last ? y : tmp[k % 2];
         const long long dstride = last ? y_stride : N;

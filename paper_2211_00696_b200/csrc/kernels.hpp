@@ -63,6 +63,29 @@ struct GemmArgs {
     const RemoteMap* remote = nullptr;  // device table: remote-store epilogue (plain stores only)
 };
 int launch_gemm(const GemmArgs& g, cudaStream_t s);  // returns number of kernel launches
+// Fused last two modes of a 3-D apply with n1 = n2 = 128 (slab12.cu): for every x-slab
+// X_s = X[z1][i0] (128 x 128), Y_s = (E1 X_s) E2^T, bitwise the two separate band tiles.
+// Batch entry z1 < Z1 uses E1 + z1*sE1, E2 + z1*sE2, band tables band1 + z1*sband1 (4 int2,
+// null = full K), X + z1*sX, Y + z1*sY; n0 slabs per entry.
+struct Slab12Args {
+    const double* E1 = nullptr;
+    long long sE1 = 0;
+    const double* E2 = nullptr;
+    long long sE2 = 0;
+    const int2* band1 = nullptr;
+    long long sband1 = 0;
+    const int2* band2 = nullptr;
+    long long sband2 = 0;
+    const double* X = nullptr;
+    long long sX = 0;
+    double* Y = nullptr;
+    long long sY = 0;
+    int n0 = 1, Z1 = 1;
+    long long z_off = 0;
+    unsigned long long* flop_counter = nullptr;
+};
+bool slab12_supported(int n1, int n2);
+int launch_slab12(const Slab12Args& g, cudaStream_t s);  // returns number of kernel launches
 // `count` dependent batched GEMM levels (plain products, row-major B, 16-byte aligned) in ONE
 // cooperative launch with a grid barrier between levels; bar = one device unsigned (zeroed by
 // the launcher).  Returns 1, or 0 when the chain does not qualify (the caller launches per level).

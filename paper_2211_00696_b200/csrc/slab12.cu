@@ -1,0 +1,206 @@
+// Fused last-two-mode product of a 3-D Kronecker apply for n1 = n2 = 128 (config 2's and config
+// 4's operators): per x-slab X_s = X[i0, :, :] (128 x 128, contiguous),
+//     Y_s = (E1 X_s) E2^T          -- mode 1 then mode 2, kron.hpp:65-87 applied twice,
+// in ONE kernel.  The mode-1 intermediate never goes to HBM: a CTA owns a 32-row quarter of a
+// slab, computes its 32 x 128 block of T = E1 X_s (the 32x128x16 band tile of gemm.cuh, operands
+// streamed by cp.async), keeps it in shared memory and multiplies it by E2^T (each warp one
+// 32-column block, its E2 fragments read straight from L1/L2 with a one-step register prefetch).
+// Per squaring step and column this saves one HBM write + read of the whole vector and one launch
+// with its partial last wave.
+//
+// Bitwise contract: every output element is accumulated over exactly the k4 steps, in the same
+// ascending order and DMMA grouping, that the two separate band tiles execute (mode 1: the 16-wide
+// k-slices of E1's 32-row block rq; mode 2: those of E2's 32-row block = the output column block),
+// so the fused result equals the unfused chain bit for bit (tests/test_gpu_slab12.py).
+#include "gemm.cuh"
+
+namespace pqb {
+
+namespace {
+constexpr int S_N = 128;                       // n1 = n2
+constexpr int S_BK = 16, S_ST = 2;             // k-slice width and cp.async stages of the mode-1 phase
+constexpr int S_SA = S_BK + 4;                 // padded row strides (conflict-free fragment reads)
+constexpr int S_SB = S_N + 4;
+constexpr int S_ASZ = 32 * S_SA, S_BSZ = S_BK * S_SB;
+constexpr int S_SMEM = S_ST * (S_ASZ + S_BSZ) * 8;  // 44 KB -> 4 CTAs (16 warps) per SM
+static_assert(32 * S_N * 8 <= S_SMEM, "the mode-1 block T aliases the pipeline buffers");
+
+// 16-slice range [lo, hi) of a band entry exactly as gemm_tile derives it for a one-block tile
+__device__ __forceinline__ void slice_range(const int2* band, long long idx, int& lo, int& hi) {
+    lo = 0;
+    hi = S_N / S_BK;
+    if (!band) return;
+    const int2 v = band[idx];
+    if (v.y > v.x) {
+        lo = v.x >> 1;
+        hi = min(hi, (v.y + 1) >> 1);
+    } else {
+        lo = hi = 0;
+    }
+}
+}  // namespace
+
+__global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
+    extern __shared__ __align__(16) double smem[];
+    const int rq = blockIdx.x;
+    const long long z = static_cast<long long>(blockIdx.y) + g.z_off;
+    const int z1 = static_cast<int>(z / g.n0);
+    const long long i0 = z - static_cast<long long>(z1) * g.n0;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int gid = lane >> 2, tig = lane & 3;
+
+    const double* __restrict__ E1 = g.E1 + z1 * g.sE1;
+    const double* __restrict__ E2 = g.E2 + z1 * g.sE2;
+    const double* __restrict__ X = g.X + z1 * g.sX + i0 * (S_N * S_N);
+    double* Y = g.Y + z1 * g.sY + i0 * (S_N * S_N) + rq * 32 * S_N;
+
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+
+    int lo1, hi1;
+    slice_range(g.band1, z1 * g.sband1 + rq, lo1, hi1);
+    const int NKT = hi1 > lo1 ? hi1 - lo1 : 0;
+
+    // ---- phase 1: T = E1[rq block] X_s  (32 x 128), cp.async 2-stage pipeline ----
+    double* sA = smem;
+    double* sB = smem + S_ST * S_ASZ;
+    const unsigned sA_base = static_cast<unsigned>(__cvta_generic_to_shared(sA));
+    const unsigned sB_base = static_cast<unsigned>(__cvta_generic_to_shared(sB));
+    // A: 32 rows x 8 chunks -> 2 per thread (rows r, r + 16); B: 16 rows x 64 chunks -> 8 per thread
+    const int ar = tid >> 3, ak = (tid & 7) * 2;
+    const double* a_p = E1 + (rq * 32 + ar) * S_N + lo1 * S_BK + ak;
+    const unsigned a_dst = sA_base + 8u * (ar * S_SA + ak);
+    const int br = tid >> 6, bn = (tid & 63) * 2;
+    const double* b_p = X + static_cast<long long>(lo1 * S_BK + br) * S_N + bn;
+    const unsigned b_dst = sB_base + 8u * (br * S_SB + bn);
+    auto load = [&](int stage) {
+#pragma unroll
+        for (int it = 0; it < 2; ++it) cp_async<2>(a_dst + 8u * (stage * S_ASZ + it * 16 * S_SA), a_p + it * 16 * S_N, true);
+#pragma unroll
+        for (int it = 0; it < 8; ++it) cp_async<2>(b_dst + 8u * (stage * S_BSZ + it * 2 * S_SB), b_p + it * 2 * S_N, true);
+        a_p += S_BK;
+        b_p += S_BK * S_N;
+    };
+
+    double acc[4][4][2];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+    if (NKT > 0) load(0);
+    cp_commit();
+    const double* tA0 = sA + gid * S_SA + tig;
+    const double* tB0 = sB + tig * S_SB + warp * 32 + gid;
+#pragma unroll 1
+    for (int kt = 0; kt < NKT; ++kt) {
+        cp_wait<0>();
+        __syncthreads();
+        if (kt + 1 < NKT) load((kt + 1) & 1);
+        cp_commit();
+        const double* tA = tA0 + (kt & 1) * S_ASZ;
+        const double* tB = tB0 + (kt & 1) * S_BSZ;
+#pragma unroll
+        for (int kk = 0; kk < S_BK; kk += 4) {
+            double a[4], b[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = tA[i * 8 * S_SA + kk];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) b[j] = tB[kk * S_SB + j * 8];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+        }
+    }
+    cp_wait<0>();
+    __syncthreads();  // every warp is done with the stage buffers: T overwrites them
+
+    // T[r][c] at r*128 + (c ^ ((r & 3) << 2)): the phase-2 A-fragment reads (rows gid, 4
+    // consecutive k) then hit 16 distinct bank pairs per half-warp; pairs (c, c+1) stay adjacent.
+    double* T = smem;
+    const int swz = (gid & 3) << 2;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int r = i * 8 + gid, c = warp * 32 + j * 8 + 2 * tig;
+            *reinterpret_cast<double2*>(T + r * S_N + (c ^ swz)) = make_double2(acc[i][j][0], acc[i][j][1]);
+            acc[i][j][0] = acc[i][j][1] = 0.0;
+        }
+    __syncthreads();
+
+    // ---- phase 2: Y[rq block, warp block] = T E2[warp block]^T, k over E2's block band ----
+    int lo2, hi2;
+    slice_range(g.band2, z1 * g.sband2 + warp, lo2, hi2);
+    const int kb = lo2 * S_BK, ke = hi2 > lo2 ? hi2 * S_BK : kb;
+    const double* e2 = E2 + (warp * 32 + gid) * S_N + tig;
+    const double* tr = T + gid * S_N;
+    double bn_[4];
+    if (ke > kb) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) bn_[j] = __ldg(e2 + j * 8 * S_N + kb);
+    }
+#pragma unroll 2
+    for (int k = kb; k < ke; k += 4) {
+        double b[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) b[j] = bn_[j];
+        if (k + 4 < ke) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bn_[j] = __ldg(e2 + j * 8 * S_N + k + 4);
+        }
+        const int kc = (k + tig) ^ swz;
+        double a[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) a[i] = tr[i * 8 * S_N + kc];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+    }
+    asm volatile("griddepcontrol.launch_dependents;");
+
+    if (g.flop_counter) {
+        unsigned long long f = 2ull * 32 * 32 * (ke - kb);
+        if (warp == 0) f += 2ull * 32 * S_N * (NKT * S_BK);
+        if (lane == 0) atomicAdd(g.flop_counter, f);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        double* row = Y + (i * 8 + gid) * S_N + warp * 32 + 2 * tig;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) *reinterpret_cast<double2*>(row + j * 8) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+bool slab12_supported(int n1, int n2) { return n1 == S_N && n2 == S_N; }
+
+int launch_slab12(const Slab12Args& g0, cudaStream_t s) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaFuncSetAttribute(k_slab12, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
+        attr_done = true;
+    }
+    const long long total = static_cast<long long>(g0.n0) * g0.Z1;
+    int launches = 0;
+    Slab12Args g = g0;
+    for (long long z0 = 0; z0 < total; z0 += 65535) {
+        g.z_off = z0;
+        const long long zc = total - z0 < 65535 ? total - z0 : 65535;
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(S_N / 32, static_cast<unsigned>(zc), 1);
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = S_SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, k_slab12, g);
+        ++launches;
+    }
+    return launches;
+}
+
+}  // namespace pqb
