@@ -292,6 +292,11 @@ int pq_ctx_destroy(pq_ctx* c) {
             cudaStreamDestroy(c->sq2);
             cudaEventDestroy(c->ev_sqfork);
         }
+        if (c->ccs) {
+            cudaStreamSynchronize(c->ccs);
+            cudaStreamDestroy(c->ccs);
+        }
+        if (c->ev_ccfork) cudaEventDestroy(c->ev_ccfork);
         for (auto s : c->sqs) {
             cudaStreamSynchronize(s);
             cudaStreamDestroy(s);
@@ -337,7 +342,7 @@ int pq_ctx_set_stream(pq_ctx* c, void* stream) {
             cudaStreamDestroy(s);
         }
         c->sqs.clear();
-        for (cudaStream_t* h : {&c->side, &c->sq2}) {
+        for (cudaStream_t* h : {&c->side, &c->sq2, &c->ccs}) {
             if (*h) {
                 cuda_check(cudaStreamSynchronize(*h), "sync helper stream");
                 cudaStreamDestroy(*h);

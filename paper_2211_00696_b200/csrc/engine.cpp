@@ -736,9 +736,52 @@ static void ensure_sq2(pq_ctx& c) {
     }
 }
 
+static void ensure_ccs(pq_ctx& c) {
+    if (c.ccs) return;
+    int prio = 0, least = 0, greatest = 0;
+    if (cudaStreamGetPriority(c.stream, &prio) != cudaSuccess || cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) {
+        cudaGetLastError();
+        prio = greatest = 0;
+    }
+    cuda_check(cudaStreamCreateWithPriority(&c.ccs, cudaStreamNonBlocking, std::max(greatest, prio - 1)), "cc stream");
+    if (!c.ev_ccfork) cuda_check(cudaEventCreateWithFlags(&c.ev_ccfork, cudaEventDisableTiming), "cc fork event");
+}
+
+// PQ_CC_DEFER=0: the host checks every CC level's error before it enqueues anything that depends
+// on the result (the pre-deferral schedule; results are the same either way)
+static bool cc_defer_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PQ_CC_DEFER");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
+// The side stream (late exponentials, phi_0) runs one priority step above the main stream, so its
+// short dependent launches are not queued behind the node sweep's CTA waves (config 2: 476.7 ->
+// 478.5 actions/s); PQ_SIDE_PRIO=0 gives it the main stream's priority.
+static bool side_prio_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("PQ_SIDE_PRIO");
+        return !(v && v[0] == '0');
+    }();
+    return on;
+}
+
 void ensure_side(pq_ctx& c) {
     if (c.side) return;
-    make_helper_stream(c, &c.side, "side stream");
+    if (side_prio_enabled()) {
+        int prio = 0, least = 0, greatest = 0;
+        if (cudaStreamGetPriority(c.stream, &prio) != cudaSuccess ||
+            cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) {
+            cudaGetLastError();
+            prio = greatest = 0;
+        }
+        cuda_check(cudaStreamCreateWithPriority(&c.side, cudaStreamNonBlocking, std::max(greatest, prio - 1)),
+                   "side stream");
+    } else {
+        make_helper_stream(c, &c.side, "side stream");
+    }
     if (!c.ev_fork) cuda_check(cudaEventCreateWithFlags(&c.ev_fork, cudaEventDisableTiming), "fork event");
     if (!c.ev_join) cuda_check(cudaEventCreateWithFlags(&c.ev_join, cudaEventDisableTiming), "join event");
 }
@@ -1618,8 +1661,37 @@ void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, con
 // take their exponentials from `px25` (the 25-point rule's nodes, exponentiated in the call's
 // single expm batch: CC nodes nest bitwise, so 7-rule node i is 25-rule node 4i); deeper levels
 // exponentiate their fresh nodes on demand.
+// A CC ladder whose convergence checks were deferred (phi_adaptive_shift with `pend`): the error
+// statistics of levels 1..levels sit in c.h_small at stride 2*nb*p, complete once c.ev_cc fires.
+// The speculation holds when every level but the last failed the test and the last passed it --
+// exactly the levels the reference evaluates (phiaction.hpp:175-240).
+struct CcPending {
+    bool active = false;
+    int levels = 0, nb = 0, p = 0;
+    double eps = 0.0;
+};
+
+static bool cc_pending_holds(pq_ctx& c, const CcPending& pd) {
+    cuda_check(cudaEventSynchronize(c.ev_cc), "cc stats wait");
+    mark(c, "cc_deferred_synced");
+    const int w = 2 * pd.nb * pd.p;
+    for (int lv = 0; lv < pd.levels; ++lv) {
+        const volatile double* hs = c.h_small + static_cast<size_t>(lv) * w;
+        double err = 0.0;
+        for (int k = 0; k < pd.nb * pd.p; ++k) {
+            const double diff = hs[2 * k], norm = hs[2 * k + 1];
+            if (diff == 0.0) continue;
+            err = std::max(err, norm == 0.0 ? std::numeric_limits<double>::infinity() : diff / norm);
+        }
+        const bool conv = err <= pd.eps;
+        if (conv != (lv == pd.levels - 1)) return false;
+    }
+    return true;
+}
+
 static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int nb, const double* bs, int p,
-                               double eps, const PhiExps& px25, double* out, int* points_used, int spec_points) {
+                               double eps, const PhiExps& px25, double* out, int* points_used, int spec_points,
+                               CcPending* pend = nullptr) {
     if (p < 1) throw std::invalid_argument("phi_adaptive: need p >= 1");
     if (!(eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
     const long long N = op.N;
@@ -1716,6 +1788,18 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
     };
     if (!c.ev_cc) cuda_check(cudaEventCreateWithFlags(&c.ev_cc, cudaEventDisableTiming), "cc event");
     const bool pinned_stats = 2 * nb * p <= 1024;
+    // Deferred checks: when the planner predicts the converging level (spec_points), every level up
+    // to it is enqueued without a host round trip -- each level's statistics go to their own slot of
+    // the mapped readback -- and the caller enqueues the squaring and phi_0 before it checks them
+    // (cc_pending_holds); a wrong prediction re-runs the call with the checks inline.
+    int spec_levels = 0;
+    if (spec_points > 0)
+        for (int pts = 13;; pts = 2 * pts - 1) {
+            ++spec_levels;
+            if (pts >= spec_points) break;
+        }
+    const bool defer = pend && cc_defer_enabled() && spec_points > 0 && 2 * nb * p * spec_levels <= 1024;
+    int dlev = 0;
     // a level whose combination runs on c.sq2 (while the speculative sweep of the next level runs
     // on the main stream): the main stream joins on ev_cc before it reads that level's sums
     bool join_pending = false;
@@ -1747,10 +1831,10 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         }
         const bool offload = fused && will_spec && !c.profiling;
         if (offload) {
-            ensure_sq2(c);
-            cuda_check(cudaEventRecord(c.ev_sqfork, main_stream), "cc fork");
-            cuda_check(cudaStreamWaitEvent(c.sq2, c.ev_sqfork, 0), "cc fork wait");
-            c.stream = c.sq2;
+            ensure_ccs(c);
+            cuda_check(cudaEventRecord(c.ev_ccfork, main_stream), "cc fork");
+            cuda_check(cudaStreamWaitEvent(c.ccs, c.ev_ccfork, 0), "cc fork wait");
+            c.stream = c.ccs;
         }
         // phiaction.hpp:225-240: max over columns of ||y - y_prev||_inf / ||y||_inf
         if (fused) {
@@ -1792,7 +1876,8 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         rule = &fine;
         slot_of = std::move(fine_slot);
         if (pinned_stats) {  // mapped: stored by a kernel, no copy engine
-            launch_store_words(stats, c.h_small_d, hstats.size(), c.stream);
+            launch_store_words(stats, c.h_small_d + (defer ? static_cast<size_t>(dlev) * hstats.size() : 0),
+                               hstats.size(), c.stream);
             count_launch(c);
         } else {
             cuda_check(cudaMemcpyAsync(hstats.data(), stats, hstats.size() * sizeof(double), cudaMemcpyDeviceToHost,
@@ -1809,6 +1894,17 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
         // spec_points nodes), its node sweep is enqueued before the host waits for this level's
         // error, so the GPU never drains at the check (a wasted sweep if this level converges).
         if (will_spec) sweep_level(level + 1, memo_rule(kClenshaw, next_points));
+        if (defer) {
+            ++dlev;
+            cur = nxt;
+            if (fine.size() < spec_points) continue;
+            pend->active = true;
+            pend->levels = dlev;
+            pend->nb = nb;
+            pend->p = p;
+            pend->eps = eps;
+            break;
+        }
         cuda_check(cudaEventSynchronize(c.ev_cc), "cc stats wait");
         mark(c, "cc_level_synced");
         cur = nxt;
@@ -2115,10 +2211,12 @@ void squaring_steps_dev(pq_ctx& c, const DevOp& op, double scale, int nb, int p,
 // phiaction.hpp:277-303, plus (when phi0_out) kron.hpp:123-128 phi_0 from the same expm batch.
 static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const double* bs, int p, int l, int n,
                          int kind, double eps, double* out, int* points_used, double* phi0_out,
-                         double* phi0_host = nullptr, double* out_host = nullptr, bool* out_copied = nullptr) {
+                         double* phi0_host = nullptr, double* out_host = nullptr, bool* out_copied = nullptr,
+                         bool allow_defer = true) {
     if (l < 0) throw std::invalid_argument("phi_with_plan: need l >= 0");
     if (p < 1) throw std::invalid_argument(kind == kGauss ? "phi_fixed: need p >= 1" : "phi_adaptive: need p >= 1");
     const NodesWeights& rule = kind == kGauss ? memo_rule(kGauss, n + 1) : memo_rule(kClenshaw, 25);
+    CcPending pend;
     // squaring chain and phi_0 exponentials are finished on the side stream during the node sweep
     // (not while profiling, so per-launch events stay unambiguous)
     const PhiExps px = phi_exponentials(c, op, scale, l, rule.x, l > 0, phi0_out != nullptr, "nodeE", true,
@@ -2141,7 +2239,7 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
             spec = 13;
             while (spec < n + 1 && spec < (1 << 15)) spec = 2 * spec - 1;
         }
-        phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, px, first, points_used, spec);
+        phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, px, first, points_used, spec, allow_defer ? &pend : nullptr);
     }
     mark(c, "nodes");
     // phi_0 needs only its exponentials and b: run its mode chain on the side stream alongside the
@@ -2186,6 +2284,23 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
         if (phi0_host)
             cuda_check(cudaMemcpyAsync(phi0_host, phi0_out, sizeof(double) * nb * op.N, cudaMemcpyDeviceToHost, c.stream),
                        "phi_0 D2H");
+    }
+    if (pend.active) {
+        // the ladder's deferred checks: everything above is enqueued, so the GPU keeps running
+        // while the host reads the levels' statistics
+        if (cc_pending_holds(c, pend)) {
+            ++c.cc_defer_hits;
+        } else {
+            ++c.cc_defer_misses;
+            // drain this run (its early host copies included) before the re-run writes the same buffers
+            for (cudaStream_t st : {c.stream, c.side, c.sq2, c.ccs})
+                if (st) cuda_check(cudaStreamSynchronize(st), "cc re-run drain");
+            for (cudaStream_t st : c.sqs) cuda_check(cudaStreamSynchronize(st), "cc re-run drain");
+            c.early.clear();  // this run's early host copies are superseded
+            if (out_copied) *out_copied = false;
+            phi_call_dev(c, op, scale, nb, bs, p, l, n, kind, eps, out, points_used, phi0_out, phi0_host, out_host,
+                         out_copied, false);
+        }
     }
 }
 
@@ -2363,6 +2478,7 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
         // waits for beta and plans; the GPU never idles for the host planner
         const int sl = memo->l, sn = memo->n;
         beta_enqueue(c, op, nb, bs);
+        mark(c, "beta_enqueued");
         const double alpha = alpha_of(op);
         const int d = op.d;
         worker_submit(c, [&c, &pi, nb, d, alpha, p, eps, mode, has_l, l, c1, c2] {

@@ -90,6 +90,10 @@ struct pq_ctx {
     std::vector<std::function<void()>> deferred;
     // two-stream squaring (engine.cpp squaring_pingpong): second stream, fork event, per-step events
     cudaStream_t sq2 = nullptr;
+    // a CC ladder level's combination offloaded under the next level's node sweep: one priority
+    // step above the main stream, so its (HBM-bound) CTAs interleave with the sweep's DMMA tiles
+    cudaStream_t ccs = nullptr;
+    cudaEvent_t ev_ccfork = nullptr;
     // per-column squaring streams when the results go to pinned host memory (descending priority:
     // column 1 runs ahead and its D2H overlaps the later columns) and their per-(group, step) events
     std::vector<cudaStream_t> sqs;
@@ -124,6 +128,8 @@ struct pq_ctx {
     };
     std::vector<PlanMemo> plan_memo;
     uint64_t plan_spec_hits = 0, plan_spec_misses = 0;
+    // deferred CC convergence checks (engine.cpp phi_call_dev): confirmed / re-run calls
+    uint64_t cc_defer_hits = 0, cc_defer_misses = 0;
     struct Worker {
         std::thread th;
         std::mutex mu;

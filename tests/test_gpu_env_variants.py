@@ -1,6 +1,7 @@
 """The engine's optional runtime switches change scheduling only, never results: with the compute
 gate on (PQ_COMPUTE_GATE=1), the squaring combination fused into the mode-product epilogue
-(PQ_SQ_FUSE=1) or plan speculation off (PQ_PLAN_SPEC=0), three concurrent host callers get
+(PQ_SQ_FUSE=1), plan speculation off (PQ_PLAN_SPEC=0), inline CC
+convergence checks (PQ_CC_DEFER=0) or separate mode-1/mode-2 launches (PQ_SLAB12=0), three concurrent host callers get
 bitwise the results of the same calls made one at a time, and bitwise the default build's."""
 import os
 import subprocess
@@ -27,7 +28,8 @@ def _run(tmp_path, name, env_extra):
 def test_runtime_switches_keep_results_bitwise(tmp_path):
     base = _run(tmp_path, "default", {})
     for name, extra in [("gate", {"PQ_COMPUTE_GATE": "1"}), ("fuse", {"PQ_SQ_FUSE": "1"}),
-                        ("nospec", {"PQ_PLAN_SPEC": "0"}), ("gate_fuse", {"PQ_COMPUTE_GATE": "1", "PQ_SQ_FUSE": "1"})]:
+                        ("nospec", {"PQ_PLAN_SPEC": "0"}), ("nodefer", {"PQ_CC_DEFER": "0"}),
+                        ("sep12", {"PQ_SLAB12": "0"}), ("noprio", {"PQ_SIDE_PRIO": "0"}), ("gate_fuse", {"PQ_COMPUTE_GATE": "1", "PQ_SQ_FUSE": "1"})]:
         got = _run(tmp_path, name, extra)
         for k in base.files:
             assert np.array_equal(got[k], base[k]), f"{name}: {k} differs from the default build"

@@ -1,7 +1,8 @@
 """Device timeline of phi_0..phi_p calls from CUPTI (torch.profiler's kineto collects every kernel
 and memcpy of the process, the engine's own kernels included): span per call, busy time (union
 of kernel intervals over all streams), the largest idle gaps and the kernels around them.
-Usage: python tools/timeline.py [config] [calls] [--host]   (--host: pinned host buffers, PQ_HOST)"""
+Usage: python tools/timeline.py [config] [calls] [--host] [--dump=file.csv]   (--host: pinned host buffers,
+PQ_HOST; --dump: every op of the last call, start offset / duration / stream)"""
 import ctypes as C
 import json
 import sys
@@ -97,3 +98,11 @@ top = sorted(names.items(), key=lambda kv: -kv[1])[:12]
 print("last call, device time by op (summed over streams):")
 for n, t in top:
     print(f"   {t:8.1f} us  {n[:100]}")
+dump = [a for a in sys.argv if a.startswith("--dump=")]
+if dump:
+    g = groups[-1]
+    t0 = g[0][0]
+    with open(dump[0].split("=", 1)[1], "w") as f:
+        f.write("start_us,dur_us,stream,name\n")
+        for s, e, n, strm in g:
+            f.write(f"{s - t0:.1f},{e - s:.1f},{strm},\"{n[:90]}\"\n")
