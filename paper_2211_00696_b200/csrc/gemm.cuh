@@ -39,6 +39,30 @@ __device__ __forceinline__ void cp_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Fine-gated DMMAs: only the fragment rows (ROWS) or columns whose bit is set in MASK.  Dispatched
+// through a switch on the run-time mask (dmma_gated), so skipped DMMAs are not issued at all -- a
+// plain `if` is if-converted into predicated DMMAs, which still occupy the tensor pipe.
+template <int MI, int NI, bool ROWS, int MASK>
+__device__ __forceinline__ void dmma_masked(double (&acc)[MI][NI][2], const double (&a)[MI], const double (&b)[NI]) {
+#pragma unroll
+    for (int i = 0; i < MI; ++i)
+#pragma unroll
+        for (int j = 0; j < NI; ++j)
+            if ((MASK >> (ROWS ? i : j)) & 1) dmma_8x8x4(acc[i][j], a[i], b[j]);
+}
+template <int MI, int NI, bool ROWS, int M = 1>
+__device__ __forceinline__ void dmma_gated(unsigned mask, double (&acc)[MI][NI][2], const double (&a)[MI],
+                                           const double (&b)[NI]) {
+    constexpr int FG = ROWS ? MI : NI;
+    static_assert(FG <= 4, "fine gating over at most 4 fragment groups");
+    if constexpr (M < (1 << FG)) {
+        if (mask == static_cast<unsigned>(M))
+            dmma_masked<MI, NI, ROWS, M>(acc, a, b);
+        else
+            dmma_gated<MI, NI, ROWS, M + 1>(mask, acc, a, b);
+    }
+}
+
 // destination row of the remote-store epilogue (kernels.hpp RemoteMap)
 __device__ __forceinline__ double* remote_row(const RemoteMap& rm, int z1, int m) {
     if (rm.mode == 1) {
@@ -237,6 +261,16 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int bx, int by, int
 
     int kt_lo = 0, KT = (g.K + BK - 1) / BK;
     int w_lo = 0, w_hi = KT;  // this warp's DMMA slices (absolute)
+    // Fine gating: per 8-row group of the exponential covered by this warp's fragments (rows i for
+    // an A exponential, columns j for a k-major B exponential), the k4 steps [lo, lo + len) its DMMAs
+    // issue, packed lo | len << 16 (kernels.hpp launch_band_ranges).  Default: every step.
+    constexpr int FG = BKM ? T::NI : T::MI;
+    // every tile that can take a band table gates per group (the same executed k4 steps whichever
+    // tile shape a mode product lands on: the fused and separate mode chains agree bitwise)
+    constexpr bool GATE = (BK == 8 || BK == 16) && FG <= 4;
+    unsigned fine[FG];
+#pragma unroll
+    for (int f = 0; f < FG; ++f) fine[f] = 0xffffu << 16;
     if constexpr (BK == 8 || BK == 16) {
         // negligible-block skip: the CTA streams the union of the 32-row exponential blocks its
         // tile covers, each warp multiplies only inside its own block's slices
@@ -278,14 +312,33 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int bx, int by, int
                 w_lo = kt_lo;
                 w_hi = KT;
             }
+#pragma unroll
+            for (int f = 0; f < FG; ++f) {
+                if (!GATE) break;
+                const int grp = (wr >> 3) + f;
+                const int2 v = grp < 4 * nb ? br[nb + grp] : make_int2(0, 0);
+                fine[f] = v.y > v.x ? static_cast<unsigned>(v.x) | (static_cast<unsigned>(v.y - v.x) << 16) : 0u;
+            }
         }
     }
     const int NKT = KT > kt_lo ? KT - kt_lo : 0;
     if (g.flop_counter && lane == 0) {
-        const long long rows = max(0, min(WM, g.M - (m0 + wm * WM))), cols = max(0, min(WN, g.N - (n0 + wn * WN)));
+        // executed DMMA work: per fragment row (column) group, its k4 steps inside the warp's slices
         const int lo = max(kt_lo, w_lo), hi = min(KT, w_hi);
-        const long long kexec = hi > lo ? min(hi * BK, g.K) - lo * BK : 0;
-        atomicAdd(g.flop_counter, static_cast<unsigned long long>(2 * rows * cols * kexec));
+        const int q0 = lo * (BK / 4), q1 = hi > lo ? (min(hi * BK, g.K) + 3) / 4 : q0;
+        unsigned long long f_exec = 0;
+#pragma unroll
+        for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+            for (int j = 0; j < T::NI; ++j) {
+                const unsigned fr = fine[BKM ? j : i];
+                const int flo = static_cast<int>(fr & 0xffffu), fhi = flo + static_cast<int>(fr >> 16);
+                const int steps = max(0, min(q1, fhi) - max(q0, flo));
+                const long long rows = max(0, min(8, g.M - (m0 + wm * WM + i * 8)));
+                const long long cols = max(0, min(8, g.N - (n0 + wn * WN + j * 8)));
+                f_exec += static_cast<unsigned long long>(2 * rows * cols * 4 * steps);
+            }
+        atomicAdd(g.flop_counter, f_exec);
     }
     k_next = kt_lo * BK;
     if constexpr (AFF) {
@@ -325,10 +378,25 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int bx, int by, int
             for (int i = 0; i < T::MI; ++i) a[i] = tA[i * 8 * T::SA + kk];
 #pragma unroll
             for (int j = 0; j < T::NI; ++j) b[j] = BKM ? tB[j * 8 * T::SB + kk] : tB[kk * T::SB + j * 8];
+            if constexpr (GATE) {
+                const unsigned kq = static_cast<unsigned>((kabs * BK + kk) >> 2);
+                unsigned mask = 0;
 #pragma unroll
-            for (int i = 0; i < T::MI; ++i)
+                for (int f = 0; f < FG; ++f) mask |= (kq - (fine[f] & 0xffffu) < (fine[f] >> 16) ? 1u : 0u) << f;
+                if (mask == (1u << FG) - 1u) {
 #pragma unroll
-                for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+                    for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                        for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+                } else {
+                    dmma_gated<T::MI, T::NI, !BKM>(mask, acc, a, b);
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                    for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+            }
         }
     }
     cp_wait<0>();

@@ -581,44 +581,65 @@ __global__ void k_imax(const int* v, int count, int* out) {
 }
 void launch_imax(const int* v, int count, int* out, cudaStream_t s) { k_imax<<<1, 32, 0, s>>>(v, count, out); }
 
-// One CTA per (matrix, 32-row block), one pass over the block's rows: one warp per 8-column
-// slice computes the slice max; the threshold is 2^-64 x the block's own max (a lower bound of the
-// matrix max, so the skip is at least as conservative as the matrix-relative criterion).
+// One CTA per (matrix, 32-row block).  Each thread reduces (8-row group, 4-column chunk) cells of
+// the block to their max |E| (NaN / Inf -> +Inf); from those:
+//  * coarse entry: {first, last+1} of the 8-column slices whose max exceeds 2^-64 x the block's own
+//    max (a lower bound of the matrix max, so at least as conservative as a matrix-relative test);
+//  * fine entries, one per 8-row group: {first, last+1} of the 4-column chunks (DMMA k4 steps)
+//    whose max exceeds 2^-64 x the GROUP's max (<= the block's: again at least as conservative).
+// Record of matrix z: [coarse rb = 0..RB) [fine g = 0..4RB), RB = ceil(n/32) (band_row_blocks).
 __global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __restrict__ E, int2* __restrict__ out) {
-    const int z = blockIdx.x, rb = blockIdx.y;
+    const int z = blockIdx.x, rb = blockIdx.y, RB = gridDim.y;
     const double* e = E + (long long)z * n * n;
-    __shared__ double smax[64];  // slices of this block, n <= 512
-    const int NS = (n + 7) / 8;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int sl = warp; sl < NS; sl += blockDim.x >> 5) {
-        double bm = 0.0;
-        int bad = 0;
-#pragma unroll
-        for (int u = 0; u < 8; ++u) {
-            const int t = lane + 32 * u;
-            const int r = rb * 32 + t / 8, c = sl * 8 + t % 8;
-            if (r < n && c < n) {
+    __shared__ double cmax[4][128];  // [group][chunk], n <= 512
+    __shared__ double gmax[4];
+    const int NC = (n + 3) / 4;
+    const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    for (int cell = threadIdx.x; cell < 4 * NC; cell += blockDim.x) {
+        const int g = cell / NC, ch = cell - g * NC;
+        double m = 0.0;
+        for (int r = rb * 32 + g * 8; r < min(n, rb * 32 + g * 8 + 8); ++r)
+            for (int c = ch * 4; c < min(n, ch * 4 + 4); ++c) {
                 const double v = fabs(__ldg(e + (long long)r * n + c));
-                bad |= !(v <= 1.7976931348623157e308);  // NaN / Inf
-                bm = fmax(bm, v);
+                m = !(v <= 1.7976931348623157e308) ? kInf : fmax(m, v);
             }
-        }
-        for (int o = 16; o > 0; o >>= 1) bm = fmax(bm, __shfl_xor_sync(0xffffffffu, bm, o));
-        bad = __any_sync(0xffffffffu, bad);
-        if (lane == 0) smax[sl] = bad ? __longlong_as_double(0x7ff0000000000000LL) : bm;
+        cmax[g][ch] = m;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
-        double g = 0.0;
-        for (int sl = 0; sl < NS; ++sl) g = fmax(g, smax[sl]);
-        const double thr = ldexp(g, -64);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp < 4) {  // group maxima
+        double m = 0.0;
+        for (int ch = lane; ch < NC; ch += 32) m = fmax(m, cmax[warp][ch]);
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0) gmax[warp] = m;
+    }
+    __syncthreads();
+    int2* rec = out + (long long)z * 5 * RB;
+    if (threadIdx.x < 4) {  // fine entry of group threadIdx.x
+        const int g = threadIdx.x;
+        const double gm = gmax[g], thr = ldexp(gm, -64);
+        int lo = NC, hi = 0;
+        if (rb * 32 + g * 8 < n)
+            for (int ch = 0; ch < NC; ++ch)
+                if (cmax[g][ch] > thr || !(gm <= 1.7976931348623157e308)) {
+                    lo = min(lo, ch);
+                    hi = ch + 1;
+                }
+        rec[RB + rb * 4 + g] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
+    } else if (threadIdx.x == 32) {  // coarse entry
+        const double bm = fmax(fmax(gmax[0], gmax[1]), fmax(gmax[2], gmax[3])), thr = ldexp(bm, -64);
+        const int NS = (n + 7) / 8;
         int lo = NS, hi = 0;
-        for (int sl = 0; sl < NS; ++sl)
-            if (smax[sl] > thr || !(g <= 1.7976931348623157e308)) {
+        for (int sl = 0; sl < NS; ++sl) {
+            double m = 0.0;
+            for (int g = 0; g < 4; ++g)
+                for (int h = 2 * sl; h < min(NC, 2 * sl + 2); ++h) m = fmax(m, cmax[g][h]);
+            if (m > thr || !(bm <= 1.7976931348623157e308)) {
                 lo = min(lo, sl);
                 hi = sl + 1;
             }
-        out[(long long)z * gridDim.y + rb] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
+        }
+        rec[rb] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
     }
 }
 void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s) {

@@ -119,12 +119,17 @@ void launch_lu_solve(int n, int count, double* P, double* Q, int* err, cudaStrea
 // n <= 128: shared-memory factorisation of P (L\U over P, pivots in piv[count*n]) + a batched
 // triangular solve of Q over 32-column slices.  Q <- P^{-1} Q.
 void launch_lu_factor_solve(int n, int count, double* P, double* Q, int* piv, int* err, cudaStream_t s);
-// Per matrix z < count (n x n, stride n*n) and 32-row block rb: out[z*ceil(n/32) + rb] = {first,
-// last+1} of the 8-wide column slices whose max |E| exceeds 2^-64 x the row block's max (<= max|E_z|;
-// NaN/Inf count as needed; an all-zero row block gives an empty range).  Dropping the rest changes
-// a mode product by at most n 2^-64 of its max-norm -- below half an ulp in practice.
+// Per matrix z < count (n x n, stride n*n) a record of band_row_blocks(n) int2 (RB = ceil(n/32)):
+//  rec[rb], rb < RB: {first, last+1} of the 8-wide column slices of 32-row block rb whose max |E|
+//    exceeds 2^-64 x the row block's max (<= max|E_z|; NaN/Inf count as needed; an all-zero row
+//    block gives an empty range) -- the k-slices a tile streams;
+//  rec[RB + g], g < 4 RB: {first, last+1} of the 4-wide column chunks (DMMA k4 steps) of 8-row
+//    group g whose max |E| exceeds 2^-64 x the group's max -- the k4 steps a DMMA row (or column,
+//    for a k-major exponential) fragment issues.
+// Dropping the rest changes a mode product by at most n 2^-64 of its max-norm -- below half an ulp
+// in practice.
 void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s);
-inline int band_row_blocks(int n) { return (n + 31) / 32; }
+inline int band_row_blocks(int n) { return 5 * ((n + 31) / 32); }  // record length (int2)
 // max over z of s_z -> *out (device int)
 void launch_imax(const int* v, int count, int* out, cudaStream_t s);
 

@@ -10,8 +10,9 @@
 //
 // Bitwise contract: every output element is accumulated over exactly the k4 steps, in the same
 // ascending order and DMMA grouping, that the two separate band tiles execute (mode 1: the 16-wide
-// k-slices of E1's 32-row block rq; mode 2: those of E2's 32-row block = the output column block),
-// so the fused result equals the unfused chain bit for bit (tests/test_gpu_slab12.py).
+// k-slices of E1's 32-row block rq, and within them the k4 steps of the element's 8-row group of E1;
+// mode 2: likewise for E2's block / group of the output column), so the fused result equals the
+// unfused chain bit for bit (tests/test_gpu_slab12.py).
 #include "gemm.cuh"
 
 namespace pqb {
@@ -38,6 +39,46 @@ __device__ __forceinline__ void slice_range(const int2* band, long long idx, int
         lo = hi = 0;
     }
 }
+// DMMAs of the fragment rows (ROWS = true) or columns whose bit is set in MASK; dispatched through a
+// switch on the run-time mask so the skipped DMMAs are not issued at all (a plain `if` around them
+// is if-converted into predicated DMMAs, which still occupy the tensor pipe)
+template <int MASK, bool ROWS>
+__device__ __forceinline__ void dmma_masked(double (&acc)[4][4][2], const double (&a)[4], const double (&b)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if ((MASK >> (ROWS ? i : j)) & 1) dmma_8x8x4(acc[i][j], a[i], b[j]);
+}
+template <bool ROWS>
+__device__ __forceinline__ void dmma_switch(unsigned mask, double (&acc)[4][4][2], const double (&a)[4],
+                                            const double (&b)[4]) {
+    switch (mask) {
+        case 1: dmma_masked<1, ROWS>(acc, a, b); break;
+        case 2: dmma_masked<2, ROWS>(acc, a, b); break;
+        case 3: dmma_masked<3, ROWS>(acc, a, b); break;
+        case 4: dmma_masked<4, ROWS>(acc, a, b); break;
+        case 5: dmma_masked<5, ROWS>(acc, a, b); break;
+        case 6: dmma_masked<6, ROWS>(acc, a, b); break;
+        case 7: dmma_masked<7, ROWS>(acc, a, b); break;
+        case 8: dmma_masked<8, ROWS>(acc, a, b); break;
+        case 9: dmma_masked<9, ROWS>(acc, a, b); break;
+        case 10: dmma_masked<10, ROWS>(acc, a, b); break;
+        case 11: dmma_masked<11, ROWS>(acc, a, b); break;
+        case 12: dmma_masked<12, ROWS>(acc, a, b); break;
+        case 13: dmma_masked<13, ROWS>(acc, a, b); break;
+        case 14: dmma_masked<14, ROWS>(acc, a, b); break;
+        case 15: dmma_masked<15, ROWS>(acc, a, b); break;
+        default: break;
+    }
+}
+
+// fine gating of 8-row group `grp` (kernels.hpp launch_band_ranges): k4 steps lo | len << 16
+__device__ __forceinline__ unsigned fine_range(const int2* band, long long rec, int grp) {
+    if (!band) return 0xffffu << 16;
+    const int2 v = band[rec + S_N / 32 + grp];
+    return v.y > v.x ? static_cast<unsigned>(v.x) | (static_cast<unsigned>(v.y - v.x) << 16) : 0u;
+}
 }  // namespace
 
 __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
@@ -59,6 +100,9 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
     int lo1, hi1;
     slice_range(g.band1, z1 * g.sband1 + rq, lo1, hi1);
     const int NKT = hi1 > lo1 ? hi1 - lo1 : 0;
+    unsigned fine[4];  // phase 1: E1 row groups of this quarter (fragment rows i)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) fine[i] = fine_range(g.band1, z1 * g.sband1, rq * 4 + i);
 
     // ---- phase 1: T = E1[rq block] X_s  (32 x 128), cp.async 2-stage pipeline ----
     double* sA = smem;
@@ -106,12 +150,20 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
             for (int i = 0; i < 4; ++i) a[i] = tA[i * 8 * S_SA + kk];
 #pragma unroll
             for (int j = 0; j < 4; ++j) b[j] = tB[kk * S_SB + j * 8];
+            const unsigned kq = static_cast<unsigned>(((lo1 + kt) * S_BK + kk) >> 2);
+            unsigned mask = 0;
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
-#pragma unroll
-                for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+            for (int i = 0; i < 4; ++i) mask |= (kq - (fine[i] & 0xffffu) < (fine[i] >> 16) ? 1u : 0u) << i;
+            dmma_switch<true>(mask, acc, a, b);
         }
     }
+    unsigned long long f1 = 0;  // executed phase-1 DMMA work of this warp
+    if (g.flop_counter)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int flo = static_cast<int>(fine[i] & 0xffffu), fhi = flo + static_cast<int>(fine[i] >> 16);
+            f1 += 2ull * 8 * 32 * 4 * max(0, min(hi1 * 4, fhi) - max(lo1 * 4, flo));
+        }
     cp_wait<0>();
     __syncthreads();  // every warp is done with the stage buffers: T overwrites them
 
@@ -133,6 +185,8 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
     int lo2, hi2;
     slice_range(g.band2, z1 * g.sband2 + warp, lo2, hi2);
     const int kb = lo2 * S_BK, ke = hi2 > lo2 ? hi2 * S_BK : kb;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) fine[j] = fine_range(g.band2, z1 * g.sband2, warp * 4 + j);  // E2 row groups = columns j
     const double* e2 = E2 + (warp * 32 + gid) * S_N + tig;
     const double* tr = T + gid * S_N;
     double bn_[4];
@@ -153,16 +207,21 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
         double a[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) a[i] = tr[i * 8 * S_N + kc];
+        const unsigned kq = static_cast<unsigned>(k >> 2);
+        unsigned mask = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+        for (int j = 0; j < 4; ++j) mask |= (kq - (fine[j] & 0xffffu) < (fine[j] >> 16) ? 1u : 0u) << j;
+        dmma_switch<false>(mask, acc, a, b);
     }
     asm volatile("griddepcontrol.launch_dependents;");
 
     if (g.flop_counter) {
-        unsigned long long f = 2ull * 32 * 32 * (ke - kb);
-        if (warp == 0) f += 2ull * 32 * S_N * (NKT * S_BK);
+        unsigned long long f = f1;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int flo = static_cast<int>(fine[j] & 0xffffu), fhi = flo + static_cast<int>(fine[j] >> 16);
+            f += 2ull * 32 * 8 * 4 * max(0, min(ke / 4, fhi) - max(kb / 4, flo));
+        }
         if (lane == 0) atomicAdd(g.flop_counter, f);
     }
 #pragma unroll

@@ -1,0 +1,8 @@
+#!/bin/bash
+OUT=gpurun_out/fine4
+mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_slab12.py tests/test_gpu_band.py -x -q -m gpu > $OUT/pytest.log 2>&1; echo "rc=$?" >> $OUT/pytest.log
+timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline >> $OUT/bench_cfg2.jsonl 2>>$OUT/bench.err
+timeout 300 python tools/gemm_breakdown.py 2 3 > $OUT/breakdown_cfg2.txt 2>&1
+for c in 3 5; do timeout 300 python tools/gemm_breakdown.py $c 1 > $OUT/breakdown_cfg$c.txt 2>&1; done
+ls -la $OUT
