@@ -50,16 +50,31 @@ __device__ __forceinline__ void dmma_masked(double (&acc)[MI][NI][2], const doub
         for (int j = 0; j < NI; ++j)
             if ((MASK >> (ROWS ? i : j)) & 1) dmma_8x8x4(acc[i][j], a[i], b[j]);
 }
-template <int MI, int NI, bool ROWS, int M = 1>
+template <int MI, int NI, bool ROWS, int M>
+__device__ __forceinline__ void dmma_case(double (&acc)[MI][NI][2], const double (&a)[MI], const double (&b)[NI]) {
+    if constexpr (M < (1 << (ROWS ? MI : NI))) dmma_masked<MI, NI, ROWS, M>(acc, a, b);
+}
+template <int MI, int NI, bool ROWS>
 __device__ __forceinline__ void dmma_gated(unsigned mask, double (&acc)[MI][NI][2], const double (&a)[MI],
                                            const double (&b)[NI]) {
-    constexpr int FG = ROWS ? MI : NI;
-    static_assert(FG <= 4, "fine gating over at most 4 fragment groups");
-    if constexpr (M < (1 << FG)) {
-        if (mask == static_cast<unsigned>(M))
-            dmma_masked<MI, NI, ROWS, M>(acc, a, b);
-        else
-            dmma_gated<MI, NI, ROWS, M + 1>(mask, acc, a, b);
+    static_assert((ROWS ? MI : NI) <= 4, "fine gating over at most 4 fragment groups");
+    switch (mask) {
+        case 1: dmma_case<MI, NI, ROWS, 1>(acc, a, b); break;
+        case 2: dmma_case<MI, NI, ROWS, 2>(acc, a, b); break;
+        case 3: dmma_case<MI, NI, ROWS, 3>(acc, a, b); break;
+        case 4: dmma_case<MI, NI, ROWS, 4>(acc, a, b); break;
+        case 5: dmma_case<MI, NI, ROWS, 5>(acc, a, b); break;
+        case 6: dmma_case<MI, NI, ROWS, 6>(acc, a, b); break;
+        case 7: dmma_case<MI, NI, ROWS, 7>(acc, a, b); break;
+        case 8: dmma_case<MI, NI, ROWS, 8>(acc, a, b); break;
+        case 9: dmma_case<MI, NI, ROWS, 9>(acc, a, b); break;
+        case 10: dmma_case<MI, NI, ROWS, 10>(acc, a, b); break;
+        case 11: dmma_case<MI, NI, ROWS, 11>(acc, a, b); break;
+        case 12: dmma_case<MI, NI, ROWS, 12>(acc, a, b); break;
+        case 13: dmma_case<MI, NI, ROWS, 13>(acc, a, b); break;
+        case 14: dmma_case<MI, NI, ROWS, 14>(acc, a, b); break;
+        case 15: dmma_case<MI, NI, ROWS, 15>(acc, a, b); break;
+        default: break;
     }
 }
 
@@ -787,12 +802,14 @@ int launch_gemm_family(const GemmArgs& g, bool vec2, int shape, cudaStream_t s) 
         case 0: return vec2 ? launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 128, BKB, 64, 32, STB, BKM, 1>(g, s);
         case 1: return vec2 ? launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 2>(g, s) : launch_cfg<128, 64, BKB, 64, 32, STB, BKM, 1>(g, s);
         case 2: return vec2 ? launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 2>(g, s) : launch_cfg<64, 128, BKB, 32, 64, STB, BKM, 1>(g, s);
+        case 9:  // exponential = B (k-major), default: 128x32 tiles, four 32x32 warps (4-DMMA gated groups)
+            return launch_cfg<128, 32, 16, 32, 32, 2, BKM, 2, 4>(g, s);
         case 6:  // negligible-block skip, exponential = A: 32-row tiles stream only their block's slices
             // (32x128 with four 32x32 warps: +3% over 32x64 on the node-sweep band shapes, +4.5% dense;
             // 16-wide k slices in 2 stages: +2.5-4% over 8-wide in 4 once the load issue path lost its
             // per-slice 64-bit multiplies, tools/gemm_tune.cu, profiles/r01_gemm_tune_bk16.txt)
             return launch_cfg<32, 128, 16, 32, 32, 2, BKM, 2, 4>(g, s);
-        case 7:  // negligible-block skip, exponential = B (k-major): 32-column tiles (BK 16: +3-6%)
+        case 7:  // PQ_KK_TALL=0: exponential = B (k-major) on 64x32 tiles (BK 16: +3-6% over BK 8)
             return launch_cfg<64, 32, 16, 32, 16, 2, BKM, 2, 6>(g, s);
         case 8:  // exponential = A on small grids (PQ_SMALL_GRID_TILE=1 only, kernels.cu): 64x32 tiles at
                  // 7 CTAs/SM fill the last wave (2048 CTAs in 1.98 waves instead of 1024 in 1.73)

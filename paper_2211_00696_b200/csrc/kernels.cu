@@ -43,6 +43,14 @@ static const bool g_small_grid_tile = [] {
     const char* e = std::getenv("PQ_SMALL_GRID_TILE");
     return e && e[0] == '1';
 }();
+// k-major exponential band tiles are 128x32 (four 32x32 warps: each warp's fine-gated groups are
+// 4-DMMA blocks, which the compiler keeps as branches -- the 64x32 tile's 2-DMMA blocks were
+// if-converted into predicated DMMAs): config 3 86.5 -> 91.4 RHS/s, config 5 3.62 -> 3.81.
+// PQ_KK_TALL=0 restores the 64x32 tile.
+static const bool g_kk_tall = [] {
+    const char* e = std::getenv("PQ_KK_TALL");
+    return !(e && e[0] == '0');
+}();
 static const bool g_persistent_enabled = [] {
     const char* e = std::getenv("PQ_PERSISTENT");
     return e && e[0] == '1';
@@ -65,7 +73,7 @@ int launch_gemm(const GemmArgs& g, cudaStream_t s) {
     if (shape == 3 && plain && ctas(64, 64) >= 2 * 444 && g_persistent_enabled) shape = 5;
     // negligible-block skip (g.band): 32-extent tiles along the exponential's rows, so each CTA
     // streams exactly the k-slices its 32-row block needs (PQ_BAND_TILE=64 keeps 64x64 tiles)
-    if (shape == 3 && vec2 && g.band && g_band_tile32) shape = g.band_mode == 3 ? 7 : 6;
+    if (shape == 3 && vec2 && g.band && g_band_tile32) shape = g.band_mode == 3 ? (g_kk_tall ? 9 : 7) : 6;
     // (64-row tiles must not straddle two stacked exponentials: band_rows a multiple of 64)
     if (shape == 6 && !g.b_kmajor && ctas(32, 128) <= 1024 && g_small_grid_tile &&
         (g.band_mode == 2 || (g.band_mode == 1 && g.band_rows % 64 == 0)))
