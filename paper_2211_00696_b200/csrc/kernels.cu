@@ -596,21 +596,34 @@ void launch_imax(const int* v, int count, int* out, cudaStream_t s) { k_imax<<<1
 //  * fine entries, one per 8-row group: {first, last+1} of the 4-column chunks (DMMA k4 steps)
 //    whose max exceeds 2^-64 x the GROUP's max (<= the block's: again at least as conservative).
 // Record of matrix z: [coarse rb = 0..RB) [fine g = 0..4RB), RB = ceil(n/32) (band_row_blocks).
-__global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __restrict__ E, int2* __restrict__ out) {
+__global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __restrict__ E, int2* __restrict__ out,
+                                                     int fine_on) {
     const int z = blockIdx.x, rb = blockIdx.y, RB = gridDim.y;
     const double* e = E + (long long)z * n * n;
-    __shared__ double cmax[4][128];  // [group][chunk], n <= 512
+    __shared__ double colmax[4][512];  // [group][column], n <= 512
+    __shared__ double cmax[4][128];    // [group][4-column chunk]
     __shared__ double gmax[4];
     const int NC = (n + 3) / 4;
     const double kInf = __longlong_as_double(0x7ff0000000000000LL);
+    // (group, column) items: consecutive threads read consecutive columns of the same 8 rows
+    for (int item = threadIdx.x; item < 4 * n; item += blockDim.x) {
+        const int g = item / n, c = item - g * n;
+        const int r0 = rb * 32 + g * 8;
+        double m = 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (r0 + u < n) {
+                const double v = fabs(__ldg(e + (long long)(r0 + u) * n + c));
+                m = !(v <= 1.7976931348623157e308) ? kInf : fmax(m, v);
+            }
+        }
+        colmax[g][c] = m;
+    }
+    __syncthreads();
     for (int cell = threadIdx.x; cell < 4 * NC; cell += blockDim.x) {
         const int g = cell / NC, ch = cell - g * NC;
         double m = 0.0;
-        for (int r = rb * 32 + g * 8; r < min(n, rb * 32 + g * 8 + 8); ++r)
-            for (int c = ch * 4; c < min(n, ch * 4 + 4); ++c) {
-                const double v = fabs(__ldg(e + (long long)r * n + c));
-                m = !(v <= 1.7976931348623157e308) ? kInf : fmax(m, v);
-            }
+        for (int c = ch * 4; c < min(n, ch * 4 + 4); ++c) m = fmax(m, colmax[g][c]);
         cmax[g][ch] = m;
     }
     __syncthreads();
@@ -627,12 +640,18 @@ __global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __rest
         const int g = threadIdx.x;
         const double gm = gmax[g], thr = ldexp(gm, -64);
         int lo = NC, hi = 0;
-        if (rb * 32 + g * 8 < n)
-            for (int ch = 0; ch < NC; ++ch)
-                if (cmax[g][ch] > thr || !(gm <= 1.7976931348623157e308)) {
-                    lo = min(lo, ch);
-                    hi = ch + 1;
-                }
+        if (rb * 32 + g * 8 < n) {
+            if (!fine_on) {
+                lo = 0;
+                hi = NC;
+            } else {
+                for (int ch = 0; ch < NC; ++ch)
+                    if (cmax[g][ch] > thr || !(gm <= 1.7976931348623157e308)) {
+                        lo = min(lo, ch);
+                        hi = ch + 1;
+                    }
+            }
+        }
         rec[RB + rb * 4 + g] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
     } else if (threadIdx.x == 32) {  // coarse entry
         const double bm = fmax(fmax(gmax[0], gmax[1]), fmax(gmax[2], gmax[3])), thr = ldexp(bm, -64);
@@ -650,10 +669,15 @@ __global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __rest
         rec[rb] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
     }
 }
+// PQ_FINE=0: fine entries span every k4 step (only the coarse 32-row-block skip applies)
+static const bool g_fine_on = [] {
+    const char* e = std::getenv("PQ_FINE");
+    return !(e && e[0] == '0');
+}();
 void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s) {
     if (count <= 0) return;
     if (n > 512) throw std::invalid_argument("band ranges: n > 512");
-    k_band_ranges<<<dim3(count, (n + 31) / 32), 256, 0, s>>>(n, E, out);
+    k_band_ranges<<<dim3(count, (n + 31) / 32), 256, 0, s>>>(n, E, out, g_fine_on ? 1 : 0);
 }
 
 
