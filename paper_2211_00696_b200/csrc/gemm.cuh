@@ -386,18 +386,42 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int bx, int by, int
         if (kabs < w_lo || kabs >= w_hi) continue;  // warp-uniform: this warp's rows need no DMMA here
         const double* tA = tA0 + st * T::ASZ;
         const double* tB = tB0 + st * T::BSZ;
+        // a slice every fragment group covers entirely runs the plain unrolled DMMA block; others
+        // step through their k4 steps with the mask dispatch (kept out of the unrolled path, so the
+        // kernel's hot loop stays small in the instruction cache)
+        bool full = true;
+        if constexpr (GATE) {
+            const unsigned q0 = static_cast<unsigned>((kabs * BK) >> 2);
 #pragma unroll
-        for (int kk = 0; kk < BK; kk += 4) {
-            double a[T::MI], b[T::NI];
+            for (int f = 0; f < FG; ++f)
+                full = full && (fine[f] & 0xffffu) <= q0 && q0 + BK / 4 <= (fine[f] & 0xffffu) + (fine[f] >> 16);
+        }
+        if (full) {
 #pragma unroll
-            for (int i = 0; i < T::MI; ++i) a[i] = tA[i * 8 * T::SA + kk];
+            for (int kk = 0; kk < BK; kk += 4) {
+                double a[T::MI], b[T::NI];
 #pragma unroll
-            for (int j = 0; j < T::NI; ++j) b[j] = BKM ? tB[j * 8 * T::SB + kk] : tB[kk * T::SB + j * 8];
-            if constexpr (GATE) {
+                for (int i = 0; i < T::MI; ++i) a[i] = tA[i * 8 * T::SA + kk];
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j) b[j] = BKM ? tB[j * 8 * T::SB + kk] : tB[kk * T::SB + j * 8];
+#pragma unroll
+                for (int i = 0; i < T::MI; ++i)
+#pragma unroll
+                    for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+            }
+        } else if constexpr (GATE) {
+#pragma unroll 1
+            for (int kk = 0; kk < BK; kk += 4) {
                 const unsigned kq = static_cast<unsigned>((kabs * BK + kk) >> 2);
                 unsigned mask = 0;
 #pragma unroll
                 for (int f = 0; f < FG; ++f) mask |= (kq - (fine[f] & 0xffffu) < (fine[f] >> 16) ? 1u : 0u) << f;
+                if (mask == 0u) continue;
+                double a[T::MI], b[T::NI];
+#pragma unroll
+                for (int i = 0; i < T::MI; ++i) a[i] = tA[i * 8 * T::SA + kk];
+#pragma unroll
+                for (int j = 0; j < T::NI; ++j) b[j] = BKM ? tB[j * 8 * T::SB + kk] : tB[kk * T::SB + j * 8];
                 if (mask == (1u << FG) - 1u) {
 #pragma unroll
                     for (int i = 0; i < T::MI; ++i)
@@ -406,11 +430,6 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int bx, int by, int
                 } else {
                     dmma_gated<T::MI, T::NI, !BKM>(mask, acc, a, b);
                 }
-            } else {
-#pragma unroll
-                for (int i = 0; i < T::MI; ++i)
-#pragma unroll
-                    for (int j = 0; j < T::NI; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
             }
         }
     }

@@ -143,18 +143,39 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
         cp_commit();
         const double* tA = tA0 + (kt & 1) * S_ASZ;
         const double* tB = tB0 + (kt & 1) * S_BSZ;
+        const unsigned q0 = static_cast<unsigned>(((lo1 + kt) * S_BK) >> 2);
+        bool full = true;
 #pragma unroll
-        for (int kk = 0; kk < S_BK; kk += 4) {
-            double a[4], b[4];
+        for (int i = 0; i < 4; ++i)
+            full = full && (fine[i] & 0xffffu) <= q0 && q0 + S_BK / 4 <= (fine[i] & 0xffffu) + (fine[i] >> 16);
+        if (full) {
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = tA[i * 8 * S_SA + kk];
+            for (int kk = 0; kk < S_BK; kk += 4) {
+                double a[4], b[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) b[j] = tB[kk * S_SB + j * 8];
-            const unsigned kq = static_cast<unsigned>(((lo1 + kt) * S_BK + kk) >> 2);
-            unsigned mask = 0;
+                for (int i = 0; i < 4; ++i) a[i] = tA[i * 8 * S_SA + kk];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) mask |= (kq - (fine[i] & 0xffffu) < (fine[i] >> 16) ? 1u : 0u) << i;
-            dmma_switch<true>(mask, acc, a, b);
+                for (int j = 0; j < 4; ++j) b[j] = tB[kk * S_SB + j * 8];
+#pragma unroll
+                for (int i = 0; i < 4; ++i)
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) dmma_8x8x4(acc[i][j], a[i], b[j]);
+            }
+        } else {
+#pragma unroll 1
+            for (int kk = 0; kk < S_BK; kk += 4) {
+                const unsigned kq = q0 + (kk >> 2);
+                unsigned mask = 0;
+#pragma unroll
+                for (int i = 0; i < 4; ++i) mask |= (kq - (fine[i] & 0xffffu) < (fine[i] >> 16) ? 1u : 0u) << i;
+                if (mask == 0u) continue;
+                double a[4], b[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = tA[i * 8 * S_SA + kk];
+#pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = tB[kk * S_SB + j * 8];
+                dmma_switch<true>(mask, acc, a, b);
+            }
         }
     }
     unsigned long long f1 = 0;  // executed phase-1 DMMA work of this warp
