@@ -13,6 +13,8 @@
 // k-slices of E1's 32-row block rq, and within them the k4 steps of the element's 8-row group of E1;
 // mode 2: likewise for E2's block / group of the output column), so the fused result equals the
 // unfused chain bit for bit (tests/test_gpu_slab12.py).
+#include <type_traits>
+
 #include "gemm.cuh"
 
 namespace pqb {
@@ -210,29 +212,59 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
     for (int j = 0; j < 4; ++j) fine[j] = fine_range(g.band2, z1 * g.sband2, warp * 4 + j);  // E2 row groups = columns j
     const double* e2 = E2 + (warp * 32 + gid) * S_N + tig;
     const double* tr = T + gid * S_N;
-    double bn_[4];
-    if (ke > kb) {
+    // k4 steps on which the set of active column groups is constant run as one loop of a
+    // mask-specialised body (E2 fragments of the active groups prefetched one step ahead)
+    auto seg = [&](auto mc, int qa, int qb) {
+        constexpr int M = decltype(mc)::value;
+        double bn_[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bn_[j] = __ldg(e2 + j * 8 * S_N + kb);
-    }
+        for (int j = 0; j < 4; ++j) bn_[j] = ((M >> j) & 1) ? __ldg(e2 + j * 8 * S_N + qa * 4) : 0.0;
 #pragma unroll 2
-    for (int k = kb; k < ke; k += 4) {
-        double b[4];
+        for (int q = qa; q < qb; ++q) {
+            double b[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) b[j] = bn_[j];
-        if (k + 4 < ke) {
+            for (int j = 0; j < 4; ++j) b[j] = bn_[j];
+            if (q + 1 < qb) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bn_[j] = __ldg(e2 + j * 8 * S_N + k + 4);
+                for (int j = 0; j < 4; ++j)
+                    if ((M >> j) & 1) bn_[j] = __ldg(e2 + j * 8 * S_N + q * 4 + 4);
+            }
+            const int kc = (q * 4 + tig) ^ swz;
+            double a[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = tr[i * 8 * S_N + kc];
+            dmma_masked<M, false>(acc, a, b);
         }
-        const int kc = (k + tig) ^ swz;
-        double a[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) a[i] = tr[i * 8 * S_N + kc];
-        const unsigned kq = static_cast<unsigned>(k >> 2);
+    };
+    for (int q = kb / 4, q1 = ke / 4; q < q1;) {
         unsigned mask = 0;
+        int qe = q1;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) mask |= (kq - (fine[j] & 0xffffu) < (fine[j] >> 16) ? 1u : 0u) << j;
-        dmma_switch<false>(mask, acc, a, b);
+        for (int j = 0; j < 4; ++j) {
+            const int lo = static_cast<int>(fine[j] & 0xffffu), hi = lo + static_cast<int>(fine[j] >> 16);
+            if (q >= lo && q < hi) mask |= 1u << j;
+            if (lo > q) qe = min(qe, lo);
+            if (hi > q) qe = min(qe, hi);
+        }
+        switch (mask) {
+            case 1: seg(std::integral_constant<int, 1>{}, q, qe); break;
+            case 2: seg(std::integral_constant<int, 2>{}, q, qe); break;
+            case 3: seg(std::integral_constant<int, 3>{}, q, qe); break;
+            case 4: seg(std::integral_constant<int, 4>{}, q, qe); break;
+            case 5: seg(std::integral_constant<int, 5>{}, q, qe); break;
+            case 6: seg(std::integral_constant<int, 6>{}, q, qe); break;
+            case 7: seg(std::integral_constant<int, 7>{}, q, qe); break;
+            case 8: seg(std::integral_constant<int, 8>{}, q, qe); break;
+            case 9: seg(std::integral_constant<int, 9>{}, q, qe); break;
+            case 10: seg(std::integral_constant<int, 10>{}, q, qe); break;
+            case 11: seg(std::integral_constant<int, 11>{}, q, qe); break;
+            case 12: seg(std::integral_constant<int, 12>{}, q, qe); break;
+            case 13: seg(std::integral_constant<int, 13>{}, q, qe); break;
+            case 14: seg(std::integral_constant<int, 14>{}, q, qe); break;
+            case 15: seg(std::integral_constant<int, 15>{}, q, qe); break;
+            default: break;
+        }
+        q = qe;
     }
     asm volatile("griddepcontrol.launch_dependents;");
 
