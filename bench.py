@@ -339,9 +339,12 @@ def roofline_line(ctx, steps: int, ms_step_dev: float, w, kstats=None) -> dict:
                        f"(ncu --set full; algorithmic {t['algorithmic_bytes_per_launch']:.3g})")
     ro = {"bound": "tensor", "achieved": ach, "peak": DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
           "frac": ach / DMMA_PEAK_TFLOPS, "traffic": traffic, "traffic_source": traffic_src,
-          "kernel": "k_gemm (FP64 DMMA mode products + expm products), all launches of the step",
-          "achieved_note": ("EXECUTED flops: each CTA adds 2*rows*cols*k_issued to a device counter; exponential "
-                            "blocks below 2^-64 max|E| are skipped (DESIGN.md 3b) and not counted"),
+          "kernel": ("k_gemm band tiles + k_slab12 (FP64 DMMA mode products) + expm products, all launches "
+                     "of the step"),
+          "achieved_note": ("EXECUTED flops: each warp adds 2*rows*cols*4 per DMMA k4 step it issued to a device "
+                            "counter; exponential blocks and 8-row groups below 2^-64 of their max are skipped "
+                            "(DESIGN.md 3b) and not counted -- since the fine gating the tiles are bound by operand "
+                            "streaming, so this fraction is below the dense-equivalent one"),
           "dense_equiv_tflops": dense, "dense_equiv_frac": dense / DMMA_PEAK_TFLOPS,
           "dense_equiv_note": "2*M*N*K of the same launches (the reference's dense mode products) / the same time",
           "launches_per_step": g_launches / steps, "gemm_ms_per_step": g_ms / steps,
