@@ -1667,6 +1667,7 @@ void phi_nodes_partial_dev(pq_ctx& c, const DevOp& op, double scale, int nb, con
 // exactly the levels the reference evaluates (phiaction.hpp:175-240).
 struct CcPending {
     bool active = false;
+    bool forked = false;  // the phi_0 fork event was recorded before the last level's combination
     int levels = 0, nb = 0, p = 0;
     double eps = 0.0;
 };
@@ -1691,7 +1692,7 @@ static bool cc_pending_holds(pq_ctx& c, const CcPending& pd) {
 
 static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int nb, const double* bs, int p,
                                double eps, const PhiExps& px25, double* out, int* points_used, int spec_points,
-                               CcPending* pend = nullptr) {
+                               CcPending* pend = nullptr, cudaEvent_t fork_ev = nullptr) {
     if (p < 1) throw std::invalid_argument("phi_adaptive: need p >= 1");
     if (!(eps > 0.0)) throw std::invalid_argument("phi_adaptive: need eps > 0");
     const long long N = op.N;
@@ -1835,6 +1836,12 @@ static void phi_adaptive_shift(pq_ctx& c, const DevOp& op, double s, int l, int 
             cuda_check(cudaEventRecord(c.ev_ccfork, main_stream), "cc fork");
             cuda_check(cudaStreamWaitEvent(c.ccs, c.ev_ccfork, 0), "cc fork wait");
             c.stream = c.ccs;
+        }
+        // deferred ladder, predicted last level: the side stream's phi_0 may start now, so its DMMA
+        // work overlaps this level's (HBM-bound) combination instead of the squaring
+        if (defer && fork_ev && fine.size() == spec_points && !offload) {
+            cuda_check(cudaEventRecord(fork_ev, c.stream), "phi_0 fork");
+            pend->forked = true;
         }
         // phiaction.hpp:225-240: max over columns of ||y - y_prev||_inf / ||y||_inf
         if (fused) {
@@ -2239,16 +2246,18 @@ static void phi_call_dev(pq_ctx& c, const DevOp& op, double scale, int nb, const
             spec = 13;
             while (spec < n + 1 && spec < (1 << 15)) spec = 2 * spec - 1;
         }
-        phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, px, first, points_used, spec, allow_defer ? &pend : nullptr);
+        if (phi0_out && l > 0 && !c.profiling) ensure_side(c);
+        phi_adaptive_shift(c, op, scale, l, nb, bs, p, eps, px, first, points_used, spec, allow_defer ? &pend : nullptr,
+                           phi0_out && l > 0 && !c.profiling ? c.ev_fork : nullptr);
     }
     mark(c, "nodes");
     // phi_0 needs only its exponentials and b: run its mode chain on the side stream alongside the
-    // squaring chain, where its CTAs fill the tails of the squaring GEMM waves (not while profiling,
-    // so per-launch events stay unambiguous)
+    // last CC level's combination (deferred ladder) or the squaring chain, where its CTAs fill the
+    // tails of the squaring GEMM waves (not while profiling, so per-launch events stay unambiguous)
     const bool side_phi0 = phi0_out && l > 0 && !c.profiling;
     if (side_phi0) {
         ensure_side(c);
-        cuda_check(cudaEventRecord(c.ev_fork, c.stream), "fork");
+        if (!pend.forked) cuda_check(cudaEventRecord(c.ev_fork, c.stream), "fork");
         cuda_check(cudaStreamWaitEvent(c.side, c.ev_fork, 0), "fork wait");
         cudaStream_t main_stream = c.stream;
         c.stream = c.side;
@@ -2478,6 +2487,9 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
         // waits for beta and plans; the GPU never idles for the host planner
         const int sl = memo->l, sn = memo->n;
         beta_enqueue(c, op, nb, bs);
+        // the shared Taylor powers depend on the operator only: enqueue them before the host builds
+        // the rest of the call (phi_exponentials finds them cached)
+        taylor_prefetch(c, op, 1.0);
         mark(c, "beta_enqueued");
         const double alpha = alpha_of(op);
         const int d = op.d;
