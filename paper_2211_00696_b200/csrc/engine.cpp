@@ -2487,15 +2487,16 @@ void phiquadmv_dev(pq_ctx& c, const DevOp& op, int nb, const double* bs, int p, 
         // waits for beta and plans; the GPU never idles for the host planner
         const int sl = memo->l, sn = memo->n;
         beta_enqueue(c, op, nb, bs);
-        // the shared Taylor powers depend on the operator only: enqueue them before the host builds
-        // the rest of the call (phi_exponentials finds them cached)
-        taylor_prefetch(c, op, 1.0);
         mark(c, "beta_enqueued");
         const double alpha = alpha_of(op);
         const int d = op.d;
         worker_submit(c, [&c, &pi, nb, d, alpha, p, eps, mode, has_l, l, c1, c2] {
             pi = plan_host(d, alpha, beta_collect(c, nb), p, eps, mode, has_l, l, c1, c2);
         });
+        // the shared Taylor powers depend on the operator only: enqueue them before the host builds
+        // the rest of the call (phi_exponentials finds them cached); after the planner job, which
+        // is on the critical path of latency-bound calls (config 1)
+        taylor_prefetch(c, op, 1.0);
         try {
             phi_call_dev(c, op, 1.0, nb, bs, p, sl, sn, mode, eps, out, &points, phi0_out, phi0_host, out_host,
                          out_copied);
