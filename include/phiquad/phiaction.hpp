@@ -81,7 +81,7 @@ inline std::vector<PhiColumns> alloc_columns(int nb, int p, int dim) {
     const int count = nb * p;
     const int threads = static_cast<long long>(dim) * count >= (1LL << 20) ? std::min(count, 8) : 1;
     parallel_for(count, threads, [&](int k) {
-        out[static_cast<size_t>(k / p)].cols[static_cast<size_t>(k % p)] = std::vector<double>(static_cast<size_t>(dim));
+        out[static_cast<size_t>(k / p)].cols[static_cast<size_t>(k % p)] = b200::result_vector(static_cast<size_t>(dim));
     });
     return out;
 }
@@ -274,7 +274,7 @@ inline std::vector<double> phi_lincomb(const KroneckerSum& a, const std::vector<
     const int dim = a.dim();
     const auto flat = detail::gather(bs, dim, "phi_lincomb");
     const auto f = detail::flatten(a);
-    std::vector<double> y(static_cast<size_t>(dim));
+    std::vector<double> y = b200::result_vector(static_cast<size_t>(dim));
     b200::check(pq_phi_lincomb(b200::context(), a.order(), f.shape.data(), f.data.data(), static_cast<int>(bs.size()),
                                flat.data(), rule.points(), rule.nodes.data(), rule.weights.data(), y.data(), PQ_HOST));
     return y;

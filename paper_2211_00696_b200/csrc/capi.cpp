@@ -7,8 +7,11 @@
 #include <chrono>
 #include <cstdlib>
 #include <cstdio>
+#include <condition_variable>
 #include <cstring>
+#include <functional>
 #include <map>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <thread>
@@ -64,9 +67,87 @@ static double* pinned_bounce(pq_ctx& c, const std::string& name, size_t count) {
     return slot.first;
 }
 
-// dst[k] <- src + k*count for each k, split over up to 8 host threads in 4 MB pieces
+// Persistent helper threads for the host copies below (creating and joining 7 std::threads per
+// copy cost ~0.1 ms, several times per drop-in call).  One job at a time; a caller that finds the
+// pool busy (another thread's call) runs its copy with its own temporary threads.
+class CopyPool {
+public:
+    static constexpr size_t kWorkers = 7;
+    // f(w, nw) for w = 0 .. nw-1, nw = workers + 1, the caller running w = 0; false if busy
+    bool try_run(const std::function<void(size_t, size_t)>& f) {
+        std::unique_lock<std::mutex> own(busy_, std::try_to_lock);
+        if (!own.owns_lock()) return false;
+        start();
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            job_ = &f;
+            pending_ = kWorkers;
+            ++gen_;
+        }
+        cv_.notify_all();
+        f(0, kWorkers + 1);
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [this] { return pending_ == 0; });
+        job_ = nullptr;
+        return true;
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+
+private:
+    void start() {
+        if (!th_.empty()) return;
+        for (size_t w = 1; w <= kWorkers; ++w)
+            th_.emplace_back([this, w] {
+                uint64_t seen = 0;
+                while (true) {
+                    const std::function<void(size_t, size_t)>* f = nullptr;
+                    {
+                        std::unique_lock<std::mutex> lk(mu_);
+                        cv_.wait(lk, [&] { return stop_ || gen_ != seen; });
+                        if (stop_) return;
+                        seen = gen_;
+                        f = job_;
+                    }
+                    (*f)(w, kWorkers + 1);
+                    std::lock_guard<std::mutex> lk(mu_);
+                    if (--pending_ == 0) done_.notify_all();
+                }
+            });
+    }
+    std::mutex busy_, mu_;
+    std::condition_variable cv_, done_;
+    std::vector<std::thread> th_;
+    const std::function<void(size_t, size_t)>* job_ = nullptr;
+    size_t pending_ = 0;
+    uint64_t gen_ = 0;
+    bool stop_ = false;
+};
+
+// Runs work(t0, step) over `total` pieces on up to 8 threads (the pool, else temporary threads).
+static void host_parallel(size_t total, const std::function<void(size_t, size_t)>& work) {
+    if (total <= 1) {
+        work(0, 1);
+        return;
+    }
+    static CopyPool pool;
+    if (total >= 4 && pool.try_run(work)) return;
+    const size_t threads = std::min<size_t>(8, total);
+    std::vector<std::thread> team;
+    for (size_t w = 1; w < threads; ++w) team.emplace_back(work, w, threads);
+    work(0, threads);
+    for (auto& t : team) t.join();
+}
+
+// dst[k] <- src + k*count for each k, split over up to 8 host threads in 512 KB pieces
 static void host_scatter(double* const* dst, const double* src, int parts, size_t count) {
-    const size_t piece = size_t(1) << 19;  // doubles (4 MB)
+    const size_t piece = size_t(1) << 16;  // doubles (512 KB)
     const size_t per = (count + piece - 1) / piece, total = per * static_cast<size_t>(parts);
     auto work = [&](size_t t0, size_t step) {
         for (size_t t = t0; t < total; t += step) {
@@ -74,15 +155,7 @@ static void host_scatter(double* const* dst, const double* src, int parts, size_
             std::memcpy(dst[k] + o, src + k * count + o, len * sizeof(double));
         }
     };
-    const size_t threads = std::min<size_t>(8, total);
-    if (threads <= 1) {
-        work(0, 1);
-        return;
-    }
-    std::vector<std::thread> team;
-    for (size_t w = 1; w < threads; ++w) team.emplace_back(work, w, threads);
-    work(0, threads);
-    for (auto& t : team) t.join();
+    host_parallel(total, work);
 }
 
 static bool host_pinned(const void* p) {
@@ -94,7 +167,7 @@ static bool host_pinned(const void* p) {
 
 // dst + k*count <- src[k] for each k (the inverse of host_scatter), same thread split
 static void host_gather(double* dst, const double* const* src, int parts, size_t count) {
-    const size_t piece = size_t(1) << 19;
+    const size_t piece = size_t(1) << 16;
     const size_t per = (count + piece - 1) / piece, total = per * static_cast<size_t>(parts);
     auto work = [&](size_t t0, size_t step) {
         for (size_t t = t0; t < total; t += step) {
@@ -102,15 +175,7 @@ static void host_gather(double* dst, const double* const* src, int parts, size_t
             std::memcpy(dst + k * count + o, src[k] + o, len * sizeof(double));
         }
     };
-    const size_t threads = std::min<size_t>(8, total);
-    if (threads <= 1) {
-        work(0, 1);
-        return;
-    }
-    std::vector<std::thread> team;
-    for (size_t w = 1; w < threads; ++w) team.emplace_back(work, w, threads);
-    work(0, threads);
-    for (auto& t : team) t.join();
+    host_parallel(total, work);
 }
 
 // Device view of a caller vector: device pointers pass through; host data is staged.  Pageable
@@ -121,9 +186,16 @@ const double* stage_in(pq_ctx& c, const double* p, size_t count, int space, cons
     double* d = ws(c, slot, count);
     const double* src = p;
     if (count >= kBounceMin && !host_pinned(p)) {
+        // four chunks: each chunk's H2D runs while the host threads fill the next one
         double* bnc = pinned_bounce(c, std::string("in:") + slot, count);
-        host_scatter(&bnc, p, 1, count);
-        src = bnc;
+        const size_t chunk = (count / 4 + 1023) & ~size_t(1023);
+        for (size_t o = 0; o < count; o += chunk) {
+            const size_t len = std::min(chunk, count - o);
+            double* dst = bnc + o;
+            host_scatter(&dst, p + o, 1, len);
+            cuda_check(cudaMemcpyAsync(d + o, bnc + o, len * sizeof(double), cudaMemcpyHostToDevice, c.stream), "H2D");
+        }
+        return d;
     }
     cuda_check(cudaMemcpyAsync(d, src, count * sizeof(double), cudaMemcpyHostToDevice, c.stream), "H2D");
     return d;
