@@ -636,37 +636,46 @@ __global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __rest
     }
     __syncthreads();
     int2* rec = out + (long long)z * 5 * RB;
-    if (threadIdx.x < 4) {  // fine entry of group threadIdx.x
-        const int g = threadIdx.x;
+    // first / last set position of a predicate over [0, count) held lane-strided by one warp
+    auto span = [&](auto pred, int count, int& lo, int& hi) {
+        lo = count;
+        hi = 0;
+        for (int base = 0; base < count; base += 32) {
+            const unsigned b = __ballot_sync(0xffffffffu, base + lane < count && pred(base + lane));
+            if (b) {
+                lo = min(lo, base + __ffs(b) - 1);
+                hi = base + 32 - __clz(b);
+            }
+        }
+    };
+    if (warp < 4) {  // fine entry of group `warp`
+        const int g = warp;
         const double gm = gmax[g], thr = ldexp(gm, -64);
+        const bool bad = !(gm <= 1.7976931348623157e308);
         int lo = NC, hi = 0;
         if (rb * 32 + g * 8 < n) {
             if (!fine_on) {
                 lo = 0;
                 hi = NC;
             } else {
-                for (int ch = 0; ch < NC; ++ch)
-                    if (cmax[g][ch] > thr || !(gm <= 1.7976931348623157e308)) {
-                        lo = min(lo, ch);
-                        hi = ch + 1;
-                    }
+                span([&](int ch) { return cmax[g][ch] > thr || bad; }, NC, lo, hi);
             }
         }
-        rec[RB + rb * 4 + g] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
-    } else if (threadIdx.x == 32) {  // coarse entry
+        if (lane == 0) rec[RB + rb * 4 + g] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
+    } else if (warp == 4) {  // coarse entry
         const double bm = fmax(fmax(gmax[0], gmax[1]), fmax(gmax[2], gmax[3])), thr = ldexp(bm, -64);
+        const bool bad = !(bm <= 1.7976931348623157e308);
         const int NS = (n + 7) / 8;
-        int lo = NS, hi = 0;
-        for (int sl = 0; sl < NS; ++sl) {
-            double m = 0.0;
-            for (int g = 0; g < 4; ++g)
-                for (int h = 2 * sl; h < min(NC, 2 * sl + 2); ++h) m = fmax(m, cmax[g][h]);
-            if (m > thr || !(bm <= 1.7976931348623157e308)) {
-                lo = min(lo, sl);
-                hi = sl + 1;
-            }
-        }
-        rec[rb] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
+        int lo, hi;
+        span(
+            [&](int sl) {
+                double m = 0.0;
+                for (int g = 0; g < 4; ++g)
+                    for (int h = 2 * sl; h < min(NC, 2 * sl + 2); ++h) m = fmax(m, cmax[g][h]);
+                return m > thr || bad;
+            },
+            NS, lo, hi);
+        if (lane == 0) rec[rb] = lo < hi ? make_int2(lo, hi) : make_int2(0, 0);
     }
 }
 // PQ_FINE=0: fine entries span every k4 step (only the coarse 32-row-block skip applies)
