@@ -461,14 +461,20 @@ ComputeGate& device_gate(int dev) {
 }
 }  // namespace
 
+// The compute gate orders concurrent host-buffer calls' compute so one call's result D2H runs
+// under the next call's compute.  Default: on for results of 512 MB and more per call -- where the
+// D2H is a large share of the call (config 3: 4.3 GB per call, e2e 77.1 -> 86.6 RHS/s; config 5:
+// 6.4 GB, 3.01 -> 3.57 actions/s) -- and off below (config 2, 84 MB: 386-388 gated vs 407-421
+// ungated with 4 callers, the serialised compute losing the overlap of one call's low-occupancy
+// phases with another's).  PQ_COMPUTE_GATE=1 gates every call of 8 MB and more, =0 none.
 bool gate_wanted(size_t result_bytes) {
-    static const bool on = [] {
-        // measured on config 2 with 4 callers: 386-388 actions/s gated, 407-421 ungated (the
-        // serialised compute loses the overlap of one call's low-occupancy phases with another's)
+    static const int mode = [] {
         const char* e = std::getenv("PQ_COMPUTE_GATE");
-        return e && std::atoi(e) != 0;
+        return e ? (std::atoi(e) != 0 ? 1 : 0) : -1;
     }();
-    return on && result_bytes >= (8u << 20);
+    if (mode == 1) return result_bytes >= (size_t(8) << 20);
+    if (mode == 0) return false;
+    return result_bytes >= (size_t(512) << 20);
 }
 
 void gate_acquire(pq_ctx& c) {
