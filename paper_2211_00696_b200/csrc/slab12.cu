@@ -83,6 +83,7 @@ __device__ __forceinline__ unsigned fine_range(const int2* band, long long rec, 
 }
 }  // namespace
 
+template <bool SKEW>
 __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
     extern __shared__ __align__(16) double smem[];
     const int rq = blockIdx.x;
@@ -212,59 +213,114 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
     for (int j = 0; j < 4; ++j) fine[j] = fine_range(g.band2, z1 * g.sband2, warp * 4 + j);  // E2 row groups = columns j
     const double* e2 = E2 + (warp * 32 + gid) * S_N + tig;
     const double* tr = T + gid * S_N;
-    // k4 steps on which the set of active column groups is constant run as one loop of a
-    // mask-specialised body (E2 fragments of the active groups prefetched one step ahead)
-    auto seg = [&](auto mc, int qa, int qb) {
-        constexpr int M = decltype(mc)::value;
-        double bn_[4];
+    if constexpr (SKEW) {
+        // Skewed k loop: column group j walks its OWN k4 range [qa_j, qa_j + len_j) -- step t
+        // multiplies T's columns at k4 = qa_j + t -- so while every group still has steps left all
+        // 16 DMMAs of a step issue (T is fully resident, so the groups need not share a k window).
+        // Each accumulator still sees its k4 steps in ascending order: bitwise the aligned loop.
+        int qa[4], len[4];
+        int lmin = 1 << 30;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) bn_[j] = ((M >> j) & 1) ? __ldg(e2 + j * 8 * S_N + qa * 4) : 0.0;
-#pragma unroll 2
-        for (int q = qa; q < qb; ++q) {
+        for (int j = 0; j < 4; ++j) {
+            const int lo = max(static_cast<int>(fine[j] & 0xffffu), kb / 4);
+            const int hi = min(static_cast<int>(fine[j] & 0xffffu) + static_cast<int>(fine[j] >> 16), ke / 4);
+            qa[j] = lo;
+            len[j] = max(0, hi - lo);
+            lmin = min(lmin, len[j]);
+        }
+        double bn_[4];
+        if (lmin > 0) {
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bn_[j] = __ldg(e2 + j * 8 * S_N + qa[j] * 4);
+        }
+#pragma unroll 1
+        for (int t = 0; t < lmin; ++t) {
             double b[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) b[j] = bn_[j];
-            if (q + 1 < qb) {
+            if (t + 1 < lmin) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if ((M >> j) & 1) bn_[j] = __ldg(e2 + j * 8 * S_N + q * 4 + 4);
+                for (int j = 0; j < 4; ++j) bn_[j] = __ldg(e2 + j * 8 * S_N + (qa[j] + t + 1) * 4);
             }
-            const int kc = (q * 4 + tig) ^ swz;
-            double a[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = tr[i * 8 * S_N + kc];
-            dmma_masked<M, false>(acc, a, b);
+            for (int j = 0; j < 4; ++j) {
+                const int kc = ((qa[j] + t) * 4 + tig) ^ swz;
+                double a[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = tr[i * 8 * S_N + kc];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dmma_8x8x4(acc[i][j], a[i], b[j]);
+            }
         }
-    };
-    for (int q = kb / 4, q1 = ke / 4; q < q1;) {
-        unsigned mask = 0;
-        int qe = q1;
+        // the groups' remaining steps (ranges of unequal length at the matrix edges)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            const int lo = static_cast<int>(fine[j] & 0xffffu), hi = lo + static_cast<int>(fine[j] >> 16);
-            if (q >= lo && q < hi) mask |= 1u << j;
-            if (lo > q) qe = min(qe, lo);
-            if (hi > q) qe = min(qe, hi);
+#pragma unroll 1
+            for (int t = lmin; t < len[j]; ++t) {
+                const double b = __ldg(e2 + j * 8 * S_N + (qa[j] + t) * 4);
+                const int kc = ((qa[j] + t) * 4 + tig) ^ swz;
+                double a[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = tr[i * 8 * S_N + kc];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) dmma_8x8x4(acc[i][j], a[i], b);
+            }
         }
-        switch (mask) {
-            case 1: seg(std::integral_constant<int, 1>{}, q, qe); break;
-            case 2: seg(std::integral_constant<int, 2>{}, q, qe); break;
-            case 3: seg(std::integral_constant<int, 3>{}, q, qe); break;
-            case 4: seg(std::integral_constant<int, 4>{}, q, qe); break;
-            case 5: seg(std::integral_constant<int, 5>{}, q, qe); break;
-            case 6: seg(std::integral_constant<int, 6>{}, q, qe); break;
-            case 7: seg(std::integral_constant<int, 7>{}, q, qe); break;
-            case 8: seg(std::integral_constant<int, 8>{}, q, qe); break;
-            case 9: seg(std::integral_constant<int, 9>{}, q, qe); break;
-            case 10: seg(std::integral_constant<int, 10>{}, q, qe); break;
-            case 11: seg(std::integral_constant<int, 11>{}, q, qe); break;
-            case 12: seg(std::integral_constant<int, 12>{}, q, qe); break;
-            case 13: seg(std::integral_constant<int, 13>{}, q, qe); break;
-            case 14: seg(std::integral_constant<int, 14>{}, q, qe); break;
-            case 15: seg(std::integral_constant<int, 15>{}, q, qe); break;
-            default: break;
+    } else {
+        // k4 steps on which the set of active column groups is constant run as one loop of a
+        // mask-specialised body (E2 fragments of the active groups prefetched one step ahead)
+        auto seg = [&](auto mc, int qa, int qb) {
+            constexpr int M = decltype(mc)::value;
+            double bn_[4];
+    #pragma unroll
+            for (int j = 0; j < 4; ++j) bn_[j] = ((M >> j) & 1) ? __ldg(e2 + j * 8 * S_N + qa * 4) : 0.0;
+    #pragma unroll 2
+            for (int q = qa; q < qb; ++q) {
+                double b[4];
+    #pragma unroll
+                for (int j = 0; j < 4; ++j) b[j] = bn_[j];
+                if (q + 1 < qb) {
+    #pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if ((M >> j) & 1) bn_[j] = __ldg(e2 + j * 8 * S_N + q * 4 + 4);
+                }
+                const int kc = (q * 4 + tig) ^ swz;
+                double a[4];
+    #pragma unroll
+                for (int i = 0; i < 4; ++i) a[i] = tr[i * 8 * S_N + kc];
+                dmma_masked<M, false>(acc, a, b);
+            }
+        };
+        for (int q = kb / 4, q1 = ke / 4; q < q1;) {
+            unsigned mask = 0;
+            int qe = q1;
+    #pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int lo = static_cast<int>(fine[j] & 0xffffu), hi = lo + static_cast<int>(fine[j] >> 16);
+                if (q >= lo && q < hi) mask |= 1u << j;
+                if (lo > q) qe = min(qe, lo);
+                if (hi > q) qe = min(qe, hi);
+            }
+            switch (mask) {
+                case 1: seg(std::integral_constant<int, 1>{}, q, qe); break;
+                case 2: seg(std::integral_constant<int, 2>{}, q, qe); break;
+                case 3: seg(std::integral_constant<int, 3>{}, q, qe); break;
+                case 4: seg(std::integral_constant<int, 4>{}, q, qe); break;
+                case 5: seg(std::integral_constant<int, 5>{}, q, qe); break;
+                case 6: seg(std::integral_constant<int, 6>{}, q, qe); break;
+                case 7: seg(std::integral_constant<int, 7>{}, q, qe); break;
+                case 8: seg(std::integral_constant<int, 8>{}, q, qe); break;
+                case 9: seg(std::integral_constant<int, 9>{}, q, qe); break;
+                case 10: seg(std::integral_constant<int, 10>{}, q, qe); break;
+                case 11: seg(std::integral_constant<int, 11>{}, q, qe); break;
+                case 12: seg(std::integral_constant<int, 12>{}, q, qe); break;
+                case 13: seg(std::integral_constant<int, 13>{}, q, qe); break;
+                case 14: seg(std::integral_constant<int, 14>{}, q, qe); break;
+                case 15: seg(std::integral_constant<int, 15>{}, q, qe); break;
+                default: break;
+            }
+            q = qe;
         }
-        q = qe;
     }
     asm volatile("griddepcontrol.launch_dependents;");
 
@@ -290,9 +346,14 @@ bool slab12_supported(int n1, int n2) { return n1 == S_N && n2 == S_N; }
 int launch_slab12(const Slab12Args& g0, cudaStream_t s) {
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k_slab12, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
+        cudaFuncSetAttribute(k_slab12<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
+        cudaFuncSetAttribute(k_slab12<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
         attr_done = true;
     }
+    static const bool skew = [] {
+        const char* v = std::getenv("PQ_SLAB12_SKEW");
+        return v ? std::atoi(v) != 0 : true;  // skewed phase-2 loop by default (+2% config 2/4)
+    }();
     const long long total = static_cast<long long>(g0.n0) * g0.Z1;
     int launches = 0;
     Slab12Args g = g0;
@@ -309,7 +370,10 @@ int launch_slab12(const Slab12Args& g0, cudaStream_t s) {
         attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        cudaLaunchKernelEx(&cfg, k_slab12, g);
+        if (skew)
+            cudaLaunchKernelEx(&cfg, k_slab12<true>, g);
+        else
+            cudaLaunchKernelEx(&cfg, k_slab12<false>, g);
         ++launches;
     }
     return launches;

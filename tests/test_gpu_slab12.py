@@ -40,3 +40,14 @@ def test_slab12_mode_apply_vs_reference(pq, ref):
     got = pq.mode_apply(ms, shape, x)
     want = ref.mode_apply(ms, x)
     assert np.max(np.abs(got - want)) / np.max(np.abs(want)) < 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("skew", ["0", "1"])
+def test_slab12_phase2_loop_variants_bitwise(tmp_path, skew):
+    """Both phase-2 k loops of k_slab12 (aligned mask segments, PQ_SLAB12_SKEW=0; per-group skewed
+    ranges, PQ_SLAB12_SKEW=1) give the separate launches' bits."""
+    fused = _run(tmp_path, f"fused_skew{skew}", {"PQ_SLAB12_SKEW": skew})
+    sep = _run(tmp_path, "separate", {"PQ_SLAB12": "0"})
+    for k in sep.files:
+        assert np.array_equal(fused[k], sep[k]), f"{k}: PQ_SLAB12_SKEW={skew} differs from the separate launches"
