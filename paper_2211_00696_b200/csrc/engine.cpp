@@ -675,9 +675,38 @@ static bool band_enabled(int n, long long N) {
     // (config 1, N = 4096: 4568 actions/s without, 3665 with)
     return !disabled && n >= 64 && n <= 512 && N >= (1LL << 18);
 }
+// Fragment-major copies of an exponential batch for k_slab12's phase 2 (PQ_E2PACK=0 disables: the
+// kernel then reads E2 row-major).  Written by the same k_band_ranges launch as the batch's band
+// table and found again from the table pointer, so they follow the tables through every call path.
+static bool e2pack_enabled(int n) {
+    static const bool on = [] {
+        const char* v = std::getenv("PQ_E2PACK");
+        return !(v && v[0] == '0');
+    }();
+    return on && slab12_enabled() && slab12_supported(n, n);
+}
+static void band_pack_register(pq_ctx& c, const int2* band, size_t matrices, double* pack, int n) {
+    const size_t recs = matrices * static_cast<size_t>(band_row_blocks(n));
+    auto& v = c.band_packs;
+    v.erase(std::remove_if(v.begin(), v.end(),
+                           [&](const pq_ctx::BandPack& e) { return e.lo < band + recs && band < e.lo + e.recs; }),
+            v.end());
+    if (pack) v.push_back({band, recs, pack, n});  // pack == null: only forget what overlapped
+}
+// pack of the matrix whose band record starts at `band` (null: none); *stride_per_matrix = doubles
+static double* band_pack_find(const pq_ctx& c, const int2* band, int n, long long* per_matrix = nullptr) {
+    if (!band) return nullptr;
+    for (const auto& e : c.band_packs)
+        if (e.n == n && band >= e.lo && band < e.lo + e.recs) {
+            const long long pd = band_pack_doubles(n);
+            if (per_matrix) *per_matrix = pd;
+            return e.pack + static_cast<long long>((band - e.lo) / band_row_blocks(n)) * pd;
+        }
+    return nullptr;
+}
 static void band_ranges(pq_ctx& c, int n, int count, const double* E, int2* band) {
     if (!band || count <= 0) return;
-    launch_band_ranges(n, count, E, band, c.stream);
+    launch_band_ranges(n, count, E, band, c.stream, band_pack_find(c, band, n));
     count_launch(c);
 }
 
@@ -1216,6 +1245,12 @@ PhiExps phi_exponentials(pq_ctx& c, const DevOp& op, double s, int l, const std:
         int2* band = band_enabled(n, op.N)
                          ? static_cast<int2*>(ws_bytes(c, tag + "_band" + std::to_string(n), sizeof(int2) * es.size() * RB))
                          : nullptr;
+        if (band)
+            band_pack_register(c, band, es.size(),
+                               op.d == 3 && e2pack_enabled(n)
+                                   ? ws(c, tag + "_pack" + std::to_string(n), es.size() * band_pack_doubles(n))
+                                   : nullptr,
+                               n);
         // the side stream is in order, so waiting on the last ev_late covers every group's late work
         const bool async = late_async && split < static_cast<int>(es.size());
         if (expm_taylor(c, n, base, s, es, out, split, async, band, op.serial)) {
@@ -1381,6 +1416,9 @@ void mode_chain(pq_ctx& c, int d, const int* n, const double* const* E, const lo
                     sg.sE2 = E_stride[2];
                     sg.band2 = bt;
                     sg.sband2 = bs;
+                    long long pd = 0;
+                    sg.E2p = band_pack_find(c, bt, n[m], &pd);
+                    sg.sE2p = (E_stride[m] / nn) * pd;
                 }
             }
             sg.X = src;
@@ -1441,6 +1479,7 @@ static void factor_bands(pq_ctx& c, const DevOp& op, const int2** out) {
             c.fac_band[k] = nullptr;
             if (!band_enabled(op.n[k], op.N)) continue;
             int2* b = static_cast<int2*>(ws_bytes(c, "facband" + std::to_string(k), sizeof(int2) * band_row_blocks(op.n[k])));
+            band_pack_register(c, b, 1, nullptr, op.n[k]);
             band_ranges(c, op.n[k], 1, op.F[k], b);
             c.fac_band[k] = b;
         }

@@ -112,6 +112,15 @@ struct pq_ctx {
     uint64_t op_serial = 0;  // incremented per operator upload (one per API call)
     // negligible-block tables of the operator's own factors (kron_matvec), per upload serial
     uint64_t fac_band_serial = 0;
+    // fragment-major copies of exponential batches (kernels.hpp launch_band_ranges pack), found from
+    // the batch's band-table pointer: records [lo, lo + recs) <-> pack + record_index * per-matrix size
+    struct BandPack {
+        const int2* lo = nullptr;
+        size_t recs = 0;
+        double* pack = nullptr;
+        int n = 0;
+    };
+    std::vector<BandPack> band_packs;
     uint64_t tri_serial = 0;  // operator upload whose factors were checked for tridiagonality
     bool tri = false;
     const int2* fac_band[3] = {nullptr, nullptr, nullptr};

@@ -596,10 +596,24 @@ void launch_imax(const int* v, int count, int* out, cudaStream_t s) { k_imax<<<1
 //  * fine entries, one per 8-row group: {first, last+1} of the 4-column chunks (DMMA k4 steps)
 //    whose max exceeds 2^-64 x the GROUP's max (<= the block's: again at least as conservative).
 // Record of matrix z: [coarse rb = 0..RB) [fine g = 0..4RB), RB = ceil(n/32) (band_row_blocks).
+//
+// pack (nullable): fragment-major copy of the matrices for tiles that read the exponential's m8n8k4
+// fragments straight from global memory (k_slab12 phase 2): matrix z, 8-row group G, k4 step q, lane
+// (gid, tig) -> E[G*8 + gid][4q + tig] at ((z*RG + G)*NC + q)*32 + lane (band_pack_doubles(n) per
+// matrix, zero padded), so a warp's fragment load is one contiguous 256-byte run instead of 8 lines.
 __global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __restrict__ E, int2* __restrict__ out,
-                                                     int fine_on) {
+                                                     int fine_on, double* __restrict__ pack) {
     const int z = blockIdx.x, rb = blockIdx.y, RB = gridDim.y;
     const double* e = E + (long long)z * n * n;
+    if (pack) {
+        const int NCp = (n + 3) / 4, RG = (n + 7) / 8;
+        double* pz = pack + (long long)z * RG * NCp * 32;
+        for (int item = threadIdx.x; item < 4 * NCp * 32; item += blockDim.x) {
+            const int ln = item & 31, q = (item >> 5) % NCp, g = (item >> 5) / NCp;
+            const int G = rb * 4 + g, r = G * 8 + (ln >> 2), cc = q * 4 + (ln & 3);
+            if (G < RG) pz[((long long)G * NCp + q) * 32 + ln] = (r < n && cc < n) ? __ldg(e + (long long)r * n + cc) : 0.0;
+        }
+    }
     __shared__ double colmax[4][512];  // [group][column], n <= 512
     __shared__ double cmax[4][128];    // [group][4-column chunk]
     __shared__ double gmax[4];
@@ -683,10 +697,10 @@ static const bool g_fine_on = [] {
     const char* e = std::getenv("PQ_FINE");
     return !(e && e[0] == '0');
 }();
-void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s) {
+void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s, double* pack) {
     if (count <= 0) return;
     if (n > 512) throw std::invalid_argument("band ranges: n > 512");
-    k_band_ranges<<<dim3(count, (n + 31) / 32), 256, 0, s>>>(n, E, out, g_fine_on ? 1 : 0);
+    k_band_ranges<<<dim3(count, (n + 31) / 32), 256, 0, s>>>(n, E, out, g_fine_on ? 1 : 0, pack);
 }
 
 

@@ -76,6 +76,9 @@ struct Slab12Args {
     long long sband1 = 0;
     const int2* band2 = nullptr;
     long long sband2 = 0;
+    // fragment-major copies of the E2 matrices (launch_band_ranges pack; null = read E2 row-major)
+    const double* E2p = nullptr;
+    long long sE2p = 0;
     const double* X = nullptr;
     long long sX = 0;
     double* Y = nullptr;
@@ -128,7 +131,9 @@ void launch_lu_factor_solve(int n, int count, double* P, double* Q, int* piv, in
 //    for a k-major exponential) fragment issues.
 // Dropping the rest changes a mode product by at most n 2^-64 of its max-norm -- below half an ulp
 // in practice.
-void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s);
+void launch_band_ranges(int n, int count, const double* E, int2* out, cudaStream_t s, double* pack = nullptr);
+// doubles per matrix of the fragment-major copy launch_band_ranges writes into `pack` (k_slab12 phase 2)
+inline long long band_pack_doubles(int n) { return static_cast<long long>((n + 7) / 8) * ((n + 3) / 4) * 32; }
 inline int band_row_blocks(int n) { return 5 * ((n + 31) / 32); }  // record length (int2)
 // max over z of s_z -> *out (device int)
 void launch_imax(const int* v, int count, int* out, cudaStream_t s);

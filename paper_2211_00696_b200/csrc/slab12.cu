@@ -83,7 +83,7 @@ __device__ __forceinline__ unsigned fine_range(const int2* band, long long rec, 
 }
 }  // namespace
 
-template <bool SKEW>
+template <bool SKEW, bool PACK>
 __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
     extern __shared__ __align__(16) double smem[];
     const int rq = blockIdx.x;
@@ -211,7 +211,11 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
     const int kb = lo2 * S_BK, ke = hi2 > lo2 ? hi2 * S_BK : kb;
 #pragma unroll
     for (int j = 0; j < 4; ++j) fine[j] = fine_range(g.band2, z1 * g.sband2, warp * 4 + j);  // E2 row groups = columns j
-    const double* e2 = E2 + (warp * 32 + gid) * S_N + tig;
+    // E2 fragment of column group j at k4 step q: row-major E2[(warp*32 + j*8 + gid)][4q + tig] (8 lines
+    // per warp load), or the fragment-major copy (PACK: one contiguous 256-byte run per warp load)
+    const double* e2 = PACK ? g.E2p + z1 * g.sE2p + static_cast<long long>(warp) * 4 * (S_N / 4) * 32 + lane
+                            : E2 + (warp * 32 + gid) * S_N + tig;
+    auto ld_e2 = [&](int j, int q) { return PACK ? __ldg(e2 + (j * (S_N / 4) + q) * 32) : __ldg(e2 + j * 8 * S_N + q * 4); };
     const double* tr = T + gid * S_N;
     if constexpr (SKEW) {
         // Skewed k loop: column group j walks its OWN k4 range [qa_j, qa_j + len_j) -- step t
@@ -231,7 +235,7 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
         double bn_[4];
         if (lmin > 0) {
 #pragma unroll
-            for (int j = 0; j < 4; ++j) bn_[j] = __ldg(e2 + j * 8 * S_N + qa[j] * 4);
+            for (int j = 0; j < 4; ++j) bn_[j] = ld_e2(j, qa[j]);
         }
 #pragma unroll 1
         for (int t = 0; t < lmin; ++t) {
@@ -240,7 +244,7 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
             for (int j = 0; j < 4; ++j) b[j] = bn_[j];
             if (t + 1 < lmin) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) bn_[j] = __ldg(e2 + j * 8 * S_N + (qa[j] + t + 1) * 4);
+                for (int j = 0; j < 4; ++j) bn_[j] = ld_e2(j, qa[j] + t + 1);
             }
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -257,7 +261,7 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
         for (int j = 0; j < 4; ++j) {
 #pragma unroll 1
             for (int t = lmin; t < len[j]; ++t) {
-                const double b = __ldg(e2 + j * 8 * S_N + (qa[j] + t) * 4);
+                const double b = ld_e2(j, qa[j] + t);
                 const int kc = ((qa[j] + t) * 4 + tig) ^ swz;
                 double a[4];
 #pragma unroll
@@ -273,7 +277,7 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
             constexpr int M = decltype(mc)::value;
             double bn_[4];
     #pragma unroll
-            for (int j = 0; j < 4; ++j) bn_[j] = ((M >> j) & 1) ? __ldg(e2 + j * 8 * S_N + qa * 4) : 0.0;
+            for (int j = 0; j < 4; ++j) bn_[j] = ((M >> j) & 1) ? ld_e2(j, qa) : 0.0;
     #pragma unroll 2
             for (int q = qa; q < qb; ++q) {
                 double b[4];
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
                 if (q + 1 < qb) {
     #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                        if ((M >> j) & 1) bn_[j] = __ldg(e2 + j * 8 * S_N + q * 4 + 4);
+                        if ((M >> j) & 1) bn_[j] = ld_e2(j, q + 1);
                 }
                 const int kc = (q * 4 + tig) ^ swz;
                 double a[4];
@@ -346,8 +350,10 @@ bool slab12_supported(int n1, int n2) { return n1 == S_N && n2 == S_N; }
 int launch_slab12(const Slab12Args& g0, cudaStream_t s) {
     static bool attr_done = false;
     if (!attr_done) {
-        cudaFuncSetAttribute(k_slab12<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
-        cudaFuncSetAttribute(k_slab12<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
+        cudaFuncSetAttribute(k_slab12<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
+        cudaFuncSetAttribute(k_slab12<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
+        cudaFuncSetAttribute(k_slab12<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
+        cudaFuncSetAttribute(k_slab12<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, S_SMEM);
         attr_done = true;
     }
     static const bool skew = [] {
@@ -370,10 +376,10 @@ int launch_slab12(const Slab12Args& g0, cudaStream_t s) {
         attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        if (skew)
-            cudaLaunchKernelEx(&cfg, k_slab12<true>, g);
+        if (g.E2p)
+            skew ? cudaLaunchKernelEx(&cfg, k_slab12<true, true>, g) : cudaLaunchKernelEx(&cfg, k_slab12<false, true>, g);
         else
-            cudaLaunchKernelEx(&cfg, k_slab12<false>, g);
+            skew ? cudaLaunchKernelEx(&cfg, k_slab12<true, false>, g) : cudaLaunchKernelEx(&cfg, k_slab12<false, false>, g);
         ++launches;
     }
     return launches;
