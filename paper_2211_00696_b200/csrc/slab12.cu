@@ -136,6 +136,10 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
 
     if (NKT > 0) load(0);
     cp_commit();
+    if (g.l2_prefetch && tid == 0 && NKT > 1)  // PQ_L2PF: the rest of this quarter's X rows (contiguous) to L2
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X + static_cast<long long>(lo1 + 1) * S_BK * S_N),
+                     "r"((NKT - 1) * S_BK * S_N * 8)
+                     : "memory");
     const double* tA0 = sA + gid * S_SA + tig;
     const double* tB0 = sB + tig * S_SB + warp * 32 + gid;
 #pragma unroll 1
@@ -363,6 +367,7 @@ int launch_slab12(const Slab12Args& g0, cudaStream_t s) {
     const long long total = static_cast<long long>(g0.n0) * g0.Z1;
     int launches = 0;
     Slab12Args g = g0;
+    g.l2_prefetch = l2_prefetch_enabled() ? 1 : 0;
     for (long long z0 = 0; z0 < total; z0 += 65535) {
         g.z_off = z0;
         const long long zc = total - z0 < 65535 ? total - z0 : 65535;
