@@ -356,17 +356,6 @@ __device__ __forceinline__ void gemm_tile(const GemmArgs& g, int bx, int by, int
         atomicAdd(g.flop_counter, f_exec);
     }
     k_next = kt_lo * BK;
-    if constexpr (!BKM && VEC == 2) {
-        // PQ_L2PF: the rows of B beyond the first slice go to L2 now (one 16-byte-aligned bulk prefetch per
-        // row segment of this tile), so the later cp.async slices wait on L2, not on HBM
-        if (g.l2_prefetch && n0 + BN <= g.N && (g.ldb & 1) == 0) {
-            const int r1 = min(KT * BK, g.K);
-            for (int r = k_next + BK + tid; r < r1; r += NT) {
-                const double* p = B + (long long)r * g.ldb + n0;
-                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(BN * 8) : "memory");
-            }
-        }
-    }
     if constexpr (AFF) {
         a_p += k_next;
         b_p += static_cast<long long>(k_next) * b_kstep;

@@ -56,9 +56,7 @@ static const bool g_persistent_enabled = [] {
     return e && e[0] == '1';
 }();
 
-int launch_gemm(const GemmArgs& g_in, cudaStream_t s) {
-    GemmArgs g = g_in;
-    g.l2_prefetch = l2_prefetch_enabled() && g.band ? 1 : 0;
+int launch_gemm(const GemmArgs& g, cudaStream_t s) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0 || g.Z <= 0) return 0;
     // 16-byte cp.async needs every row start and batch offset 16-byte aligned.
     const bool vec2 = (g.K % 2 == 0) && (g.b_kmajor || g.N % 2 == 0) && g.lda % 2 == 0 && g.ldb % 2 == 0 &&

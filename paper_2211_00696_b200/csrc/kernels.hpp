@@ -59,20 +59,11 @@ struct GemmArgs {
     long long band_stride = 0;
     int band_mode = 0, band_rows = 0;
     // profiling: every CTA adds the flops it actually executed (2 rows cols k) here
-    // PQ_L2PF=1: each CTA prefetches the rest of its B k-range into L2 before its first slice lands
-    int l2_prefetch = 0;
     unsigned long long* flop_counter = nullptr;
     const char* tag = nullptr;  // call site, for the profiling breakdown only
     const RemoteMap* remote = nullptr;  // device table: remote-store epilogue (plain stores only)
 };
-int launch_gemm(const GemmArgs& g, cudaStream_t s);
-inline bool l2_prefetch_enabled() {
-    static const bool on = [] {
-        const char* v = std::getenv("PQ_L2PF");
-        return v && v[0] != '0';
-    }();
-    return on;
-}  // returns number of kernel launches
+int launch_gemm(const GemmArgs& g, cudaStream_t s);  // returns number of kernel launches
 // Fused last two modes of a 3-D apply with n1 = n2 = 128 (slab12.cu): for every x-slab
 // X_s = X[z1][i0] (128 x 128), Y_s = (E1 X_s) E2^T, bitwise the two separate band tiles.
 // Batch entry z1 < Z1 uses E1 + z1*sE1, E2 + z1*sE2, band tables band1 + z1*sband1 (4 int2,
@@ -95,7 +86,6 @@ struct Slab12Args {
     long long sY = 0;
     int n0 = 1, Z1 = 1;
     long long z_off = 0;
-    int l2_prefetch = 0;  // PQ_L2PF=1: the CTA's X k-range prefetched into L2 (one bulk prefetch)
     unsigned long long* flop_counter = nullptr;
 };
 bool slab12_supported(int n1, int n2);

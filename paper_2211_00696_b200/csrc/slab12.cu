@@ -106,6 +106,11 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
     unsigned fine[4];  // phase 1: E1 row groups of this quarter (fragment rows i)
 #pragma unroll
     for (int i = 0; i < 4; ++i) fine[i] = fine_range(g.band1, z1 * g.sband1, rq * 4 + i);
+    // phase 2's band entries are requested now (lane 0: the warp's coarse entry, lanes 1-4: its four
+    // fine entries) and handed out by shuffles after phase 1, instead of a dependent L2 round trip there
+    int2 pre2 = make_int2(0, 0);
+    if (g.band2 && lane < 5)
+        pre2 = g.band2[z1 * g.sband2 + (lane == 0 ? warp : S_N / 32 + warp * 4 + lane - 1)];
 
     // ---- phase 1: T = E1[rq block] X_s  (32 x 128), cp.async 2-stage pipeline ----
     double* sA = smem;
@@ -136,10 +141,6 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
 
     if (NKT > 0) load(0);
     cp_commit();
-    if (g.l2_prefetch && tid == 0 && NKT > 1)  // PQ_L2PF: the rest of this quarter's X rows (contiguous) to L2
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X + static_cast<long long>(lo1 + 1) * S_BK * S_N),
-                     "r"((NKT - 1) * S_BK * S_N * 8)
-                     : "memory");
     const double* tA0 = sA + gid * S_SA + tig;
     const double* tB0 = sB + tig * S_SB + warp * 32 + gid;
 #pragma unroll 1
@@ -210,11 +211,25 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
     __syncthreads();
 
     // ---- phase 2: Y[rq block, warp block] = T E2[warp block]^T, k over E2's block band ----
-    int lo2, hi2;
-    slice_range(g.band2, z1 * g.sband2 + warp, lo2, hi2);
+    int lo2 = 0, hi2 = S_N / S_BK;
+    {
+        const int cx = __shfl_sync(0xffffffffu, pre2.x, 0), cy = __shfl_sync(0xffffffffu, pre2.y, 0);
+        if (g.band2) {  // as slice_range
+            if (cy > cx) {
+                lo2 = cx >> 1;
+                hi2 = min(hi2, (cy + 1) >> 1);
+            } else {
+                lo2 = hi2 = 0;
+            }
+        }
+    }
     const int kb = lo2 * S_BK, ke = hi2 > lo2 ? hi2 * S_BK : kb;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) fine[j] = fine_range(g.band2, z1 * g.sband2, warp * 4 + j);  // E2 row groups = columns j
+    for (int j = 0; j < 4; ++j) {  // E2 row groups = columns j (as fine_range)
+        const int fx = __shfl_sync(0xffffffffu, pre2.x, j + 1), fy = __shfl_sync(0xffffffffu, pre2.y, j + 1);
+        fine[j] = !g.band2 ? 0xffffu << 16
+                           : fy > fx ? static_cast<unsigned>(fx) | (static_cast<unsigned>(fy - fx) << 16) : 0u;
+    }
     // E2 fragment of column group j at k4 step q: row-major E2[(warp*32 + j*8 + gid)][4q + tig] (8 lines
     // per warp load), or the fragment-major copy (PACK: one contiguous 256-byte run per warp load)
     const double* e2 = PACK ? g.E2p + z1 * g.sE2p + static_cast<long long>(warp) * 4 * (S_N / 4) * 32 + lane
@@ -263,9 +278,11 @@ __global__ void __launch_bounds__(128, 4) k_slab12(const Slab12Args g) {
         // the groups' remaining steps (ranges of unequal length at the matrix edges)
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
+            double bnx = lmin < len[j] ? ld_e2(j, qa[j] + lmin) : 0.0;
 #pragma unroll 1
             for (int t = lmin; t < len[j]; ++t) {
-                const double b = ld_e2(j, qa[j] + t);
+                const double b = bnx;
+                if (t + 1 < len[j]) bnx = ld_e2(j, qa[j] + t + 1);
                 const int kc = ((qa[j] + t) * 4 + tig) ^ swz;
                 double a[4];
 #pragma unroll
@@ -367,7 +384,6 @@ int launch_slab12(const Slab12Args& g0, cudaStream_t s) {
     const long long total = static_cast<long long>(g0.n0) * g0.Z1;
     int launches = 0;
     Slab12Args g = g0;
-    g.l2_prefetch = l2_prefetch_enabled() ? 1 : 0;
     for (long long z0 = 0; z0 < total; z0 += 65535) {
         g.z_off = z0;
         const long long zc = total - z0 < 65535 ? total - z0 : 65535;

@@ -1,0 +1,19 @@
+#!/bin/bash
+# Session 4: k_slab12 with phase 2's band entries requested at kernel start + prefetched remainder loops
+OUT=gpurun_out/s4e
+mkdir -p $OUT
+timeout 900 python -m pytest tests/test_gpu_slab12.py tests/test_gpu_configs.py tests/test_gpu_band.py tests/test_gpu_env_variants.py -x -q -m gpu > $OUT/tests.txt 2>&1; echo "tests rc=$?" >> $OUT/tests.txt
+for rep in 1 2 3; do
+  timeout 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline 2>>$OUT/err.txt | python -c "
+import sys,json
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print(round(d['value'],2), round(d['ms_per_step'],4), 'e2e', round(d['e2e']['value'],2), 'frac', round(d['roofline']['frac'],3))" >> $OUT/ab.txt
+done
+timeout 300 python bench.py --config 4 --steps 5 --warmup 3 --no-cpu-baseline 2>>$OUT/err.txt | python -c "
+import sys,json
+for l in sys.stdin:
+    if l.startswith('{'):
+        d=json.loads(l); print('cfg4', round(d['value'],2), round(d['ms_per_step'],4), 'e2e', round(d['e2e']['value'],2))" >> $OUT/ab.txt
+timeout 300 python tools/gemm_breakdown.py 2 3 > $OUT/breakdown_cfg2.txt 2>&1
+ls -la $OUT
