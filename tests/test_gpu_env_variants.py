@@ -29,7 +29,9 @@ def test_runtime_switches_keep_results_bitwise(tmp_path):
     base = _run(tmp_path, "default", {})
     for name, extra in [("gate", {"PQ_COMPUTE_GATE": "1"}), ("fuse", {"PQ_SQ_FUSE": "1"}),
                         ("nospec", {"PQ_PLAN_SPEC": "0"}), ("nodefer", {"PQ_CC_DEFER": "0"}),
-                        ("sep12", {"PQ_SLAB12": "0"}), ("noprio", {"PQ_SIDE_PRIO": "0"}), ("kk64", {"PQ_KK_TALL": "0"}), ("gate_fuse", {"PQ_COMPUTE_GATE": "1", "PQ_SQ_FUSE": "1"})]:
+                        ("sep12", {"PQ_SLAB12": "0"}), ("noprio", {"PQ_SIDE_PRIO": "0"}), ("kk64", {"PQ_KK_TALL": "0"}),
+                        ("nopack", {"PQ_E2PACK": "0"}), ("noskew_nopack", {"PQ_SLAB12_SKEW": "0", "PQ_E2PACK": "0"}),
+                        ("noskew", {"PQ_SLAB12_SKEW": "0"}), ("gate_fuse", {"PQ_COMPUTE_GATE": "1", "PQ_SQ_FUSE": "1"})]:
         got = _run(tmp_path, name, extra)
         for k in base.files:
             assert np.array_equal(got[k], base[k]), f"{name}: {k} differs from the default build"
