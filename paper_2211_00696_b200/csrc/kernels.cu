@@ -605,7 +605,10 @@ __global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __rest
                                                      int fine_on, double* __restrict__ pack) {
     const int z = blockIdx.x, rb = blockIdx.y, RB = gridDim.y;
     const double* e = E + (long long)z * n * n;
-    if (pack) {
+    // n a multiple of 8 (every n the pack is used for): the copy is written from the values the
+    // reduction below loads anyway; other n take a separate pass with zero padding
+    const bool pack_inline = pack && (n & 7) == 0;
+    if (pack && !pack_inline) {
         const int NCp = (n + 3) / 4, RG = (n + 7) / 8;
         double* pz = pack + (long long)z * RG * NCp * 32;
         for (int item = threadIdx.x; item < 4 * NCp * 32; item += blockDim.x) {
@@ -624,10 +627,14 @@ __global__ void __launch_bounds__(256) k_band_ranges(int n, const double* __rest
         const int g = item / n, c = item - g * n;
         const int r0 = rb * 32 + g * 8;
         double m = 0.0;
+        // fragment-major position of (row r0 + u, column c): ((G * n/4 + c/4) * 32 + 4u + c%4
+        double* pk = pack_inline ? pack + (((long long)z * (n >> 3) + rb * 4 + g) * (n >> 2) + (c >> 2)) * 32 + (c & 3) : nullptr;
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             if (r0 + u < n) {
-                const double v = fabs(__ldg(e + (long long)(r0 + u) * n + c));
+                const double raw = __ldg(e + (long long)(r0 + u) * n + c);
+                if (pk) pk[4 * u] = raw;
+                const double v = fabs(raw);
                 m = !(v <= 1.7976931348623157e308) ? kInf : fmax(m, v);
             }
         }
