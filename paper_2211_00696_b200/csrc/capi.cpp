@@ -449,6 +449,7 @@ int pq_ctx_release_workspace(pq_ctx* c) {
         free_graveyard(*c);
         for (auto& kv : c->bufs) ws_free_now(*c, kv.second.p);
         c->bufs.clear();
+        c->band_packs.clear();  // the fragment-major copies went with the workspace
         c->fac_cache.clear();
         trim_pool(*c);
     });
