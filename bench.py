@@ -566,7 +566,10 @@ def run_ours_phi(args, world, rank, local) -> None:
     # at least 4 calls per caller: with fewer, the simultaneous start and the last caller's tail
     # dominate the region (config 2, 6 callers: 385-409 actions/s over 10 calls, 438 over 24)
     k_multi = max(args.steps, 4 * ncall)
-    ms_e2e2_max = max_over_ranks(e2e_callers(k_multi), world)
+    # the region is short (tens of ms at config 2) and runs on shared host cores: three repetitions,
+    # the MEDIAN is reported and all three are listed (one noisy box measured 406 / 518 / 518)
+    reps_ms = [max_over_ranks(e2e_callers(k_multi), world) for _ in range(1 if nodes else 3)]
+    ms_e2e2_max = sorted(reps_ms)[len(reps_ms) // 2]
     comm_bytes = comm.stats(reset=True)[0] / args.steps if nodes else None
     e2e_multi = units * k_multi / args.steps / (ms_e2e2_max / 1e3)
     # a deployment runs as many host callers as pays: small problems (config 1, ~0.2 ms per call)
@@ -589,12 +592,13 @@ def run_ours_phi(args, world, rank, local) -> None:
                 "d2h_bytes_per_step": int(nb * (w.p + 1) * NO * 8), "callers": e2e_callers,
                 "single_caller_value": e2e_single, "multi_caller_value": e2e_multi, "multi_callers": ncall,
                 "multi_caller_calls": k_multi,
+                "multi_caller_reps": [units * k_multi / args.steps / (m / 1e3) for m in reps_ms],
                 "distinct_rhs": {"device": npool, "pinned_host": npin},
                 "note": ("pq_phi_0p with pinned host b in and all p+1 vectors back every step; concurrent "
                          "host threads with their own contexts/streams overlap one call's PCIe transfers with "
                          "another's compute; value = the better of single_caller_value (one synchronous caller) "
                          "and multi_caller_value (multi_callers threads sharing multi_caller_calls calls, at least 4 "
-                         "each), `callers` says which; the operator's "
+                         "each; the median of the repetitions listed in multi_caller_reps), `callers` says which; the operator's "
                          "factors are uploaded once (bit-identical factors are not re-copied) and not counted")},
     }
     if nodes:
